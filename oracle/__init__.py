@@ -1,0 +1,294 @@
+"""fp64 CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+Thin ctypes binding over oracle/hdf_oracle.c (plain C, fp64).  Only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may import this
+package.  It shares no code with paper_1811_02363_b200 (the CUDA path) and never imports it.
+
+Functions follow PAPER.md (see the C file for per-function citations):
+  cluster        bisecting K-means (readings R1-R5)
+  gram, pinv     A_kl = phi(mu_k - mu_l) and MATLAB-style pinv (R6)
+  filter         Algorithm 1 with the R9 degenerate-normaliser rule
+  filter_pixels  the same filter evaluated at selected pixels from (temp1)/(temp2)
+  bruteforce     (num)/(den), window clipped to Omega (R8)
+  nystrom        Appendix A identity written as a direct window sum
+  filter_hard    hard-assignment variant (coeffICIP)/(HDapprox2)
+  conv2          omega * x with the clipped window
+  mse, psnr      (rmse), intensities normalised by R
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "hdf_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+OK, ERR_ARG, ERR_K, ERR_MEM = 0, 1, 2, 3
+KIND = {"gaussian": 0, "box": 1}
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (fp64, -ffp-contract=off, OpenMP)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
+               "-Wall", "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+def _L():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = C.CDLL(_LIB)
+            D = C.POINTER(C.c_double)
+            I32 = C.POINTER(C.c_int32)
+            LP = C.POINTER(C.c_long)
+            U8 = C.POINTER(C.c_uint8)
+            i, d, l = C.c_int, C.c_double, C.c_long
+            lib.orc_phi.argtypes = [D, i, d]; lib.orc_phi.restype = d
+            lib.orc_radius.argtypes = [i, d, i]; lib.orc_radius.restype = i
+            lib.orc_spatial_taps.argtypes = [i, d, i, D]
+            lib.orc_cluster.argtypes = [D, l, i, i, i, i, D, I32, D, D, C.POINTER(C.c_int)]
+            lib.orc_gram.argtypes = [D, i, i, d, D]
+            lib.orc_pinv_sym.argtypes = [D, i, D, D, C.POINTER(C.c_int), D]
+            lib.orc_conv2.argtypes = [D, D, i, i, i, d, i]
+            lib.orc_bruteforce_pixels.argtypes = [D, i, D, i, i, i, i, d, i, d, LP, l, D, D]
+            lib.orc_filter.argtypes = [D, i, D, i, i, i, i, d, i, d, i, D, d, D, D, U8, LP]
+            lib.orc_filter_pixels.argtypes = [D, i, D, i, i, i, i, d, i, d, i, D, d, LP, l, D, D, U8]
+            lib.orc_nystrom_pixels.argtypes = [D, i, D, i, i, i, i, d, i, d, i, D, LP, l, D, D]
+            lib.orc_coefficients.argtypes = [D, l, i, D, i, d, D, D]
+            lib.orc_filter_hard.argtypes = [D, i, D, i, i, i, i, d, i, d, i, D, I32, D]
+            for fn in ("orc_spatial_taps", "orc_cluster", "orc_gram", "orc_pinv_sym", "orc_conv2",
+                       "orc_bruteforce_pixels", "orc_filter", "orc_filter_pixels",
+                       "orc_nystrom_pixels", "orc_filter_hard", "orc_coefficients"):
+                getattr(lib, fn).restype = C.c_int
+            _lib = lib
+    return _lib
+
+
+def _d(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _pd(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _check(st: int, what: str):
+    if st != OK:
+        raise RuntimeError(f"oracle {what} failed with status {st}")
+
+
+class OracleKError(ValueError):
+    def __init__(self, achievable: int):
+        super().__init__(f"K exceeds the number of distinct guide vectors ({achievable})")
+        self.achievable = achievable
+
+
+def radius(kind: str, sigma_s: float, r: int = -1) -> int:
+    return _L().orc_radius(KIND[kind], float(sigma_s), int(r))
+
+
+def phi(x, sigma_r: float) -> float:
+    x = _d(x).reshape(-1)
+    return _L().orc_phi(_pd(x), x.size, float(sigma_r))
+
+
+def spatial_taps(kind: str, sigma_s: float, r: int = -1) -> np.ndarray:
+    R = radius(kind, sigma_s, r)
+    w = np.zeros(2 * R + 1)
+    _check(_L().orc_spatial_taps(KIND[kind], float(sigma_s), R, _pd(w)), "taps")
+    return w
+
+
+def cluster(p, K: int, cap: int = 4096, max_iter: int = 50):
+    """Bisecting K-means of the guide p [..., rho].  Returns (centres [K,rho] fp64, labels [N]
+    int32, leaf_sse [K], E_K)."""
+    p = _d(p)
+    rho = p.shape[-1]
+    P = p.reshape(-1, rho)
+    N = P.shape[0]
+    cen = np.zeros((K, rho))
+    lab = np.zeros(N, dtype=np.int32)
+    sse = np.zeros(K)
+    ek = C.c_double(0.0)
+    ach = C.c_int(0)
+    st = _L().orc_cluster(_pd(P), N, rho, int(K), int(cap), int(max_iter), _pd(cen),
+                          lab.ctypes.data_as(C.POINTER(C.c_int32)), _pd(sse), C.byref(ek), C.byref(ach))
+    if st == ERR_K:
+        raise OracleKError(ach.value)
+    _check(st, "cluster")
+    return cen, lab, sse, ek.value
+
+
+def gram(mu, sigma_r: float) -> np.ndarray:
+    mu = _d(mu)
+    K, rho = mu.shape
+    A = np.zeros((K, K))
+    _check(_L().orc_gram(_pd(mu), K, rho, float(sigma_r), _pd(A)), "gram")
+    return A
+
+
+def pinv(A):
+    """Returns (A^+, eigenvalues, rank, tol) by cyclic Jacobi, MATLAB tolerance (R6)."""
+    A = _d(A)
+    K = A.shape[0]
+    Ap = np.zeros((K, K))
+    lam = np.zeros(K)
+    rank = C.c_int(0)
+    tol = C.c_double(0.0)
+    _check(_L().orc_pinv_sym(_pd(A), K, _pd(Ap), _pd(lam), C.byref(rank), C.byref(tol)), "pinv")
+    return Ap, lam, rank.value, tol.value
+
+
+def coefficients(p, mu, sigma_r: float):
+    """Algorithm 1 loops for1/for2: returns (b [N,K], c [N,K]) with c(i) = A^+ b(i)."""
+    p = _d(p)
+    rho = p.shape[-1]
+    P = p.reshape(-1, rho)
+    N = P.shape[0]
+    mu = _d(mu)
+    K = mu.shape[0]
+    b = np.zeros((K, N))
+    c = np.zeros((K, N))
+    _check(_L().orc_coefficients(_pd(P), N, rho, _pd(mu), K, float(sigma_r), _pd(b), _pd(c)), "coefficients")
+    return b.T.copy(), c.T.copy()
+
+
+def conv2(x, kind: str, sigma_s: float, r: int = -1) -> np.ndarray:
+    x = _d(x)
+    H, W = x.shape
+    out = np.zeros_like(x)
+    _check(_L().orc_conv2(_pd(x), _pd(out), H, W, KIND[kind], float(sigma_s), int(r)), "conv2")
+    return out
+
+
+def _fp(f, p):
+    f = _d(f)
+    p = _d(p)
+    if f.ndim == 2:
+        f = f[..., None]
+    if p.ndim == 2:
+        p = p[..., None]
+    assert f.shape[:2] == p.shape[:2]
+    return f, p
+
+
+def _pix(pix):
+    if pix is None:
+        return None, 0
+    a = np.ascontiguousarray(np.asarray(pix, dtype=np.int64).reshape(-1))
+    return a, a.size
+
+
+def bruteforce(f, p, kind: str, sigma_s: float, sigma_r: float, r: int = -1, pix=None):
+    """(num)/(den) of P:43-51.  Returns (g, eta): full images, or per selected pixel if pix given."""
+    f, p = _fp(f, p)
+    H, W, n = f.shape
+    rho = p.shape[2]
+    a, npx = _pix(pix)
+    cnt = npx if a is not None else H * W
+    g = np.zeros((cnt, n))
+    eta = np.zeros(cnt)
+    lp = a.ctypes.data_as(C.POINTER(C.c_long)) if a is not None else None
+    _check(_L().orc_bruteforce_pixels(_pd(f), n, _pd(p), rho, H, W, KIND[kind], float(sigma_s), int(r),
+                                      float(sigma_r), lp, npx, _pd(g), _pd(eta)), "bruteforce")
+    if a is None:
+        return g.reshape(H, W, n), eta.reshape(H, W)
+    return g, eta
+
+
+def filter(f, p, kind: str, sigma_s: float, sigma_r: float, mu, r: int = -1, tau: float = 0.5):
+    """Algorithm 1 with rule R9.  Returns (g [H,W,n], eta_hat [H,W], flagged [H,W] bool, n_flagged)."""
+    f, p = _fp(f, p)
+    H, W, n = f.shape
+    rho = p.shape[2]
+    mu = _d(mu)
+    K = mu.shape[0]
+    g = np.zeros((H, W, n))
+    eta = np.zeros((H, W))
+    fl = np.zeros((H, W), dtype=np.uint8)
+    nf = C.c_long(0)
+    st = _L().orc_filter(_pd(f), n, _pd(p), rho, H, W, KIND[kind], float(sigma_s), int(r), float(sigma_r),
+                         K, _pd(mu), float(tau), _pd(g), _pd(eta), fl.ctypes.data_as(C.POINTER(C.c_uint8)),
+                         C.byref(nf))
+    _check(st, "filter")
+    return g, eta, fl.astype(bool), nf.value
+
+
+def filter_pixels(f, p, kind: str, sigma_s: float, sigma_r: float, mu, pix, r: int = -1, tau: float = 0.5):
+    """The same filter at selected pixels.  Returns (g [npix,n], eta_hat [npix], flagged [npix])."""
+    f, p = _fp(f, p)
+    H, W, n = f.shape
+    rho = p.shape[2]
+    mu = _d(mu)
+    K = mu.shape[0]
+    a, npx = _pix(pix)
+    g = np.zeros((npx, n))
+    eta = np.zeros(npx)
+    fl = np.zeros(npx, dtype=np.uint8)
+    st = _L().orc_filter_pixels(_pd(f), n, _pd(p), rho, H, W, KIND[kind], float(sigma_s), int(r),
+                                float(sigma_r), K, _pd(mu), float(tau), a.ctypes.data_as(C.POINTER(C.c_long)),
+                                npx, _pd(g), _pd(eta), fl.ctypes.data_as(C.POINTER(C.c_uint8)))
+    _check(st, "filter_pixels")
+    return g, eta, fl.astype(bool)
+
+
+def nystrom(f, p, kind: str, sigma_s: float, sigma_r: float, mu, r: int = -1, pix=None):
+    """Appendix A identity as a direct window sum (pin P7).  Returns (g, eta)."""
+    f, p = _fp(f, p)
+    H, W, n = f.shape
+    rho = p.shape[2]
+    mu = _d(mu)
+    K = mu.shape[0]
+    a, npx = _pix(pix)
+    cnt = npx if a is not None else H * W
+    g = np.zeros((cnt, n))
+    eta = np.zeros(cnt)
+    lp = a.ctypes.data_as(C.POINTER(C.c_long)) if a is not None else None
+    _check(_L().orc_nystrom_pixels(_pd(f), n, _pd(p), rho, H, W, KIND[kind], float(sigma_s), int(r),
+                                   float(sigma_r), K, _pd(mu), lp, npx, _pd(g), _pd(eta)), "nystrom")
+    if a is None:
+        return g.reshape(H, W, n), eta.reshape(H, W)
+    return g, eta
+
+
+def filter_hard(f, p, kind: str, sigma_s: float, sigma_r: float, mu, labels, r: int = -1):
+    """Hard-assignment variant g(i) = v_s(i)/r_s(i), s = label of i."""
+    f, p = _fp(f, p)
+    H, W, n = f.shape
+    rho = p.shape[2]
+    mu = _d(mu)
+    K = mu.shape[0]
+    lab = np.ascontiguousarray(np.asarray(labels, dtype=np.int32).reshape(-1))
+    g = np.zeros((H, W, n))
+    _check(_L().orc_filter_hard(_pd(f), n, _pd(p), rho, H, W, KIND[kind], float(sigma_s), int(r),
+                                float(sigma_r), K, _pd(mu), lab.ctypes.data_as(C.POINTER(C.c_int32)), _pd(g)),
+           "filter_hard")
+    return g
+
+
+def mse(a, b, R: float = 1.0) -> float:
+    """(rmse): |Omega|^-1 sum_i ||a(i) - b(i)||^2 on intensities divided by R."""
+    a = _d(a)
+    b = _d(b)
+    if a.ndim == 2:
+        a = a[..., None]
+        b = b[..., None]
+    d = (a - b) / R
+    return float(np.mean(np.sum(d * d, axis=-1)))
+
+
+def psnr(a, b, R: float = 1.0) -> float:
+    m = mse(a, b, R)
+    return float("inf") if m == 0.0 else float(-10.0 * np.log10(m))
