@@ -1,0 +1,182 @@
+/*
+ * hdf.h -- C ABI of the B200 (sm_100a) implementation of the fast high-dimensional bilateral /
+ * nonlocal-means filter of Nair & Chaudhury (arXiv 1811.02363).
+ *
+ * Citations "P:n" are lines of the paper's text; "Rn" are the readings of the paper
+ * listed in DESIGN.md section 3.  Every entry point below is plain C: device or host pointers,
+ * sizes and a CUDA stream passed as void* (a cudaStream_t; NULL = legacy default stream).
+ *
+ * Conventions (all entry points):
+ *  - Layout.  Images are row-major, channel-fastest ("HWC"): f [H][W][n], p [H][W][rho],
+ *    g [H][W][n], float32.  Centres are [K][rho] float32.  Pixel (y, x) is index y*W + x.
+ *  - Ownership.  The caller owns every buffer (inputs, outputs, workspace).  The library never
+ *    allocates or frees device memory, and keeps no pointer after the enqueued work completes.
+ *    Device buffers must stay alive until the stream has reached the end of the enqueued work.
+ *  - Alignment.  Device pointers must be 16-byte aligned (torch allocations are 512-byte aligned).
+ *  - Aliasing.  f may alias p (the bilateral filter, f = p).  g must not alias f, p or ws.
+ *  - Asynchrony.  Calls enqueue work on `stream` and return without waiting, except where an
+ *    optional *_host output pointer is non-NULL (documented per call): then the call
+ *    synchronises `stream` before returning.  Argument errors are detected before anything is
+ *    enqueued; nothing is launched on error.
+ *  - Errors.  Every call returns an hdf_status.  hdf_last_error() gives a message for the last
+ *    failing call on the calling thread.  Launch failures map to HDF_ERR_CUDA; asynchronous device
+ *    faults surface at the caller's next synchronisation.
+ *  - Finite inputs are a precondition and are not checked.
+ *  - There is no CPU fallback: every arithmetic step runs in this library's CUDA kernels.
+ */
+#ifndef HDF_H_
+#define HDF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HDF_OK = 0,
+    HDF_ERR_ARG = 1,        /* invalid argument (shape, range, NULL, alignment, aliasing) */
+    HDF_ERR_K = 2,          /* K exceeds the number of distinct guide vectors (R5)          */
+    HDF_ERR_WORKSPACE = 3,  /* ws_bytes smaller than the *_workspace_bytes() requirement    */
+    HDF_ERR_CUDA = 4,       /* a CUDA runtime call or launch failed                          */
+    HDF_WARN_ILLCOND = 5    /* A (defAb) is numerically singular: A^+ truncated (R6)         */
+} hdf_status;
+
+typedef enum {
+    HDF_SPATIAL_GAUSSIAN = 0, /* omega(i) = exp(-||i||^2 / 2 sigma_s^2) on [-S,S]^2 */
+    HDF_SPATIAL_BOX = 1       /* omega = 1 on [-S,S]^2 (nonlocal means)                 */
+} hdf_spatial_kind;
+
+/* Limits of this build. */
+#define HDF_MAX_K 128
+#define HDF_MAX_RHO 64
+#define HDF_MAX_N 64
+#define HDF_MAX_RADIUS 32
+
+/* Library version string, e.g. "hdf 0.1.0 sm_100a". */
+const char *hdf_version(void);
+
+/* Message of the last failing hdf_* call on this thread ("" if none).  Valid until the next
+ * hdf_* call on the same thread. */
+const char *hdf_last_error(void);
+
+/* ---------------------------------------------------------------------------------------------
+ * Step 1 -- cluster the range space Theta = {p(i)} (Algorithm 1 line "cluster" P:294)
+ * with bisecting K-means: repeatedly split the leaf of largest SSE (R2) by 2-means seeded with the
+ * farthest pair of a stride sample of <= 1024 members (R3), Lloyd iterations until no assignment
+ * changes or 50 iterations (R4).  mu_k = centroid of C_k.  Runs as one persistent
+ * cooperative kernel; independent leaf splits run concurrently (results identical to the
+ * sequential procedure).
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+    int32_t status;        /* HDF_OK or HDF_ERR_K                                              */
+    int32_t achievable_k;  /* leaves reached; the number of distinct guide vectors on HDF_ERR_K  */
+    int32_t rounds;        /* concurrent split rounds executed                                 */
+    int32_t lloyd_iters;   /* lock-step Lloyd iterations executed (all rounds)                 */
+    double e_k;            /* clustering error E_K = sum_k sum_{p(i) in C_k} ||p(i)-mu_k||^2     */
+} hdf_cluster_info;
+
+/* Device workspace (bytes) for hdf_cluster on an H x W guide of dimension rho. */
+size_t hdf_cluster_workspace_bytes(int H, int W, int rho, int K);
+
+/*
+ * hdf_cluster
+ *   p        [H][W][rho] float32, device (read only)
+ *   K        1 <= K <= HDF_MAX_K number of clusters
+ *   centres  [K][rho] float32, device, out: mu_k (rounded from fp64 means)
+ *   labels   [H][W] int32, device, out: k such that p(i) in C_k; may be NULL
+ *   info_host  hdf_cluster_info*, host, out; may be NULL.  Non-NULL synchronises `stream` and
+ *              returns HDF_ERR_K if K exceeds the number of distinct guide vectors (R5).  With
+ *              NULL the call is fully asynchronous and, in that (documented) error case, centres
+ *              k >= achievable_k are copies of centre 0 (A then has duplicate centres and the
+ *              pseudo-inverse handles the rank deficiency, R6).
+ *   ws, ws_bytes  device workspace of at least hdf_cluster_workspace_bytes(H, W, rho, K)
+ *   stream   cudaStream_t as void*
+ */
+int hdf_cluster(const float *p, int H, int W, int rho, int K, float *centres, int32_t *labels,
+                hdf_cluster_info *info_host, void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Steps 2-6 -- Algorithm 1:
+ *   A_kl = phi(mu_k - mu_l), A^+ (P:235-240);
+ *   b_k(j) = phi(p(j) - mu_k), u_k = b_k f;
+ *   v_k = omega * u_k, r_k = omega * b_k: K(n+1) separable convolutions, window clipped to Omega
+ *   (zero extension, R8);
+ *   c(i) = A^+ b(i); g(i) = sum_k c_k v_k / sum_k c_k r_k.
+ * Degenerate normaliser (R9): if eta_hat(i) = sum_k c_k r_k < tau * omega(0) phi(0), g(i) is
+ * replaced by the direct (num)/(den) value of P:43-51 at i, computed on the GPU.
+ * ------------------------------------------------------------------------------------------- */
+
+/* Device workspace (bytes) for hdf_filter.  radius < 0 means ceil(3 sigma_s) (Gaussian). */
+size_t hdf_filter_workspace_bytes(int H, int W, int n, int rho, int K, int kind, float sigma_s, int radius);
+
+/*
+ * hdf_filter
+ *   f        [H][W][n] float32, device (read only), 1 <= n <= HDF_MAX_N
+ *   p        [H][W][rho] float32, device (read only), 1 <= rho <= HDF_MAX_RHO; may alias f
+ *   kind     hdf_spatial_kind
+ *   sigma_s  Gaussian spatial sigma (> 0; ignored for the box)
+ *   radius   window half-width S; < 0 -> ceil(3 sigma_s) for the Gaussian; required for the
+ *            box; 0 <= S <= HDF_MAX_RADIUS
+ *   sigma_r  range sigma (> 0), phi(x) = exp(-||x||^2 / 2 sigma_r^2)
+ *   K        number of centres, 1 <= K <= HDF_MAX_K
+ *   centres  [K][rho] float32, device; NULL -> hdf_cluster is run first inside this call (then
+ *            ws must also hold the clustering workspace, which hdf_filter_workspace_bytes includes)
+ *   tau      degenerate-normaliser threshold (R9); 0 disables the rule; callers pass 0.5
+ *   g        [H][W][n] float32, device, out
+ *   n_flagged_host  int32*, host, out: number of pixels that took the R9 fallback; may be NULL.
+ *            Non-NULL synchronises `stream`; the call then also returns HDF_WARN_ILLCOND when A was
+ *            numerically singular (its pseudo-inverse truncated eigenvalues below tol, R6).
+ *   ws, ws_bytes  device workspace of at least hdf_filter_workspace_bytes(...)
+ *   stream   cudaStream_t as void*
+ */
+int hdf_filter(const float *f, int n, const float *p, int rho, int H, int W, int kind, float sigma_s,
+               int radius, float sigma_r, int K, const float *centres, float tau, float *g,
+               int32_t *n_flagged_host, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * hdf_filter_host -- the whole hot path end to end from HOST buffers: copies f and p to the device
+ * workspace, clusters, filters, and copies g back, all on `stream`, then synchronises it.
+ *   f_host [H][W][n], p_host [H][W][rho] (may be the same pointer), g_host [H][W][n]: host float32
+ *   (pinned memory gives full-rate copies; pageable memory works but is slower).
+ *   centres_host [K][rho] out, may be NULL.  info_host may be NULL.
+ *   ws: device workspace of at least hdf_filter_host_workspace_bytes(...).
+ */
+size_t hdf_filter_host_workspace_bytes(int H, int W, int n, int rho, int K, int kind, float sigma_s, int radius);
+int hdf_filter_host(const float *f_host, int n, const float *p_host, int rho, int H, int W, int kind,
+                    float sigma_s, int radius, float sigma_r, int K, float tau, float *g_host,
+                    float *centres_host, int32_t *n_flagged_host, hdf_cluster_info *info_host,
+                    void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Per-stage device timing (benchmarking / tracing).  When enabled, every
+ * stage of hdf_cluster / hdf_filter / hdf_filter_host records a pair of CUDA events on the call's
+ * stream around its kernel launch (or copy).
+ * ------------------------------------------------------------------------------------------- */
+typedef enum {
+    HDF_STAGE_CLUSTER = 0,   /* k_bisect_kmeans                        step 1               */
+    HDF_STAGE_PINV = 1,      /* k_gram_pinv                            step 2               */
+    HDF_STAGE_COEFFS = 2,    /* k_coeffs: c = A^+ b planes             step 5 (for2)        */
+    HDF_STAGE_VPASS = 3,     /* k_range_vpass: b, u + column pass      steps 3, 4           */
+    HDF_STAGE_HPASS = 4,     /* k_hpass_combine: row pass + combine    steps 4, 6           */
+    HDF_STAGE_FALLBACK = 5,  /* k_fallback: direct (num)/(den), R9     step 6               */
+    HDF_STAGE_H2D = 6,       /* hdf_filter_host input copies                                */
+    HDF_STAGE_D2H = 7,       /* hdf_filter_host output copies                               */
+    HDF_NUM_STAGES = 8
+} hdf_stage;
+
+/* Turn event recording on (on != 0) or off.  Process-wide; returns HDF_OK. */
+int hdf_profile_enable(int on);
+
+/* Wait for every event pair recorded since the last collect, then write per-stage sums:
+ *   ms_total [HDF_NUM_STAGES] host, out: summed device milliseconds per stage (may be NULL)
+ *   launches [HDF_NUM_STAGES] host, out: number of recorded launches per stage (may be NULL)
+ * Clears the recorded set.  Returns HDF_OK or HDF_ERR_CUDA. */
+int hdf_profile_collect(double *ms_total, int32_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HDF_H_ */

@@ -111,7 +111,7 @@ def spatial_taps(kind: str, sigma_s: float, r: int = -1) -> np.ndarray:
     return w
 
 
-def cluster(p, K: int, cap: int = 4096, max_iter: int = 50):
+def cluster(p, K: int, cap: int = 1024, max_iter: int = 50):
     """Bisecting K-means of the guide p [..., rho].  Returns (centres [K,rho] fp64, labels [N]
     int32, leaf_sse [K], E_K)."""
     p = _d(p)

@@ -101,7 +101,7 @@ static void leaf_stats(const double *p, int rho, Leaf *L) {
     L->sse = s;
 }
 
-/* Farthest pair within the stride sample members[0::stride], stride = ceil(m / cap) (R3).
+/* Farthest pair within the stride sample members[0::stride], stride = ceil(m / cap), cap = 1024 (R3).
  * Ties keep the lexicographically smallest (a, b) in sample order. */
 static void farthest_pair(const double *p, int rho, const Leaf *L, int cap, long *pa, long *pb) {
     long m = L->m;
@@ -205,7 +205,7 @@ static void two_means(const double *p, int rho, const Leaf *L, int cap, int max_
  * orc_cluster: bisecting K-means (Algorithm 1 line "cluster").
  *   p        [N, rho] guide vectors (row-major pixel order)
  *   K        number of leaves
- *   cap      farthest-pair sample cap (4096, R3); max_iter Lloyd cap (50, R4)
+ *   cap      farthest-pair sample cap (1024, R3); max_iter Lloyd cap (50, R4)
  *   centres  out [K, rho] leaf means (mu_k = centroid of C_k)
  *   labels   out [N] leaf id of every pixel (may be NULL)
  *   leaf_sse out [K] (may be NULL); E_K out (may be NULL)

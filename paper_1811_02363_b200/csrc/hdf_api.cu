@@ -1,0 +1,693 @@
+// hdf_api.cu -- the C ABI (include/hdf.h): argument checking, workspace carving, launches.
+// Every arithmetic step of the hot path runs in this library's kernels; there is no CPU fallback.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "hdf_dispatch.h"
+#include "k_cluster.cuh"
+#include "k_coeffs.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define HDF_CUDA(call)                                                                             \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) return fail(HDF_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+// Bump allocator over the caller's workspace (256-byte aligned slices).  With base == nullptr it
+// only measures.
+struct Carver {
+    char* base;
+    size_t off = 0;
+    explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+    template <class T>
+    T* take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += sizeof(T) * count;
+        return p;
+    }
+};
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+// ------------------------------------------------------------------ per-stage event profiling ----
+// When enabled (hdf_profile_enable), every stage records a start/end CUDA event pair on the call's
+// stream; hdf_profile_collect() waits for them and returns the summed device time per stage.
+struct ProfRec {
+    int stage;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof_pending;
+std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event() {
+    if (!g_prof_pool.empty()) {
+        cudaEvent_t e = g_prof_pool.back();
+        g_prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    ProfRec r;
+    cudaStream_t st;
+    bool on;
+    ProfScope(int stage, cudaStream_t s) : st(s) {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        on = g_prof_on;
+        if (on) {
+            r.stage = stage;
+            r.a = prof_event();
+            r.b = prof_event();
+            cudaEventRecord(r.a, st);
+        }
+    }
+    ~ProfScope() {
+        if (!on) return;
+        cudaEventRecord(r.b, st);
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        g_prof_pending.push_back(r);
+    }
+};
+
+// ------------------------------------------------------------------------ cluster workspace ----
+struct ClusterPlan {
+    int CH, maxch, slotmax, pstride;
+};
+ClusterPlan cluster_plan(long long N, int rho, int K) {
+    ClusterPlan c;
+    c.CH = (int)std::max<long long>(1024, (N + 1023) / 1024);
+    c.maxch = (int)((N + c.CH - 1) / c.CH) + K + 1;
+    c.maxch = std::max(c.maxch, 2048);   // also holds the per-block root partials
+    c.slotmax = K;
+    c.pstride = 2 * rho + 4;
+    return c;
+}
+
+hdf::ClusterArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho, int K) {
+    const long long N = (long long)H * W;
+    const ClusterPlan pl = cluster_plan(N, rho, K);
+    hdf::ClusterArgs A;
+    memset(&A, 0, sizeof(A));
+    A.p = p;
+    A.N = (int)N;
+    A.rho = rho;
+    A.K = K;
+    A.CH = pl.CH;
+    A.maxch = pl.maxch;
+    A.slotmax = pl.slotmax;
+    A.pstride = pl.pstride;
+    for (int b = 0; b < 2; b++) A.pts[b] = cv.take<float>((size_t)N * rho);
+    for (int b = 0; b < 2; b++) A.idx[b] = cv.take<int>((size_t)N);
+    for (int b = 0; b < 2; b++) A.side[b] = cv.take<unsigned char>((size_t)N);
+    A.leaves = cv.take<hdf::CLeaf>(K);
+    A.lmean = cv.take<double>((size_t)K * rho);
+    A.cmean0 = cv.take<double>((size_t)K * rho);
+    A.cmean1 = cv.take<double>((size_t)K * rho);
+    A.slots = cv.take<hdf::CSlot>(pl.slotmax);
+    A.c0g = cv.take<double>((size_t)pl.slotmax * rho);
+    A.c1g = cv.take<double>((size_t)pl.slotmax * rho);
+    A.chunks = cv.take<hdf::CChunk>(pl.maxch);
+    A.part = cv.take<double>((size_t)pl.maxch * pl.pstride);
+    A.fpd = cv.take<double>((size_t)pl.slotmax * hdf::kFpCap);
+    A.fpi = cv.take<int>((size_t)pl.slotmax * hdf::kFpCap);
+    A.ctrl = cv.take<int>(hdf::C_NUM);
+    A.ek = cv.take<double>(1);
+    return A;
+}
+
+size_t cluster_smem(int rho, int K) {
+    const ClusterPlan pl = cluster_plan(1, rho, K);
+    const int nvL = 2 * rho + 4;
+    return sizeof(double) * (size_t)(hdf::kClWarps * nvL + 2 * pl.slotmax * rho + nvL);
+}
+
+int check_common(int H, int W, int rho, int K) {
+    if (H < 1 || W < 1) return fail(HDF_ERR_ARG, "H, W must be >= 1 (got %d, %d)", H, W);
+    if ((long long)H * W > (1LL << 30)) return fail(HDF_ERR_ARG, "H*W too large");
+    if (rho < 1 || rho > HDF_MAX_RHO) return fail(HDF_ERR_ARG, "rho must be in [1, %d] (got %d)", HDF_MAX_RHO, rho);
+    if (K < 1 || K > HDF_MAX_K) return fail(HDF_ERR_ARG, "K must be in [1, %d] (got %d)", HDF_MAX_K, K);
+    return HDF_OK;
+}
+
+bool misaligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) != 0; }
+
+int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres, int32_t* labels,
+                   hdf_cluster_info* info, void* ws, cudaStream_t st) {
+    Carver cv(ws);
+    hdf::ClusterArgs A = carve_cluster(cv, p, H, W, rho, K);
+    A.centres = centres;
+    A.labels = labels;
+    static std::mutex mu;
+    static int occ_cache[HDF_MAX_K + 1][HDF_MAX_RHO + 1];
+    const size_t smem = cluster_smem(rho, K);
+    int dev = 0, nsm = 0, occ = 0;
+    HDF_CUDA(cudaGetDevice(&dev));
+    HDF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        occ = occ_cache[K][rho];
+        if (occ == 0) {
+            HDF_CUDA(cudaFuncSetAttribute(hdf::k_bisect_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            HDF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hdf::k_bisect_kmeans, hdf::kClThreads, smem));
+            occ = std::max(1, std::min(occ, 2));
+            occ_cache[K][rho] = occ;
+        }
+    }
+    HDF_CUDA(cudaFuncSetAttribute(hdf::k_bisect_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = std::min(nsm * occ, A.maxch);
+    void* args[] = {&A};
+    {
+        ProfScope prof(HDF_STAGE_CLUSTER, st);
+        HDF_CUDA(cudaLaunchCooperativeKernel((void*)hdf::k_bisect_kmeans, dim3(grid), dim3(hdf::kClThreads), args,
+                                             smem, st));
+    }
+    if (info) {
+        int ctrl[hdf::C_NUM];
+        double ek = 0.0;
+        HDF_CUDA(cudaMemcpyAsync(ctrl, A.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, st));
+        HDF_CUDA(cudaMemcpyAsync(&ek, A.ek, sizeof(double), cudaMemcpyDeviceToHost, st));
+        HDF_CUDA(cudaStreamSynchronize(st));
+        info->status = ctrl[hdf::C_STATUS];
+        info->achievable_k = ctrl[hdf::C_NLEAVES];
+        info->rounds = ctrl[hdf::C_ROUNDS];
+        info->lloyd_iters = ctrl[hdf::C_ITERS];
+        info->e_k = ek;
+        if (info->status == HDF_ERR_K)
+            return fail(HDF_ERR_K, "K=%d exceeds the number of distinct guide vectors (%d)", K, info->achievable_k);
+    }
+    return HDF_OK;
+}
+
+// ------------------------------------------------------------------------- filter planning -----
+int padded_radius(int R, bool box) {
+    for (int i = 0; i < hdf::kNumRadii; i++) {
+        if (box && hdf::kRadii[i] == R) return R;
+        if (!box && hdf::kRadii[i] >= R) return hdf::kRadii[i];
+    }
+    return -1;
+}
+
+struct FilterPlan {
+    int R, Rp, Wp, NP, P;
+    bool box;
+    // F1
+    hdf::VLaunch vl;
+    int Pg, TY;
+    // F2
+    hdf::HLaunch hl;
+    int RR, NJW, NWC, NS, Lbox, stage_bytes, planes_bytes;
+};
+
+int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, FilterPlan* fp, int nsm) {
+    FilterPlan& F = *fp;
+    F.box = (kind == HDF_SPATIAL_BOX);
+    if (kind != HDF_SPATIAL_GAUSSIAN && kind != HDF_SPATIAL_BOX) return fail(HDF_ERR_ARG, "unknown spatial kind %d", kind);
+    if (radius < 0) {
+        if (F.box) return fail(HDF_ERR_ARG, "the box kernel needs an explicit radius");
+        if (!(sigma_s > 0.f)) return fail(HDF_ERR_ARG, "sigma_s must be > 0");
+        radius = (int)std::ceil(3.0 * (double)sigma_s);
+    }
+    if (!F.box && !(sigma_s > 0.f)) return fail(HDF_ERR_ARG, "sigma_s must be > 0");
+    if (radius > HDF_MAX_RADIUS) return fail(HDF_ERR_ARG, "radius %d exceeds HDF_MAX_RADIUS=%d", radius, HDF_MAX_RADIUS);
+    F.R = radius;
+    // Running-sum box kernels need a compiled radius equal to S; any other box radius (and S = 0)
+    // runs through the FIR kernels with unit taps on [-S, S] and zero taps beyond (exact).
+    if (F.box && (radius == 0 || padded_radius(radius, true) < 0)) F.box = false;
+    F.Rp = padded_radius(radius == 0 ? 1 : radius, F.box);
+    if (F.Rp < 0) return fail(HDF_ERR_ARG, "radius %d is not supported by this build", radius);
+    F.Wp = round_up(W, 4);
+    F.NP = n + 1;
+    F.P = K * F.NP;
+    // F1: planes per CTA and rows per CTA
+    const int J = hdf::vpass_j(F.Rp);
+    const int NT = hdf::vpass_nt(F.Rp);
+    F.Pg = std::min(NT / 32, F.P);
+    const int gx = (W + hdf::kVTX - 1) / hdf::kVTX, gz = (F.P + F.Pg - 1) / F.Pg;
+    int TY = round_up(std::max(4 * F.Rp, 64), J);
+    while (TY > 2 * J && (long long)gx * gz * ((H + TY - 1) / TY) < 3LL * nsm) TY = round_up(TY / 2, J);
+    F.TY = std::max(TY, J);
+    const int nk_max = (F.Pg + F.NP - 1) / F.NP + 1;
+    F.vl.grid = dim3(gx, (H + F.TY - 1) / F.TY, gz);
+    F.vl.threads = 32 * F.Pg;
+    F.vl.smem = sizeof(float) * (size_t)(round_up(nk_max * 64, 4) + 2 * F.Pg * J * hdf::kVTX);
+    // F2
+    const int NP = F.NP;
+    int maxjp = 1;
+    if (NP <= 7) { F.RR = 8; F.NJW = NP; }
+    else if (NP <= 15) { F.RR = 4; F.NJW = NP; }
+    else if (NP <= 31) { F.RR = 2; F.NJW = NP; }
+    else if (NP <= 62) { F.RR = 2; F.NJW = (NP + 1) / 2; maxjp = 2; }
+    else { F.RR = 2; F.NJW = (NP + 3) / 4; maxjp = 4; }
+    F.NWC = (F.RR / 2) * F.NJW;
+    const int R4 = (F.Rp + 3) & ~3;
+    F.Lbox = hdf::kHTW + 2 * R4 + 4;
+    F.planes_bytes = round_up(F.Lbox * F.RR * NP * 4, 128);
+    F.stage_bytes = F.planes_bytes + round_up(hdf::kCoefBox * F.RR * 4, 128);
+    const int fixed = 128 + round_up(F.RR * hdf::kHTW * 4, 128) + 128;
+    const int budget = 200 * 1024;
+    F.NS = std::min(4, (budget - fixed) / F.stage_bytes);
+    if (F.NS < 2) return fail(HDF_ERR_ARG, "tile does not fit shared memory (n=%d, R=%d)", n, radius);
+    F.hl.grid = dim3((W + hdf::kHTW - 1) / hdf::kHTW, (H + F.RR - 1) / F.RR);
+    F.hl.threads = 32 * (F.NWC + 1);
+    F.hl.smem = fixed + (size_t)F.NS * F.stage_bytes;
+    F.hl.maxjp = maxjp;
+    return HDF_OK;
+}
+
+struct FilterWS {
+    float* planes;
+    float* cpl;
+    float* Ap32;
+    double* Ap64;
+    double* Vscratch;
+    int* status;
+    int* flag_count;
+    int* flag_list;
+    float* centres;   // internal centres (when the caller passes NULL)
+    void* cluster_ws;
+};
+
+FilterWS carve_filter(Carver& cv, int H, int W, int n, int rho, int K, int Wp, bool with_cluster) {
+    FilterWS w;
+    const int NP = n + 1;
+    w.planes = cv.take<float>((size_t)K * NP * H * Wp);
+    w.cpl = cv.take<float>((size_t)K * H * Wp);
+    w.Ap32 = cv.take<float>((size_t)K * K);
+    w.Ap64 = cv.take<double>((size_t)K * K);
+    w.Vscratch = cv.take<double>((size_t)K * K);
+    w.status = cv.take<int>(4);
+    w.flag_count = w.status + 1;
+    w.flag_list = cv.take<int>((size_t)H * W);
+    w.centres = cv.take<float>((size_t)K * rho);
+    w.cluster_ws = nullptr;
+    if (with_cluster) {
+        cv.off = (cv.off + 255) & ~size_t(255);
+        w.cluster_ws = cv.base ? cv.base + cv.off : nullptr;
+        Carver c2(w.cluster_ws);
+        carve_cluster(c2, nullptr, H, W, rho, K);
+        cv.off += c2.off;
+    }
+    return w;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+int encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t pitch_bytes,
+             uint64_t plane_bytes, uint32_t b0, uint32_t b1, uint32_t b2) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(HDF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {pitch_bytes, plane_bytes};
+    cuuint32_t box[3] = {b0, b1, b2};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(HDF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return HDF_OK;
+}
+
+int nsm_of_device() {
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return nsm;
+}
+
+void fill_taps(float* taps, int kind, float sigma_s, int R, int Rp) {
+    for (int i = 0; i < hdf::kMaxTaps; i++) taps[i] = 0.f;
+    for (int t = -Rp; t <= Rp; t++) {
+        float w = 0.f;
+        if (t >= -R && t <= R) {
+            if (kind == HDF_SPATIAL_BOX) w = 1.f;
+            else w = (float)std::exp(-(double)(t * t) / (2.0 * (double)sigma_s * (double)sigma_s));
+        }
+        taps[t + Rp] = w;
+    }
+}
+
+int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int kind, float sigma_s, int radius,
+               float sigma_r, int K, const float* centres, float tau, float* g, int32_t* n_flagged_host, void* ws,
+               size_t ws_bytes, cudaStream_t st) {
+    int rc = check_common(H, W, rho, K);
+    if (rc) return rc;
+    if (!f || !p || !g || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
+    if (n < 1 || n > HDF_MAX_N) return fail(HDF_ERR_ARG, "n must be in [1, %d] (got %d)", HDF_MAX_N, n);
+    if (!(sigma_r > 0.f)) return fail(HDF_ERR_ARG, "sigma_r must be > 0");
+    if (!(tau >= 0.f)) return fail(HDF_ERR_ARG, "tau must be >= 0");
+    if (misaligned(f) || misaligned(p) || misaligned(g) || misaligned(ws) || (centres && misaligned(centres)))
+        return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
+    if (g == f || g == p) return fail(HDF_ERR_ARG, "g must not alias f or p");
+    FilterPlan F;
+    const int nsm = nsm_of_device();
+    rc = make_plan(H, W, n, K, kind, sigma_s, radius, &F, nsm);
+    if (rc) return rc;
+    const size_t need = hdf_filter_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
+    if (ws_bytes < need) return fail(HDF_ERR_WORKSPACE, "workspace %zu < required %zu bytes", ws_bytes, need);
+    Carver cv(ws);
+    FilterWS w = carve_filter(cv, H, W, n, rho, K, F.Wp, true);
+    const float neg_inv2sr2 = (float)(-1.0 / (2.0 * (double)sigma_r * (double)sigma_r));
+
+    // step 1 (optional): cluster the guide inside this call
+    if (!centres) {
+        rc = launch_cluster(p, H, W, rho, K, w.centres, nullptr, nullptr, w.cluster_ws, st);
+        if (rc) return rc;
+        centres = w.centres;
+    }
+    // step 2: A and A^+ (one CTA, fp64)
+    {
+        hdf::PinvOut po{w.Ap32, w.Ap64, w.status, w.Vscratch};
+        const size_t smem = hdf::pinv_smem_bytes(K);
+        HDF_CUDA(cudaFuncSetAttribute(hdf::k_gram_pinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ProfScope prof(HDF_STAGE_PINV, st);
+        hdf::k_gram_pinv<<<1, hdf::kPinvThreads, smem, st>>>(centres, K, rho, -1.0 / (2.0 * (double)sigma_r * sigma_r), po);
+        HDF_CUDA(cudaGetLastError());
+    }
+    // loop for2: c(i) = A^+ b(i) -> K coefficient planes
+    {
+        hdf::CoefParams cp;
+        cp.p = p;
+        cp.centres = centres;
+        cp.Ap32 = w.Ap32;
+        cp.cpl = w.cpl;
+        cp.cstride = (long long)H * F.Wp;
+        cp.H = H;
+        cp.W = W;
+        cp.Wp = F.Wp;
+        cp.rho = rho;
+        cp.K = K;
+        cp.neg_inv2sr2 = neg_inv2sr2;
+        const int K8 = (K + 7) & ~7;
+        const size_t smem = sizeof(float) * ((size_t)K * K8 + (size_t)K * rho + (size_t)K * hdf::kCoefPix);
+        HDF_CUDA(cudaFuncSetAttribute(hdf::k_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const long long npix = (long long)H * W;
+        ProfScope prof(HDF_STAGE_COEFFS, st);
+        hdf::k_coeffs<<<(unsigned)((npix + hdf::kCoefPix - 1) / hdf::kCoefPix), hdf::kCoefPix, smem, st>>>(cp);
+        HDF_CUDA(cudaGetLastError());
+    }
+    HDF_CUDA(cudaMemsetAsync(w.flag_count, 0, sizeof(int), st));
+    float taps[hdf::kMaxTaps];
+    fill_taps(taps, kind, sigma_s, F.R, F.Rp);
+    // F1: range weights + column pass
+    {
+        hdf::VParams vp;
+        vp.f = f;
+        vp.p = p;
+        vp.centres = centres;
+        vp.planes = w.planes;
+        vp.pstride = (long long)H * F.Wp;
+        vp.n = n;
+        vp.rho = rho;
+        vp.H = H;
+        vp.W = W;
+        vp.Wp = F.Wp;
+        vp.K = K;
+        vp.NP = F.NP;
+        vp.P = F.P;
+        vp.Pg = F.Pg;
+        vp.TY = F.TY;
+        vp.neg_inv2sr2 = neg_inv2sr2;
+        memcpy(vp.taps, taps, sizeof(taps));
+        hdf::VLaunch vl = F.vl;
+        vl.smem = sizeof(float) * (size_t)(round_up((((F.Pg + F.NP - 1) / F.NP) + 1) * rho, 4) +
+                                           2 * F.Pg * hdf::vpass_j(F.Rp) * hdf::kVTX);
+        ProfScope prof(HDF_STAGE_VPASS, st);
+        HDF_CUDA(hdf::launch_vpass(F.Rp, F.box, vl, st, vp));
+    }
+    // F2: row pass + combine + normalise (TMA-fed)
+    {
+        CUtensorMap tp, tc;
+        rc = encode3d(&tp, w.planes, (uint64_t)W, (uint64_t)H, (uint64_t)F.P, (uint64_t)F.Wp * 4,
+                      (uint64_t)H * F.Wp * 4, (uint32_t)F.Lbox, (uint32_t)F.RR, (uint32_t)F.NP);
+        if (rc) return rc;
+        rc = encode3d(&tc, w.cpl, (uint64_t)W, (uint64_t)H, (uint64_t)K, (uint64_t)F.Wp * 4, (uint64_t)H * F.Wp * 4,
+                      (uint32_t)hdf::kCoefBox, (uint32_t)F.RR, 1u);
+        if (rc) return rc;
+        hdf::HParams hp;
+        hp.g = g;
+        hp.flag_count = w.flag_count;
+        hp.flag_list = w.flag_list;
+        hp.n = n;
+        hp.NP = F.NP;
+        hp.H = H;
+        hp.W = W;
+        hp.K = K;
+        hp.RR = F.RR;
+        hp.NJW = F.NJW;
+        hp.NWC = F.NWC;
+        hp.NS = F.NS;
+        hp.Lbox = F.Lbox;
+        hp.stage_bytes = F.stage_bytes;
+        hp.planes_bytes = F.planes_bytes;
+        hp.tau_floor = tau * taps[F.Rp] * taps[F.Rp] * 1.0f;   // tau * omega(0) * phi(0)
+        memcpy(hp.taps, taps, sizeof(taps));
+        ProfScope prof(HDF_STAGE_HPASS, st);
+        HDF_CUDA(hdf::launch_hpass(F.Rp, F.box, F.hl, st, tp, tc, hp));
+    }
+    // F3: direct (num)/(den) for the flagged pixels (R9)
+    if (tau > 0.f) {
+        hdf::FBParams fb;
+        fb.f = f;
+        fb.p = p;
+        fb.g = g;
+        fb.flag_count = w.flag_count;
+        fb.flag_list = w.flag_list;
+        fb.n = n;
+        fb.rho = rho;
+        fb.H = H;
+        fb.W = W;
+        fb.R = F.R;
+        fb.neg_inv2sr2 = neg_inv2sr2;
+        float t2[hdf::kMaxTaps];
+        fill_taps(t2, kind, sigma_s, F.R, F.R);
+        memcpy(fb.taps, t2, sizeof(t2));
+        ProfScope prof(HDF_STAGE_FALLBACK, st);
+        hdf::k_fallback<<<2 * nsm, 256, 0, st>>>(fb);
+        HDF_CUDA(cudaGetLastError());
+    }
+    if (n_flagged_host) {
+        int hv[2] = {0, 0};
+        HDF_CUDA(cudaMemcpyAsync(hv, w.status, sizeof(hv), cudaMemcpyDeviceToHost, st));
+        HDF_CUDA(cudaStreamSynchronize(st));
+        *n_flagged_host = hv[1];
+        if (hv[0] == HDF_WARN_ILLCOND) return fail(HDF_WARN_ILLCOND, "A is numerically singular; A^+ truncated (R6)");
+    }
+    return HDF_OK;
+}
+
+}  // namespace
+
+namespace hdf {
+
+template <int R>
+cudaError_t launch_vpass_t(bool box, const VLaunch& L, cudaStream_t st, const VParams& P);
+template <int R>
+cudaError_t launch_hpass_t(bool box, const HLaunch& L, cudaStream_t st, const CUtensorMap& tp, const CUtensorMap& tc,
+                           const HParams& P);
+
+cudaError_t launch_vpass(int R, bool box, const VLaunch& L, cudaStream_t st, const VParams& P) {
+    switch (R) {
+#define HDF_CASE(r) \
+    case r: return launch_vpass_t<r>(box, L, st, P);
+        HDF_CASE(1) HDF_CASE(2) HDF_CASE(3) HDF_CASE(4) HDF_CASE(5) HDF_CASE(6) HDF_CASE(8) HDF_CASE(9)
+        HDF_CASE(10) HDF_CASE(12) HDF_CASE(15) HDF_CASE(16) HDF_CASE(20) HDF_CASE(24) HDF_CASE(32)
+#undef HDF_CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+cudaError_t launch_hpass(int R, bool box, const HLaunch& L, cudaStream_t st, const CUtensorMap& tp,
+                         const CUtensorMap& tc, const HParams& P) {
+    switch (R) {
+#define HDF_CASE(r) \
+    case r: return launch_hpass_t<r>(box, L, st, tp, tc, P);
+        HDF_CASE(1) HDF_CASE(2) HDF_CASE(3) HDF_CASE(4) HDF_CASE(5) HDF_CASE(6) HDF_CASE(8) HDF_CASE(9)
+        HDF_CASE(10) HDF_CASE(12) HDF_CASE(15) HDF_CASE(16) HDF_CASE(20) HDF_CASE(24) HDF_CASE(32)
+#undef HDF_CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace hdf
+
+// =============================================================================== C ABI ========
+extern "C" {
+
+const char* hdf_version(void) { return "hdf 0.1.0 sm_100a"; }
+
+const char* hdf_last_error(void) { return g_err.c_str(); }
+
+int hdf_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = (on != 0);
+    return HDF_OK;
+}
+
+int hdf_profile_collect(double* ms_total, int32_t* launches) {
+    g_err.clear();
+    std::vector<ProfRec> recs;
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        recs.swap(g_prof_pending);
+    }
+    for (int s = 0; s < HDF_NUM_STAGES; s++) {
+        if (ms_total) ms_total[s] = 0.0;
+        if (launches) launches[s] = 0;
+    }
+    int rc = HDF_OK;
+    for (const ProfRec& r : recs) {
+        float ms = 0.f;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+        if (e != cudaSuccess && rc == HDF_OK) rc = fail(HDF_ERR_CUDA, "profile event: %s", cudaGetErrorString(e));
+        if (r.stage >= 0 && r.stage < HDF_NUM_STAGES) {
+            if (ms_total) ms_total[r.stage] += ms;
+            if (launches) launches[r.stage] += 1;
+        }
+    }
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (const ProfRec& r : recs) {
+        g_prof_pool.push_back(r.a);
+        g_prof_pool.push_back(r.b);
+    }
+    return rc;
+}
+
+size_t hdf_cluster_workspace_bytes(int H, int W, int rho, int K) {
+    if (H < 1 || W < 1 || rho < 1 || K < 1) return 0;
+    Carver cv(nullptr);
+    carve_cluster(cv, nullptr, H, W, rho, K);
+    return cv.off + 256;
+}
+
+int hdf_cluster(const float* p, int H, int W, int rho, int K, float* centres, int32_t* labels,
+                hdf_cluster_info* info_host, void* ws, size_t ws_bytes, void* stream) {
+    g_err.clear();
+    int rc = check_common(H, W, rho, K);
+    if (rc) return rc;
+    if (!p || !centres || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
+    if (misaligned(p) || misaligned(centres) || misaligned(ws) || (labels && misaligned(labels)))
+        return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
+    const size_t need = hdf_cluster_workspace_bytes(H, W, rho, K);
+    if (ws_bytes < need) return fail(HDF_ERR_WORKSPACE, "workspace %zu < required %zu bytes", ws_bytes, need);
+    return launch_cluster(p, H, W, rho, K, centres, labels, info_host, ws, static_cast<cudaStream_t>(stream));
+}
+
+size_t hdf_filter_workspace_bytes(int H, int W, int n, int rho, int K, int kind, float sigma_s, int radius) {
+    (void)kind;
+    (void)sigma_s;
+    (void)radius;
+    if (H < 1 || W < 1 || n < 1 || rho < 1 || K < 1) return 0;
+    Carver cv(nullptr);
+    carve_filter(cv, H, W, n, rho, K, round_up(W, 4), true);
+    return cv.off + 256;
+}
+
+int hdf_filter(const float* f, int n, const float* p, int rho, int H, int W, int kind, float sigma_s, int radius,
+               float sigma_r, int K, const float* centres, float tau, float* g, int32_t* n_flagged_host, void* ws,
+               size_t ws_bytes, void* stream) {
+    g_err.clear();
+    return run_filter(f, n, p, rho, H, W, kind, sigma_s, radius, sigma_r, K, centres, tau, g, n_flagged_host, ws,
+                      ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t hdf_filter_host_workspace_bytes(int H, int W, int n, int rho, int K, int kind, float sigma_s, int radius) {
+    const size_t base = hdf_filter_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
+    if (!base) return 0;
+    Carver cv(nullptr);
+    cv.take<float>((size_t)H * W * n);
+    cv.take<float>((size_t)H * W * rho);
+    cv.take<float>((size_t)H * W * n);
+    cv.take<float>((size_t)K * rho);
+    return base + cv.off + 256;
+}
+
+int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, int H, int W, int kind, float sigma_s,
+                    int radius, float sigma_r, int K, float tau, float* g_host, float* centres_host,
+                    int32_t* n_flagged_host, hdf_cluster_info* info_host, void* ws, size_t ws_bytes, void* stream) {
+    g_err.clear();
+    int rc = check_common(H, W, rho, K);
+    if (rc) return rc;
+    if (!f_host || !p_host || !g_host || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
+    if (n < 1 || n > HDF_MAX_N) return fail(HDF_ERR_ARG, "n must be in [1, %d]", HDF_MAX_N);
+    const size_t need = hdf_filter_host_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
+    if (ws_bytes < need) return fail(HDF_ERR_WORKSPACE, "workspace %zu < required %zu bytes", ws_bytes, need);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Carver cv(ws);
+    const size_t fbytes = hdf_filter_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
+    void* fws = cv.take<char>(fbytes);
+    float* fd = cv.take<float>((size_t)H * W * n);
+    float* pd = cv.take<float>((size_t)H * W * rho);
+    float* gd = cv.take<float>((size_t)H * W * n);
+    float* cd = cv.take<float>((size_t)K * rho);
+    const float* pdev = fd;
+    {
+        ProfScope prof(HDF_STAGE_H2D, st);
+        HDF_CUDA(cudaMemcpyAsync(fd, f_host, sizeof(float) * (size_t)H * W * n, cudaMemcpyHostToDevice, st));
+        if (p_host != f_host || rho != n) {
+            HDF_CUDA(cudaMemcpyAsync(pd, p_host, sizeof(float) * (size_t)H * W * rho, cudaMemcpyHostToDevice, st));
+            pdev = pd;
+        }
+    }
+    // cluster (in the filter workspace's cluster region) then filter
+    Carver c2(fws);
+    FilterWS w = carve_filter(c2, H, W, n, rho, K, round_up(W, 4), true);
+    rc = launch_cluster(pdev, H, W, rho, K, cd, nullptr, info_host, w.cluster_ws, st);
+    if (rc) return rc;
+    rc = run_filter(fd, n, pdev, rho, H, W, kind, sigma_s, radius, sigma_r, K, cd, tau, gd, nullptr, fws, fbytes, st);
+    if (rc) return rc;
+    int hv[2] = {0, 0};
+    {
+        ProfScope prof(HDF_STAGE_D2H, st);
+        HDF_CUDA(cudaMemcpyAsync(g_host, gd, sizeof(float) * (size_t)H * W * n, cudaMemcpyDeviceToHost, st));
+        if (centres_host)
+            HDF_CUDA(cudaMemcpyAsync(centres_host, cd, sizeof(float) * (size_t)K * rho, cudaMemcpyDeviceToHost, st));
+        HDF_CUDA(cudaMemcpyAsync(hv, w.status, sizeof(hv), cudaMemcpyDeviceToHost, st));
+    }
+    HDF_CUDA(cudaStreamSynchronize(st));
+    if (n_flagged_host) *n_flagged_host = hv[1];
+    return HDF_OK;
+}
+
+}  // extern "C"

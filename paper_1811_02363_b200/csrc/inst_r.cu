@@ -1,0 +1,46 @@
+// inst_r.cu -- explicit instantiation of the radius-templated filter kernels for one radius.
+// Compiled once per radius with -DHDF_R=<R> (the build runs these compilations in parallel).
+#include "hdf_dispatch.h"
+
+#ifndef HDF_R
+#error "compile with -DHDF_R=<radius>"
+#endif
+
+namespace hdf {
+
+template <int R>
+cudaError_t launch_vpass_t(bool box, const VLaunch& L, cudaStream_t st, const VParams& P) {
+    constexpr int J = vpass_j(R), NT = vpass_nt(R);
+    void (*kern)(const VParams) = box ? k_range_vpass<R, J, true, NT> : k_range_vpass<R, J, false, NT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    if (e != cudaSuccess) return e;
+    kern<<<L.grid, L.threads, L.smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+template <int R, int MAXJP>
+static cudaError_t hp(bool box, const HLaunch& L, cudaStream_t st, const CUtensorMap& tp, const CUtensorMap& tc,
+                      const HParams& P) {
+    void (*kern)(const CUtensorMap, const CUtensorMap, const HParams) =
+        box ? k_hpass_combine<R, MAXJP, true> : k_hpass_combine<R, MAXJP, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    if (e != cudaSuccess) return e;
+    kern<<<L.grid, L.threads, L.smem, st>>>(tp, tc, P);
+    return cudaGetLastError();
+}
+
+template <int R>
+cudaError_t launch_hpass_t(bool box, const HLaunch& L, cudaStream_t st, const CUtensorMap& tp, const CUtensorMap& tc,
+                           const HParams& P) {
+    switch (L.maxjp) {
+        case 1: return hp<R, 1>(box, L, st, tp, tc, P);
+        case 2: return hp<R, 2>(box, L, st, tp, tc, P);
+        default: return hp<R, 4>(box, L, st, tp, tc, P);
+    }
+}
+
+template cudaError_t launch_vpass_t<HDF_R>(bool, const VLaunch&, cudaStream_t, const VParams&);
+template cudaError_t launch_hpass_t<HDF_R>(bool, const HLaunch&, cudaStream_t, const CUtensorMap&, const CUtensorMap&,
+                                           const HParams&);
+
+}  // namespace hdf

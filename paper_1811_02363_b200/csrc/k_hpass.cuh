@@ -1,0 +1,260 @@
+// k_hpass.cuh -- F2: row half of the separable convolutions fused with the combine and normalise.
+//
+// For every cluster k (Algorithm 1 loop for3) and plane q = k(n+1)+c of the
+// column-filtered planes t_q produced by F1:
+//   v_{k,c}(i) = sum_{t=-R}^{R} w_t t_q(y, x - t)   (row half of omega * u_k),
+//   r_k(i)     = same for the b_k plane,
+// then  num_c(i) += c_k(i) v_{k,c}(i),  den(i) += c_k(i) r_k(i)  (HDapprox/approxDen)
+// and finally g(i) = num(i) / den(i).  Columns outside [0, W) contribute zero (R8).
+// Pixels with den < tau omega(0) phi(0) are appended to a list for the direct fallback (R9).
+//
+// Data movement: one producer lane issues, per cluster k, one 3-D TMA (cp.async.bulk.tensor) of the
+// (n+1) planes' tile [n+1][RR][Lbox] (Lbox = 128 + 2 R4 (+4), halo zero-filled by TMA out of bounds)
+// and one of the coefficient tile c_k [RR][132] into a multi-stage shared-memory ring guarded by
+// full/empty mbarriers.  Consumer warps own (row pair, plane set); a lane owns 8 consecutive pixels
+// of one row.  Lbox == 4 (mod 8) floats makes the float4 window loads bank-conflict free
+// (a quarter-warp covers 2 rows x 4 chunks).
+#pragma once
+#include "hdf_common.cuh"
+
+namespace hdf {
+
+constexpr int kHTW = 128;   // columns per CTA tile
+constexpr int kHPix = 8;    // consecutive pixels per lane
+constexpr int kCoefBox = kHTW + 4;
+
+struct HParams {
+    float* g;              // [H][W][n]
+    int* flag_count;       // device counter
+    int* flag_list;        // [H*W] flagged pixel indices
+    int n, NP, H, W, K;
+    int RR;                // rows per CTA (even)
+    int NJW;               // plane-warps per row pair
+    int NWC;               // consumer warps = (RR/2) * NJW
+    int NS;                // pipeline stages
+    int Lbox;              // inner box length (floats)
+    int stage_bytes;       // bytes per stage (planes + coef, 128-aligned parts)
+    int planes_bytes;      // bytes of the plane part of a stage
+    float tau_floor;       // tau * omega(0) * phi(0); <= 0 disables flagging
+    float taps[kMaxTaps];
+};
+
+template <int R>
+constexpr int h_r4() { return (R + 3) & ~3; }
+
+template <int R, int MAXJP, bool BOX>
+__global__ void __launch_bounds__(1024, 1)
+    k_hpass_combine(const __grid_constant__ CUtensorMap tm_planes, const __grid_constant__ CUtensorMap tm_coef,
+                    const __grid_constant__ HParams P) {
+    constexpr int R4 = (R + 3) & ~3;
+    constexpr int WIN = kHPix + 2 * R4;   // window floats per lane (multiple of 4)
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    // 128-byte aligned base (TMA destinations); the launcher adds 128 bytes of slack
+    unsigned char* sm_h = sm_raw + ((128u - (smem_u32(sm_raw) & 127u)) & 127u);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm_h);
+    uint64_t* empty = full + 8;
+    float* den_s = reinterpret_cast<float*>(sm_h + 128);          // [RR][128]
+    unsigned char* stages = sm_h + 128 + ((P.RR * kHTW * 4 + 127) & ~127);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x0 = blockIdx.x * kHTW, y0 = blockIdx.y * P.RR;
+
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&tm_planes);
+        prefetch_tmap(&tm_coef);
+        for (int s = 0; s < P.NS; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], P.NWC);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == P.NWC) {   // ---------------- producer warp ----------------
+        if (lane == 0) {
+            for (int k = 0; k < P.K; k++) {
+                const int s = k % P.NS, r = k / P.NS;
+                if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
+                unsigned char* st = stages + (size_t)s * P.stage_bytes;
+                mbar_arrive_expect_tx(&full[s], (uint32_t)(P.Lbox * P.RR * P.NP * 4 + kCoefBox * P.RR * 4));
+                tma_load_3d(st, &tm_planes, &full[s], x0 - R4, y0, k * P.NP);
+                tma_load_3d(st + P.planes_bytes, &tm_coef, &full[s], x0, y0, k);
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    const int npairs = P.RR >> 1;
+    const int rp = warp % npairs, jw = warp / npairs;
+    const int row = 2 * rp + (lane & 1);
+    const int xl = (lane >> 1) * kHPix;
+    float acc[MAXJP][kHPix];
+#pragma unroll
+    for (int a = 0; a < MAXJP; a++)
+#pragma unroll
+        for (int i = 0; i < kHPix; i++) acc[a][i] = 0.f;
+
+    for (int k = 0; k < P.K; k++) {
+        const int s = k % P.NS, r = k / P.NS;
+        mbar_wait(&full[s], r & 1);
+        const unsigned char* st = stages + (size_t)s * P.stage_bytes;
+        const float* cf = reinterpret_cast<const float*>(st + P.planes_bytes) + row * kCoefBox + xl;
+        float c[kHPix];
+        {
+            const float4 c0 = *reinterpret_cast<const float4*>(cf);
+            const float4 c1 = *reinterpret_cast<const float4*>(cf + 4);
+            c[0] = c0.x; c[1] = c0.y; c[2] = c0.z; c[3] = c0.w;
+            c[4] = c1.x; c[5] = c1.y; c[6] = c1.z; c[7] = c1.w;
+        }
+#pragma unroll
+        for (int a = 0; a < MAXJP; a++) {
+            const int j = jw + a * P.NJW;
+            if (j < P.NP) {
+                const float* base = reinterpret_cast<const float*>(st) + (j * P.RR + row) * P.Lbox + xl;
+                float h[kHPix];
+                if (BOX) {
+                    float w[WIN];
+#pragma unroll
+                    for (int s4 = 0; s4 < WIN / 4; s4++) {
+                        const float4 v = *reinterpret_cast<const float4*>(base + 4 * s4);
+                        w[4 * s4] = v.x; w[4 * s4 + 1] = v.y; w[4 * s4 + 2] = v.z; w[4 * s4 + 3] = v.w;
+                    }
+                    float run = 0.f;
+#pragma unroll
+                    for (int d = -R; d <= R; d++) run += w[R4 + d];
+                    h[0] = run;
+#pragma unroll
+                    for (int i = 1; i < kHPix; i++) {
+                        run = run + w[i + R4 + R] - w[i - 1 + R4 - R];
+                        h[i] = run;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kHPix; i++) h[i] = 0.f;
+#pragma unroll
+                    for (int s4 = 0; s4 < WIN / 4; s4++) {
+                        const float4 v = *reinterpret_cast<const float4*>(base + 4 * s4);
+                        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            const int sidx = 4 * s4 + e;
+#pragma unroll
+                            for (int i = 0; i < kHPix; i++) {
+                                const int d = sidx - i - R4;   // column offset of this value from pixel i
+                                if (d >= -R && d <= R) h[i] = fmaf(P.taps[R - d], vv[e], h[i]);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < kHPix; i++) acc[a][i] = fmaf(c[i], h[i], acc[a][i]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    // ---------------- epilogue: normalise, flag, store ----------------
+    const int nc = P.NWC * 32;
+    const int y = y0 + row;
+#pragma unroll
+    for (int a = 0; a < MAXJP; a++) {
+        const int j = jw + a * P.NJW;
+        if (j == P.n) {
+#pragma unroll
+            for (int i = 0; i < kHPix; i++) {
+                den_s[row * kHTW + xl + i] = acc[a][i];
+                const int x = x0 + xl + i;
+                const bool flag = (P.tau_floor > 0.f) && (acc[a][i] < P.tau_floor) && (x < P.W) && (y < P.H);
+                const unsigned m = __ballot_sync(__activemask(), flag);
+                if (m) {
+                    int basei = 0;
+                    const int leader = __ffs(m) - 1;
+                    if (lane == leader) basei = atomicAdd(P.flag_count, __popc(m));
+                    basei = __shfl_sync(__activemask(), basei, leader);
+                    if (flag) P.flag_list[basei + __popc(m & ((1u << lane) - 1))] = y * P.W + x;
+                }
+            }
+        }
+    }
+    named_sync(1, nc);
+    // stage g tile [RR][128][n] in the (now idle) ring and write it out coalesced
+    float* gst = reinterpret_cast<float*>(stages);
+#pragma unroll
+    for (int a = 0; a < MAXJP; a++) {
+        const int j = jw + a * P.NJW;
+        if (j < P.n) {
+#pragma unroll
+            for (int i = 0; i < kHPix; i++)
+                gst[(row * kHTW + xl + i) * P.n + j] = acc[a][i] / den_s[row * kHTW + xl + i];
+        }
+    }
+    named_sync(1, nc);
+    const int ncols = min(kHTW, P.W - x0);
+    const int seg = ncols * P.n;
+    for (int rr = 0; rr < P.RR; rr++) {
+        const int yy = y0 + rr;
+        if (yy >= P.H) break;
+        float* dst = P.g + ((long long)yy * P.W + x0) * P.n;
+        const float* src = gst + rr * kHTW * P.n;
+        for (int e = threadIdx.x; e < seg; e += nc) dst[e] = src[e];
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// F3: direct (num)/(den) for the pixels flagged by rule R9.  One warp per pixel; lanes
+// stride over the (2S+1)^2 window; fp32 accumulation, warp reduction, channels in chunks of 8.
+// ---------------------------------------------------------------------------------------------
+struct FBParams {
+    const float* f;
+    const float* p;
+    float* g;
+    const int* flag_count;
+    const int* flag_list;
+    int n, rho, H, W, R;
+    float neg_inv2sr2;
+    float taps[kMaxTaps];
+};
+
+static __global__ void __launch_bounds__(256) k_fallback(const __grid_constant__ FBParams P) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int cnt = *P.flag_count;
+    const int side = 2 * P.R + 1, win = side * side;
+    for (int t = gw; t < cnt; t += nw) {
+        const int i = P.flag_list[t];
+        const int y = i / P.W, x = i % P.W;
+        const float* pi = P.p + (long long)i * P.rho;
+        for (int c0 = 0; c0 < P.n; c0 += 8) {
+            float num[8];
+            float den = 0.f;
+#pragma unroll
+            for (int u = 0; u < 8; u++) num[u] = 0.f;
+            for (int e = lane; e < win; e += 32) {
+                const int ty = e / side - P.R, tx = e % side - P.R;
+                const int yy = y - ty, xx = x - tx;
+                if (yy < 0 || yy >= P.H || xx < 0 || xx >= P.W) continue;
+                const long long jj = (long long)yy * P.W + xx;
+                const float* pj = P.p + jj * P.rho;
+                float d2 = 0.f;
+                for (int d = 0; d < P.rho; d++) {
+                    float dd = pj[d] - pi[d];
+                    d2 = fmaf(dd, dd, d2);
+                }
+                const float wt = P.taps[ty + P.R] * P.taps[tx + P.R] * expf(d2 * P.neg_inv2sr2);
+                den += wt;
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+                    if (c0 + u < P.n) num[u] = fmaf(wt, P.f[jj * P.n + c0 + u], num[u]);
+            }
+            den = warp_sum(den);
+#pragma unroll
+            for (int u = 0; u < 8; u++) num[u] = warp_sum(num[u]);
+            if (lane == 0)
+                for (int u = 0; u < 8 && c0 + u < P.n; u++) P.g[(long long)i * P.n + c0 + u] = num[u] / den;
+        }
+    }
+}
+
+}  // namespace hdf

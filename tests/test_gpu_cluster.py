@@ -1,0 +1,103 @@
+"""GPU clustering (hdf_cluster) against the oracle's bisecting K-means and brute force.
+
+north_star: "The GPU clustering must give an error against brute force within 5% of the oracle's."
+Reading R15: MSE of [hdf_cluster -> hdf_filter] against brute-force (num)/(den) must be
+<= 1.05 x MSE of [oracle.cluster -> oracle.filter] against the same brute force.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hdf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1811_02363_b200 as h
+    h.lib()
+    return h
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+@pytest.mark.parametrize("name,H,W", [("c1", None, None), ("c2a", None, None), ("c2b", None, None),
+                                      ("c3", None, None), ("c4", None, None), ("c1", 77, 61)])
+def test_five_percent_rule_against_bruteforce(hdf, name, H, W):
+    cfg, f, p = synth.make(name, H, W)
+    g_bf, _ = oracle.bruteforce(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, r=cfg.radius)
+    cen_o, _, _, ek_o = oracle.cluster(p, cfg.K)
+    g_o, _, _, _ = oracle.filter(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, cen_o, r=cfg.radius)
+    pd = _dev(p)
+    cen_g, lab_g, info = hdf.cluster(pd, cfg.K, labels=True)
+    fd = pd if cfg.bilateral else _dev(f)
+    g_g = hdf.filter(fd, pd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                     centres=cen_g).g.cpu().numpy()
+    mse_o = oracle.mse(g_o, g_bf, cfg.R_range)
+    mse_g = oracle.mse(g_g, g_bf, cfg.R_range)
+    assert mse_g <= 1.05 * mse_o + 1e-12, f"{name}: GPU MSE {mse_g:.4e} vs oracle {mse_o:.4e}"
+    # clustering error E_K of the GPU centres within 5% of the oracle's
+    assert abs(info.e_k - ek_o) <= 0.05 * ek_o + 1e-9
+    # labels partition the pixels into K non-empty clusters whose means are the centres
+    lab = lab_g.cpu().numpy().reshape(-1)
+    P = p.reshape(-1, p.shape[-1]).astype(np.float64)
+    cg = cen_g.cpu().numpy().astype(np.float64)
+    assert lab.min() >= 0 and lab.max() < cfg.K and len(np.unique(lab)) == cfg.K
+    for k in range(cfg.K):
+        m = P[lab == k].mean(0)
+        assert np.allclose(cg[k], m, rtol=1e-5, atol=1e-4 * cfg.R_range)
+    # E_K reported = SSE of the labelled partition
+    sse = sum(((P[lab == k] - P[lab == k].mean(0)) ** 2).sum() for k in range(cfg.K))
+    assert abs(info.e_k - sse) <= 1e-6 * sse + 1e-9
+
+
+@pytest.mark.parametrize("name", ["c1", "c2b", "c4"])
+def test_same_trajectory_as_oracle(hdf, name):
+    """The GPU runs the oracle's procedure (R2-R4) in fp64: same centres up to fp32 rounding."""
+    cfg, f, p = synth.make(name)
+    cen_o, lab_o, _, ek_o = oracle.cluster(p, cfg.K)
+    cen_g, lab_g, info = hdf.cluster(_dev(p), cfg.K, labels=True)
+    cg = cen_g.cpu().numpy().astype(np.float64)
+    assert np.allclose(cg, cen_o, rtol=1e-6, atol=1e-5 * cfg.R_range)
+    assert np.array_equal(lab_g.cpu().numpy().reshape(-1), lab_o)
+    assert abs(info.e_k - ek_o) <= 1e-9 * ek_o
+
+
+def test_k1_is_global_mean(hdf):
+    cfg, f, p = synth.make("c1")
+    cen, lab, info = hdf.cluster(_dev(p), 1, labels=True)
+    P = p.reshape(-1, 3).astype(np.float64)
+    assert np.allclose(cen.cpu().numpy(), P.mean(0), rtol=1e-6)
+    assert int(lab.max()) == 0 and int(lab.min()) == 0
+    assert abs(info.e_k - ((P - P.mean(0)) ** 2).sum()) <= 1e-9 * info.e_k
+
+
+def test_k_distinct_values(hdf):
+    lab, pal, p = synth.gen_kdistinct(48, 40, 9, 4, seed=21)
+    cen, lab_g, info = hdf.cluster(_dev(p), 9, labels=True)
+    assert info.e_k == 0.0
+    got = sorted(map(tuple, np.round(cen.cpu().numpy().astype(np.float64), 3)))
+    want = sorted(map(tuple, np.round(pal.astype(np.float64), 3)))
+    assert got == want
+
+
+def test_e_k_non_increasing_in_k(hdf):
+    cfg, f, p = synth.make("c2a", 128, 128)
+    pd = _dev(p)
+    eks = [hdf.cluster(pd, K)[2].e_k for K in (1, 2, 4, 8, 16, 32, 64)]
+    assert all(b <= a * (1 + 1e-12) for a, b in zip(eks, eks[1:]))
+
+
+def test_rho_31_and_6(hdf):
+    for name in ("c3", "c4"):
+        cfg, f, p = synth.make(name, 64, 96)
+        cen_o, lab_o, _, ek_o = oracle.cluster(p, 12)
+        cen_g, lab_g, info = hdf.cluster(_dev(p), 12, labels=True)
+        assert abs(info.e_k - ek_o) <= 1e-6 * ek_o
