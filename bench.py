@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path (cluster + pinv + K(n+1) convolutions + combine) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2b] [--impl ours|reference]
+
+One step = one pass of the whole hot path (S1 cluster, S2 pinv, S3-S6
+filter) over one synthetic image resident in HBM, through the C ABI (hdf_filter with centres=NULL
+clusters inside the call).  Default workload = BASELINE.json configs[1] with K=32 ("c2b":
+512x512x3 colour bilateral, sigma_s=5 (R=15), sigma_r=40).  L2 is flushed (a 512 MiB write)
+between timed steps, outside the timed events.
+
+Multi-GPU (torchrun, one process per GPU): the path partitions into independent images; every
+rank filters its own seeded image with no collective on the data path ("scaling": "weak"); the
+step time is the max over ranks.
+
+Rank 0 prints ONE JSON line.  --impl reference times the fp64 CPU oracle (test infrastructure,
+oracle/) on the host cores instead; --all prints one line per config (exploration only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+
+METRIC = "Mpixel/s per filter (cluster+convolve+combine)"
+UNIT = "Mpixel/s"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------------------------ clocks ----
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thr = threading.Thread(target=self._read, daemon=True)
+            self.thr.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, samples = [], None, set(), 0
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                s, mx = float(parts[1]), float(parts[2])
+            except ValueError:
+                continue
+            samples += 1
+            smax = mx
+            sm.append(s)
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": samples}
+
+
+# ---------------------------------------------------------------------------- algorithmic work ----
+def stage_work(cfg, K: int, H: int, W: int):
+    """Algorithmic bytes and FP32 FMA-pipe ops per launch of each filter kernel.
+    bytes: what the minimal version of the kernel must move (planes written once, read once; the
+    coefficient planes c are a design choice of this build and are not counted)."""
+    n, rho, R = cfg.n, cfg.rho, cfg.radius
+    npx = H * W
+    n_in = n if cfg.bilateral else n + rho
+    planes = K * (n + 1)
+    taps = 2 * R + 1
+    return {
+        "vpass": {"bytes": 4 * npx * (n_in + planes), "fma": npx * (planes * taps + K * (rho + 1 + n))},
+        "hpass": {"bytes": 4 * npx * (planes + n),
+                  "fma": npx * (planes * (taps if cfg.kind == "gaussian" else 4) + planes + n)},
+        "coeffs": {"bytes": 4 * npx * rho, "fma": npx * (K * K + K * (rho + 1))},
+        "filter": {"bytes": 4 * npx * (n_in + 2 * planes + n)},        # SURVEY 8(d) B_req
+    }
+
+
+def fma_peak(sm_mhz: float, nsm: int = 148) -> float:
+    """FP32 FMA-pipe roof = SMs x 128 lanes x clock."""
+    return nsm * 128 * sm_mhz * 1e6
+
+
+# ------------------------------------------------------------------------------------ our arm ----
+def run_ours(args, rank: int, world: int, dist):
+    import torch
+
+    import paper_1811_02363_b200 as hdf
+    import synth
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    cfg, f, p = synth.make(args.config)
+    if world > 1 and rank > 0:       # independent image per rank (weak scaling)
+        cfg2, f, p = _rank_image(args.config, rank)
+    H, W = f.shape[:2]
+    K = cfg.K
+    fd = torch.from_numpy(f).to(dev)
+    pd = fd if cfg.bilateral else torch.from_numpy(p).to(dev)
+    ws = hdf.Workspace()
+    g = torch.empty_like(fd)
+    kw = dict(kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r, K=K, tau=0.5,
+              out=g, ws=ws)
+
+    def step():
+        hdf.filter(fd, pd, **kw)        # centres=None: clustering runs inside the call
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+
+    # ---- timed region: K steps, events around each step, L2 flushed between steps ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    time.sleep(0.3)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    hdf.profile_collect()
+    hdf.profile_enable(True)
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    hdf.profile_enable(False)
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop()
+    prof = hdf.profile_collect()
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if dist is not None:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    ms_step = t_ms / args.steps
+    value = world * H * W / (ms_step * 1e-3) / 1e6
+
+    # ---- end to end through the public host API: H2D + cluster + filter + D2H each step ----
+    fh = torch.from_numpy(f).pin_memory()
+    ph = fh if cfg.bilateral else torch.from_numpy(p).pin_memory()
+    gh = torch.empty_like(fh).pin_memory()
+    ws2 = hdf.Workspace()
+    for _ in range(max(1, args.warmup)):
+        hdf.filter_host(fh, ph, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                        K=K, out=gh, ws=ws2)
+    e2e_ms = []
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        hdf.filter_host(fh, ph, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                        K=K, out=gh, ws=ws2)
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e_t = sum(e2e_ms)
+    if dist is not None:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_val = world * H * W / (e2e_t / args.steps * 1e-3) / 1e6
+    h2d = fh.numel() * 4 + (0 if cfg.bilateral else ph.numel() * 4)
+    d2h = gh.numel() * 4 + K * cfg.rho * 4 + 8
+
+    # ---- roofline of the dominant kernel (live event timings above) ----
+    peaks = _peaks()
+    work = stage_work(cfg, K, H, W)
+    kern = {k: v for k, v in prof.items() if k in ("cluster", "pinv", "coeffs", "vpass", "hpass", "fallback")}
+    per_launch = {k: (ms / n if n else 0.0) for k, (ms, n) in kern.items()}
+    dom = max(per_launch, key=per_launch.get)
+    sm_mhz = clk.get("sm_mhz") or peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1965.0)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    roof = None
+    if dom in work:
+        t = per_launch[dom] * 1e-3
+        hbm_gbs = work[dom]["bytes"] / t / 1e9
+        fma_s = work[dom]["fma"] / t
+        t_hbm = work[dom]["bytes"] / (hbm_peak * 1e9)
+        t_alu = work[dom]["fma"] / fma_peak(sm_mhz, nsm)
+        if t_alu > t_hbm:
+            roof = {"bound": "alu", "achieved": round(fma_s / 1e12, 3), "peak": round(fma_peak(sm_mhz, nsm) / 1e12, 3),
+                    "unit": "TFMA/s (fp32)", "frac": round(fma_s / fma_peak(sm_mhz, nsm), 4),
+                    "peak_basis": f"{nsm} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (median SM clock in the timed region)",
+                    "hbm_achieved_gbs": round(hbm_gbs, 1), "hbm_frac": round(hbm_gbs / hbm_peak, 4)}
+        else:
+            roof = {"bound": "hbm", "achieved": round(hbm_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(hbm_gbs / hbm_peak, 4), "peak_basis": "measured copy (MEASURED_PEAKS.json hbm_gbs)"}
+        roof.update({"kernel": dom, "traffic": None, "ms_per_launch": round(per_launch[dom], 4)})
+    else:
+        roof = {"bound": "latency", "kernel": dom, "achieved": None, "peak": None, "unit": None, "frac": None,
+                "traffic": None, "ms_per_launch": round(per_launch[dom], 4)}
+    t_filter = sum(per_launch[k] for k in ("pinv", "coeffs", "vpass", "hpass", "fallback")) * 1e-3
+    filt = {"ms": round(t_filter * 1e3, 4), "B_req_bytes": work["filter"]["bytes"],
+            "hbm_gbs": round(work["filter"]["bytes"] / t_filter / 1e9, 1),
+            "hbm_frac": round(work["filter"]["bytes"] / t_filter / 1e9 / hbm_peak, 4)}
+    launches = sum(n for k, (ms, n) in kern.items())
+    return {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, SURVEY 8(d) generators)",
+        "config": {"workload": args.config, "note": cfg.note, "H": H, "W": W, "n": cfg.n, "rho": cfg.rho,
+                   "K": K, "kind": cfg.kind, "sigma_s": cfg.sigma_s, "radius": cfg.radius, "sigma_r": cfg.sigma_r,
+                   "images_per_step": world, "parallelism": f"independent image per rank x{world}",
+                   "l2": "flushed between steps (512 MiB write, outside the timed events)"},
+        "stages_ms_per_step": {k: round(ms / args.steps, 4) for k, (ms, n) in prof.items() if n},
+        "filter": filt, "roofline": roof, "gpu_launches": launches, "clocks": clk,
+        "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+    }
+
+
+def _rank_image(name: str, rank: int):
+    import synth
+    cfg = synth.CONFIGS[name]
+    # same recipe, seed offset by rank (an independent image of the same workload)
+    import dataclasses
+    cfg2 = dataclasses.replace(cfg, seed=cfg.seed + 1000 * rank)
+    old = synth.CONFIGS[name]
+    synth.CONFIGS[name] = cfg2
+    try:
+        return synth.make(name)
+    finally:
+        synth.CONFIGS[name] = old
+
+
+# --------------------------------------------------------------------------- oracle timing ----
+def oracle_sample(config: str, budget_s: float):
+    """Time the fp64 CPU oracle (as it stands) on host cores: cluster + filter of the workload's
+    image, or of a top strip of rows if one full image would exceed the budget."""
+    import oracle
+    import synth
+    cfg, f, p = synth.make(config)
+    H, W = f.shape[:2]
+    rows = H
+    est_per_px = 8e-6 if cfg.n <= 6 else 6e-5
+    if H * W * est_per_px > budget_s:
+        rows = max(16, int(budget_s / (W * est_per_px)))
+    fs, ps = np.ascontiguousarray(f[:rows]), np.ascontiguousarray(p[:rows])
+    t0 = time.perf_counter()
+    cen, _, _, _ = oracle.cluster(ps, cfg.K)
+    oracle.filter(fs, ps, cfg.kind, cfg.sigma_s, cfg.sigma_r, cen, r=cfg.radius)
+    dt = time.perf_counter() - t0
+    sample = f"{rows}x{W} rows of the {config} image ({'full image' if rows == H else 'top strip'}): oracle.cluster + oracle.filter, fp64"
+    return rows * W / dt / 1e6, dt, sample
+
+
+def cores():
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def run_reference(args):
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    vals = []
+    budget = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    sample = ""
+    for i in range(args.warmup + args.steps):
+        v, dt, sample = oracle_sample(args.config, budget)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    return {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8(d) generators)",
+            "impl": "reference", "config": {"workload": args.config},
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2b")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--all", action="store_true", help="one line per config (exploration)")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    configs = ["c1", "c2a", "c2b", "c3", "c4", "c5"] if args.all else [args.config]
+    for c in configs:
+        args.config = c
+        out = run_ours(args, rank, world, dist)
+        if rank == 0 and not args.no_cpu_baseline and not args.all:
+            os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+            v, dt, sample = oracle_sample(c, 20.0)
+            out["cpu_baseline"] = {"value": round(v, 4), "unit": UNIT, "cores": cores(), "kind": "oracle",
+                                   "sample": sample, "seconds": round(dt, 2)}
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
