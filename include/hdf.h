@@ -67,7 +67,7 @@ const char *hdf_last_error(void);
  * farthest pair of a stride sample of <= 1024 members (R3), Lloyd iterations until no assignment
  * changes or 50 iterations (R4).  mu_k = centroid of C_k.  Runs as one persistent
  * cooperative kernel; independent leaf splits run concurrently (results identical to the
- * sequential procedure).
+ * sequential procedure).  Up to 32 splits are computed per round.
  * ------------------------------------------------------------------------------------------- */
 typedef struct {
     int32_t status;        /* HDF_OK or HDF_ERR_K                                              */
@@ -75,6 +75,17 @@ typedef struct {
     int32_t rounds;        /* concurrent split rounds executed                                 */
     int32_t lloyd_iters;   /* lock-step Lloyd iterations executed (all rounds)                 */
     double e_k;            /* clustering error E_K = sum_k sum_{p(i) in C_k} ||p(i)-mu_k||^2     */
+    double t_plan_us;      /* diagnostics: device time per phase (globaltimer, block 0)        */
+    double t_seed_us;      /*   farthest-pair seeding                                            */
+    double t_lloyd_us;     /*   lock-step Lloyd iterations                                       */
+    double t_part_us;      /*   stable partition + child SSE                                     */
+    double t_sync_us;      /*   waiting in grid barriers (all phases, excluded from the above)   */
+    double t_pass_us;      /*   Lloyd assignment passes (excluded from t_lloyd_us)               */
+    double t_pass_side_us; /*     of which: assignment, sum, block-reduction sub-phases          */
+    double t_pass_sum_us;  /*     (cluster-mode rounds: seeding, Lloyd, partition of block 0's    */
+    double t_pass_red_us;  /*      splits)                                                        */
+    int32_t launch_ctas;   /* CTAs of the cooperative launch                                      */
+    int32_t cluster_ctas;  /* CTAs per thread-block cluster                                       */
 } hdf_cluster_info;
 
 /* Device workspace (bytes) for hdf_cluster on an H x W guide of dimension rho. */
@@ -165,6 +176,11 @@ typedef enum {
     HDF_STAGE_D2H = 7,       /* hdf_filter_host output copies                               */
     HDF_NUM_STAGES = 8
 } hdf_stage;
+
+/* Diagnostics: events (tag, globaltimer ns) recorded by block 0 during the last hdf_cluster call
+ * that used workspace `ws` with the same H, W, rho, K.  out: host [2 * cap]; returns the number of
+ * events copied (synchronous), or -1 on a CUDA error. */
+int hdf_cluster_trace(const float *p_unused, int H, int W, int rho, int K, void *ws, long long *out, int cap);
 
 /* Turn event recording on (on != 0) or off.  Process-wide; returns HDF_OK. */
 int hdf_profile_enable(int on);

@@ -27,7 +27,7 @@ MAX_K, MAX_RHO, MAX_N, MAX_RADIUS = 128, 64, 64, 32
 # every symbol include/hdf.h declares (checked by the CPU tests)
 EXPORTS = ("hdf_version", "hdf_last_error", "hdf_cluster_workspace_bytes", "hdf_cluster",
            "hdf_filter_workspace_bytes", "hdf_filter", "hdf_filter_host_workspace_bytes", "hdf_filter_host",
-           "hdf_profile_enable", "hdf_profile_collect")
+           "hdf_profile_enable", "hdf_profile_collect", "hdf_cluster_trace")
 STAGES = ("cluster", "pinv", "coeffs", "vpass", "hpass", "fallback", "h2d", "d2h")
 
 
@@ -45,7 +45,11 @@ class HdfKError(HdfError):
 
 class ClusterInfo(C.Structure):
     _fields_ = [("status", C.c_int32), ("achievable_k", C.c_int32), ("rounds", C.c_int32),
-                ("lloyd_iters", C.c_int32), ("e_k", C.c_double)]
+                ("lloyd_iters", C.c_int32), ("e_k", C.c_double), ("t_plan_us", C.c_double),
+                ("t_seed_us", C.c_double), ("t_lloyd_us", C.c_double), ("t_part_us", C.c_double),
+                ("t_sync_us", C.c_double), ("t_pass_us", C.c_double), ("t_pass_side_us", C.c_double),
+                ("t_pass_sum_us", C.c_double), ("t_pass_red_us", C.c_double), ("launch_ctas", C.c_int32),
+                ("cluster_ctas", C.c_int32)]
 
 
 _lib = None
@@ -79,6 +83,8 @@ def lib():
         L.hdf_profile_enable.restype = i
         L.hdf_profile_collect.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int32)]
         L.hdf_profile_collect.restype = i
+        L.hdf_cluster_trace.argtypes = [vp, i, i, i, i, vp, C.POINTER(C.c_longlong), i]
+        L.hdf_cluster_trace.restype = i
         _lib = L
     return _lib
 
@@ -242,3 +248,11 @@ def profile_collect() -> dict:
     if st != OK:
         _raise(st)
     return {name: (ms[i], n[i]) for i, name in enumerate(STAGES)}
+
+
+def cluster_trace(p: torch.Tensor, K: int, ws: Workspace | None = None):
+    """Diagnostics: (tag, ns) events of block 0 in the last cluster() call on workspace ws."""
+    H, W, rho = _hwc(p, "p")
+    buf = (C.c_longlong * (2 * 4096))()
+    n = lib().hdf_cluster_trace(None, H, W, rho, K, (ws or _default_ws).buf.data_ptr(), buf, 4096)
+    return [(buf[2 * i], buf[2 * i + 1]) for i in range(max(n, 0))]

@@ -100,30 +100,27 @@ struct ProfScope {
 
 // ------------------------------------------------------------------------ cluster workspace ----
 struct ClusterPlan {
-    int CH, maxch, slotmax, pstride;
+    int slotmax, maxrec, pstride;
 };
-ClusterPlan cluster_plan(long long N, int rho, int K) {
+ClusterPlan cluster_plan(int rho, int K) {
     ClusterPlan c;
-    c.CH = (int)std::max<long long>(1024, (N + 1023) / 1024);
-    c.maxch = (int)((N + c.CH - 1) / c.CH) + K + 1;
-    c.maxch = std::max(c.maxch, 2048);   // also holds the per-block root partials
-    c.slotmax = K;
+    c.slotmax = std::min(K, hdf::kSlotCap);
+    c.maxrec = hdf::kMaxGrid + c.slotmax;
     c.pstride = 2 * rho + 4;
     return c;
 }
 
 hdf::ClusterArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho, int K) {
     const long long N = (long long)H * W;
-    const ClusterPlan pl = cluster_plan(N, rho, K);
+    const ClusterPlan pl = cluster_plan(rho, K);
     hdf::ClusterArgs A;
     memset(&A, 0, sizeof(A));
     A.p = p;
     A.N = (int)N;
     A.rho = rho;
     A.K = K;
-    A.CH = pl.CH;
-    A.maxch = pl.maxch;
     A.slotmax = pl.slotmax;
+    A.maxrec = pl.maxrec;
     A.pstride = pl.pstride;
     for (int b = 0; b < 2; b++) A.pts[b] = cv.take<float>((size_t)N * rho);
     for (int b = 0; b < 2; b++) A.idx[b] = cv.take<int>((size_t)N);
@@ -135,20 +132,29 @@ hdf::ClusterArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho
     A.slots = cv.take<hdf::CSlot>(pl.slotmax);
     A.c0g = cv.take<double>((size_t)pl.slotmax * rho);
     A.c1g = cv.take<double>((size_t)pl.slotmax * rho);
-    A.chunks = cv.take<hdf::CChunk>(pl.maxch);
-    A.part = cv.take<double>((size_t)pl.maxch * pl.pstride);
+    for (int b = 0; b < 2; b++) A.rec[b] = cv.take<double>((size_t)pl.maxrec * pl.pstride);
     A.fpd = cv.take<double>((size_t)pl.slotmax * hdf::kFpCap);
     A.fpi = cv.take<int>((size_t)pl.slotmax * hdf::kFpCap);
     A.ctrl = cv.take<int>(hdf::C_NUM);
+    A.timers = cv.take<long long>(hdf::T_NUM);
+    A.trace = cv.take<long long>(1 + 2 * hdf::kTraceCap);
     A.ek = cv.take<double>(1);
     return A;
 }
 
-size_t cluster_smem(int rho, int K) {
-    const ClusterPlan pl = cluster_plan(1, rho, K);
-    const int nvL = 2 * rho + 4;
-    return sizeof(double) * (size_t)(hdf::kClWarps * nvL + 2 * pl.slotmax * rho + nvL);
+// Dynamic shared memory of k_bisect_kmeans: fixed scratch plus the point tile, which takes what is
+// left of a 200 KB budget (1 CTA per SM).
+constexpr size_t kClSmemBudget = 200 * 1024;
+size_t cluster_fixed_smem(int rho, int K) {
+    const ClusterPlan pl = cluster_plan(rho, K);
+    const size_t dbl = (size_t)(2 * hdf::kClThreads + 2 * pl.slotmax * rho + pl.slotmax * pl.pstride + 2 * rho + 16);
+    return sizeof(double) * (dbl + hdf::kRecBuf) + 2 * 16384 + 64;
 }
+int cluster_tile_floats(int rho, int K) {
+    const long long avail = (long long)kClSmemBudget - (long long)cluster_fixed_smem(rho, K);
+    return (int)std::max<long long>(4 * rho, (avail / 4) & ~3LL);
+}
+size_t cluster_smem(int rho, int K) { return cluster_fixed_smem(rho, K) + sizeof(float) * cluster_tile_floats(rho, K); }
 
 int check_common(int H, int W, int rho, int K) {
     if (H < 1 || W < 1) return fail(HDF_ERR_ARG, "H, W must be >= 1 (got %d, %d)", H, W);
@@ -166,36 +172,90 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
     hdf::ClusterArgs A = carve_cluster(cv, p, H, W, rho, K);
     A.centres = centres;
     A.labels = labels;
+    A.tileF = cluster_tile_floats(rho, K);
+    // Launch shape: a cooperative grid of thread-block clusters (16 CTAs when the device can keep
+    // enough of them resident, else 8), one CTA per SM.  Cached per (K, rho).
+    struct Shape {
+        int cdim, nclusters;
+    };
     static std::mutex mu;
-    static int occ_cache[HDF_MAX_K + 1][HDF_MAX_RHO + 1];
+    static Shape cache[HDF_MAX_K + 1][HDF_MAX_RHO + 1];
     const size_t smem = cluster_smem(rho, K);
-    int dev = 0, nsm = 0, occ = 0;
-    HDF_CUDA(cudaGetDevice(&dev));
-    HDF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    Shape sh;
     {
         std::lock_guard<std::mutex> lk(mu);
-        occ = occ_cache[K][rho];
-        if (occ == 0) {
+        sh = cache[K][rho];
+        if (sh.cdim == 0) {
             HDF_CUDA(cudaFuncSetAttribute(hdf::k_bisect_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            HDF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hdf::k_bisect_kmeans, hdf::kClThreads, smem));
-            occ = std::max(1, std::min(occ, 2));
-            occ_cache[K][rho] = occ;
+            HDF_CUDA(cudaFuncSetAttribute(hdf::k_bisect_kmeans, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            for (int cdim : {16, 8, 4, 2, 1}) {
+                cudaLaunchConfig_t cfg = {};
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = cdim;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.gridDim = dim3(cdim);
+                cfg.blockDim = dim3(hdf::kClThreads);
+                cfg.dynamicSmemBytes = smem;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                int ncl = 0;
+                if (cudaOccupancyMaxActiveClusters(&ncl, (void*)hdf::k_bisect_kmeans, &cfg) != cudaSuccess) {
+                    cudaGetLastError();
+                    ncl = 0;
+                }
+                ncl = std::min(ncl, hdf::kMaxGrid / cdim);
+                if (ncl * cdim >= 64 || (cdim == 1 && ncl > 0)) {
+                    sh.cdim = cdim;
+                    sh.nclusters = ncl;
+                    break;
+                }
+            }
+            if (sh.cdim == 0) return fail(HDF_ERR_CUDA, "no resident launch shape for the clustering kernel");
+            cache[K][rho] = sh;
         }
     }
     HDF_CUDA(cudaFuncSetAttribute(hdf::k_bisect_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int grid = std::min(nsm * occ, A.maxch);
-    void* args[] = {&A};
+    // rounds whose largest leaf exceeds ~4 shared tiles per CTA of a cluster run grid-wide instead
+    A.big = (long long)sh.cdim * 4 * std::min(A.tileF / rho, 16384);
     {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = sh.cdim;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(sh.cdim * sh.nclusters);
+        cfg.blockDim = dim3(hdf::kClThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
         ProfScope prof(HDF_STAGE_CLUSTER, st);
-        HDF_CUDA(cudaLaunchCooperativeKernel((void*)hdf::k_bisect_kmeans, dim3(grid), dim3(hdf::kClThreads), args,
-                                             smem, st));
+        HDF_CUDA(cudaLaunchKernelEx(&cfg, hdf::k_bisect_kmeans, A));
     }
     if (info) {
         int ctrl[hdf::C_NUM];
         double ek = 0.0;
+        long long tm[hdf::T_NUM];
         HDF_CUDA(cudaMemcpyAsync(ctrl, A.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, st));
         HDF_CUDA(cudaMemcpyAsync(&ek, A.ek, sizeof(double), cudaMemcpyDeviceToHost, st));
+        HDF_CUDA(cudaMemcpyAsync(tm, A.timers, sizeof(tm), cudaMemcpyDeviceToHost, st));
         HDF_CUDA(cudaStreamSynchronize(st));
+        info->t_plan_us = tm[hdf::T_PLAN] * 1e-3;
+        info->t_seed_us = tm[hdf::T_SEED] * 1e-3;
+        info->t_lloyd_us = tm[hdf::T_LLOYD] * 1e-3;
+        info->t_part_us = tm[hdf::T_PART] * 1e-3;
+        info->t_sync_us = tm[hdf::T_SYNC] * 1e-3;
+        info->t_pass_us = tm[hdf::T_PASS] * 1e-3;
+        info->t_pass_side_us = tm[hdf::T_P_SIDE] * 1e-3;
+        info->t_pass_sum_us = tm[hdf::T_P_SUM] * 1e-3;
+        info->t_pass_red_us = tm[hdf::T_P_RED] * 1e-3;
+        info->launch_ctas = (int)(sh.cdim * sh.nclusters);
+        info->cluster_ctas = sh.cdim;
         info->status = ctrl[hdf::C_STATUS];
         info->achievable_k = ctrl[hdf::C_NLEAVES];
         info->rounds = ctrl[hdf::C_ROUNDS];
@@ -557,6 +617,20 @@ extern "C" {
 const char* hdf_version(void) { return "hdf 0.1.0 sm_100a"; }
 
 const char* hdf_last_error(void) { return g_err.c_str(); }
+
+// Diagnostics: copy the clustering trace of the last hdf_cluster call that used `ws` (block 0
+// events: tag, globaltimer ns).  Returns the number of events.
+int hdf_cluster_trace(const float* p_unused, int H, int W, int rho, int K, void* ws, long long* out, int cap) {
+    (void)p_unused;
+    Carver cv(ws);
+    hdf::ClusterArgs A = carve_cluster(cv, nullptr, H, W, rho, K);
+    long long n = 0;
+    if (cudaMemcpy(&n, A.trace, sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    n = std::min<long long>(n, cap);
+    if (n > 0 && cudaMemcpy(out, A.trace + 1, sizeof(long long) * 2 * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    return (int)n;
+}
 
 int hdf_profile_enable(int on) {
     std::lock_guard<std::mutex> lk(g_prof_mu);

@@ -1,11 +1,31 @@
-import sys, numpy as np, torch
+import sys, time, numpy as np, torch
 sys.path.insert(0, '.')
-import synth, paper_1811_02363_b200 as hdf
-name = sys.argv[1] if len(sys.argv) > 1 else 'c1'
-H = int(sys.argv[2]) if len(sys.argv) > 2 else None
-cfg, f, p = synth.make(name, H, H)
-cen, lab, info = hdf.cluster(torch.from_numpy(p).cuda(), cfg.K, labels=True)
-print('status', info.status, 'ach', info.achievable_k, 'rounds', info.rounds, 'iters', info.lloyd_iters, 'E_K', info.e_k)
-import oracle
-c, l, s, ek = oracle.cluster(p, cfg.K)
-print('oracle E_K', ek, 'max centre diff', np.abs(cen.cpu().numpy() - c).max(), 'labels eq', (lab.cpu().numpy().reshape(-1) == l).mean())
+import synth, oracle, paper_1811_02363_b200 as hdf
+# warm the GPU up (clocks ramp from idle) before timing
+_a = torch.randn(8192, 8192, device="cuda")
+for _ in range(20):
+    _a @ _a
+torch.cuda.synchronize()
+for name in sys.argv[1:]:
+    cfg, f, p = synth.make(name)
+    pd = torch.from_numpy(p).cuda()
+    for rep in range(3):
+        torch.cuda.synchronize(); t = time.perf_counter()
+        cen, lab, info = hdf.cluster(pd, cfg.K, labels=True)
+        dt = time.perf_counter() - t
+    print(name, 'status', info.status, 'rounds', info.rounds, 'iters', info.lloyd_iters, 'E_K %.10e' % info.e_k,
+          'wall %.3f ms' % (dt * 1e3), 'grid', info.launch_ctas, 'cl', info.cluster_ctas, 'plan %.1f seed %.1f pass %.1f (side %.1f sum %.1f red %.1f) fin %.1f part %.1f sync %.1f us' % (info.t_plan_us, info.t_seed_us, info.t_pass_us, info.t_pass_side_us, info.t_pass_sum_us, info.t_pass_red_us, info.t_lloyd_us, info.t_part_us, info.t_sync_us))
+    c, l, s, ek = oracle.cluster(p, cfg.K)
+    print('   oracle E_K %.10e' % ek, 'max centre diff', np.abs(cen.cpu().numpy() - c).max(), 'labels eq', (lab.cpu().numpy().reshape(-1) == l).mean())
+
+if "--trace" in sys.argv or True:
+    tr = hdf.cluster_trace(pd, cfg.K)
+    t0 = tr[0][1] if tr else 0
+    prev = t0
+    line = []
+    for tag, t in tr[:400]:
+        line.append("%d:%.1f" % (tag & 0xFFFF, (t - prev) / 1e3))
+        prev = t
+    print("trace (tag:us since previous)", " ".join(line))
+    c0, c1 = tr[0][0] >> 16, tr[-1][0] >> 16
+    print("effective SM clock over the trace: %.0f MHz" % ((c1 - c0) / max(tr[-1][1] - tr[0][1], 1) * 1e3))
