@@ -6,6 +6,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o m2 m2.cu
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <vector>
 #include <cuda_runtime.h>
 namespace cg = cooperative_groups;
 
@@ -114,6 +115,86 @@ __global__ void k_lat(int iters, long long* out, double* sink) {
     long long t3 = clock64();
     if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t2 - t1; out[2] = t3 - t2; }
     sink[threadIdx.x] = a + fa;
+}
+
+// (g) generic vs explicit shared loads: pair loop like the farthest-pair seed (fp64 distance of
+// 1024 fp32 points of dim 3 held in shared memory), one CTA of 512 threads.
+__global__ void k_pairs(const float* src, int generic_ptr, long long* out, double* sink) {
+    __shared__ float pts[1024 * 3];
+    for (int i = threadIdx.x; i < 3072; i += blockDim.x) pts[i] = src[i];
+    __syncthreads();
+    const float* P = generic_ptr ? (const float*)((volatile const float*)pts) : pts;
+    long long t0 = clock64();
+    double best = -1; int arg = -1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int a = warp; a < 1024; a += 16) {
+        const float* xa = P + a * 3;
+        for (int b = a + 1 + lane; b < 1024; b += 32) {
+            const float* xb = P + b * 3;
+            double dd = 0.0;
+            for (int d = 0; d < 3; d++) {
+                double t = __dsub_rn((double)xa[d], (double)xb[d]);
+                dd = __dadd_rn(dd, __dmul_rn(t, t));
+            }
+            if (dd > best) { best = dd; arg = b; }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *out = clock64() - t0;
+    sink[threadIdx.x] = best + arg;
+}
+
+__device__ __forceinline__ double d2_rn(double acc, double a, double b) {
+    double t = __dsub_rn(a, b);
+    return __dadd_rn(acc, __dmul_rn(t, t));
+}
+template <class Base>
+__device__ __forceinline__ void row_farthest(int a, int sN, int rho, Base base, double& best, int& arg) {
+    const int lane = threadIdx.x & 31;
+    constexpr float u = 5.9604644775390625e-08f;
+    const float* xa = base(a);
+    float m = 0.f;
+    for (int q = a + 1 + lane; q < sN; q += 32) {
+        const float* xb = base(q);
+        float acc = 0.f;
+        for (int d = 0; d < rho; d++) { const float t = xa[d] - xb[d]; acc = fmaf(t, t, acc); }
+        m = fmaxf(m, acc);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float thr = m * (1.0f - 8.0f * (float)(rho + 3) * u);
+    best = -1.0; arg = -1;
+    for (int q = a + 1 + lane; q < sN; q += 32) {
+        const float* xb = base(q);
+        float acc = 0.f;
+        for (int d = 0; d < rho; d++) { const float t = xa[d] - xb[d]; acc = fmaf(t, t, acc); }
+        if (acc >= thr) {
+            double dd = 0.0;
+            for (int d = 0; d < rho; d++) dd = d2_rn(dd, (double)xa[d], (double)xb[d]);
+            if (dd > best) { best = dd; arg = q; }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+        if (oa >= 0 && (arg < 0 || ob > best || (ob == best && oa < arg))) { best = ob; arg = oa; }
+    }
+}
+__global__ void k_rowfar(const float* src, int rho, long long* out, double* sink) {
+    extern __shared__ float tp[];
+    for (int i = threadIdx.x; i < 1024 * rho; i += blockDim.x) tp[i] = src[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    long long t0 = clock64();
+    double bv = -1; int ba = -1;
+    for (int ra = 16 * warp; ra < 1024; ra += 16 * 16) {
+        double best; int arg;
+        const float* tpc = tp;
+        row_farthest(ra, 1024, rho, [&](int q) { return tpc + (size_t)q * rho; }, best, arg);
+        if (arg >= 0 && (ba < 0 || best > bv)) { bv = best; ba = ra; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *out = clock64() - t0;
+    sink[threadIdx.x] = bv + ba;
 }
 
 int main() {
@@ -239,6 +320,40 @@ int main() {
             cudaMemcpy(hl, dl, 24, cudaMemcpyDeviceToHost);
             printf("(f) dependent latency, %d threads in 1 CTA: DFMA %.1f clk, DMUL+DADD %.1f clk, FFMA %.1f clk\n", nthr,
                    hl[0] / 10000.0, hl[1] / 10000.0, hl[2] / 10000.0);
+        }
+    }
+    {
+        float* dsrc;
+        cudaMalloc(&dsrc, 3072 * 4);
+        cudaMemset(dsrc, 0, 3072 * 4);
+        long long* dl;
+        double* ds;
+        cudaMalloc(&dl, 64);
+        cudaMalloc(&ds, 8 * 1024);
+        for (int g = 0; g < 2; g++) {
+            long long hl = 0;
+            for (int rep = 0; rep < 2; rep++) k_pairs<<<1, 512>>>(dsrc, g, dl, ds);
+            cudaDeviceSynchronize();
+            cudaMemcpy(&hl, dl, 8, cudaMemcpyDeviceToHost);
+            printf("(g) 1024-point farthest pair, 1 CTA x 512 threads, %s: %lld clk = %.1f clk per pair per thread\n",
+                   g ? "volatile-generic" : "plain", hl, hl / (523776.0 / 512));
+        }
+    }
+    {
+        float* dsrc;
+        cudaMalloc(&dsrc, 1024 * 64 * 4);
+        std::vector<float> h(1024 * 64);
+        for (size_t i = 0; i < h.size(); i++) h[i] = (float)((i * 2654435761u) % 1000) * 0.255f;
+        cudaMemcpy(dsrc, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+        long long* dl; double* ds;
+        cudaMalloc(&dl, 64); cudaMalloc(&ds, 8 * 1024);
+        for (int rho : {3, 31}) {
+            long long hl = 0;
+            cudaFuncSetAttribute(k_rowfar, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * rho * 4);
+            for (int rep = 0; rep < 2; rep++) k_rowfar<<<1, 512, 1024 * rho * 4>>>(dsrc, rho, dl, ds);
+            cudaDeviceSynchronize();
+            cudaMemcpy(&hl, dl, 8, cudaMemcpyDeviceToHost);
+            printf("(h) row_farthest, 64 rows of a 1024 sample, rho=%d, 1 CTA x 512: %lld clk = %.2f us\n", rho, hl, hl / ghz / 1e3);
         }
     }
     return 0;

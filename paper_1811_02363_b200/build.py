@@ -21,7 +21,7 @@ RADII = (1, 2, 3, 4, 5, 6, 8, 9, 10, 12, 15, 16, 20, 24, 32)   # keep in sync wi
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-         "-I" + os.path.join(ROOT, "include")]
+         "-I" + os.path.join(ROOT, "include")] + os.environ.get("HDF_EXTRA_FLAGS", "").split()
 
 
 def _sources_digest() -> str:

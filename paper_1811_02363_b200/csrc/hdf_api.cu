@@ -142,19 +142,24 @@ hdf::ClusterArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho
     return A;
 }
 
-// Dynamic shared memory of k_bisect_kmeans: fixed scratch plus the point tile, which takes what is
-// left of a 200 KB budget (1 CTA per SM).
-constexpr size_t kClSmemBudget = 200 * 1024;
+// Dynamic shared memory of k_bisect_kmeans: fixed scratch, then the point tile (tileF floats) and
+// its side bytes (2 per point), which take what is left of the budget (1 CTA per SM; the kernel's
+// static shared memory is ~13 KB of the 227 KB per CTA).
+constexpr size_t kClSmemBudget = 210 * 1024;
 size_t cluster_fixed_smem(int rho, int K) {
     const ClusterPlan pl = cluster_plan(rho, K);
     const size_t dbl = (size_t)(2 * hdf::kClThreads + 2 * pl.slotmax * rho + pl.slotmax * pl.pstride + 2 * rho + 16);
-    return sizeof(double) * (dbl + hdf::kRecBuf) + 2 * 16384 + 64;
+    return sizeof(double) * (dbl + hdf::kRecBuf) + 64;
 }
 int cluster_tile_floats(int rho, int K) {
-    const long long avail = (long long)kClSmemBudget - (long long)cluster_fixed_smem(rho, K);
-    return (int)std::max<long long>(4 * rho, (avail / 4) & ~3LL);
+    const double avail = (double)kClSmemBudget - (double)cluster_fixed_smem(rho, K);
+    const long long f = (long long)(avail / (4.0 + 2.0 / rho)) & ~3LL;
+    return (int)std::max<long long>(4 * rho, f);
 }
-size_t cluster_smem(int rho, int K) { return cluster_fixed_smem(rho, K) + sizeof(float) * cluster_tile_floats(rho, K); }
+size_t cluster_smem(int rho, int K) {
+    const int tf = cluster_tile_floats(rho, K);
+    return cluster_fixed_smem(rho, K) + sizeof(float) * tf + 2 * (size_t)std::min(tf / rho, 16384);
+}
 
 int check_common(int H, int W, int rho, int K) {
     if (H < 1 || W < 1) return fail(HDF_ERR_ARG, "H, W must be >= 1 (got %d, %d)", H, W);
@@ -217,8 +222,11 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
         }
     }
     HDF_CUDA(cudaFuncSetAttribute(hdf::k_bisect_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    // rounds whose largest leaf exceeds ~4 shared tiles per CTA of a cluster run grid-wide instead
-    A.big = (long long)sh.cdim * 4 * std::min(A.tileF / rho, 16384);
+    // rounds whose largest leaf does not stay resident in one cluster's shared memory run grid-wide
+    A.big = (long long)sh.cdim * std::min(A.tileF / rho, 16384);
+#ifdef HDF_NO_MODE_A
+    A.big = 1LL << 40;
+#endif
     {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[2];

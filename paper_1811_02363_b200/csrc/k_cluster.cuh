@@ -182,6 +182,81 @@ HDF_DEV int block_sum_int(int x, int* ired) {
 // Block range of the round's concatenated active points.
 HDF_DEV long long blk_lo(long long T, int b, int G) { return T * b / G; }
 
+// Farthest partner of sample row a (warp-cooperative, R3): the exact fp64 maximum of
+// ||x_a - x_b||^2 over b > a, ties -> lowest b, as the oracle computes it.  Pass 1 finds the row's
+// fp32 maximum M (|d32 - d| <= (rho + 3) u d for fp32 inputs, u = 2^-24); pass 2 re-evaluates in
+// fp64 (the oracle's operation sequence) only the pairs with d32 >= M (1 - 8 (rho + 3) u), which
+// contain every pair whose fp64 value can be the row maximum.  `base(q)` points at sample member q.
+// RHO > 0: compile-time dimension (row point in registers, two candidates in flight per lane).
+template <int RHO, class Base>
+HDF_DEV float pair_d32(const float* xa_r, const float* xb, int rho) {
+    float acc = 0.f;
+    if (RHO > 0) {
+#pragma unroll
+        for (int d = 0; d < (RHO > 0 ? RHO : 1); d++) {
+            const float t = xa_r[d] - xb[d];
+            acc = fmaf(t, t, acc);
+        }
+    } else {
+        for (int d = 0; d < rho; d++) {
+            const float t = xa_r[d] - xb[d];
+            acc = fmaf(t, t, acc);
+        }
+    }
+    return acc;
+}
+
+template <int RHO, class Base>
+HDF_DEV void row_farthest_t(int a, int sN, int rho, Base base, double& best, int& arg) {
+    const int lane = threadIdx.x & 31;
+    constexpr float u = 5.9604644775390625e-08f;
+    constexpr int RR = RHO > 0 ? RHO : 1;
+    float xr[RR];
+    const float* xa = base(a);
+    if (RHO > 0) {
+#pragma unroll
+        for (int d = 0; d < RR; d++) xr[d] = xa[d];
+    }
+    const float* xav = RHO > 0 ? xr : xa;
+    float m = 0.f;
+    int q = a + 1 + lane;
+    for (; q + 32 < sN; q += 64) {
+        const float d1 = pair_d32<RHO, Base>(xav, base(q), rho);
+        const float d2 = pair_d32<RHO, Base>(xav, base(q + 32), rho);
+        m = fmaxf(m, fmaxf(d1, d2));
+    }
+    if (q < sN) m = fmaxf(m, pair_d32<RHO, Base>(xav, base(q), rho));
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float thr = m * (1.0f - 8.0f * (float)(rho + 3) * u);
+    best = -1.0;
+    arg = -1;
+    for (q = a + 1 + lane; q < sN; q += 32) {
+        const float* xb = base(q);
+        if (pair_d32<RHO, Base>(xav, xb, rho) >= thr) {
+            double dd = 0.0;
+            for (int d = 0; d < rho; d++) dd = d2_rn(dd, (double)xa[d], (double)xb[d]);
+            if (dd > best) { best = dd; arg = q; }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+        if (oa >= 0 && (arg < 0 || ob > best || (ob == best && oa < arg))) { best = ob; arg = oa; }
+    }
+}
+
+template <class Base>
+HDF_DEV void row_farthest(int a, int sN, int rho, Base base, double& best, int& arg) {
+    switch (rho) {
+        case 1: row_farthest_t<1>(a, sN, rho, base, best, arg); break;
+        case 2: row_farthest_t<2>(a, sN, rho, base, best, arg); break;
+        case 3: row_farthest_t<3>(a, sN, rho, base, best, arg); break;
+        case 4: row_farthest_t<4>(a, sN, rho, base, best, arg); break;
+        case 6: row_farthest_t<6>(a, sN, rho, base, best, arg); break;
+        default: row_farthest_t<0>(a, sN, rho, base, best, arg); break;
+    }
+}
+
 // ------------------------------------------------------------------------------ plan (block 0) --
 // Commit computed splits in sequential order; select the next batch of slots; lay out the blocks.
 // Block 0 stages the leaf table in shared memory; thread 0 then runs the (serial) logic on it.
@@ -471,22 +546,47 @@ HDF_DEV void sts_u8(unsigned char* p, unsigned v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(smem_u32(p)), "h"((unsigned short)v) : "memory");
 }
 
-HDF_DEV void side_phase(const float* xt, int np, int rho, const Centres2& C2, const unsigned char* prev,
-                        unsigned char* cur, unsigned char* sw, int it, int& n1, int& chg) {
+template <int RHO>
+HDF_DEV void side_phase_t(const float* xt, int np, int rho_rt, const Centres2& C2, const unsigned char* prev,
+                          unsigned char* cur, unsigned char* sw, int it, int& n1, int& chg) {
     constexpr int U = 4;
     constexpr float u = 5.9604644775390625e-08f;   // 2^-24
+    const int rho = RHO > 0 ? RHO : rho_rt;
     const float kc = 2.0f * u * 6.1f * (C2.n0 + C2.n1);
     const float kd = 2.0f * u * (float)(rho + 7);
+    constexpr int RR = RHO > 0 ? RHO : 1;
+    float g0r[RR], g1r[RR];
+    if (RHO > 0) {
+#pragma unroll
+        for (int d = 0; d < RR; d++) { g0r[d] = lds_f(C2.f0 + d); g1r[d] = lds_f(C2.f1 + d); }
+    }
     for (int t0 = threadIdx.x; t0 < np; t0 += U * kClThreads) {
         float a0[U], a1[U];
 #pragma unroll
         for (int q = 0; q < U; q++) { a0[q] = 0.f; a1[q] = 0.f; }
-        for (int d = 0; d < rho; d++) {
-            const float g0 = lds_f(C2.f0 + d), g1 = lds_f(C2.f1 + d);
+        if (RHO > 0) {
+            float xv[U][RR];
 #pragma unroll
             for (int q = 0; q < U; q++) {
-                const int t = t0 + q * kClThreads;
-                if (t < np) {
+                const int t = min(t0 + q * kClThreads, np - 1);
+#pragma unroll
+                for (int d = 0; d < RR; d++) xv[q][d] = lds_f(xt + (size_t)t * RR + d);
+            }
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+#pragma unroll
+                for (int d = 0; d < RR; d++) {
+                    const float e0 = xv[q][d] - g0r[d], e1 = xv[q][d] - g1r[d];
+                    a0[q] = fmaf(e0, e0, a0[q]);
+                    a1[q] = fmaf(e1, e1, a1[q]);
+                }
+            }
+        } else {
+            for (int d = 0; d < rho; d++) {
+                const float g0 = lds_f(C2.f0 + d), g1 = lds_f(C2.f1 + d);
+#pragma unroll
+                for (int q = 0; q < U; q++) {
+                    const int t = min(t0 + q * kClThreads, np - 1);
                     const float x = lds_f(xt + (size_t)t * rho + d);
                     const float e0 = x - g0, e1 = x - g1;
                     a0[q] = fmaf(e0, e0, a0[q]);
@@ -519,6 +619,18 @@ HDF_DEV void side_phase(const float* xt, int np, int rho, const Centres2& C2, co
                 n1 += sd;
             }
         }
+    }
+}
+
+HDF_DEV void side_phase(const float* xt, int np, int rho, const Centres2& C2, const unsigned char* prev,
+                        unsigned char* cur, unsigned char* sw, int it, int& n1, int& chg) {
+    switch (rho) {
+        case 1: side_phase_t<1>(xt, np, rho, C2, prev, cur, sw, it, n1, chg); break;
+        case 2: side_phase_t<2>(xt, np, rho, C2, prev, cur, sw, it, n1, chg); break;
+        case 3: side_phase_t<3>(xt, np, rho, C2, prev, cur, sw, it, n1, chg); break;
+        case 4: side_phase_t<4>(xt, np, rho, C2, prev, cur, sw, it, n1, chg); break;
+        case 6: side_phase_t<6>(xt, np, rho, C2, prev, cur, sw, it, n1, chg); break;
+        default: side_phase_t<0>(xt, np, rho, C2, prev, cur, sw, it, n1, chg); break;
     }
 }
 
@@ -926,20 +1038,13 @@ HDF_DEV void cl_split_cluster(const ClusterArgs& A, const SSlot& S, int leaf, in
         double bv = -1.0;
         long long ba = -1, bb = -1;
         for (int ra = r + C * warp; ra < sN; ra += C * kClWarps) {   // rows ascending within the warp
-            const float* xa = insm ? tp + (size_t)ra * rho : P + (gbase + (long long)ra * stride) * rho;
-            double best = -1.0;
-            int arg = -1;
-            for (int q = ra + 1 + lane; q < sN; q += 32) {
-                const float* xb = insm ? tp + (size_t)q * rho : P + (gbase + (long long)q * stride) * rho;
-                double dd = 0.0;
-                for (int d = 0; d < rho; d++) dd = d2_rn(dd, (double)xa[d], (double)xb[d]);
-                if (dd > best) { best = dd; arg = q; }
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-                if (oa >= 0 && (arg < 0 || ob > best || (ob == best && oa < arg))) { best = ob; arg = oa; }
-            }
+            double best;
+            int arg;
+            const float* tpc = tp;
+            if (insm)
+                row_farthest(ra, sN, rho, [&](int q) { return tpc + (size_t)q * rho; }, best, arg);
+            else
+                row_farthest(ra, sN, rho, [&](int q) { return P + (gbase + (long long)q * stride) * rho; }, best, arg);
             if (arg >= 0 && (ba < 0 || best > bv)) { bv = best; ba = ra; bb = arg; }
         }
         if (lane == 0) {
@@ -1323,6 +1428,7 @@ __global__ void __launch_bounds__(kClThreads) k_bisect_kmeans(const ClusterArgs 
             continue;
         }
 
+#ifndef HDF_NO_MODE_A
         // ---------------- farthest pair rows (R3) ----------------
         // Work items (slot, c): rows a = c, c + kFpItems, ... of the slot's stride sample, so every
         // item holds about the same number of pairs.  The block stages the slot's sample into the
@@ -1356,20 +1462,14 @@ __global__ void __launch_bounds__(kClThreads) k_bisect_kmeans(const ClusterArgs 
                     staged = sl;
                 }
                 for (int a = c + kFpItems * warp; a < s; a += kFpItems * kClWarps) {
-                    const float* xa = insm ? tp + (size_t)a * rho : P + (size_t)(start + (long long)a * stride) * rho;
-                    double best = -1.0;
-                    int arg = -1;
-                    for (int bb = a + 1 + lane; bb < s; bb += 32) {
-                        const float* xb = insm ? tp + (size_t)bb * rho : P + (size_t)(start + (long long)bb * stride) * rho;
-                        double dd = 0.0;
-                        for (int d = 0; d < rho; d++) dd = d2_rn(dd, (double)xa[d], (double)xb[d]);
-                        if (dd > best) { best = dd; arg = bb; }
-                    }
-                    for (int o = 16; o > 0; o >>= 1) {
-                        double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                        int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-                        if (oa >= 0 && (arg < 0 || ob > best || (ob == best && oa < arg))) { best = ob; arg = oa; }
-                    }
+                    double best;
+                    int arg;
+                    const float* tpc = tp;
+                    if (insm)
+                        row_farthest(a, s, rho, [&](int q) { return tpc + (size_t)q * rho; }, best, arg);
+                    else
+                        row_farthest(a, s, rho, [&](int q) { return P + (size_t)(start + (long long)q * stride) * rho; },
+                                     best, arg);
                     if (lane == 0) {
                         A.fpd[(size_t)sl * kFpCap + a] = best;
                         A.fpi[(size_t)sl * kFpCap + a] = arg;
@@ -1595,6 +1695,7 @@ __global__ void __launch_bounds__(kClThreads) k_bisect_kmeans(const ClusterArgs 
         if (blockIdx.x == 0 && tid == 0) A.ctrl[C_ITERS] = ldi(&A.ctrl[C_ITERS]) + it + 1;
         gsync();
         tick(T_PART);
+#endif
     }
 
     // ---------------- outputs ----------------
