@@ -66,26 +66,19 @@ const char *hdf_last_error(void);
  * with bisecting K-means: repeatedly split the leaf of largest SSE (R2) by 2-means seeded with the
  * farthest pair of a stride sample of <= 1024 members (R3), Lloyd iterations until no assignment
  * changes or 50 iterations (R4).  mu_k = centroid of C_k.  Runs as one persistent
- * cooperative kernel; independent leaf splits run concurrently (results identical to the
- * sequential procedure).  Up to 32 splits are computed per round.
+ * cooperative kernel that expands the tree of splits best-first in parallel (thread-block clusters
+ * as workers); the result is the sequential procedure's.
  * ------------------------------------------------------------------------------------------- */
 typedef struct {
-    int32_t status;        /* HDF_OK or HDF_ERR_K                                              */
-    int32_t achievable_k;  /* leaves reached; the number of distinct guide vectors on HDF_ERR_K  */
-    int32_t rounds;        /* concurrent split rounds executed                                 */
-    int32_t lloyd_iters;   /* lock-step Lloyd iterations executed (all rounds)                 */
-    double e_k;            /* clustering error E_K = sum_k sum_{p(i) in C_k} ||p(i)-mu_k||^2     */
-    double t_plan_us;      /* diagnostics: device time per phase (globaltimer, block 0)        */
-    double t_seed_us;      /*   farthest-pair seeding                                            */
-    double t_lloyd_us;     /*   lock-step Lloyd iterations                                       */
-    double t_part_us;      /*   stable partition + child SSE                                     */
-    double t_sync_us;      /*   waiting in grid barriers (all phases, excluded from the above)   */
-    double t_pass_us;      /*   Lloyd assignment passes (excluded from t_lloyd_us)               */
-    double t_pass_side_us; /*     of which: assignment, sum, block-reduction sub-phases          */
-    double t_pass_sum_us;  /*     (cluster-mode rounds: seeding, Lloyd, partition of block 0's    */
-    double t_pass_red_us;  /*      splits)                                                        */
-    int32_t launch_ctas;   /* CTAs of the cooperative launch                                      */
-    int32_t cluster_ctas;  /* CTAs per thread-block cluster                                       */
+    int32_t status;          /* HDF_OK or HDF_ERR_K                                              */
+    int32_t achievable_k;    /* leaves reached; the number of distinct guide vectors on HDF_ERR_K */
+    int32_t splits_computed; /* 2-means splits computed, including speculative ones not needed   */
+    int32_t lloyd_iters;     /* Lloyd passes executed over all computed splits                   */
+    double e_k;              /* clustering error E_K = sum_k sum_{p(i) in C_k} ||p(i)-mu_k||^2     */
+    int32_t grid_splits;     /* splits computed by the whole grid (nodes larger than a cluster)    */
+    int32_t tile_points;     /* guide vectors a CTA keeps resident in shared memory                */
+    int32_t launch_ctas;     /* CTAs of the cooperative launch                                      */
+    int32_t cluster_ctas;    /* CTAs per thread-block cluster (one worker)                          */
 } hdf_cluster_info;
 
 /* Device workspace (bytes) for hdf_cluster on an H x W guide of dimension rho. */
@@ -177,9 +170,11 @@ typedef enum {
     HDF_NUM_STAGES = 8
 } hdf_stage;
 
-/* Diagnostics: events (tag, globaltimer ns) recorded by block 0 during the last hdf_cluster call
- * that used workspace `ws` with the same H, W, rho, K.  out: host [2 * cap]; returns the number of
- * events copied (synchronous), or -1 on a CUDA error. */
+/* Diagnostics: events recorded by the clustering workers during the last hdf_cluster call that
+ * used workspace `ws` with the same H, W, rho, K: out[2e] = tag | node << 8 | worker << 28 (tags:
+ * 1 claim start, 2 split start, 3 seeds chosen, 4 Lloyd done, 5 children published; worker -1 =
+ * the whole grid), out[2e+1] = globaltimer ns.  out: host [2 * cap]; returns the number of events
+ * copied (synchronous), or -1 on a CUDA error. */
 int hdf_cluster_trace(const float *p_unused, int H, int W, int rho, int K, void *ws, long long *out, int cap);
 
 /* Turn event recording on (on != 0) or off.  Process-wide; returns HDF_OK. */

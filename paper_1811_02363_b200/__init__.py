@@ -44,12 +44,9 @@ class HdfKError(HdfError):
 
 
 class ClusterInfo(C.Structure):
-    _fields_ = [("status", C.c_int32), ("achievable_k", C.c_int32), ("rounds", C.c_int32),
-                ("lloyd_iters", C.c_int32), ("e_k", C.c_double), ("t_plan_us", C.c_double),
-                ("t_seed_us", C.c_double), ("t_lloyd_us", C.c_double), ("t_part_us", C.c_double),
-                ("t_sync_us", C.c_double), ("t_pass_us", C.c_double), ("t_pass_side_us", C.c_double),
-                ("t_pass_sum_us", C.c_double), ("t_pass_red_us", C.c_double), ("launch_ctas", C.c_int32),
-                ("cluster_ctas", C.c_int32)]
+    _fields_ = [("status", C.c_int32), ("achievable_k", C.c_int32), ("splits_computed", C.c_int32),
+                ("lloyd_iters", C.c_int32), ("e_k", C.c_double), ("grid_splits", C.c_int32),
+                ("tile_points", C.c_int32), ("launch_ctas", C.c_int32), ("cluster_ctas", C.c_int32)]
 
 
 _lib = None
@@ -251,8 +248,9 @@ def profile_collect() -> dict:
 
 
 def cluster_trace(p: torch.Tensor, K: int, ws: Workspace | None = None):
-    """Diagnostics: (tag, ns) events of block 0 in the last cluster() call on workspace ws."""
+    """Diagnostics: (tag | node << 8 | worker << 28, globaltimer ns) events of the clustering workers
+    in the last cluster() call on workspace ws (see hdf_cluster_trace in include/hdf.h)."""
     H, W, rho = _hwc(p, "p")
-    buf = (C.c_longlong * (2 * 4096))()
-    n = lib().hdf_cluster_trace(None, H, W, rho, K, (ws or _default_ws).buf.data_ptr(), buf, 4096)
+    buf = (C.c_longlong * (2 * 8192))()
+    n = lib().hdf_cluster_trace(None, H, W, rho, K, (ws or _default_ws).buf.data_ptr(), buf, 8192)
     return [(buf[2 * i], buf[2 * i + 1]) for i in range(max(n, 0))]

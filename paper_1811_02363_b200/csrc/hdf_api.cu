@@ -13,7 +13,7 @@
 #include <vector>
 
 #include "hdf_dispatch.h"
-#include "k_cluster.cuh"
+#include "k_bisect.cuh"
 #include "k_coeffs.cuh"
 
 namespace {
@@ -99,66 +99,67 @@ struct ProfScope {
 };
 
 // ------------------------------------------------------------------------ cluster workspace ----
-struct ClusterPlan {
-    int slotmax, maxrec, pstride;
-};
-ClusterPlan cluster_plan(int rho, int K) {
-    ClusterPlan c;
-    c.slotmax = std::min(K, hdf::kSlotCap);
-    c.maxrec = hdf::kMaxGrid + c.slotmax;
-    c.pstride = 2 * rho + 4;
-    return c;
-}
+// k_bisect (k_bisect.cuh) works in a caller-provided workspace: two ping-pong copies of the guide
+// and its pixel index, grid-mode side words and exchange records, the node table.
+constexpr int kBisectMaxGrid = 256;     // upper bound of the cooperative grid (records, side words)
+constexpr int kBisectMinGrid = 32;      // the launch never uses fewer CTAs (streamed ranges <= N / 32)
+int bisect_maxn(int K) { return 16 * K + 64; }
 
-hdf::ClusterArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho, int K) {
+hdf::BisectArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho, int K) {
     const long long N = (long long)H * W;
-    const ClusterPlan pl = cluster_plan(rho, K);
-    hdf::ClusterArgs A;
+    hdf::BisectArgs A;
     memset(&A, 0, sizeof(A));
     A.p = p;
     A.N = (int)N;
     A.rho = rho;
     A.K = K;
-    A.slotmax = pl.slotmax;
-    A.maxrec = pl.maxrec;
-    A.pstride = pl.pstride;
-    for (int b = 0; b < 2; b++) A.pts[b] = cv.take<float>((size_t)N * rho);
+    A.maxn = bisect_maxn(K);
+    A.wcap = (int)((N + (long long)kBisectMinGrid * 32 - 1) / ((long long)kBisectMinGrid * 32)) + 2;
+    for (int b = 0; b < 2; b++) {
+        A.ptsw[b] = cv.take<float>((size_t)N * rho + 16);
+        A.pts[b] = A.ptsw[b];
+    }
+    A.pts[hdf::kBufInput] = p;
     for (int b = 0; b < 2; b++) A.idx[b] = cv.take<int>((size_t)N);
-    for (int b = 0; b < 2; b++) A.side[b] = cv.take<unsigned char>((size_t)N);
-    A.leaves = cv.take<hdf::CLeaf>(K);
-    A.lmean = cv.take<double>((size_t)K * rho);
-    A.cmean0 = cv.take<double>((size_t)K * rho);
-    A.cmean1 = cv.take<double>((size_t)K * rho);
-    A.slots = cv.take<hdf::CSlot>(pl.slotmax);
-    A.c0g = cv.take<double>((size_t)pl.slotmax * rho);
-    A.c1g = cv.take<double>((size_t)pl.slotmax * rho);
-    for (int b = 0; b < 2; b++) A.rec[b] = cv.take<double>((size_t)pl.maxrec * pl.pstride);
-    A.fpd = cv.take<double>((size_t)pl.slotmax * hdf::kFpCap);
-    A.fpi = cv.take<int>((size_t)pl.slotmax * hdf::kFpCap);
-    A.ctrl = cv.take<int>(hdf::C_NUM);
-    A.timers = cv.take<long long>(hdf::T_NUM);
-    A.trace = cv.take<long long>(1 + 2 * hdf::kTraceCap);
+    A.sidew = cv.take<uint32_t>((size_t)kBisectMaxGrid * 2 * A.wcap);
+    A.rec = cv.take<double>((size_t)2 * kBisectMaxGrid * hdf::kRecV);
+    A.nsse = cv.take<double>(A.maxn);
+    A.nm = cv.take<int>(A.maxn);
+    A.nstart = cv.take<int>(A.maxn);
+    A.nstate = cv.take<int>(A.maxn);
+    A.nparent = cv.take<int>(A.maxn);
+    A.nchild = cv.take<int>(A.maxn);
+    A.nbuf = cv.take<int>(A.maxn);
+    A.nmean = cv.take<double>((size_t)A.maxn * rho);
+    A.nfinal = cv.take<int>(A.maxn);
+    A.node_of = cv.take<int>((size_t)N);
+    A.ctl = cv.take<int>(hdf::B_NUM);
+    A.trace = cv.take<long long>(1 + 2 * hdf::kBisectTraceCap);
     A.ek = cv.take<double>(1);
     return A;
 }
 
-// Dynamic shared memory of k_bisect_kmeans: fixed scratch, then the point tile (tileF floats) and
-// its side bytes (2 per point), which take what is left of the budget (1 CTA per SM; the kernel's
-// static shared memory is ~13 KB of the 227 KB per CTA).
-constexpr size_t kClSmemBudget = 210 * 1024;
-size_t cluster_fixed_smem(int rho, int K) {
-    const ClusterPlan pl = cluster_plan(rho, K);
-    const size_t dbl = (size_t)(2 * hdf::kClThreads + 2 * pl.slotmax * rho + pl.slotmax * pl.pstride + 2 * rho + 16);
-    return sizeof(double) * (dbl + hdf::kRecBuf) + 64;
+// Dynamic shared memory of k_bisect for a tile of `cap` points: the tile (cap * rho + 8 floats),
+// two side-word buffers, the stride sample (rho <= kSampRho).
+size_t bisect_dyn_smem(int rho, int cap) {
+    const size_t x = (((size_t)cap * rho + 8) * 4 + 15) / 16 * 16;
+    const size_t w = 2 * ((size_t)cap / 32 + 2) * 4;
+    const size_t smp = rho <= hdf::kSampRho ? (size_t)hdf::kFpCap * rho * 4 : 0;
+    return x + w + smp;
 }
-int cluster_tile_floats(int rho, int K) {
-    const double avail = (double)kClSmemBudget - (double)cluster_fixed_smem(rho, K);
-    const long long f = (long long)(avail / (4.0 + 2.0 / rho)) & ~3LL;
-    return (int)std::max<long long>(4 * rho, f);
-}
-size_t cluster_smem(int rho, int K) {
-    const int tf = cluster_tile_floats(rho, K);
-    return cluster_fixed_smem(rho, K) + sizeof(float) * tf + 2 * (size_t)std::min(tf / rho, 16384);
+
+using BisectKernel = void (*)(const hdf::BisectArgs);
+BisectKernel bisect_kernel(int rho) {
+    switch (rho) {
+        case 1: return hdf::k_bisect<1>;
+        case 2: return hdf::k_bisect<2>;
+        case 3: return hdf::k_bisect<3>;
+        case 4: return hdf::k_bisect<4>;
+        case 5: return hdf::k_bisect<5>;
+        case 6: return hdf::k_bisect<6>;
+        case 7: return hdf::k_bisect<7>;
+        default: return hdf::k_bisect<0>;
+    }
 }
 
 int check_common(int H, int W, int rho, int K) {
@@ -171,29 +172,51 @@ int check_common(int H, int W, int rho, int K) {
 
 bool misaligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) != 0; }
 
+// Cluster size of the phase-2 workers (HDF_BISECT_CLUSTER=16|8|4|2 overrides; default 16 when the
+// device keeps enough 16-CTA clusters resident, else 8).
+int env_cluster_dim() {
+    const char* e = getenv("HDF_BISECT_CLUSTER");
+    return e ? atoi(e) : 0;
+}
+
 int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres, int32_t* labels,
                    hdf_cluster_info* info, void* ws, cudaStream_t st) {
     Carver cv(ws);
-    hdf::ClusterArgs A = carve_cluster(cv, p, H, W, rho, K);
+    hdf::BisectArgs A = carve_cluster(cv, p, H, W, rho, K);
     A.centres = centres;
     A.labels = labels;
-    A.tileF = cluster_tile_floats(rho, K);
-    // Launch shape: a cooperative grid of thread-block clusters (16 CTAs when the device can keep
-    // enough of them resident, else 8), one CTA per SM.  Cached per (K, rho).
+    BisectKernel kern = bisect_kernel(rho);
+    // Launch shape (cached per rho): one 512-thread CTA per SM with the largest tile that fits, in a
+    // cooperative grid of thread-block clusters.
     struct Shape {
-        int cdim, nclusters;
+        int cdim, nclusters, cap;
+        size_t smem;
     };
     static std::mutex mu;
-    static Shape cache[HDF_MAX_K + 1][HDF_MAX_RHO + 1];
-    const size_t smem = cluster_smem(rho, K);
+    static Shape cache[HDF_MAX_RHO + 1];
     Shape sh;
     {
         std::lock_guard<std::mutex> lk(mu);
-        sh = cache[K][rho];
+        sh = cache[rho];
         if (sh.cdim == 0) {
-            HDF_CUDA(cudaFuncSetAttribute(hdf::k_bisect_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            HDF_CUDA(cudaFuncSetAttribute(hdf::k_bisect_kmeans, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            int dev = 0, optin = 0;
+            HDF_CUDA(cudaGetDevice(&dev));
+            HDF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+            cudaFuncAttributes fa;
+            HDF_CUDA(cudaFuncGetAttributes(&fa, kern));
+            const long long budget = (long long)optin - (long long)fa.sharedSizeBytes - 1024;
+            int cap = 0;
+            for (int c = 512; ; c += 512) {
+                if ((long long)bisect_dyn_smem(rho, c) > budget) break;
+                cap = c;
+            }
+            if (cap == 0) return fail(HDF_ERR_CUDA, "clustering kernel: no shared-memory tile fits");
+            const size_t smem = bisect_dyn_smem(rho, cap);
+            HDF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            HDF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            const int want = env_cluster_dim();
             for (int cdim : {16, 8, 4, 2, 1}) {
+                if (want > 0 && cdim != want) continue;
                 cudaLaunchConfig_t cfg = {};
                 cudaLaunchAttribute at[1];
                 at[0].id = cudaLaunchAttributeClusterDimension;
@@ -201,32 +224,30 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
                 at[0].val.clusterDim.y = 1;
                 at[0].val.clusterDim.z = 1;
                 cfg.gridDim = dim3(cdim);
-                cfg.blockDim = dim3(hdf::kClThreads);
+                cfg.blockDim = dim3(hdf::kBT);
                 cfg.dynamicSmemBytes = smem;
                 cfg.attrs = at;
                 cfg.numAttrs = 1;
                 int ncl = 0;
-                if (cudaOccupancyMaxActiveClusters(&ncl, (void*)hdf::k_bisect_kmeans, &cfg) != cudaSuccess) {
+                if (cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg) != cudaSuccess) {
                     cudaGetLastError();
                     ncl = 0;
                 }
-                ncl = std::min(ncl, hdf::kMaxGrid / cdim);
-                if (ncl * cdim >= 64 || (cdim == 1 && ncl > 0)) {
+                ncl = std::min(ncl, kBisectMaxGrid / cdim);
+                if (ncl * cdim >= std::max(kBisectMinGrid, 96) || (want > 0 && ncl * cdim >= kBisectMinGrid)) {
                     sh.cdim = cdim;
                     sh.nclusters = ncl;
                     break;
                 }
             }
             if (sh.cdim == 0) return fail(HDF_ERR_CUDA, "no resident launch shape for the clustering kernel");
-            cache[K][rho] = sh;
+            sh.cap = cap;
+            sh.smem = smem;
+            cache[rho] = sh;
         }
     }
-    HDF_CUDA(cudaFuncSetAttribute(hdf::k_bisect_kmeans, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    // rounds whose largest leaf does not stay resident in one cluster's shared memory run grid-wide
-    A.big = (long long)sh.cdim * std::min(A.tileF / rho, 16384);
-#ifdef HDF_NO_MODE_A
-    A.big = 1LL << 40;
-#endif
+    A.cap = sh.cap;
+    A.ccap = (long long)sh.cdim * sh.cap;
     {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[2];
@@ -237,38 +258,31 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
         at[1].val.clusterDim.y = 1;
         at[1].val.clusterDim.z = 1;
         cfg.gridDim = dim3(sh.cdim * sh.nclusters);
-        cfg.blockDim = dim3(hdf::kClThreads);
-        cfg.dynamicSmemBytes = smem;
+        cfg.blockDim = dim3(hdf::kBT);
+        cfg.dynamicSmemBytes = sh.smem;
         cfg.stream = st;
         cfg.attrs = at;
         cfg.numAttrs = 2;
         ProfScope prof(HDF_STAGE_CLUSTER, st);
-        HDF_CUDA(cudaLaunchKernelEx(&cfg, hdf::k_bisect_kmeans, A));
+        HDF_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
     }
     if (info) {
-        int ctrl[hdf::C_NUM];
+        int ctrl[hdf::B_NUM];
         double ek = 0.0;
-        long long tm[hdf::T_NUM];
-        HDF_CUDA(cudaMemcpyAsync(ctrl, A.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, st));
+        HDF_CUDA(cudaMemcpyAsync(ctrl, A.ctl, sizeof(ctrl), cudaMemcpyDeviceToHost, st));
         HDF_CUDA(cudaMemcpyAsync(&ek, A.ek, sizeof(double), cudaMemcpyDeviceToHost, st));
-        HDF_CUDA(cudaMemcpyAsync(tm, A.timers, sizeof(tm), cudaMemcpyDeviceToHost, st));
         HDF_CUDA(cudaStreamSynchronize(st));
-        info->t_plan_us = tm[hdf::T_PLAN] * 1e-3;
-        info->t_seed_us = tm[hdf::T_SEED] * 1e-3;
-        info->t_lloyd_us = tm[hdf::T_LLOYD] * 1e-3;
-        info->t_part_us = tm[hdf::T_PART] * 1e-3;
-        info->t_sync_us = tm[hdf::T_SYNC] * 1e-3;
-        info->t_pass_us = tm[hdf::T_PASS] * 1e-3;
-        info->t_pass_side_us = tm[hdf::T_P_SIDE] * 1e-3;
-        info->t_pass_sum_us = tm[hdf::T_P_SUM] * 1e-3;
-        info->t_pass_red_us = tm[hdf::T_P_RED] * 1e-3;
+        memset(info, 0, sizeof(*info));
         info->launch_ctas = (int)(sh.cdim * sh.nclusters);
         info->cluster_ctas = sh.cdim;
-        info->status = ctrl[hdf::C_STATUS];
-        info->achievable_k = ctrl[hdf::C_NLEAVES];
-        info->rounds = ctrl[hdf::C_ROUNDS];
-        info->lloyd_iters = ctrl[hdf::C_ITERS];
+        info->status = ctrl[hdf::B_STATUS];
+        info->achievable_k = ctrl[hdf::B_ACH];
+        info->splits_computed = ctrl[hdf::B_SPLITS];
+        info->lloyd_iters = ctrl[hdf::B_ITERS];
+        info->grid_splits = ctrl[hdf::B_GRIDSPLITS];
+        info->tile_points = sh.cap;
         info->e_k = ek;
+        if (info->status == HDF_ERR_CUDA) return fail(HDF_ERR_CUDA, "clustering kernel: internal node-table overflow");
         if (info->status == HDF_ERR_K)
             return fail(HDF_ERR_K, "K=%d exceeds the number of distinct guide vectors (%d)", K, info->achievable_k);
     }
@@ -631,13 +645,13 @@ const char* hdf_last_error(void) { return g_err.c_str(); }
 int hdf_cluster_trace(const float* p_unused, int H, int W, int rho, int K, void* ws, long long* out, int cap) {
     (void)p_unused;
     Carver cv(ws);
-    hdf::ClusterArgs A = carve_cluster(cv, nullptr, H, W, rho, K);
-    long long n = 0;
-    if (cudaMemcpy(&n, A.trace, sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-    n = std::min<long long>(n, cap);
+    hdf::BisectArgs A = carve_cluster(cv, nullptr, H, W, rho, K);
+    int n = 0;
+    if (cudaMemcpy(&n, A.ctl + hdf::B_TRACE_N, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    n = std::min(std::min(n, hdf::kBisectTraceCap), cap);
     if (n > 0 && cudaMemcpy(out, A.trace + 1, sizeof(long long) * 2 * n, cudaMemcpyDeviceToHost) != cudaSuccess)
         return -1;
-    return (int)n;
+    return n;
 }
 
 int hdf_profile_enable(int on) {
