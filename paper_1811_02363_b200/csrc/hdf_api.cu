@@ -103,7 +103,7 @@ struct ProfScope {
 // and its pixel index, grid-mode side words and exchange records, the node table.
 constexpr int kBisectMaxGrid = 256;     // upper bound of the cooperative grid (records, side words)
 constexpr int kBisectMinGrid = 32;      // the launch never uses fewer CTAs (streamed ranges <= N / 32)
-int bisect_maxn(int K) { return 16 * K + 64; }
+int bisect_maxn(int K) { (void)K; return 512; }   // claim scans hold 512 nodes in registers (16 per lane)
 
 hdf::BisectArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho, int K) {
     const long long N = (long long)H * W;
@@ -204,7 +204,7 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
             HDF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
             cudaFuncAttributes fa;
             HDF_CUDA(cudaFuncGetAttributes(&fa, kern));
-            const long long budget = (long long)optin - (long long)fa.sharedSizeBytes - 1024;
+            const long long budget = (long long)optin - (long long)fa.sharedSizeBytes;
             int cap = 0;
             for (int c = 512; ; c += 512) {
                 if ((long long)bisect_dyn_smem(rho, c) > budget) break;
@@ -248,6 +248,11 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
     }
     A.cap = sh.cap;
     A.ccap = (long long)sh.cdim * sh.cap;
+    {   // worker trace (diagnostics, hdf_cluster_trace): off unless HDF_BISECT_TRACE=1
+        const char* e = getenv("HDF_BISECT_TRACE");
+        if (!(e && atoi(e) != 0)) A.trace = nullptr;
+    }
+    if (const char* e = getenv("HDF_BISECT_GRID_ABOVE")) A.ccap = std::min<long long>(A.ccap, atoll(e));
     {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[2];
@@ -282,7 +287,9 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
         info->grid_splits = ctrl[hdf::B_GRIDSPLITS];
         info->tile_points = sh.cap;
         info->e_k = ek;
-        if (info->status == HDF_ERR_CUDA) return fail(HDF_ERR_CUDA, "clustering kernel: internal node-table overflow");
+        if (info->status == HDF_ERR_CUDA)
+            return fail(HDF_ERR_CUDA, "clustering kernel: internal error (abort %d, nodes %d, splits %d, not done %d)",
+                        ctrl[hdf::B_ABORT], ctrl[hdf::B_NALLOC], ctrl[hdf::B_SPLITS], ctrl[hdf::B_NOTDONE]);
         if (info->status == HDF_ERR_K)
             return fail(HDF_ERR_K, "K=%d exceeds the number of distinct guide vectors (%d)", K, info->achievable_k);
     }

@@ -24,9 +24,12 @@
 //   * phase 1 (grid mode): while the best claimable node does not fit one thread-block cluster's
 //     shared memory, the whole cooperative grid splits it (lock-step, grid barriers, points
 //     streamed through shared-memory tiles);
-//   * phase 2 (cluster mode): every thread-block cluster is a worker; a claimed node's members stay
-//     resident in the cluster's shared memory (TMA bulk copies) for the whole split; partial sums
-//     are exchanged through distributed shared memory, one cluster barrier per Lloyd iteration.
+//   * phase 2 (cluster mode): while a claimable node does not fit one CTA's tile, every
+//     thread-block cluster is a worker; a claimed node's members stay resident in the cluster's
+//     shared memory (TMA bulk copies) for the whole split; partial sums are pushed into every peer's
+//     shared memory with st.async and counted by an mbarrier (no cluster barrier per iteration);
+//   * phase 3 (CTA mode): every CTA is a worker on the remaining (small) nodes, no inter-CTA
+//     synchronisation inside a split.
 // Every split writes its children's members as a stable partition of the parent's segment into the
 // other ping-pong buffer (children are sub-segments of the parent's segment).
 // Exactness vs the fp64 oracle: nearer-centre decisions are taken in fp32 with a proven error
@@ -48,12 +51,13 @@ constexpr int kMaxIter = 50;        // Lloyd cap (R4)
 constexpr int kRecV = 2 * HDF_MAX_RHO + 8;   // exchanged record length (doubles)
 constexpr int kSampRho = 8;         // the stride sample is staged in shared memory for rho <= 8
 constexpr int kBisectTraceCap = 8192;
+constexpr int kGB = 384;            // doubles of the shared staging of gathered peer records
 
 // control words
 enum {
-    B_NALLOC = 0,  // node ids allocated
-    B_INPROG,      // claimed splits not yet published
-    B_VERSION,     // number of publications
+    B_INPROG = 0,  // claimed splits not yet published   } one 64-bit word (updated atomically
+    B_VERSION,     // number of publications             } together, read as one snapshot)
+    B_NALLOC,      // node ids allocated
     B_STATUS,      // HDF_OK / HDF_ERR_K / internal error
     B_ACH,         // leaves reached (achievable K)
     B_TASK,        // phase-1 task (node id or -1)
@@ -62,7 +66,8 @@ enum {
     B_ITERS,       // Lloyd passes executed (all splits)
     B_GRIDSPLITS,  // splits computed in grid mode
     B_TRACE_N,     // trace events recorded
-    B_ABORT,       // node table overflow (never expected)
+    B_ABORT,       // internal error: 1 node table overflow, 2 cluster range not resident (never expected)
+    B_NOTDONE,     // diagnostics: split-set nodes without a computed split (never expected)
     B_NUM
 };
 enum { ST_FREE = 0, ST_CLAIMED = 1, ST_DONE = 2, ST_NONE = 3 };
@@ -103,6 +108,21 @@ HDF_DEV int ld_acq(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+HDF_DEV int ld_rlx(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+HDF_DEV void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+HDF_DEV unsigned long long ld_acq64(const int* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// (in progress, version) word at ctl[B_INPROG]: low 32 bits in progress, high 32 bits version
+HDF_DEV unsigned long long* syncword(const int* ctl) {
+    return reinterpret_cast<unsigned long long*>(const_cast<int*>(ctl) + B_INPROG);
+}
 HDF_DEV void st_rel(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -134,7 +154,7 @@ HDF_DEV void trace_ev(const BisectArgs& A, int tag, int node, int worker) {
     if (A.trace == nullptr) return;
     const int s = atomicAdd(&A.ctl[B_TRACE_N], 1);
     if (s < kBisectTraceCap) {
-        A.trace[1 + 2 * s] = (long long)tag | ((long long)(node & 0xFFFFF) << 8) | ((long long)worker << 28);
+        A.trace[1 + 2 * s] = (long long)tag | ((long long)(node & 0xFFFFF) << 8) | ((long long)(worker & 0xFFF) << 28);
         A.trace[2 + 2 * s] = gtimer();
     }
 }
@@ -195,53 +215,250 @@ HDF_DEV int block_exscan(int x, int* wsum, int* total) {
 }
 
 // ------------------------------------------------------------------------------ shared state ---
+constexpr int kPushV = 16;          // values per pushed record (small rho: 2 rho + 2 <= 16)
+constexpr int kMaxC = 16;           // CTAs per cluster
 struct SplitSm {
     double c0[HDF_MAX_RHO], c1[HDF_MAX_RHO];   // centres (fp64, the oracle's values)
     float f0[HDF_MAX_RHO], f1[HDF_MAX_RHO];    // fp32-rounded centres
-    double tot[kRecV];                          // gathered totals
-    double rx[2][kRecV];                        // posted record (cluster mode, read over DSMEM)
+    double tot[kRecV];                          // reduced totals
+    double outv[kRecV];                         // this CTA's record of the current exchange
+    union {
+        double rxb[2][kMaxC][kPushV];           // pushed records of the cluster (push exchange)
+        struct {
+            double rx[2][kRecV];                // posted record (pull exchange over DSMEM)
+            double gb[kGB];                     // staged peer records (pull / grid exchanges)
+        };
+    };
     double red[kBW * 16];
     double wv[kBW];
     long long wa[kBW], wb[kBW];
     int wsum[kBW];
     int wp[kBT];                                // word prefix of a tile
+    double tcta[HDF_MAX_RHO];                   // the CTA's total of its members (small rho)
+    float xmax[HDF_MAX_RHO];                    // max |p_d| over the guide (decision bounds)
+    float fpc[HDF_MAX_RHO];                     // farthest-pair pruning: sample centroid
+    float fpr[2];                               //   max squared radius, lower bound of the diameter
+    float wt[HDF_MAX_RHO], mt[HDF_MAX_RHO];     // fp32 c1 - c0, c0 + c1 (linear side test)
+    short fpo[kFpCap];                          // farthest pair: the sample's outer points
     int iv[8];
     long long lv[4];
     uint64_t bar;                               // TMA mbarrier
+    uint64_t xbar[2];                           // push-exchange mbarriers (by parity)
     uint32_t tma_phase;
     int task, cbase;
 };
 
+HDF_DEV uint32_t mapa_u32(uint32_t laddr, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(laddr), "r"(rank));
+    return r;
+}
+HDF_DEV void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+HDF_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.b32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
 // -------------------------------------------------------------------------------- groups ------
-// A split runs on a group of CTAs: one thread-block cluster (records over DSMEM, cluster barrier)
-// or the whole cooperative grid (records in global memory, grid barrier).
+// A split runs on a group of CTAs.  Every exchange: each CTA assembles its record in S.outv[0, nv)
+// (visible to its threads), exchange() makes every CTA's record of parity `par` readable through
+// peer(), and the reductions below combine them in rank order (identical results in every CTA).
+//   GridGrp     the whole cooperative grid: records in global memory, grid barrier;
+//   ClusterGrp  a thread-block cluster, pull: records in shared memory read over DSMEM after a
+//               cluster barrier (any record length);
+//   PushGrp     a thread-block cluster, push: every CTA stores its record into every peer's shared
+//               memory with st.async, completion counted by the receiver's mbarrier (no barrier,
+//               no remote read round trip; records <= kPushV values);
+//   CtaGrp      one CTA.
+struct GridGrp {
+    int rank, size;
+    double* rec;
+    static constexpr bool kGrid = true, kLocal = false;
+    HDF_DEV void sync() { cg::this_grid().sync(); }
+    HDF_DEV void exchange(SplitSm& S, int par, int nv) {
+        double* rp = rec + ((size_t)par * size + rank) * kRecV;
+        for (int v = threadIdx.x; v < nv; v += kBT) rp[v] = S.outv[v];
+        __threadfence();
+        cg::this_grid().sync();
+    }
+    HDF_DEV double peer(SplitSm&, int par, int q, int v) const {
+        return __ldcg(rec + ((size_t)par * size + q) * kRecV + v);
+    }
+    HDF_DEV void send(SplitSm&, int par, int v, double x) { rec[((size_t)par * size + rank) * kRecV + v] = x; }
+    HDF_DEV void wait(SplitSm&, int, int) {
+        __threadfence();
+        cg::this_grid().sync();
+    }
+    HDF_DEV void wait_warp0(SplitSm& S, int par, int nv) { wait(S, par, nv); }
+};
 struct ClusterGrp {
     int rank, size;
-    HDF_DEV void sync() const { cg::this_cluster().sync(); }
-    HDF_DEV double* post(SplitSm& S, int par) const { return S.rx[par]; }
+    static constexpr bool kGrid = false, kLocal = false;
+    HDF_DEV void sync() { cg::this_cluster().sync(); }
+    HDF_DEV void exchange(SplitSm& S, int par, int nv) {
+        for (int v = threadIdx.x; v < nv; v += kBT) S.rx[par][v] = S.outv[v];
+        cg::this_cluster().sync();
+    }
     HDF_DEV double peer(SplitSm& S, int par, int q, int v) const {
         const double* p = cg::this_cluster().map_shared_rank(&S.rx[par][0], q);
         return p[v];
     }
-    static constexpr bool kGrid = false;
+    HDF_DEV void send(SplitSm& S, int par, int v, double x) { S.rx[par][v] = x; }
+    HDF_DEV void wait(SplitSm&, int, int) { cg::this_cluster().sync(); }
+    HDF_DEV void wait_warp0(SplitSm& S, int par, int nv) { wait(S, par, nv); }
 };
-struct GridGrp {
+struct PushGrp {
     int rank, size;
-    double* rec;
-    HDF_DEV void sync() const { cg::this_grid().sync(); }
-    HDF_DEV double* post(SplitSm&, int par) const { return rec + ((size_t)par * size + rank) * kRecV; }
-    HDF_DEV double peer(SplitSm&, int par, int q, int v) const {
-        return __ldcg(rec + ((size_t)par * size + q) * kRecV + v);
+    uint32_t ph;   // phase bits of S.xbar[0..1] (every thread keeps its own copy)
+    static constexpr bool kGrid = false, kLocal = true;
+    HDF_DEV void sync() { cg::this_cluster().sync(); }
+    HDF_DEV void exchange(SplitSm& S, int par, int nv) {
+        const int tid = threadIdx.x;
+        if (tid == 0) mbar_arrive_expect_tx(&S.xbar[par], (uint32_t)(size * nv * 8));
+        for (int t = tid; t < size * nv; t += kBT) {
+            const int q = t / nv, v = t - q * nv;
+            st_async_f64(mapa_u32(smem_u32(&S.rxb[par][rank][v]), q), S.outv[v], mapa_u32(smem_u32(&S.xbar[par]), q));
+        }
+        mbar_wait_cluster(&S.xbar[par], (ph >> par) & 1u);
+        ph ^= 1u << par;
     }
-    static constexpr bool kGrid = true;
+    HDF_DEV double peer(SplitSm& S, int par, int q, int v) const { return S.rxb[par][q][v]; }
+    // push one value of this CTA's record to every CTA of the cluster (itself included)
+    HDF_DEV void send(SplitSm& S, int par, int v, double x) {
+        const uint32_t la = smem_u32(&S.rxb[par][rank][v]), lb = smem_u32(&S.xbar[par]);
+        for (int q = 0; q < size; q++) st_async_f64(mapa_u32(la, q), x, mapa_u32(lb, q));
+    }
+    HDF_DEV void wait(SplitSm& S, int par, int nv) {
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(&S.xbar[par], (uint32_t)(size * nv * 8));
+        mbar_wait_cluster(&S.xbar[par], (ph >> par) & 1u);
+        ph ^= 1u << par;
+    }
+    // only warp 0 waits (the other warps keep their phase bits in step)
+    HDF_DEV void wait_warp0(SplitSm& S, int par, int nv) {
+        if (threadIdx.x < 32) {
+            if (threadIdx.x == 0) mbar_arrive_expect_tx(&S.xbar[par], (uint32_t)(size * nv * 8));
+            mbar_wait_cluster(&S.xbar[par], (ph >> par) & 1u);
+        }
+        ph ^= 1u << par;
+    }
+};
+struct CtaGrp {
+    int rank = 0, size = 1;
+    static constexpr bool kGrid = false, kLocal = true;
+    HDF_DEV void sync() { __syncthreads(); }
+    HDF_DEV void exchange(SplitSm&, int, int) { __syncthreads(); }
+    HDF_DEV double peer(SplitSm& S, int, int, int v) const { return S.outv[v]; }
+    HDF_DEV void send(SplitSm& S, int, int v, double x) { S.outv[v] = x; }
+    HDF_DEV void wait(SplitSm&, int, int) { __syncthreads(); }
+    HDF_DEV void wait_warp0(SplitSm&, int, int) { __syncwarp(); }
 };
 
-// Sum record value v over the group's CTAs in rank order.
+// out[v] = sum over the group's CTAs (rank order) of record value v, v < nv; pre[v] (optional) =
+// the same sum over ranks below this CTA's.  Remote records are first staged in shared memory in
+// chunks with every load in flight at once (one DSMEM / L2 round trip per chunk).  Block-wide;
+// out/pre are shared and valid on return.
 template <class Grp>
-HDF_DEV double gather_sum(const Grp& g, SplitSm& S, int par, int v) {
-    double s = 0.0;
-    for (int q = 0; q < g.size; q++) s += g.peer(S, par, q, v);
-    return s;
+HDF_DEV void group_sum(const Grp& g, SplitSm& S, int par, int nv, double* out, double* pre) {
+    const int tid = threadIdx.x;
+    double acc = 0.0, pacc = 0.0;
+    if (Grp::kLocal) {
+        if (tid < nv) {
+            for (int q = 0; q < g.size; q++) {
+                const double x = g.peer(S, par, q, tid);
+                acc += x;
+                if (q < g.rank) pacc += x;
+            }
+        }
+    } else {
+        const int qc = max(1, kGB / nv);
+        for (int q0 = 0; q0 < g.size; q0 += qc) {
+            const int nq = min(qc, g.size - q0);
+            for (int f = tid; f < nq * nv; f += kBT) {
+                const int q = f / nv, v = f - q * nv;
+                S.gb[f] = g.peer(S, par, q0 + q, v);
+            }
+            __syncthreads();
+            if (tid < nv) {
+                for (int q = 0; q < nq; q++) {
+                    const double x = S.gb[q * nv + tid];
+                    acc += x;
+                    if (q0 + q < g.rank) pacc += x;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (tid < nv) {
+        out[tid] = acc;
+        if (pre) pre[tid] = pacc;
+    }
+    __syncthreads();
+}
+// Sum over the group's CTAs (rank order) of record value v, by the calling thread, for groups whose
+// records are local (all loads issued back to back).
+template <class Grp>
+HDF_DEV double local_sum(const Grp& g, SplitSm& S, int par, int v) {
+    double x[kMaxC];
+#pragma unroll
+    for (int q = 0; q < kMaxC; q++) x[q] = (q < g.size) ? g.peer(S, par, q, v) : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kMaxC; q++)
+        if (q < g.size) acc += x[q];
+    return acc;
+}
+// Best (value desc, a asc) candidate over the group's records (fields 0 = value, 1 = a, 2 = b).
+// Returns it in S.lv[0], S.lv[1] (a, b); shared, valid on return.
+template <class Grp>
+HDF_DEV void group_argmax(const Grp& g, SplitSm& S, int par) {
+    const int tid = threadIdx.x;
+    constexpr int qc = kGB / 3;
+    double bvv = -1.0;
+    long long ia = -1, ib = -1;
+    for (int q0 = 0; q0 < g.size; q0 += qc) {
+        const int nq = min(qc, g.size - q0);
+        if (!Grp::kLocal) {
+            for (int f = tid; f < nq * 3; f += kBT) {
+                const int q = f / 3, v = f - q * 3;
+                S.gb[f] = g.peer(S, par, q0 + q, v);
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            for (int q = 0; q < nq; q++) {
+                double qv, fa, fb;
+                if (Grp::kLocal) {
+                    qv = g.peer(S, par, q0 + q, 0);
+                    fa = g.peer(S, par, q0 + q, 1);
+                    fb = g.peer(S, par, q0 + q, 2);
+                } else {
+                    qv = S.gb[3 * q];
+                    fa = S.gb[3 * q + 1];
+                    fb = S.gb[3 * q + 2];
+                }
+                const long long qa = (long long)fa, qb = (long long)fb;
+                if (cand_better(qv, qa, bvv, ia)) { bvv = qv; ia = qa; ib = qb; }
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        S.lv[0] = ia;
+        S.lv[1] = ib;
+    }
+    __syncthreads();
 }
 
 // ------------------------------------------------------------------------------- tile loads ---
@@ -314,9 +531,13 @@ HDF_DEV float pair_d32(const float* xa, const float* xb, int rho) {
 
 template <int RHO, class Base>
 HDF_DEV void row_farthest(int a, int sN, int rho, Base base, double& best, int& arg) {
+    // One pass: a lane keeps its running fp32 maximum M_l and re-evaluates in fp64 every pair whose
+    // d32 >= M_l (1 - 8 (rho + 3) u) at the time it is seen -- a superset of the pairs that can be
+    // the lane's fp64 maximum, whose fp64 maximum is therefore exact.
     const int lane = threadIdx.x & 31;
     constexpr float u = 5.9604644775390625e-08f;
     constexpr int RR = RHO > 0 ? RHO : 1;
+    const float shrink = 1.0f - 8.0f * (float)(rho + 3) * u;
     float xr[RR];
     const float* xa = base(a);
     if (RHO > 0) {
@@ -324,21 +545,14 @@ HDF_DEV void row_farthest(int a, int sN, int rho, Base base, double& best, int& 
         for (int d = 0; d < RR; d++) xr[d] = xa[d];
     }
     const float* xav = RHO > 0 ? xr : xa;
-    float mx = 0.f;
-    int q = a + 1 + lane;
-    for (; q + 32 < sN; q += 64) {
-        const float d1 = pair_d32<RHO, Base>(xav, base(q), rho);
-        const float d2 = pair_d32<RHO, Base>(xav, base(q + 32), rho);
-        mx = fmaxf(mx, fmaxf(d1, d2));
-    }
-    if (q < sN) mx = fmaxf(mx, pair_d32<RHO, Base>(xav, base(q), rho));
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float thr = mx * (1.0f - 8.0f * (float)(rho + 3) * u);
+    float mx = -1.0f;
     best = -1.0;
     arg = -1;
-    for (q = a + 1 + lane; q < sN; q += 32) {
+    for (int q = a + 1 + lane; q < sN; q += 32) {
         const float* xb = base(q);
-        if (pair_d32<RHO, Base>(xav, xb, rho) >= thr) {
+        const float d32 = pair_d32<RHO, Base>(xav, xb, rho);
+        if (d32 >= mx * shrink) {
+            mx = fmaxf(mx, d32);
             double dd = 0.0;
             for (int d = 0; d < rho; d++) dd = d2_rn(dd, (double)xa[d], (double)xb[d]);
             if (dd > best) { best = dd; arg = q; }
@@ -384,43 +598,116 @@ HDF_DEV void cert_consts(const SplitSm& S, int rho, float& kd, float& kc) {
     kc = 2.0f * u * 6.1f * (n0 + n1);
 }
 
-// Small rho (compile-time): thread per point, fp64 per-side sums in registers.  Tile points
-// j = j0 + tid; word j/32 of the tile holds the sides of 32 consecutive points (bit = lane).
+// Small rho (compile-time): the side is decided from the linear form
+//   D = ||x - c0||^2 - ||x - c1||^2 = sum_d w_d (2 x_d - m_d),  w = c1 - c0,  m = c0 + c1,
+// evaluated in fp32 with w, m rounded to fp32 (2 FMAs per dimension).  Error bound, u = 2^-24,
+// X_d = max |p_d| over the guide (S.xmax):
+//   |D~ - D| <= u sum_d |w~_d| ((4.05 + 2.02 rho) X_d + (3.05 + 1.01 rho) |m~_d|)     (rounding of w, m,
+//   2x - m, products and the FMA chain), doubled for safety, plus the fp64 error of the oracle's own
+//   distances 2^-51 (rho + 2) sum_d (X_d + |m~_d| + |w~_d|)^2.  |D~| above the bound decides the side
+//   exactly as the oracle does (d0 <= d1 -> side 0); otherwise the oracle's fp64 sequence decides.
+// Thread per point, two points per thread per step (points j0 + tid and j0 + kBT + tid).  Word j/32
+// of the tile holds the sides of 32 consecutive points (bit = lane).  Per thread: fp64 sums of the
+// side-1 points s1 (DFMA with a 0/1 factor) and, when TOT, of all points (the CTA's total T; side-0
+// sums are T - s1).  The side-1 and change counts come from the ballots (lane 0's copy is reduced).
 template <int RHO>
-HDF_DEV void pass_small(const float* X, int tn, const uint32_t* prevW, uint32_t* curW, bool cmp, const SplitSm& S,
-                        double (&s)[2 * RHO], int& n1, int& chg) {
+HDF_DEV void lin_consts(const SplitSm& S, float (&wt)[RHO], float (&mt)[RHO], float& bound) {
+    constexpr float u = 5.9604644775390625e-08f;
+    float b1 = 0.f, b2 = 0.f;
+#pragma unroll
+    for (int d = 0; d < RHO; d++) {
+        wt[d] = S.wt[d];
+        mt[d] = S.mt[d];
+        const float aw = fabsf(wt[d]), am = fabsf(mt[d]), X = S.xmax[d];
+        b1 = fmaf(aw, (4.05f + 2.02f * RHO) * X + (3.05f + 1.01f * RHO) * am, b1);
+        b2 = fmaf(X + am + aw, X + am + aw, b2);
+    }
+    bound = (2.0f * u * b1 + 4.5e-16f * (RHO + 2) * b2) * 1.001f;   // fp32 evaluation margin
+}
+// fp32 w = c1 - c0, m = c0 + c1 of the current centres (threads d < rho; callers synchronise)
+HDF_DEV void set_lin(SplitSm& S, int rho) {
+    for (int d = threadIdx.x; d < rho; d += kBT) {
+        S.wt[d] = (float)(S.c1[d] - S.c0[d]);
+        S.mt[d] = (float)(S.c0[d] + S.c1[d]);
+    }
+}
+
+template <int RHO, bool TOT>
+HDF_DEV void pass_small(const float* X, int tn, const uint32_t* prevW, uint32_t* curW, bool cmp, bool full,
+                        const SplitSm& S, double (&s1)[RHO], double (&st)[RHO], int& n1, int& chg) {
+    // Incremental side-1 sums: s1 persists across the Lloyd iterations; a pass adds the points that
+    // moved to side 1 and subtracts those that left it (full: s1 starts from 0 and every side-1 point
+    // is added).  After the first iterations few points move, so the fp64 work nearly vanishes.
+    // U points per thread per step (points j0 + h kBT + tid) for instruction-level parallelism.
+    constexpr int U = 4;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    float f0[RHO], f1[RHO];
+    float wt[RHO], mt[RHO], bound;
+    lin_consts<RHO>(S, wt, mt, bound);
+    for (int j0 = 0; j0 < tn; j0 += U * kBT) {
+        float x[U][RHO];
+        bool sd[U], cert[U];
+        uint32_t pw[U];
+        bool allc = true;
 #pragma unroll
-    for (int d = 0; d < RHO; d++) { f0[d] = S.f0[d]; f1[d] = S.f1[d]; }
-    float kd, kc;
-    cert_consts(S, RHO, kd, kc);
-#pragma unroll 2
-    for (int j0 = 0; j0 < tn; j0 += kBT) {
-        const int j = j0 + tid;
-        const bool ok = j < tn;
-        float x[RHO];
-        float a0 = 0.f, a1 = 0.f;
+        for (int h = 0; h < U; h++) {
+            const int wi = (j0 >> 5) + h * kBW + warp;
+            const bool has = j0 + h * kBT < tn;   // uniform
+            pw[h] = (cmp && has) ? prevW[wi] : 0u;
+            const int j = j0 + h * kBT + tid;
+            const bool ok = j < tn;
+            float D = 0.f;
 #pragma unroll
-        for (int d = 0; d < RHO; d++) {
-            x[d] = ok ? lds_f(X + (size_t)j * RHO + d) : 0.f;
-            const float e0 = x[d] - f0[d], e1 = x[d] - f1[d];
-            a0 = fmaf(e0, e0, a0);
-            a1 = fmaf(e1, e1, a1);
+            for (int d = 0; d < RHO; d++) {
+                x[h][d] = ok ? lds_f(X + (size_t)j * RHO + d) : 0.f;
+                D = fmaf(wt[d], fmaf(2.0f, x[h][d], -mt[d]), D);
+            }
+            cert[h] = !ok || fabsf(D) > bound;
+            sd[h] = ok && D > 0.f;
+            allc = allc && cert[h];
         }
-        const int sd = ok ? side_of(x, RHO, a0, a1, kd, kc, S) : 0;
-        const uint32_t w = __ballot_sync(0xffffffffu, sd != 0);
-        if (lane == 0) {
-            const int wi = (j0 >> 5) + warp;
-            if (cmp) chg += __popc(w ^ prevW[wi]);
-            curW[wi] = w;
-        }
-        n1 += sd;
+        if (__ballot_sync(0xffffffffu, !allc)) {   // rare: the oracle's fp64 sequence
 #pragma unroll
-        for (int d = 0; d < RHO; d++) {
-            const double xd = (double)x[d];
-            s[d] += sd ? 0.0 : xd;
-            s[RHO + d] += sd ? xd : 0.0;
+            for (int h = 0; h < U; h++) {
+                if (!cert[h]) {
+                    double dd0 = 0.0, dd1 = 0.0;
+#pragma unroll
+                    for (int d = 0; d < RHO; d++) {
+                        const double v = (double)x[h][d];
+                        dd0 = d2_rn(dd0, v, S.c0[d]);
+                        dd1 = d2_rn(dd1, v, S.c1[d]);
+                    }
+                    sd[h] = !(dd0 <= dd1);
+                }
+            }
+        }
+        uint32_t anym = 0;
+        uint32_t mk[U];
+#pragma unroll
+        for (int h = 0; h < U; h++) {
+            const uint32_t w = __ballot_sync(0xffffffffu, sd[h]);
+            const bool has = j0 + h * kBT < tn;
+            if (lane == 0 && has) curW[(j0 >> 5) + h * kBW + warp] = w;
+            if (cmp) chg += __popc(w ^ pw[h]);
+            n1 += __popc(w);
+            mk[h] = full ? w : (w ^ pw[h]);   // points whose sum term changes
+            anym |= mk[h];
+        }
+        if (anym) {
+#pragma unroll
+            for (int h = 0; h < U; h++) {
+                const double k = ((mk[h] >> lane) & 1u) ? (sd[h] ? 1.0 : -1.0) : 0.0;
+#pragma unroll
+                for (int d = 0; d < RHO; d++) s1[d] = fma(k, (double)x[h][d], s1[d]);
+            }
+        }
+        if (TOT) {
+#pragma unroll
+            for (int d = 0; d < RHO; d++) {
+                double acc = 0.0;
+#pragma unroll
+                for (int h = 0; h < U; h++) acc += (double)x[h][d];
+                st[d] += acc;
+            }
         }
     }
 }
@@ -486,8 +773,7 @@ struct SplitIO {
 };
 
 template <int RHO, class Grp>
-HDF_DEV void split_node(const BisectArgs& A, const Grp& g, SplitSm& S, const SplitIO& io, int v, int cbase,
-                        int worker) {
+HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& io, int v, int cbase, int worker) {
     const int rho = RHO > 0 ? RHO : A.rho;
     const int nv = 2 * rho + 2;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -496,11 +782,11 @@ HDF_DEV void split_node(const BisectArgs& A, const Grp& g, SplitSm& S, const Spl
     const int nbuf = (buf == kBufInput) ? 0 : (buf ^ 1);
     const int a = (int)((long long)m * r / C), e = (int)((long long)m * (r + 1) / C), np = e - a;
     const float* Pg = A.pts[buf] + (size_t)start * rho;   // the node's points
-    const bool resident = (m + C - 1) / C <= A.cap;   // uniform over the group (np <= ceil(m / C))
-    // Phase 1 splits every claimable node larger than a cluster's resident capacity, so a cluster
-    // worker never streams (its range always fits); guard the invariant.
+    const bool resident = (m + C - 1) / C <= A.cap;      // uniform over the group (np <= ceil(m / C))
+    // Grid mode splits every claimable node larger than a cluster's capacity and cluster mode every
+    // node larger than one CTA's, so only grid mode ever streams; guard the invariant.
     if (!Grp::kGrid && !resident) {
-        if (tid == 0) atomicExch(&A.ctl[B_ABORT], 1);
+        if (tid == 0) atomicExch(&A.ctl[B_ABORT], 2);
         return;
     }
     const int wsm = A.cap / 32 + 2;
@@ -540,20 +826,109 @@ HDF_DEV void split_node(const BisectArgs& A, const Grp& g, SplitSm& S, const Spl
             }
         }
         __syncthreads();
+        if (lead) trace_ev(A, 7, v, worker);
     }
     {
+        // Row pruning (exact): for any point c, ||x_a - x_b|| <= ||x_a - c|| + R with R = max_b ||x_b - c||,
+        // so row a cannot hold the maximum when (||x_a - c|| + R)^2 < L, L = a lower bound of the largest
+        // pair distance (here: the farthest partner of the point farthest from c).  fp32 estimates carry
+        // 1e-4 relative margins (their errors are < 1e-5 for rho <= 64); skipped rows hold only pairs
+        // strictly below the maximum, so the argmax and its tie-breaking are unchanged.
+        const float* sp = io.dynS;
+        auto sbase = [&](int q) { return insm ? sp + (size_t)q * rho : Pg + (size_t)q * stride * rho; };
+        for (int d = warp; d < rho; d += kBW) {            // centroid of the sample (fp32, any c works)
+            float acc = 0.f;
+            for (int q = lane; q < sN; q += 32) acc += sbase(q)[d];
+            acc = warp_sum(acc);
+            if (lane == 0) S.fpc[d] = acc / (float)sN;
+        }
+        __syncthreads();
+        float r2m = -1.f;
+        int rmi = 0;
+        for (int q = tid; q < sN; q += kBT) {
+            const float* x = sbase(q);
+            float r2 = 0.f;
+            for (int d = 0; d < rho; d++) {
+                const float t = x[d] - S.fpc[d];
+                r2 = fmaf(t, t, r2);
+            }
+            if (r2 > r2m) { r2m = r2; rmi = q; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const float orr = __shfl_xor_sync(0xffffffffu, r2m, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, rmi, o);
+            if (orr > r2m) { r2m = orr; rmi = oi; }
+        }
+        if (lane == 0) { S.wv[warp] = (double)r2m; S.wa[warp] = rmi; }
+        __syncthreads();
+        if (tid == 0) {
+            double m = -1.0;
+            long long mi = 0;
+            for (int w = 0; w < kBW; w++)
+                if (S.wv[w] > m) { m = S.wv[w]; mi = S.wa[w]; }
+            S.fpr[0] = (float)m;
+            S.iv[0] = (int)mi;
+        }
+        __syncthreads();
+        const float R = sqrtf(S.fpr[0]);
+        {
+            const float* xi = sbase(S.iv[0]);
+            float lm = 0.f;
+            for (int q = tid; q < sN; q += kBT) {
+                const float* x = sbase(q);
+                float d2 = 0.f;
+                for (int d = 0; d < rho; d++) {
+                    const float t = x[d] - xi[d];
+                    d2 = fmaf(t, t, d2);
+                }
+                lm = fmaxf(lm, d2);
+            }
+            for (int o = 16; o > 0; o >>= 1) lm = fmaxf(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+            __syncthreads();
+            if (lane == 0) S.wv[warp] = (double)lm;
+            __syncthreads();
+            if (tid == 0) {
+                double m = 0.0;
+                for (int w = 0; w < kBW; w++) m = fmax(m, S.wv[w]);
+                S.fpr[1] = (float)m;
+            }
+            __syncthreads();
+        }
+        const float lowb = S.fpr[1] * (1.0f - 1e-4f);
+        // The outer points O = {q : (||x_q - c|| + R)^2 >= L}: both ends of any pair reaching L lie in O
+        // (||x_a - x_b|| <= ||x_a - c|| + ||x_b - c|| <= ||x_a - c|| + R).  O in sample order.
+        int nO = 0;
+        for (int q0 = 0; q0 < sN; q0 += kBT) {
+            const int q = q0 + tid;
+            bool in = false;
+            if (q < sN) {
+                const float* x = sbase(q);
+                float r2 = 0.f;
+                for (int d = 0; d < rho; d++) {
+                    const float t = x[d] - S.fpc[d];
+                    r2 = fmaf(t, t, r2);
+                }
+                const float ub = (sqrtf(r2) + R) * (1.0f + 1e-4f);
+                in = ub * ub >= lowb;
+            }
+            int tot;
+            const int pos = block_exscan(in ? 1 : 0, S.wsum, &tot);
+            if (in) S.fpo[nO + pos] = (short)q;
+            nO += tot;
+        }
+        __syncthreads();
         double bv = -1.0;
         long long ba = -1, bb = -1;
-        for (int ra = r + C * warp; ra < sN; ra += C * kBW) {   // rows ascend within the warp
+        for (int ia = r + C * warp; ia < nO; ia += C * kBW) {   // rows ascend within the warp
             double best;
             int arg;
             if (insm) {
-                const float* sp = io.dynS;
-                row_farthest<RHO>(ra, sN, rho, [&](int q) { return sp + (size_t)q * rho; }, best, arg);
+                row_farthest<RHO>(ia, nO, rho, [&](int q) { return sp + (size_t)S.fpo[q] * rho; }, best, arg);
             } else {
-                row_farthest<RHO>(ra, sN, rho, [&](int q) { return Pg + (size_t)q * stride * rho; }, best, arg);
+                row_farthest<RHO>(ia, nO, rho, [&](int q) { return Pg + (size_t)S.fpo[q] * stride * rho; }, best,
+                                  arg);
             }
-            if (arg >= 0 && (ba < 0 || best > bv)) { bv = best; ba = ra; bb = arg; }
+            if (arg >= 0 && (ba < 0 || best > bv)) { bv = best; ba = S.fpo[ia]; bb = S.fpo[arg]; }
         }
         if (lane == 0) { S.wv[warp] = bv; S.wa[warp] = ba; S.wb[warp] = bb; }
         __syncthreads();
@@ -562,27 +937,19 @@ HDF_DEV void split_node(const BisectArgs& A, const Grp& g, SplitSm& S, const Spl
             long long ia = -1, ib = -1;
             for (int w = 0; w < kBW; w++)
                 if (cand_better(S.wv[w], S.wa[w], bvv, ia)) { bvv = S.wv[w]; ia = S.wa[w]; ib = S.wb[w]; }
-            double* rp = g.post(S, par);
-            rp[0] = bvv;
-            rp[1] = (double)ia;
-            rp[2] = (double)ib;
+            S.outv[0] = bvv;
+            S.outv[1] = (double)ia;
+            S.outv[2] = (double)ib;
         }
+        __syncthreads();
     }
-    if (Grp::kGrid) __threadfence();
-    g.sync();
-    if (tid == 0) {
-        double bvv = -1.0;
-        long long ia = -1, ib = -1;
-        for (int q = 0; q < C; q++) {
-            const double qv = g.peer(S, par, q, 0);
-            const long long qa = (long long)g.peer(S, par, q, 1), qb = (long long)g.peer(S, par, q, 2);
-            if (cand_better(qv, qa, bvv, ia)) { bvv = qv; ia = qa; ib = qb; }
-        }
-        if (ia < 0) { ia = 0; ib = (sN > 1) ? 1 : 0; }
-        S.lv[0] = ia;
-        S.lv[1] = ib;
-    }
+    if (lead) trace_ev(A, 8, v, worker);
+    g.exchange(S, par, 3);
+    if (lead) trace_ev(A, 9, v, worker);
+    group_argmax(g, S, par);
     par ^= 1;
+    if (lead) trace_ev(A, 10, v, worker);
+    if (tid == 0 && S.lv[0] < 0) { S.lv[0] = 0; S.lv[1] = (sN > 1) ? 1 : 0; }
     __syncthreads();
     for (int f = tid; f < 2 * rho; f += kBT) {
         const int w = f / rho, d = f - w * rho;
@@ -591,45 +958,129 @@ HDF_DEV void split_node(const BisectArgs& A, const Grp& g, SplitSm& S, const Spl
         (w ? S.c1 : S.c0)[d] = (double)x;
         (w ? S.f1 : S.f0)[d] = x;
     }
+    __syncthreads();
+    set_lin(S, rho);
     const float* X = rt.ptr;
     if (resident) tile_wait(S, rt);
     __syncthreads();
     if (lead) trace_ev(A, 3, v, worker);
 
     // ---- 3. Lloyd iterations (R4) ----
-    int it = 0, fbw = 0;
+    // Record of a pass (per CTA): [0, rho) side-0 sums, [rho, 2 rho) side-1 sums, 2 rho: side-1 count,
+    // 2 rho + 1: changed sides.  Each value v is reduced by thread v and sent straight from it.
+    int it = 0, fbw = 0, fpar = 0;
     bool conv = false;
+    long long tph[4] = {0, 0, 0, 0};   // diagnostics (lead thread): pass, reduce, exchange, update
+    long long tq = lead ? gtimer() : 0;
+    auto tick = [&](int ph) {
+        if (lead && A.trace) {
+            const long long t1 = gtimer();
+            tph[ph] += t1 - tq;
+            tq = t1;
+        }
+    };
+    constexpr int RH = RHO > 0 ? RHO : 1;
+    double s1p[RH], stp[RH];   // small rho: per-thread side-1 sums (persistent) and totals
+#pragma unroll
+    for (int q = 0; q < RH; q++) { s1p[q] = 0.0; stp[q] = 0.0; }
+    long long n1tot = 0, chgtot = 0;
     for (; it < kMaxIter; it++) {
         uint32_t* curW = (it & 1) ? W1 : W0;
         const uint32_t* prevW = (it & 1) ? W0 : W1;
         bool redo = false;
-        long long n1tot = 0, chgtot = 0;
         while (true) {
             int n1 = 0, chg = 0;
-            double* rp = g.post(S, par);
             if (RHO > 0) {
-                double s[2 * (RHO > 0 ? RHO : 1)];
+                const bool full = (it == 0) || redo;
+                const bool tot = (it == 0 && !redo);   // the CTA's total T, once per split
+                if (full) {
 #pragma unroll
-                for (int q = 0; q < 2 * (RHO > 0 ? RHO : 1); q++) s[q] = 0.0;
+                    for (int q = 0; q < RH; q++) s1p[q] = 0.0;
+                }
                 for (int t0 = 0; t0 < np; t0 += A.cap) {
                     const int tn = min(A.cap, np - t0);
                     const float* T = resident ? X : load_tile(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
-                    pass_small<(RHO > 0 ? RHO : 1)>(T, tn, prevW + (t0 >> 5), curW + (t0 >> 5), it > 0, S, s, n1, chg);
+                    if (tot)
+                        pass_small<RH, true>(T, tn, prevW + (t0 >> 5), curW + (t0 >> 5), it > 0, full, S, s1p, stp, n1,
+                                             chg);
+                    else
+                        pass_small<RH, false>(T, tn, prevW + (t0 >> 5), curW + (t0 >> 5), it > 0, full, S, s1p, stp,
+                                              n1, chg);
                 }
+                tick(0);
                 double vv[16];
 #pragma unroll
                 for (int q = 0; q < 16; q++) vv[q] = 0.0;
 #pragma unroll
-                for (int q = 0; q < 2 * (RHO > 0 ? RHO : 1); q++) vv[q] = s[q];
-                vv[2 * rho] = (double)n1;
-                vv[2 * rho + 1] = (double)chg;
+                for (int q = 0; q < RH; q++) { vv[q] = tot ? stp[q] : 0.0; vv[RH + q] = s1p[q]; }
+                vv[2 * RH] = (lane == 0) ? (double)n1 : 0.0;     // ballot counts: lane 0's copy
+                vv[2 * RH + 1] = (lane == 0) ? (double)chg : 0.0;
                 const int vi = warp_reduce_scatter16(vv);
                 if ((lane & 1) == 0) S.red[warp * 16 + vi] = vv[0];
                 __syncthreads();
-                if (tid < nv) {
-                    double acc = 0.0;
-                    for (int w = 0; w < kBW; w++) acc += S.red[w * 16 + tid];
-                    rp[tid] = acc;
+                if (Grp::kLocal) {
+                    // warp 0: the CTA's record, the exchange, the group totals and the new centres
+                    if (warp == 0) {
+                        double x = 0.0;
+                        if (lane < nv) {
+                            double t[kBW], u1[kBW];
+#pragma unroll
+                            for (int w = 0; w < kBW; w++) {
+                                t[w] = S.red[w * 16 + lane];
+                                u1[w] = (lane < RH) ? S.red[w * 16 + RH + lane] : 0.0;
+                            }
+                            double ts = 0.0, us = 0.0;
+#pragma unroll
+                            for (int w = 0; w < kBW; w++) { ts += t[w]; us += u1[w]; }
+                            if (lane < RH) {   // side-0 sums = T - s1 (T of the first pass)
+                                if (tot) S.tcta[lane] = ts;
+                                x = (tot ? ts : S.tcta[lane]) - us;
+                            } else {
+                                x = ts;
+                            }
+                            g.send(S, par, lane, x);
+                        }
+                        tick(1);
+                        g.wait_warp0(S, par, nv);
+                        tick(2);
+                        const double tv = (lane < nv) ? local_sum(g, S, par, lane) : 0.0;
+                        const long long n1t = (long long)__shfl_sync(0xffffffffu, tv, 2 * RH);
+                        const long long cht = (long long)__shfl_sync(0xffffffffu, tv, 2 * RH + 1);
+                        const double t1 = __shfl_sync(0xffffffffu, tv, (RH + lane) & 31);
+                        const bool upd = !(it > 0 && cht == 0) && (redo || !(n1t == 0 || n1t == m));
+                        if (upd && lane < RH) {
+                            const double c0 = tv / (double)(m - n1t), c1 = t1 / (double)n1t;
+                            S.c0[lane] = c0;
+                            S.c1[lane] = c1;
+                            S.f0[lane] = (float)c0;
+                            S.f1[lane] = (float)c1;
+                            S.wt[lane] = (float)(c1 - c0);
+                            S.mt[lane] = (float)(c0 + c1);
+                        }
+                        if (lane == 0) {
+                            S.lv[2] = n1t;
+                            S.lv[3] = cht;
+                        }
+                    } else {
+                        g.wait_warp0(S, par, nv);   // phase bookkeeping only
+                    }
+                    __syncthreads();
+                } else {
+                    if (tid < nv) {
+                        double x = 0.0;
+                        if (tid < RH) {   // side-0 sums = T - s1 (T of the first pass)
+                            double t = 0.0, u1 = 0.0;
+                            for (int w = 0; w < kBW; w++) { t += S.red[w * 16 + tid]; u1 += S.red[w * 16 + RH + tid]; }
+                            if (tot) S.tcta[tid] = t;
+                            x = (tot ? t : S.tcta[tid]) - u1;
+                        } else {
+                            for (int w = 0; w < kBW; w++) x += S.red[w * 16 + tid];
+                        }
+                        g.send(S, par, tid, x);
+                    }
+                    tick(1);
+                    g.wait(S, par, nv);
+                    tick(2);
                 }
             } else {
                 double s0[kGenDims], s1[kGenDims];
@@ -646,7 +1097,7 @@ HDF_DEV void split_node(const BisectArgs& A, const Grp& g, SplitSm& S, const Spl
                 for (int q = 0; q < kGenDims; q++) {
                     const int d = warp + kBW * q;
                     const double x0 = warp_sum(s0[q]), x1 = warp_sum(s1[q]);
-                    if (lane == 0 && d < rho) { rp[d] = x0; rp[rho + d] = x1; }
+                    if (lane == 0 && d < rho) { S.outv[d] = x0; S.outv[rho + d] = x1; }
                 }
                 n1 = __reduce_add_sync(0xffffffffu, n1);
                 chg = __reduce_add_sync(0xffffffffu, chg);
@@ -655,17 +1106,26 @@ HDF_DEV void split_node(const BisectArgs& A, const Grp& g, SplitSm& S, const Spl
                 if (tid < 2) {
                     double acc = 0.0;
                     for (int w = 0; w < kBW; w++) acc += S.red[w * 2 + tid];
-                    rp[2 * rho + tid] = acc;
+                    S.outv[2 * rho + tid] = acc;
                 }
+                __syncthreads();
+                g.exchange(S, par, nv);
             }
-            if (Grp::kGrid) __threadfence();
-            g.sync();
-            // every CTA sums the records in rank order: bit-identical totals in the group
-            if (tid < nv) S.tot[tid] = gather_sum(g, S, par, tid);
+            // totals over the group in rank order (bit-identical in every CTA); n1 and the change count
+            // are read by every thread, the sums by the threads of the centre update below
+            if (Grp::kLocal && RHO > 0) {   // warp 0 has reduced the totals and updated the centres
+                n1tot = S.lv[2];
+                chgtot = S.lv[3];
+            } else if (Grp::kLocal) {
+                n1tot = (long long)local_sum(g, S, par, 2 * rho);
+                chgtot = (long long)local_sum(g, S, par, 2 * rho + 1);
+            } else {
+                group_sum(g, S, par, nv, S.tot, nullptr);
+                n1tot = (long long)S.tot[2 * rho];
+                chgtot = (long long)S.tot[2 * rho + 1];
+            }
+            fpar = par;
             par ^= 1;
-            __syncthreads();
-            n1tot = (long long)S.tot[2 * rho];
-            chgtot = (long long)S.tot[2 * rho + 1];
             if (redo || !(n1tot == 0 || n1tot == m)) break;
             // Empty side: move its centre to the member farthest from the other centre (ties -> first
             // in member order), then redo this iteration's assignment (R4).
@@ -693,102 +1153,77 @@ HDF_DEV void split_node(const BisectArgs& A, const Grp& g, SplitSm& S, const Spl
                 long long ia = -1;
                 for (int w = 0; w < kBW; w++)
                     if (cand_better(S.wv[w], S.wa[w], bvv, ia)) { bvv = S.wv[w]; ia = S.wa[w]; }
-                double* rq = g.post(S, par);
-                rq[0] = bvv;
-                rq[1] = (double)ia;
+                S.outv[0] = bvv;
+                S.outv[1] = (double)ia;
+                S.outv[2] = -1.0;
             }
-            if (Grp::kGrid) __threadfence();
-            g.sync();
-            if (tid == 0) {
-                double bvv = -1.0;
-                long long ia = -1;
-                for (int q = 0; q < C; q++) {
-                    const double qv = g.peer(S, par, q, 0);
-                    const long long qa = (long long)g.peer(S, par, q, 1);
-                    if (cand_better(qv, qa, bvv, ia)) { bvv = qv; ia = qa; }
-                }
-                S.lv[2] = ia < 0 ? 0 : ia;
-            }
-            par ^= 1;
             __syncthreads();
+            g.exchange(S, par, 3);
+            group_argmax(g, S, par);
+            par ^= 1;
+            const long long pick = S.lv[0] < 0 ? 0 : S.lv[0];
             for (int d = tid; d < rho; d += kBT) {
-                const float x = __ldcg(Pg + (size_t)S.lv[2] * rho + d);
+                const float x = __ldcg(Pg + (size_t)pick * rho + d);
                 if (side1_empty) { S.c1[d] = (double)x; S.f1[d] = x; }
                 else { S.c0[d] = (double)x; S.f0[d] = x; }
             }
+            __syncthreads();
+            set_lin(S, rho);
             __syncthreads();
             redo = true;
         }
         fbw = it & 1;
         if (it > 0 && chgtot == 0) { conv = true; break; }   // the final partition is this pass's
+        if (Grp::kLocal && RHO > 0) {                        // centres already updated by warp 0
+            tick(3);
+            continue;
+        }
         for (int d = tid; d < rho; d += kBT) {
-            const double c0 = S.tot[d] / (double)(m - n1tot), c1 = S.tot[rho + d] / (double)n1tot;
+            double t0v, t1v;
+            if (Grp::kLocal) {
+                t0v = local_sum(g, S, fpar, d);
+                t1v = local_sum(g, S, fpar, rho + d);
+            } else {
+                t0v = S.tot[d];
+                t1v = S.tot[rho + d];
+            }
+            const double c0 = t0v / (double)(m - n1tot), c1 = t1v / (double)n1tot;
             S.c0[d] = c0;
             S.c1[d] = c1;
             S.f0[d] = (float)c0;
             S.f1[d] = (float)c1;
+            S.wt[d] = (float)(c1 - c0);
+            S.mt[d] = (float)(c0 + c1);
         }
         __syncthreads();
+        tick(3);
     }
     if (!conv) it = kMaxIter - 1;
-    if (lead) trace_ev(A, 4, v, worker);
+    if (lead) {
+        trace_ev(A, 4, v, worker);
+        trace_ev(A, 6, it + 1, worker);
+        for (int q = 0; q < 4; q++) trace_ev(A, 20 + q, (int)(tph[q] / 100), worker);   // 0.1 us units
+    }
     const uint32_t* FW = fbw ? W1 : W0;
-
-    // ---- 4. child SSE (w.r.t. the child means = current centres) and side-0 counts ----
-    {
-        double se0 = 0.0, se1 = 0.0;
-        int cnt0 = 0;
-        for (int t0 = 0; t0 < np; t0 += A.cap) {
-            const int tn = min(A.cap, np - t0);
-            const float* T = resident ? X : load_tile(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
-            for (int j0 = 0; j0 < tn; j0 += kBT) {
-                const int j = j0 + tid;
-                const uint32_t w = FW[((t0 + j0) >> 5) + warp];
-                if (j < tn) {
-                    const int sd = (w >> lane) & 1u;
-                    const double dd = dist_rn(T + (size_t)j * rho, sd ? S.c1 : S.c0, rho);
-                    if (sd) se1 += dd;
-                    else { se0 += dd; cnt0++; }
-                }
-            }
-        }
-        double vv[16];
-#pragma unroll
-        for (int q = 0; q < 16; q++) vv[q] = 0.0;
-        vv[0] = (double)cnt0;
-        vv[1] = se0;
-        vv[2] = se1;
-        const int vi = warp_reduce_scatter16(vv);
-        if ((lane & 1) == 0) S.red[warp * 16 + vi] = vv[0];
-        __syncthreads();
-        double* rp = g.post(S, par);
-        if (tid < 3) {
-            double acc = 0.0;
-            for (int w = 0; w < kBW; w++) acc += S.red[w * 16 + tid];
-            rp[tid] = acc;
-        }
-        if (Grp::kGrid) __threadfence();
-        g.sync();
-        if (tid < 4) {
-            double acc = 0.0, pre = 0.0;
-            for (int q = 0; q < C; q++) {
-                const double x = g.peer(S, par, q, tid < 3 ? tid : 0);
-                if (q < r) pre += x;
-                acc += x;
-            }
-            S.tot[tid] = (tid == 3) ? pre : acc;   // tot[0] = m0, tot[1] = sse0, tot[2] = sse1, tot[3] = pre0
-        }
-        par ^= 1;
+    // final partition sizes from the last pass's records: side-1 members of lower ranks, total
+    long long pre1l = 0;
+    if (Grp::kLocal) {
+        for (int q = 0; q < r; q++) pre1l += (long long)g.peer(S, fpar, q, 2 * rho);
+    } else {
+        group_sum(g, S, fpar, nv, S.tot, S.outv);   // outv: sums over the lower ranks
+        pre1l = (long long)S.outv[2 * rho];
         __syncthreads();
     }
-    const int m0 = (int)S.tot[0];
-    const int pre0 = (int)S.tot[3], pre1 = a - pre0;
+    const int m0 = m - (int)n1tot;
+    const int pre1 = (int)pre1l, pre0 = a - pre1;
 
-    // ---- 5. stable partition into the other buffer: children are [start, start+m0), [start+m0, start+m) ----
+    // ---- 4. stable partition into the other buffer (children [start, start+m0), [start+m0, start+m)),
+    //         fused with the children's SSE w.r.t. their means (= the final centres) ----
     {
         float* Po = A.ptsw[nbuf] + (size_t)start * rho;
         int* Io = A.idx[nbuf] + start;
         const int* Ii = (buf == kBufInput) ? nullptr : A.idx[buf] + start;
+        double se0 = 0.0, se1 = 0.0;
         int run0 = 0;
         for (int t0 = 0; t0 < np; t0 += A.cap) {
             const int tn = min(A.cap, np - t0);
@@ -808,29 +1243,69 @@ HDF_DEV void split_node(const BisectArgs& A, const Grp& g, SplitSm& S, const Spl
                 S.wp[tid] = zp;
                 __syncthreads();
                 const int jlo = w0 * 32, jhi = min(tn, (w0 + kBT) * 32);
-                for (int j0 = jlo; j0 < jhi; j0 += kBT) {
-                    const int j = j0 + tid;
-                    const int wl = ((j0 - jlo) >> 5) + warp;
-                    const uint32_t w = FW[((t0 + j0) >> 5) + warp];
-                    if (j < jhi) {
-                        const int sd = (w >> lane) & 1u;
-                        const int zb = S.wp[wl] + __popc(~w & ((1u << lane) - 1u));   // side-0 before j in the chunk
-                        const int jj = t0 + j;                                       // CTA-relative index
-                        const int z0 = run0 + zb;                                    // side-0 before jj
-                        const int dst = sd ? (m0 + pre1 + (jj - z0)) : (pre0 + z0);
-                        const float* x = T + (size_t)j * rho;
-                        float* o = Po + (size_t)dst * rho;
-                        for (int d = 0; d < rho; d++) o[d] = lds_f(x + d);
-                        const int pix = Ii ? __ldcg(Ii + a + jj) : (start + a + jj);
-                        Io[dst] = pix;
-                        if (A.labels) A.node_of[pix] = cbase + sd;
+                constexpr int U = 4;   // pixel indices of U points in flight per thread
+                for (int jb = jlo; jb < jhi; jb += U * kBT) {
+                    int pix[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int jj = t0 + jb + u * kBT + tid;
+                        pix[u] = (jb + u * kBT + tid < jhi) ? (Ii ? __ldcg(Ii + a + jj) : (start + a + jj)) : 0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int j0 = jb + u * kBT;
+                        if (j0 >= jhi) break;
+                        const int j = j0 + tid;
+                        const int wl = ((j0 - jlo) >> 5) + warp;
+                        const uint32_t w = FW[((t0 + j0) >> 5) + warp];
+                        if (j < jhi) {
+                            const int sd = (w >> lane) & 1u;
+                            const int zb = S.wp[wl] + __popc(~w & ((1u << lane) - 1u));   // side-0 before j (chunk)
+                            const int jj = t0 + j;                                       // CTA-relative index
+                            const int z0 = run0 + zb;                                    // side-0 before jj
+                            const int dst = sd ? (m0 + pre1 + (jj - z0)) : (pre0 + z0);
+                            const float* x = T + (size_t)j * rho;
+                            float* o = Po + (size_t)dst * rho;
+                            const double* cc = sd ? S.c1 : S.c0;
+                            double dd = 0.0;
+                            for (int d = 0; d < rho; d++) {
+                                const float xv = lds_f(x + d);
+                                o[d] = xv;
+                                dd = d2_rn(dd, (double)xv, cc[d]);
+                            }
+                            if (sd) se1 += dd;
+                            else se0 += dd;
+                            Io[dst] = pix[u];
+                            if (A.labels) A.node_of[pix[u]] = cbase + sd;
+                        }
                     }
                 }
                 run0 += ztot;
                 __syncthreads();
             }
         }
+        // children's SSE over the group
+        double vv[16];
+#pragma unroll
+        for (int q = 0; q < 16; q++) vv[q] = 0.0;
+        vv[0] = se0;
+        vv[1] = se1;
+        const int vi = warp_reduce_scatter16(vv);
+        if ((lane & 1) == 0) S.red[warp * 16 + vi] = vv[0];
+        __syncthreads();
+        if (tid < 2) {
+            double x = 0.0;
+            for (int w = 0; w < kBW; w++) x += S.red[w * 16 + tid];
+            S.outv[tid] = x;
+        }
+        __syncthreads();
+        if (lead) trace_ev(A, 12, v, worker);
+        g.exchange(S, par, 2);
+        group_sum(g, S, par, 2, S.tot + 1, nullptr);   // tot[1] = sse0, tot[2] = sse1
+        par ^= 1;
     }
+
+    if (lead) trace_ev(A, 13, v, worker);
     __threadfence();
     g.sync();   // the whole group's scatter is complete and visible
     // ---- 6. publish the children ----
@@ -861,8 +1336,9 @@ HDF_DEV void split_node(const BisectArgs& A, const Grp& g, SplitSm& S, const Spl
         atomicAdd(&A.ctl[B_SPLITS], 1);
         atomicAdd(&A.ctl[B_ITERS], it + 1);
         if (Grp::kGrid) atomicAdd(&A.ctl[B_GRIDSPLITS], 1);
-        atomicAdd(&A.ctl[B_VERSION], 1);
-        atomicAdd(&A.ctl[B_INPROG], -1);
+        // termination protocol (claim_node): the version bump and the in-progress decrement are one
+        // atomic update of the (in progress, version) word
+        atomicAdd(syncword(A.ctl), (1ULL << 32) - 1ULL);
         trace_ev(A, 5, v, worker);
     }
 }
@@ -870,51 +1346,84 @@ HDF_DEV void split_node(const BisectArgs& A, const Grp& g, SplitSm& S, const Spl
 // ------------------------------------------------------------------------------- the claim ----
 // Warp-cooperative.  Chooses the FREE node of largest SSE (ties -> lowest id) with SSE > 0 and >= 2
 // members, and claims it if fewer than K-1 published nodes precede it in (SSE desc, id asc) order.
-// mode 1 (grid phase): only a node larger than `bigcap` points is claimed, else -1 is returned.
-// mode 2 (cluster phase): when nothing is claimable, waits until a publication changes the table;
-// returns -1 once nothing is claimable and no split is in progress.
+// Only nodes larger than `bigcap` points are considered.  mode 1 (grid phase, a single claimer):
+// returns -1 when nothing is claimable.  mode 2 (cluster / CTA phases): when nothing is claimable,
+// waits until a publication changes the table; returns -1 once nothing is claimable and no split is
+// in progress.
 struct Claim {
     int task, cbase;
 };
-HDF_DEV Claim claim_node(const BisectArgs& A, int mode, long long bigcap) {
+HDF_DEV Claim claim_node(const BisectArgs& A, int mode, long long bigcap, int wid) {
     const int lane = threadIdx.x & 31;
-    int backoff = 32;
+    int backoff = 16;
     while (true) {
         if (ld_acq(&A.ctl[B_ABORT])) return {-1, 0};
         int ver0 = 0, n = 0;
         if (lane == 0) {
-            ver0 = ld_acq(&A.ctl[B_VERSION]);
+            ver0 = (int)(ld_acq64(A.ctl) >> 32);
             n = ld_acq(&A.ctl[B_NALLOC]);
         }
         ver0 = __shfl_sync(0xffffffffu, ver0, 0);
         n = min(__shfl_sync(0xffffffffu, n, 0), A.maxn);
-        double bs = -1.0;
-        int bi = -1;
-        const long long mmin = (mode == 1) ? bigcap + 1 : 2;   // phase 1: only nodes too big for a cluster
-        for (int i = lane; i < n; i += 32) {
-            if (ld_acq(&A.nstate[i]) == ST_FREE) {
-                const double s = __ldcg(&A.nsse[i]);
-                if (s > 0.0 && __ldcg(&A.nm[i]) >= mmin && (bi < 0 || s > bs)) { bs = s; bi = i; }
-            }
+        const long long mmin = max(bigcap + 1, 2LL);
+        // states (relaxed, all in flight), then one acquire fence before the fields they publish
+        constexpr int kScan = 16;
+        int stv[kScan];
+#pragma unroll
+        for (int u = 0; u < kScan; u++) {
+            const int i = lane + 32 * u;
+            stv[u] = (i < n) ? ld_rlx(&A.nstate[i]) : ST_NONE;
         }
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, bs, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (oi >= 0 && (bi < 0 || ob > bs || (ob == bs && oi < bi))) { bs = ob; bi = oi; }
+        fence_acq_rel();
+        double ssev[kScan];
+        unsigned elig = 0;   // FREE, SSE > 0, large enough
+#pragma unroll
+        for (int u = 0; u < kScan; u++) {
+            const int i = lane + 32 * u;
+            ssev[u] = (stv[u] != ST_NONE) ? __ldcg(&A.nsse[i]) : -1.0;
+            if (stv[u] == ST_FREE && ssev[u] > 0.0 && __ldcg(&A.nm[i]) >= mmin) elig |= 1u << u;
         }
-        if (bi >= 0) {
-            int cnt = 0;
-            for (int i = lane; i < n; i += 32) {
-                if (ld_acq(&A.nstate[i]) != ST_NONE) {
-                    const double s = __ldcg(&A.nsse[i]);
-                    cnt += (s > bs || (s == bs && i < bi)) ? 1 : 0;
+        // Candidates in (SSE desc, id asc) order.  Idle workers start at different ranks of that order
+        // (wid modulo the number of candidates, at most 8 deep) so that they do not all race for the
+        // same node; a lost race moves on to the next candidate without rescanning.  A candidate that
+        // fails the rank test ends the walk (every later one fails it too); if candidates were
+        // skipped, the walk is repeated from the top.
+        const int nel0 = __reduce_add_sync(0xffffffffu, __popc(elig));
+        bool lost = false;
+        for (int walk = 0; walk < 2 && nel0 > 0; walk++) {
+            unsigned el = elig;
+            int skip = (walk == 0 && mode != 1) ? (wid % min(nel0, 8)) : 0;
+            const bool skipped = skip > 0;
+            while (true) {
+                double bs = -1.0;
+                int bi = -1;
+#pragma unroll
+                for (int u = 0; u < kScan; u++) {
+                    if ((el >> u) & 1u) {
+                        const int i = lane + 32 * u;
+                        if (bi < 0 || ssev[u] > bs) { bs = ssev[u]; bi = i; }
+                    }
                 }
-            }
-            cnt = __reduce_add_sync(0xffffffffu, cnt);
-            if (cnt < A.K - 1) {
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ob = __shfl_xor_sync(0xffffffffu, bs, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (oi >= 0 && (bi < 0 || ob > bs || (ob == bs && oi < bi))) { bs = ob; bi = oi; }
+                }
+                if (bi < 0) break;
+                if ((bi & 31) == lane) el &= ~(1u << (bi >> 5));   // consumed from the local snapshot
+                if (skip > 0) { skip--; continue; }
+                int cnt = 0;
+#pragma unroll
+                for (int u = 0; u < kScan; u++) {
+                    const int i = lane + 32 * u;
+                    if (stv[u] != ST_NONE) cnt += (ssev[u] > bs || (ssev[u] == bs && i < bi)) ? 1 : 0;
+                }
+                cnt = __reduce_add_sync(0xffffffffu, cnt);
+                if (cnt >= A.K - 1) break;
                 int got = 0, cb = 0;
                 if (lane == 0) {
-                    atomicAdd(&A.ctl[B_INPROG], 1);
+                    atomicAdd(syncword(A.ctl), 1ULL);
+                    __threadfence();   // the in-progress count is visible before the claim is
                     if (atomicCAS(&A.nstate[bi], ST_FREE, ST_CLAIMED) == ST_FREE) {
                         cb = atomicAdd(&A.ctl[B_NALLOC], 2);
                         got = 1;
@@ -923,25 +1432,34 @@ HDF_DEV Claim claim_node(const BisectArgs& A, int mode, long long bigcap) {
                             got = 0;
                         }
                     } else {
-                        atomicAdd(&A.ctl[B_INPROG], -1);
+                        atomicAdd(syncword(A.ctl), ~0ULL);   // in progress - 1 (no borrow: it was incremented)
                     }
                 }
                 got = __shfl_sync(0xffffffffu, got, 0);
                 cb = __shfl_sync(0xffffffffu, cb, 0);
                 if (got) return {bi, cb};
-                continue;
+                lost = true;
             }
+            if (!skipped) break;
         }
         if (mode == 1) return {-1, 0};
+        if (lost) continue;   // lost races: rescan at once
         int done = 0;
         if (lane == 0) {
-            const int ip = ld_acq(&A.ctl[B_INPROG]);
-            const int v1 = ld_acq(&A.ctl[B_VERSION]);
-            done = (ip == 0 && v1 == ver0) ? 1 : 0;
+            const unsigned long long sw = ld_acq64(A.ctl);
+            done = ((unsigned)sw == 0u && (int)(sw >> 32) == ver0) ? 1 : 0;
         }
         if (__shfl_sync(0xffffffffu, done, 0)) return {-1, 0};
-        __nanosleep(backoff);
-        backoff = min(2 * backoff, 512);
+        // wait for the next publication (or for the in-progress count to reach 0) before rescanning
+        if (lane == 0) {
+            for (int spin = 0; spin < 4096; spin++) {
+                const unsigned long long sw = ld_acq64(A.ctl);
+                if ((int)(sw >> 32) != ver0 || (unsigned)sw == 0u || ld_acq(&A.ctl[B_ABORT])) break;
+                __nanosleep(backoff);
+                backoff = min(2 * backoff, 256);
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -1027,6 +1545,7 @@ HDF_DEV void finalise(const BisectArgs& A, unsigned char* dyn) {
         *A.ek = ek;
         int status = (nS < K - 1) ? HDF_ERR_K : HDF_OK;
         if (s_cnt[1] != 0 || __ldcg(&A.ctl[B_ABORT])) status = HDF_ERR_CUDA;
+        A.ctl[B_NOTDONE] = s_cnt[1];
         A.ctl[B_STATUS] = status;
         A.ctl[B_ACH] = ach;
     }
@@ -1051,34 +1570,59 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
 
     if (tid == 0) {
         mbar_init(&S.bar, 1);
+        mbar_init(&S.xbar[0], 1);
+        mbar_init(&S.xbar[1], 1);
         fence_barrier_init();
         S.tma_phase = 0;
+    }
+    cg::this_cluster().sync();   // the exchange mbarriers are initialised before any peer signals them
+    const bool b0 = (blockIdx.x == 0 && tid == 0);
+    if (b0 && A.trace) {   // (the counter is zeroed below; event 0 is written at slot 0 directly)
+        A.trace[1] = 30;
+        A.trace[2] = gtimer();
     }
     // ---- init: node table, root statistics (mean, SSE) in a fixed order ----
     for (long long i = gtid; i < A.maxn; i += gth) A.nstate[i] = ST_NONE;
     if (A.labels)
         for (long long i = gtid; i < A.N; i += gth) A.node_of[i] = 0;
-    if (gtid < B_NUM) A.ctl[gtid] = 0;
+    if (gtid < B_NUM) A.ctl[gtid] = (gtid == B_TRACE_N && A.trace) ? 1 : 0;
     const long long per = ((long long)A.N + G - 1) / G;
     const long long rb0 = min((long long)A.N, (long long)blockIdx.x * per), rb1 = min((long long)A.N, rb0 + per);
     double* rec0 = A.rec;
     double* rec1 = A.rec + (size_t)G * kRecV;
     for (int d0 = 0; d0 < rho; d0 += 8) {
         double acc[16];
+        float mx[8];
 #pragma unroll
         for (int j = 0; j < 16; j++) acc[j] = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) mx[j] = 0.f;
         for (long long t = rb0 + tid; t < rb1; t += kBT) {
 #pragma unroll
             for (int j = 0; j < 8; j++)
-                if (d0 + j < rho) acc[j] += (double)__ldg(A.p + t * rho + d0 + j);
+                if (d0 + j < rho) {
+                    const float x = __ldg(A.p + t * rho + d0 + j);
+                    acc[j] += (double)x;
+                    mx[j] = fmaxf(mx[j], fabsf(x));
+                }
         }
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            for (int o = 16; o > 0; o >>= 1) mx[j] = fmaxf(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], o));
         const int vi = warp_reduce_scatter16(acc);
         if (((tid & 31) & 1) == 0) S.red[(tid >> 5) * 16 + vi] = acc[0];
+        if ((tid & 31) == 0)
+#pragma unroll
+            for (int j = 0; j < 8; j++) S.red[(tid >> 5) * 16 + 8 + j] = (double)mx[j];
         __syncthreads();
         if (tid < 8 && d0 + tid < rho) {
-            double s = 0.0;
-            for (int w = 0; w < kBW; w++) s += S.red[w * 16 + tid];
+            double s = 0.0, m = 0.0;
+            for (int w = 0; w < kBW; w++) {
+                s += S.red[w * 16 + tid];
+                m = fmax(m, S.red[w * 16 + 8 + tid]);
+            }
             rec0[(size_t)blockIdx.x * kRecV + d0 + tid] = s;
+            rec0[(size_t)blockIdx.x * kRecV + HDF_MAX_RHO + d0 + tid] = m;   // max |p_d| of the block
         }
         __syncthreads();
     }
@@ -1092,6 +1636,9 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
         double s = 0.0;
         for (int b = 0; b < G; b++) s += __ldcg(rec0 + (size_t)b * kRecV + d);
         S.c0[d] = s / (double)A.N;
+        float m = 0.f;
+        for (int b = 0; b < G; b++) m = fmaxf(m, (float)__ldcg(rec0 + (size_t)b * kRecV + HDF_MAX_RHO + d));
+        S.xmax[d] = m;
     }
     __syncthreads();
     {
@@ -1126,41 +1673,74 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
     __threadfence();
     grid.sync();
 
+    if (b0) trace_ev(A, 31, 0, 0);
     // ---- phase 1: nodes too large for one cluster, split by the whole grid ----
-    GridGrp gg{(int)blockIdx.x, G, A.rec};
-    while (true) {
-        if (blockIdx.x == 0 && tid < 32) {
-            const Claim c = claim_node(A, 1, A.ccap);
-            if (tid == 0) {
-                A.ctl[B_TASK] = c.task;
-                A.ctl[B_TASKC] = c.cbase;
-                __threadfence();
+    cg::cluster_group cl = cg::this_cluster();
+    const long long ccap = min(A.ccap, (long long)cl.num_blocks() * A.cap);
+    {
+        GridGrp gg{(int)blockIdx.x, G, A.rec};
+        while (true) {
+            if (blockIdx.x == 0 && tid < 32) {
+                const Claim c = claim_node(A, 1, ccap, 0);
+                if (tid == 0) {
+                    A.ctl[B_TASK] = c.task;
+                    A.ctl[B_TASKC] = c.cbase;
+                    __threadfence();
+                }
             }
+            grid.sync();
+            const int task = __ldcg(&A.ctl[B_TASK]);
+            const int cb = __ldcg(&A.ctl[B_TASKC]);
+            if (task < 0) break;
+            split_node<RHO>(A, gg, S, io, task, cb, -1);
+            grid.sync();
         }
-        grid.sync();
-        const int task = __ldcg(&A.ctl[B_TASK]);
-        const int cb = __ldcg(&A.ctl[B_TASKC]);
-        if (task < 0) break;
-        split_node<RHO>(A, gg, S, io, task, cb, -1);
-        grid.sync();
     }
 
-    // ---- phase 2: every thread-block cluster is a worker ----
+    if (b0) trace_ev(A, 32, 0, 0);
+    // ---- phase 2: nodes larger than one CTA's tile; every thread-block cluster is a worker ----
+    if (cl.num_blocks() > 1) {
+        const int worker = blockIdx.x / (int)cl.num_blocks();
+        auto run = [&](auto& g) {
+            while (true) {
+                if (g.rank == 0 && tid < 32) {
+                    if (tid == 0) trace_ev(A, 1, 0, worker);
+                    const Claim c = claim_node(A, 2, A.cap, worker);
+                    if (tid == 0) { S.task = c.task; S.cbase = c.cbase; }
+                }
+                cl.sync();
+                const int task = *cl.map_shared_rank(&S.task, 0);
+                const int cb = *cl.map_shared_rank(&S.cbase, 0);
+                cl.sync();
+                if (task < 0) break;
+                split_node<RHO>(A, g, S, io, task, cb, worker);
+            }
+        };
+        if (RHO > 0) {
+            PushGrp g{(int)cl.block_rank(), (int)cl.num_blocks(), 0u};
+            run(g);
+        } else {
+            ClusterGrp g{(int)cl.block_rank(), (int)cl.num_blocks()};
+            run(g);
+        }
+    }
+    __threadfence();
+    grid.sync();
+
+    if (b0) trace_ev(A, 33, 0, 0);
+    // ---- phase 3: every CTA is a worker ----
     {
-        cg::cluster_group cl = cg::this_cluster();
-        const ClusterGrp g{(int)cl.block_rank(), (int)cl.num_blocks()};
-        const int worker = blockIdx.x / g.size;
+        CtaGrp g;
+        const int worker = 1000 + blockIdx.x;
         while (true) {
-            if (g.rank == 0 && tid < 32) {
+            if (tid < 32) {
                 if (tid == 0) trace_ev(A, 1, 0, worker);
-                const Claim c = claim_node(A, 2, 0);
+                const Claim c = claim_node(A, 2, 0, blockIdx.x);
                 if (tid == 0) { S.task = c.task; S.cbase = c.cbase; }
             }
-            cl.sync();
-            int* rt = cl.map_shared_rank(&S.task, 0);
-            int* rc = cl.map_shared_rank(&S.cbase, 0);
-            const int task = *rt, cb = *rc;
-            cl.sync();
+            __syncthreads();
+            const int task = S.task, cb = S.cbase;
+            __syncthreads();
             if (task < 0) break;
             split_node<RHO>(A, g, S, io, task, cb, worker);
         }
@@ -1168,8 +1748,10 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
     __threadfence();
     grid.sync();
 
-    // ---- phase 3: split set, leaf ids, centres, E_K, labels ----
+    // ---- phase 4: split set, leaf ids, centres, E_K, labels ----
+    if (b0) trace_ev(A, 34, 0, 0);
     if (blockIdx.x == 0) finalise(A, dsm);
+    if (b0) trace_ev(A, 35, 0, 0);
     __threadfence();
     grid.sync();
     if (A.labels) {

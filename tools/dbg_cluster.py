@@ -1,6 +1,6 @@
 """Clustering diagnostics on the GPU: python tools/dbg_cluster.py c1 c2b ...
 Times hdf.cluster, compares with the oracle, and summarises the worker trace (per-node split spans)."""
-import sys, time, numpy as np, torch
+import os, sys, time, numpy as np, torch
 sys.path.insert(0, '.')
 import synth, oracle, paper_1811_02363_b200 as hdf
 _a = torch.randn(8192, 8192, device="cuda")       # warm the clocks up
@@ -10,6 +10,7 @@ torch.cuda.synchronize()
 for name in sys.argv[1:]:
     cfg, f, p = synth.make(name)
     pd = torch.from_numpy(p).cuda()
+    os.environ["HDF_BISECT_TRACE"] = "0"
     ts = []
     for rep in range(5):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -21,21 +22,48 @@ for name in sys.argv[1:]:
     print(f"{name}: K={cfg.K} status {info.status} splits {info.splits_computed} (grid {info.grid_splits}) "
           f"iters {info.lloyd_iters} E_K {info.e_k:.10e} ms {min(ts):.3f} (reps {' '.join('%.3f' % t for t in ts)}) "
           f"grid {info.launch_ctas} cl {info.cluster_ctas} tile {info.tile_points}")
+    os.environ["HDF_BISECT_TRACE"] = "1"
+    hdf.cluster(pd, cfg.K, labels=True)
+    os.environ["HDF_BISECT_TRACE"] = "0"
     tr = hdf.cluster_trace(pd, cfg.K)
     if tr:
         t0 = min(t for _, t in tr)
-        spans = {}
-        for w, t in tr:
-            tag, node, worker = w & 0xFF, (w >> 8) & 0xFFFFF, w >> 28
-            if tag in (2, 3, 4, 5):
-                spans.setdefault(node, {})[tag] = (t - t0) / 1e3
-                spans[node]["w"] = worker
         last = max(t for _, t in tr)
         print(f"   trace: {len(tr)} events, span {(last - t0) / 1e3:.1f} us")
-        for node in sorted(spans, key=lambda n: spans[n].get(2, 0)):
-            s = spans[node]
-            print(f"     node {node:4d} w{s['w']:3d} start {s.get(2, -1):8.1f} seeds +{s.get(3, 0) - s.get(2, 0):6.1f} "
-                  f"lloyd +{s.get(4, 0) - s.get(3, 0):6.1f} part +{s.get(5, 0) - s.get(4, 0):6.1f} end {s.get(5, -1):8.1f}")
+        marks = {30: "start", 31: "root ready", 32: "cluster phase", 33: "CTA phase", 34: "finalise", 35: "done"}
+        print("   timeline: " + "  ".join(f"{marks[w & 0xFF]} {(t - t0) / 1e3:.1f}" for w, t in sorted(tr, key=lambda x: x[1])
+                                         if (w & 0xFF) in marks))
+        # per worker, events in time order; a split = tag 2 .. tag 5 of one node
+        byw = {}
+        for w, t in sorted(tr, key=lambda x: x[1]):
+            byw.setdefault(w >> 28, []).append((w & 0xFF, (w >> 8) & 0xFFFFF, (t - t0) / 1e3))
+        names = {1: "claim", 2: "start", 7: "sample", 8: "rows", 9: "sync", 10: "argmax", 3: "seeds", 4: "lloyd",
+                 11: "sse", 12: "xchg", 13: "scatter", 5: "publ"}
+        rows = []
+        for wk, evs in byw.items():
+            cur = None
+            for tag, node, t in evs:
+                if tag == 2:
+                    cur = {"w": wk, "node": node, "t": {2: t}, "it": 0}
+                    rows.append(cur)
+                elif tag == 6 and cur is not None:
+                    cur["it"] = node
+                elif 20 <= tag < 24 and cur is not None:
+                    cur.setdefault("ph", [0, 0, 0, 0])[tag - 20] = node / 10.0
+                elif cur is not None and tag in names:
+                    cur["t"][tag] = t
+        for rw in sorted(rows, key=lambda r: r["t"][2]):
+            tt = rw["t"]
+            seq = [2, 7, 8, 9, 10, 3, 4, 11, 12, 13, 5]
+            parts = []
+            prev = tt[2]
+            for tag in seq[1:]:
+                if tag in tt:
+                    parts.append(f"{names[tag]}+{tt[tag] - prev:.1f}")
+                    prev = tt[tag]
+            ph = rw.get("ph")
+            phs = f" [pass {ph[0]:.1f} red {ph[1]:.1f} xchg {ph[2]:.1f} upd {ph[3]:.1f}]" if ph else ""
+            print(f"     node {rw['node']:4d} w{rw['w']:4d} it {rw['it']:2d} @{tt[2]:7.1f} " + " ".join(parts) + phs)
     c, l, s, ek = oracle.cluster(p, cfg.K)
     print('   oracle E_K %.10e' % ek, 'max centre diff', np.abs(cen.cpu().numpy() - c).max(),
           'labels eq', (lab.cpu().numpy().reshape(-1) == l).mean(), flush=True)
