@@ -193,11 +193,11 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
         size_t smem;
     };
     static std::mutex mu;
-    static Shape cache[HDF_MAX_RHO + 1];
+    static Shape cache[17][HDF_MAX_RHO + 1];   // by requested cluster size (0 = default) and rho
     Shape sh;
     {
         std::lock_guard<std::mutex> lk(mu);
-        sh = cache[rho];
+        sh = cache[std::min(std::max(env_cluster_dim(), 0), 16)][rho];
         if (sh.cdim == 0) {
             int dev = 0, optin = 0;
             HDF_CUDA(cudaGetDevice(&dev));
@@ -243,7 +243,7 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
             if (sh.cdim == 0) return fail(HDF_ERR_CUDA, "no resident launch shape for the clustering kernel");
             sh.cap = cap;
             sh.smem = smem;
-            cache[rho] = sh;
+            cache[std::min(std::max(env_cluster_dim(), 0), 16)][rho] = sh;
         }
     }
     A.cap = sh.cap;
@@ -253,6 +253,8 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
         if (!(e && atoi(e) != 0)) A.trace = nullptr;
     }
     if (const char* e = getenv("HDF_BISECT_GRID_ABOVE")) A.ccap = std::min<long long>(A.ccap, atoll(e));
+    A.ctamax = std::min<long long>(A.cap, 2048);   // smaller nodes: one CTA each (measured best on c2b)
+    if (const char* e = getenv("HDF_BISECT_CTA_MAX")) A.ctamax = std::min<long long>(A.cap, atoll(e));
     {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[2];

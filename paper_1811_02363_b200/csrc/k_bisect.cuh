@@ -79,6 +79,7 @@ struct BisectArgs {
     int cap;            // points per CTA tile (multiple of kBT)
     int wcap;           // side words per CTA in the global scratch (streamed ranges)
     long long ccap;     // points a cluster keeps resident (C * cap)
+    long long ctamax;   // nodes larger than this go to cluster workers (<= cap)
     const float* pts[3];   // ping-pong leaf storage; pts[2] = p
     float* ptsw[2];
     int* idx[2];
@@ -282,35 +283,70 @@ HDF_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
 //               memory with st.async, completion counted by the receiver's mbarrier (no barrier,
 //               no remote read round trip; records <= kPushV values);
 //   CtaGrp      one CTA.
+enum { XSUM = 0, XARGMAX = 1 };
+// The whole cooperative grid, hierarchically: CTA records are combined inside each thread-block
+// cluster over DSMEM (sums in rank order, or the best candidate), the cluster's first CTA posts the
+// cluster record to global memory, one grid barrier, and every CTA reads the (few) cluster records.
+// Record-level accessors (nrec / rec) therefore see cluster records; the order of every sum is
+// fixed (clusters in order, CTAs in rank order inside a cluster), so all CTAs agree bit for bit.
 struct GridGrp {
-    int rank, size;
-    double* rec;
+    int rank, size;           // CTA rank / count in the grid
+    int crank, csize, cid;    // rank in the cluster, cluster size, cluster index
+    int ncl;                  // clusters in the grid
+    double* rec;              // [2][ncl][kRecV] cluster records
     static constexpr bool kGrid = true, kLocal = false;
     HDF_DEV void sync() { cg::this_grid().sync(); }
-    HDF_DEV void exchange(SplitSm& S, int par, int nv) {
-        double* rp = rec + ((size_t)par * size + rank) * kRecV;
-        for (int v = threadIdx.x; v < nv; v += kBT) rp[v] = S.outv[v];
+    HDF_DEV void exchange(SplitSm& S, int par, int nv, int kind = XSUM) {
+        cg::cluster_group cl = cg::this_cluster();
+        for (int v = threadIdx.x; v < nv; v += kBT) S.rx[par][v] = S.outv[v];
+        cl.sync();
+        if (crank == 0) {
+            double* rp = rec + ((size_t)par * ncl + cid) * kRecV;
+            if (kind == XSUM) {
+                for (int v = threadIdx.x; v < nv; v += kBT) {
+                    double acc = 0.0;
+                    for (int q = 0; q < csize; q++) acc += cl.map_shared_rank(&S.rx[par][0], q)[v];
+                    rp[v] = acc;
+                }
+            } else if (threadIdx.x == 0) {
+                double bvv = -1.0;
+                long long ia = -1, ib = -1;
+                for (int q = 0; q < csize; q++) {
+                    const double* y = cl.map_shared_rank(&S.rx[par][0], q);
+                    const long long qa = (long long)y[1], qb = (long long)y[2];
+                    if (cand_better(y[0], qa, bvv, ia)) { bvv = y[0]; ia = qa; ib = qb; }
+                }
+                rp[0] = bvv;
+                rp[1] = (double)ia;
+                rp[2] = (double)ib;
+            }
+        }
         __threadfence();
         cg::this_grid().sync();
     }
+    HDF_DEV int nrec() const { return ncl; }
     HDF_DEV double peer(SplitSm&, int par, int q, int v) const {
-        return __ldcg(rec + ((size_t)par * size + q) * kRecV + v);
+        return __ldcg(rec + ((size_t)par * ncl + q) * kRecV + v);
     }
-    HDF_DEV void send(SplitSm&, int par, int v, double x) { rec[((size_t)par * size + rank) * kRecV + v] = x; }
-    HDF_DEV void wait(SplitSm&, int, int) {
-        __threadfence();
-        cg::this_grid().sync();
+    // sum of value v over the CTAs of lower grid rank (clusters before this one, then the CTAs of
+    // this cluster before this CTA); the cluster-local records of parity par are still in place
+    HDF_DEV double prefix(SplitSm& S, int par, int v) const {
+        double acc = 0.0;
+        for (int c = 0; c < cid; c++) acc += __ldcg(rec + ((size_t)par * ncl + c) * kRecV + v);
+        cg::cluster_group cl = cg::this_cluster();
+        for (int q = 0; q < crank; q++) acc += cl.map_shared_rank(&S.rx[par][0], q)[v];
+        return acc;
     }
-    HDF_DEV void wait_warp0(SplitSm& S, int par, int nv) { wait(S, par, nv); }
 };
 struct ClusterGrp {
     int rank, size;
     static constexpr bool kGrid = false, kLocal = false;
     HDF_DEV void sync() { cg::this_cluster().sync(); }
-    HDF_DEV void exchange(SplitSm& S, int par, int nv) {
+    HDF_DEV void exchange(SplitSm& S, int par, int nv, int = XSUM) {
         for (int v = threadIdx.x; v < nv; v += kBT) S.rx[par][v] = S.outv[v];
         cg::this_cluster().sync();
     }
+    HDF_DEV int nrec() const { return size; }
     HDF_DEV double peer(SplitSm& S, int par, int q, int v) const {
         const double* p = cg::this_cluster().map_shared_rank(&S.rx[par][0], q);
         return p[v];
@@ -324,7 +360,8 @@ struct PushGrp {
     uint32_t ph;   // phase bits of S.xbar[0..1] (every thread keeps its own copy)
     static constexpr bool kGrid = false, kLocal = true;
     HDF_DEV void sync() { cg::this_cluster().sync(); }
-    HDF_DEV void exchange(SplitSm& S, int par, int nv) {
+    HDF_DEV int nrec() const { return size; }
+    HDF_DEV void exchange(SplitSm& S, int par, int nv, int = XSUM) {
         const int tid = threadIdx.x;
         if (tid == 0) mbar_arrive_expect_tx(&S.xbar[par], (uint32_t)(size * nv * 8));
         for (int t = tid; t < size * nv; t += kBT) {
@@ -358,24 +395,26 @@ struct CtaGrp {
     int rank = 0, size = 1;
     static constexpr bool kGrid = false, kLocal = true;
     HDF_DEV void sync() { __syncthreads(); }
-    HDF_DEV void exchange(SplitSm&, int, int) { __syncthreads(); }
+    HDF_DEV void exchange(SplitSm&, int, int, int = XSUM) { __syncthreads(); }
+    HDF_DEV int nrec() const { return 1; }
     HDF_DEV double peer(SplitSm& S, int, int, int v) const { return S.outv[v]; }
     HDF_DEV void send(SplitSm& S, int, int v, double x) { S.outv[v] = x; }
     HDF_DEV void wait(SplitSm&, int, int) { __syncthreads(); }
     HDF_DEV void wait_warp0(SplitSm&, int, int) { __syncwarp(); }
 };
 
-// out[v] = sum over the group's CTAs (rank order) of record value v, v < nv; pre[v] (optional) =
-// the same sum over ranks below this CTA's.  Remote records are first staged in shared memory in
-// chunks with every load in flight at once (one DSMEM / L2 round trip per chunk).  Block-wide;
-// out/pre are shared and valid on return.
+// out[v] = sum over the group's records (rank order) of value v, v < nv; pre[v] (optional) = the
+// same sum over the CTAs of lower rank than this one.  Remote records are first staged in shared
+// memory in chunks with every load in flight at once (one DSMEM / L2 round trip per chunk).
+// Block-wide; out/pre are shared and valid on return.
 template <class Grp>
 HDF_DEV void group_sum(const Grp& g, SplitSm& S, int par, int nv, double* out, double* pre) {
     const int tid = threadIdx.x;
+    const int nr = g.nrec();
     double acc = 0.0, pacc = 0.0;
     if (Grp::kLocal) {
         if (tid < nv) {
-            for (int q = 0; q < g.size; q++) {
+            for (int q = 0; q < nr; q++) {
                 const double x = g.peer(S, par, q, tid);
                 acc += x;
                 if (q < g.rank) pacc += x;
@@ -383,8 +422,8 @@ HDF_DEV void group_sum(const Grp& g, SplitSm& S, int par, int nv, double* out, d
         }
     } else {
         const int qc = max(1, kGB / nv);
-        for (int q0 = 0; q0 < g.size; q0 += qc) {
-            const int nq = min(qc, g.size - q0);
+        for (int q0 = 0; q0 < nr; q0 += qc) {
+            const int nq = min(qc, nr - q0);
             for (int f = tid; f < nq * nv; f += kBT) {
                 const int q = f / nv, v = f - q * nv;
                 S.gb[f] = g.peer(S, par, q0 + q, v);
@@ -394,10 +433,13 @@ HDF_DEV void group_sum(const Grp& g, SplitSm& S, int par, int nv, double* out, d
                 for (int q = 0; q < nq; q++) {
                     const double x = S.gb[q * nv + tid];
                     acc += x;
-                    if (q0 + q < g.rank) pacc += x;
+                    if (!Grp::kGrid && q0 + q < g.rank) pacc += x;
                 }
             }
             __syncthreads();
+        }
+        if constexpr (Grp::kGrid) {
+            if (pre && tid < nv) pacc = g.prefix(S, par, tid);
         }
     }
     if (tid < nv) {
@@ -406,29 +448,17 @@ HDF_DEV void group_sum(const Grp& g, SplitSm& S, int par, int nv, double* out, d
     }
     __syncthreads();
 }
-// Sum over the group's CTAs (rank order) of record value v, by the calling thread, for groups whose
-// records are local (all loads issued back to back).
-template <class Grp>
-HDF_DEV double local_sum(const Grp& g, SplitSm& S, int par, int v) {
-    double x[kMaxC];
-#pragma unroll
-    for (int q = 0; q < kMaxC; q++) x[q] = (q < g.size) ? g.peer(S, par, q, v) : 0.0;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < kMaxC; q++)
-        if (q < g.size) acc += x[q];
-    return acc;
-}
 // Best (value desc, a asc) candidate over the group's records (fields 0 = value, 1 = a, 2 = b).
 // Returns it in S.lv[0], S.lv[1] (a, b); shared, valid on return.
 template <class Grp>
 HDF_DEV void group_argmax(const Grp& g, SplitSm& S, int par) {
     const int tid = threadIdx.x;
     constexpr int qc = kGB / 3;
+    const int nr = g.nrec();
     double bvv = -1.0;
     long long ia = -1, ib = -1;
-    for (int q0 = 0; q0 < g.size; q0 += qc) {
-        const int nq = min(qc, g.size - q0);
+    for (int q0 = 0; q0 < nr; q0 += qc) {
+        const int nq = min(qc, nr - q0);
         if (!Grp::kLocal) {
             for (int f = tid; f < nq * 3; f += kBT) {
                 const int q = f / 3, v = f - q * 3;
@@ -460,7 +490,19 @@ HDF_DEV void group_argmax(const Grp& g, SplitSm& S, int par) {
     }
     __syncthreads();
 }
-
+// Sum over the group's CTAs (rank order) of record value v, by the calling thread, for groups whose
+// records are local (all loads issued back to back).
+template <class Grp>
+HDF_DEV double local_sum(const Grp& g, SplitSm& S, int par, int v) {
+    double x[kMaxC];
+#pragma unroll
+    for (int q = 0; q < kMaxC; q++) x[q] = (q < g.size) ? g.peer(S, par, q, v) : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kMaxC; q++)
+        if (q < g.size) acc += x[q];
+    return acc;
+}
 // ------------------------------------------------------------------------------- tile loads ---
 // Load `tn` points (rho floats each) starting at global `src` into the shared tile `dyn`: the 16-byte
 // aligned body with TMA bulk copies (completion on S.bar), the < 16-byte tail with plain loads (never
@@ -944,7 +986,7 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
         __syncthreads();
     }
     if (lead) trace_ev(A, 8, v, worker);
-    g.exchange(S, par, 3);
+    g.exchange(S, par, 3, XARGMAX);
     if (lead) trace_ev(A, 9, v, worker);
     group_argmax(g, S, par);
     par ^= 1;
@@ -1018,7 +1060,7 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
                 const int vi = warp_reduce_scatter16(vv);
                 if ((lane & 1) == 0) S.red[warp * 16 + vi] = vv[0];
                 __syncthreads();
-                if (Grp::kLocal) {
+                if constexpr (Grp::kLocal) {
                     // warp 0: the CTA's record, the exchange, the group totals and the new centres
                     if (warp == 0) {
                         double x = 0.0;
@@ -1076,10 +1118,11 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
                         } else {
                             for (int w = 0; w < kBW; w++) x += S.red[w * 16 + tid];
                         }
-                        g.send(S, par, tid, x);
+                        S.outv[tid] = x;
                     }
+                    __syncthreads();
                     tick(1);
-                    g.wait(S, par, nv);
+                    g.exchange(S, par, nv);
                     tick(2);
                 }
             } else {
@@ -1158,7 +1201,7 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
                 S.outv[2] = -1.0;
             }
             __syncthreads();
-            g.exchange(S, par, 3);
+            g.exchange(S, par, 3, XARGMAX);
             group_argmax(g, S, par);
             par ^= 1;
             const long long pick = S.lv[0] < 0 ? 0 : S.lv[0];
@@ -1678,7 +1721,8 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
     cg::cluster_group cl = cg::this_cluster();
     const long long ccap = min(A.ccap, (long long)cl.num_blocks() * A.cap);
     {
-        GridGrp gg{(int)blockIdx.x, G, A.rec};
+        GridGrp gg{(int)blockIdx.x, G, (int)cl.block_rank(), (int)cl.num_blocks(),
+                   (int)(blockIdx.x / cl.num_blocks()), (int)(G / cl.num_blocks()), A.rec};
         while (true) {
             if (blockIdx.x == 0 && tid < 32) {
                 const Claim c = claim_node(A, 1, ccap, 0);
@@ -1705,7 +1749,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
             while (true) {
                 if (g.rank == 0 && tid < 32) {
                     if (tid == 0) trace_ev(A, 1, 0, worker);
-                    const Claim c = claim_node(A, 2, A.cap, worker);
+                    const Claim c = claim_node(A, 2, A.ctamax, worker);
                     if (tid == 0) { S.task = c.task; S.cbase = c.cbase; }
                 }
                 cl.sync();
