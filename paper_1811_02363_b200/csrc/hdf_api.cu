@@ -338,18 +338,18 @@ int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, F
     F.Wp = round_up(W, 4);
     F.NP = n + 1;
     F.P = K * F.NP;
-    // F1: planes per CTA and rows per CTA
-    const int J = hdf::vpass_j(F.Rp);
-    const int NT = hdf::vpass_nt(F.Rp);
-    F.Pg = std::min(NT / 32, F.P);
-    const int gx = (W + hdf::kVTX - 1) / hdf::kVTX, gz = (F.P + F.Pg - 1) / F.Pg;
-    int TY = round_up(std::max(4 * F.Rp, 64), J);
-    while (TY > 2 * J && (long long)gx * gz * ((H + TY - 1) / TY) < 3LL * nsm) TY = round_up(TY / 2, J);
-    F.TY = std::max(TY, J);
-    const int nk_max = (F.Pg + F.NP - 1) / F.NP + 1;
-    F.vl.grid = dim3(gx, (H + F.TY - 1) / F.TY, gz);
-    F.vl.threads = 32 * F.Pg;
-    F.vl.smem = sizeof(float) * (size_t)(round_up(nk_max * 64, 4) + 2 * F.Pg * J * hdf::kVTX);
+    // F1: planes per CTA; a persistent grid (one 512-thread CTA per SM) with equal shares of the
+    // (strip, plane group) x rows space
+    {
+        const int npl = hdf::vfir_npl(hdf::vpass_pack(F.Rp));
+        F.Pg = npl;
+        const long long gx = (W + hdf::kVTX - 1) / hdf::kVTX, gz = (F.P + npl - 1) / npl;
+        F.TY = (int)gx;   // reused: number of strips
+        const long long cols = gx * gz;
+        F.vl.grid = dim3((unsigned)std::max(1LL, std::min<long long>(nsm, cols * H)));
+        F.vl.threads = hdf::kVNT;
+        F.vl.smem = 0;   // depends on rho and on f aliasing p: set at launch
+    }
     // F2
     const int NP = F.NP;
     int maxjp = 1;
@@ -537,13 +537,26 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         vp.K = K;
         vp.NP = F.NP;
         vp.P = F.P;
-        vp.Pg = F.Pg;
-        vp.TY = F.TY;
+        vp.nstrip = F.TY;
+        vp.ncol = F.TY * ((F.P + F.Pg - 1) / F.Pg);
+        vp.f_is_p = (f == p) ? 1 : 0;
         vp.neg_inv2sr2 = neg_inv2sr2;
-        memcpy(vp.taps, taps, sizeof(taps));
+        for (int t = 0; t <= HDF_MAX_RADIUS; t++) {
+            const float wv = (t <= F.Rp) ? taps[F.Rp + t] : 0.f;
+            uint32_t b;
+            memcpy(&b, &wv, 4);
+            vp.tw[t] = ((unsigned long long)b << 32) | b;
+        }
+        for (int t = 0; t < 2 * HDF_MAX_RADIUS + 1; t++) vp.tws[t] = (t <= 2 * F.Rp) ? taps[t] : 0.f;
         hdf::VLaunch vl = F.vl;
-        vl.smem = sizeof(float) * (size_t)(round_up((((F.Pg + F.NP - 1) / F.NP) + 1) * rho, 4) +
-                                           2 * F.Pg * hdf::vpass_j(F.Rp) * hdf::kVTX);
+        {
+            const int J = hdf::vpass_j(F.Rp);
+            const int RW = vp.f_is_p ? rho : rho + n;
+            const size_t mus_len = (size_t)round_up(hdf::vfir_nkmax(F.NP, F.Pg) * rho, 4);
+            const size_t raw_len = (size_t)round_up(J * hdf::kVTX * RW, 4);
+            const size_t zs_len = (size_t)J * F.Pg * hdf::kVTX;
+            vl.smem = sizeof(float) * (mus_len + 2 * raw_len + 2 * zs_len);
+        }
         ProfScope prof(HDF_STAGE_VPASS, st);
         HDF_CUDA(hdf::launch_vpass(F.Rp, F.box, vl, st, vp));
     }

@@ -13,15 +13,20 @@ namespace hdf {
 constexpr int kRadii[] = {1, 2, 3, 4, 5, 6, 8, 9, 10, 12, 15, 16, 20, 24, 32};
 constexpr int kNumRadii = sizeof(kRadii) / sizeof(kRadii[0]);
 
-// J (rows per F1 step) = largest divisor of 2R that is <= 8.
-constexpr int vpass_j(int R) {
-    int best = 1;
-    for (int j = 1; j <= 8; j++)
-        if ((2 * R) % j == 0) best = j;
-    return best;
+// F1 (k_range_vpass): packed column pairs when the u64 register window 2R + J stays <= 42 entries,
+// else one column per thread (float window <= 80).  J = rows per step, a divisor of 2R, <= 16
+// (fewer, longer steps amortise the per-step synchronisation).
+constexpr bool vpass_pack(int R) {
+    for (int j = 16; j >= 1; j--)
+        if ((2 * R) % j == 0 && 2 * R + j <= 42) return true;
+    return false;
 }
-// F1 threads per CTA from the register window size S = 2R + J.
-constexpr int vpass_nt(int R) { return (2 * R + vpass_j(R)) <= 40 ? 1024 : ((2 * R + vpass_j(R)) <= 64 ? 768 : 512); }
+constexpr int vpass_j(int R) {
+    const int lim = vpass_pack(R) ? 42 : 80;
+    for (int j = 16; j >= 1; j--)
+        if ((2 * R) % j == 0 && 2 * R + j <= lim) return j;
+    return 1;
+}
 
 struct VLaunch {
     dim3 grid;

@@ -8,14 +8,25 @@
 
 namespace hdf {
 
-template <int R>
-cudaError_t launch_vpass_t(bool box, const VLaunch& L, cudaStream_t st, const VParams& P) {
-    constexpr int J = vpass_j(R), NT = vpass_nt(R);
-    void (*kern)(const VParams) = box ? k_range_vpass<R, J, true, NT> : k_range_vpass<R, J, false, NT>;
+template <int R, int RHO, int NPC>
+static cudaError_t vp(bool box, const VLaunch& L, cudaStream_t st, const VParams& P) {
+    constexpr int J = vpass_j(R);
+    constexpr bool PK = vpass_pack(R);
+    void (*kern)(const VParams) =
+        box ? k_range_vpass<R, J, true, PK, RHO, NPC> : k_range_vpass<R, J, false, PK, RHO, NPC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
     if (e != cudaSuccess) return e;
     kern<<<L.grid, L.threads, L.smem, st>>>(P);
     return cudaGetLastError();
+}
+
+// (rho, n + 1) specialisations of the range-weight stage: colour guides (rho 3, n 3) and the PCA-6
+// NLM guide (rho 6, n 3); anything else runs the generic loops.
+template <int R>
+cudaError_t launch_vpass_t(bool box, const VLaunch& L, cudaStream_t st, const VParams& P) {
+    if (P.rho == 3 && P.NP == 4) return vp<R, 3, 4>(box, L, st, P);
+    if (P.rho == 6 && P.NP == 4) return vp<R, 6, 4>(box, L, st, P);
+    return vp<R, 0, 0>(box, L, st, P);
 }
 
 template <int R, int MAXJP>
