@@ -346,7 +346,7 @@ int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, F
         const long long gx = (W + hdf::kVTX - 1) / hdf::kVTX, gz = (F.P + npl - 1) / npl;
         F.TY = (int)gx;   // reused: number of strips
         const long long cols = gx * gz;
-        F.vl.grid = dim3((unsigned)std::max(1LL, std::min<long long>(nsm, cols * H)));
+        F.vl.grid = dim3((unsigned)std::max(1LL, std::min<long long>(std::max(1, nsm - 1), cols * H)));
         F.vl.threads = hdf::kVNT;
         F.vl.smem = 0;   // depends on rho and on f aliasing p: set at launch
     }
@@ -441,6 +441,30 @@ int encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2, 
     return HDF_OK;
 }
 
+// Library-owned side stream and fork/join events (per device): k_gram_pinv runs on it, concurrently
+// with the column pass (which leaves one SM free for it), and the main stream waits for it before the
+// coefficient kernel.  Created once, never destroyed (process lifetime).
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+int side_stream(SideStream* out) {
+    static std::mutex mu;
+    static SideStream cache[64];
+    int dev = 0;
+    HDF_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(HDF_ERR_CUDA, "device index %d out of range", dev);
+    std::lock_guard<std::mutex> lk(mu);
+    SideStream& c = cache[dev];
+    if (!c.s) {
+        HDF_CUDA(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
+        HDF_CUDA(cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming));
+        HDF_CUDA(cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming));
+    }
+    *out = c;
+    return HDF_OK;
+}
+
 int nsm_of_device() {
     int dev = 0, nsm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -487,37 +511,22 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         if (rc) return rc;
         centres = w.centres;
     }
-    // step 2: A and A^+ (one CTA, fp64)
+    // step 2: A and A^+ (one CTA, fp64) on the side stream, concurrent with the column pass
+    SideStream ss;
+    rc = side_stream(&ss);
+    if (rc) return rc;
+    HDF_CUDA(cudaEventRecord(ss.fork, st));
+    HDF_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
     {
         hdf::PinvOut po{w.Ap32, w.Ap64, w.status, w.Vscratch};
         const size_t smem = hdf::pinv_smem_bytes(K);
         HDF_CUDA(cudaFuncSetAttribute(hdf::k_gram_pinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        ProfScope prof(HDF_STAGE_PINV, st);
-        hdf::k_gram_pinv<<<1, hdf::kPinvThreads, smem, st>>>(centres, K, rho, -1.0 / (2.0 * (double)sigma_r * sigma_r), po);
+        ProfScope prof(HDF_STAGE_PINV, ss.s);
+        hdf::k_gram_pinv<<<1, hdf::kPinvThreads, smem, ss.s>>>(centres, K, rho, -1.0 / (2.0 * (double)sigma_r * sigma_r),
+                                                              po);
         HDF_CUDA(cudaGetLastError());
     }
-    // loop for2: c(i) = A^+ b(i) -> K coefficient planes
-    {
-        hdf::CoefParams cp;
-        cp.p = p;
-        cp.centres = centres;
-        cp.Ap32 = w.Ap32;
-        cp.cpl = w.cpl;
-        cp.cstride = (long long)H * F.Wp;
-        cp.H = H;
-        cp.W = W;
-        cp.Wp = F.Wp;
-        cp.rho = rho;
-        cp.K = K;
-        cp.neg_inv2sr2 = neg_inv2sr2;
-        const int K8 = (K + 7) & ~7;
-        const size_t smem = sizeof(float) * ((size_t)K * K8 + (size_t)K * rho + (size_t)K * hdf::kCoefPix);
-        HDF_CUDA(cudaFuncSetAttribute(hdf::k_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const long long npix = (long long)H * W;
-        ProfScope prof(HDF_STAGE_COEFFS, st);
-        hdf::k_coeffs<<<(unsigned)((npix + hdf::kCoefPix - 1) / hdf::kCoefPix), hdf::kCoefPix, smem, st>>>(cp);
-        HDF_CUDA(cudaGetLastError());
-    }
+    HDF_CUDA(cudaEventRecord(ss.join, ss.s));
     HDF_CUDA(cudaMemsetAsync(w.flag_count, 0, sizeof(int), st));
     float taps[hdf::kMaxTaps];
     fill_taps(taps, kind, sigma_s, F.R, F.Rp);
@@ -559,6 +568,41 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         }
         ProfScope prof(HDF_STAGE_VPASS, st);
         HDF_CUDA(hdf::launch_vpass(F.Rp, F.box, vl, st, vp));
+    }
+    HDF_CUDA(cudaStreamWaitEvent(st, ss.join, 0));   // A^+ is ready
+    // loop for2: c(i) = A^+ b(i) -> K coefficient planes
+    {
+        hdf::CoefParams cp;
+        cp.p = p;
+        cp.centres = centres;
+        cp.Ap32 = w.Ap32;
+        cp.cpl = w.cpl;
+        cp.cstride = (long long)H * F.Wp;
+        cp.H = H;
+        cp.W = W;
+        cp.Wp = F.Wp;
+        cp.rho = rho;
+        cp.K = K;
+        cp.neg_inv2sr2 = neg_inv2sr2;
+        const long long npix = (long long)H * W;
+        const unsigned nblk = (unsigned)((npix + hdf::kCoefPix - 1) / hdf::kCoefPix);
+        void (*kt)(const hdf::CoefParams) = nullptr;
+        if (K == 8) kt = hdf::k_coeffs_t<8>;
+        else if (K == 16) kt = hdf::k_coeffs_t<16>;
+        else if (K == 32) kt = hdf::k_coeffs_t<32>;
+        else if (K == 64) kt = hdf::k_coeffs_t<64>;
+        ProfScope prof(HDF_STAGE_COEFFS, st);
+        if (kt) {   // compile-time K: b in registers, broadcast A^+ rows
+            const size_t smem = sizeof(float) * ((size_t)K * K + (size_t)K * rho);
+            HDF_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            kt<<<nblk, hdf::kCoefPix, smem, st>>>(cp);
+        } else {
+            const int K8 = (K + 7) & ~7;
+            const size_t smem = sizeof(float) * ((size_t)K * K8 + (size_t)K * rho + (size_t)K * hdf::kCoefPix);
+            HDF_CUDA(cudaFuncSetAttribute(hdf::k_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            hdf::k_coeffs<<<nblk, hdf::kCoefPix, smem, st>>>(cp);
+        }
+        HDF_CUDA(cudaGetLastError());
     }
     // F2: row pass + combine + normalise (TMA-fed)
     {

@@ -20,7 +20,8 @@ struct PinvOut {
     double* Vscratch;  // [K][K] fp64 global scratch for the Jacobi slow path
 };
 
-constexpr int kPinvThreads = 512;
+constexpr int kPinvThreads = 1024;
+constexpr int kPinvMaxE = (HDF_MAX_K * HDF_MAX_K + kPinvThreads - 1) / kPinvThreads;   // elements per thread
 
 __global__ void __launch_bounds__(kPinvThreads) k_gram_pinv(const float* __restrict__ centres, int K, int rho,
                                                              double neg_inv2sr2, PinvOut out) {
@@ -31,13 +32,24 @@ __global__ void __launch_bounds__(kPinvThreads) k_gram_pinv(const float* __restr
     __shared__ int fail;
     __shared__ double red[32];
     const int tid = threadIdx.x, nt = blockDim.x;
+    const int KK = K * K;
+    const int ne = (KK - tid + nt - 1) / nt;   // elements owned by this thread: e = tid + m nt
+    int ei[kPinvMaxE], ej[kPinvMaxE];
+#pragma unroll
+    for (int m = 0; m < kPinvMaxE; m++) {
+        const int e = tid + m * nt;
+        ei[m] = (e < KK) ? e / K : 0;
+        ej[m] = (e < KK) ? e - ei[m] * K : 0;
+    }
 
     // Gram matrix in fp64 (exact promotion of the fp32 centres).
-    for (int e = tid; e < K * K; e += nt) {
-        int k = e / K, l = e % K;
+#pragma unroll
+    for (int m = 0; m < kPinvMaxE; m++) {
+        if (m >= ne) break;
+        const int k = ei[m], l = ej[m];
         double s = 0.0;
         for (int d = 0; d < rho; d++) s = d2_rn(s, (double)centres[k * rho + d], (double)centres[l * rho + d]);
-        A[e] = (k == l) ? 1.0 : exp(s * neg_inv2sr2);
+        A[k * K + l] = (k == l) ? 1.0 : exp(s * neg_inv2sr2);
     }
     if (tid == 0) fail = 0;
     __syncthreads();
@@ -50,18 +62,27 @@ __global__ void __launch_bounds__(kPinvThreads) k_gram_pinv(const float* __restr
     double normA = 0.0;
     for (int k = 0; k < K; k++) normA = fmax(normA, rowsum[k]);
 
-    // In-place Gauss-Jordan inversion (SPD, no pivoting).
+    // Gauss-Jordan inversion (SPD, no pivoting).  Step k maps S -> S' with S'[k][j] = S[k][j] / p and
+    // S'[i][j] = S[i][j] - S[i][k] S'[k][j] (i != k), column k of the identity carried along in place
+    // (the classic in-place scheme, same operations and rounding).  Every thread computes its
+    // elements' new values into registers, then all write: two barriers per pivot.
     for (int k = 0; k < K; k++) {
-        double piv = A[k * K + k];
+        const double piv = A[k * K + k];
         if (!(piv > 0.0) || !isfinite(piv)) { if (tid == 0) fail = 1; break; }
-        double pinv = 1.0 / piv;
-        for (int i = tid; i < K; i += nt) col[i] = A[i * K + k];
+        const double pinv = __drcp_rn(piv);   // correctly rounded 1 / piv
+        double nv[kPinvMaxE];
+#pragma unroll
+        for (int m = 0; m < kPinvMaxE; m++) {
+            if (m >= ne) break;
+            const int i = ei[m], j = ej[m];
+            const double akj = (j == k) ? pinv : A[k * K + j] * pinv;   // the new pivot row
+            nv[m] = (i == k) ? akj : ((j == k) ? 0.0 : A[i * K + j]) - A[i * K + k] * akj;
+        }
         __syncthreads();
-        for (int j = tid; j < K; j += nt) A[k * K + j] = ((j == k) ? 1.0 : A[k * K + j]) * pinv;
-        __syncthreads();
-        for (int e = tid; e < K * K; e += nt) {
-            int i = e / K, j = e % K;
-            if (i != k) A[e] = ((j == k) ? 0.0 : A[e]) - col[i] * A[k * K + j];
+#pragma unroll
+        for (int m = 0; m < kPinvMaxE; m++) {
+            if (m >= ne) break;
+            A[ei[m] * K + ej[m]] = nv[m];
         }
         __syncthreads();
     }
@@ -213,6 +234,80 @@ __global__ void __launch_bounds__(kCoefPix) k_coeffs(const CoefParams P) {
 #pragma unroll
         for (int u = 0; u < 8; u++)
             if (k0 + u < K) out[(long long)(k0 + u) * P.cstride] = acc[u];
+    }
+}
+
+// Compile-time K (8, 16, 32, 64): b(i) in registers, A^+ (symmetric) rows as broadcast float4 from
+// shared memory, accumulators in chunks of up to 32 coefficients.  b = 2^(d2 log2(e) (-1/2 sr^2))
+// (ex2.approx, relative error < 2^-21).
+template <int KC>
+__global__ void __launch_bounds__(kCoefPix) k_coeffs_t(const CoefParams P) {
+    extern __shared__ __align__(16) float sm_ct[];
+    constexpr int KH = KC < 32 ? KC : 32;
+    const int rho = P.rho;
+    float* Asm = sm_ct;                   // [KC][KC], row l = A^+[l][*] = A^+[*][l]
+    float* mus = Asm + KC * KC;           // [KC][rho]
+    const int tid = threadIdx.x;
+    for (int e = tid; e < KC * KC; e += kCoefPix) Asm[e] = P.Ap32[e];
+    for (int e = tid; e < KC * rho; e += kCoefPix) mus[e] = P.centres[e];
+    __syncthreads();
+    const long long npix = (long long)P.H * P.W;
+    const long long i = (long long)blockIdx.x * kCoefPix + tid;
+    if (i >= npix) return;
+    const float c2 = P.neg_inv2sr2 * 1.4426950408889634f;
+    const float* pi = P.p + i * rho;
+    float b[KC];
+    if (rho <= 8) {
+        float x[8];
+#pragma unroll
+        for (int d = 0; d < 8; d++) x[d] = (d < rho) ? __ldg(pi + d) : 0.f;
+#pragma unroll
+        for (int k = 0; k < KC; k++) {
+            float d2 = 0.f;
+#pragma unroll
+            for (int d = 0; d < 8; d++)
+                if (d < rho) {
+                    const float t = x[d] - mus[k * rho + d];
+                    d2 = fmaf(t, t, d2);
+                }
+            float y;
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d2 * c2));
+            b[k] = y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < KC; k++) {
+            float d2 = 0.f;
+            for (int d = 0; d < rho; d++) {
+                const float t = __ldg(pi + d) - mus[k * rho + d];
+                d2 = fmaf(t, t, d2);
+            }
+            float y;
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d2 * c2));
+            b[k] = y;
+        }
+    }
+    const int y = (int)(i / P.W), x = (int)(i - (long long)y * P.W);
+    float* out = P.cpl + (long long)y * P.Wp + x;
+#pragma unroll
+    for (int k0 = 0; k0 < KC; k0 += KH) {
+        float acc[KH];
+#pragma unroll
+        for (int u = 0; u < KH; u++) acc[u] = 0.f;
+#pragma unroll
+        for (int l = 0; l < KC; l++) {
+            const float4* a4 = reinterpret_cast<const float4*>(Asm + l * KC + k0);
+#pragma unroll
+            for (int u4 = 0; u4 < KH / 4; u4++) {
+                const float4 a = a4[u4];
+                acc[4 * u4] = fmaf(a.x, b[l], acc[4 * u4]);
+                acc[4 * u4 + 1] = fmaf(a.y, b[l], acc[4 * u4 + 1]);
+                acc[4 * u4 + 2] = fmaf(a.z, b[l], acc[4 * u4 + 2]);
+                acc[4 * u4 + 3] = fmaf(a.w, b[l], acc[4 * u4 + 3]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < KH; u++) out[(long long)(k0 + u) * P.cstride] = acc[u];
     }
 }
 
