@@ -1,7 +1,14 @@
-# one gpurun call: build check, smoke, GPU tests, bench (default + all configs), ncu launch list + full capture
+# one gpurun call: smoke, all GPU tests, bench (default + all configs), ncu launch list + full capture
 mkdir -p gpurun_out
+TAG=${TAG:-r01}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
 nproc > gpurun_out/nproc.txt; lscpu | head -20 >> gpurun_out/nproc.txt
-bash tools/gpu_tests.sh
-bash tools/gpu_bench.sh
-bash tools/gpu_ncu.sh ${TAG:-r01}
+timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+tail -3 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+timeout 900 python bench.py --all --steps 10 --no-cpu-baseline > gpurun_out/bench_all.json 2> gpurun_out/bench_all.err; echo all rc=$?
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
+$CMD > gpurun_out/ncu_plain_$TAG.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo launches rc=$?
+ncu --set full --clock-control none --import-source on -k regex:"k_range_vpass|k_hpass_combine|k_coeffs" -s 3 -c 3 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo full rc=$?
