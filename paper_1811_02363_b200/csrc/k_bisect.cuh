@@ -120,6 +120,9 @@ HDF_DEV unsigned long long ld_acq64(const int* p) {
     asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+HDF_DEV void red_release_add64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 // (in progress, version) word at ctl[B_INPROG]: low 32 bits in progress, high 32 bits version
 HDF_DEV unsigned long long* syncword(const int* ctl) {
     return reinterpret_cast<unsigned long long*>(const_cast<int*>(ctl) + B_INPROG);
@@ -452,9 +455,34 @@ HDF_DEV void group_sum(const Grp& g, SplitSm& S, int par, int nv, double* out, d
 // Returns it in S.lv[0], S.lv[1] (a, b); shared, valid on return.
 template <class Grp>
 HDF_DEV void group_argmax(const Grp& g, SplitSm& S, int par) {
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     constexpr int qc = kGB / 3;
     const int nr = g.nrec();
+    if (Grp::kLocal && nr <= 32) {
+        // one warp: lane q holds record q, warp-wide (value desc, a asc) reduction
+        if (tid < 32) {
+            double bvv = -1.0;
+            long long ia = -1, ib = -1;
+            if (lane < nr) {
+                bvv = g.peer(S, par, lane, 0);
+                ia = (long long)g.peer(S, par, lane, 1);
+                ib = (long long)g.peer(S, par, lane, 2);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bvv, o);
+                const long long oa = __shfl_xor_sync(0xffffffffu, ia, o);
+                const long long ob = __shfl_xor_sync(0xffffffffu, ib, o);
+                if (cand_better(ov, oa, bvv, ia)) { bvv = ov; ia = oa; ib = ob; }
+            }
+            if (lane == 0) {
+                S.lv[0] = ia;
+                S.lv[1] = ib;
+            }
+        }
+        __syncthreads();
+        return;
+    }
     double bvv = -1.0;
     long long ia = -1, ib = -1;
     for (int q0 = 0; q0 < nr; q0 += qc) {
@@ -878,64 +906,54 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
         // strictly below the maximum, so the argmax and its tie-breaking are unchanged.
         const float* sp = io.dynS;
         auto sbase = [&](int q) { return insm ? sp + (size_t)q * rho : Pg + (size_t)q * stride * rho; };
-        for (int d = warp; d < rho; d += kBW) {            // centroid of the sample (fp32, any c works)
-            float acc = 0.f;
-            for (int q = lane; q < sN; q += 32) acc += sbase(q)[d];
-            acc = warp_sum(acc);
-            if (lane == 0) S.fpc[d] = acc / (float)sN;
-        }
+        // c = the node's mean (any point works; fp32), R = max ||x - c|| over the sample.  Every warp
+        // takes the point farthest from c among its share of the sample and scans all samples for that
+        // point's farthest partner: L = the largest of those pair distances (one barrier in all).
+        if (tid < rho) S.fpc[tid] = (float)__ldcg(&A.nmean[(size_t)v * rho + tid]);
         __syncthreads();
-        float r2m = -1.f;
-        int rmi = 0;
-        for (int q = tid; q < sN; q += kBT) {
-            const float* x = sbase(q);
-            float r2 = 0.f;
-            for (int d = 0; d < rho; d++) {
-                const float t = x[d] - S.fpc[d];
-                r2 = fmaf(t, t, r2);
-            }
-            if (r2 > r2m) { r2m = r2; rmi = q; }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            const float orr = __shfl_xor_sync(0xffffffffu, r2m, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, rmi, o);
-            if (orr > r2m) { r2m = orr; rmi = oi; }
-        }
-        if (lane == 0) { S.wv[warp] = (double)r2m; S.wa[warp] = rmi; }
-        __syncthreads();
-        if (tid == 0) {
-            double m = -1.0;
-            long long mi = 0;
-            for (int w = 0; w < kBW; w++)
-                if (S.wv[w] > m) { m = S.wv[w]; mi = S.wa[w]; }
-            S.fpr[0] = (float)m;
-            S.iv[0] = (int)mi;
-        }
-        __syncthreads();
-        const float R = sqrtf(S.fpr[0]);
         {
-            const float* xi = sbase(S.iv[0]);
-            float lm = 0.f;
-            for (int q = tid; q < sN; q += kBT) {
+            float r2m = -1.f;
+            int rmi = 0;
+            for (int q = warp * 32 + lane; q < sN; q += kBT) {
                 const float* x = sbase(q);
-                float d2 = 0.f;
+                float r2 = 0.f;
                 for (int d = 0; d < rho; d++) {
-                    const float t = x[d] - xi[d];
-                    d2 = fmaf(t, t, d2);
+                    const float t = x[d] - S.fpc[d];
+                    r2 = fmaf(t, t, r2);
                 }
-                lm = fmaxf(lm, d2);
+                if (r2 > r2m) { r2m = r2; rmi = q; }
             }
-            for (int o = 16; o > 0; o >>= 1) lm = fmaxf(lm, __shfl_xor_sync(0xffffffffu, lm, o));
-            __syncthreads();
-            if (lane == 0) S.wv[warp] = (double)lm;
-            __syncthreads();
-            if (tid == 0) {
-                double m = 0.0;
-                for (int w = 0; w < kBW; w++) m = fmax(m, S.wv[w]);
-                S.fpr[1] = (float)m;
+            for (int o = 16; o > 0; o >>= 1) {
+                const float orr = __shfl_xor_sync(0xffffffffu, r2m, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, rmi, o);
+                if (orr > r2m || (orr == r2m && oi < rmi)) { r2m = orr; rmi = oi; }
             }
+            float lm = 0.f;
+            // (a sample in global memory is strided and wide: one warp's partner scan bounds L there)
+            if (r2m >= 0.f && (insm || warp == 0)) {
+                const float* xi = sbase(rmi);
+                for (int q = lane; q < sN; q += 32) {
+                    const float* x = sbase(q);
+                    float d2 = 0.f;
+                    for (int d = 0; d < rho; d++) {
+                        const float t = x[d] - xi[d];
+                        d2 = fmaf(t, t, d2);
+                    }
+                    lm = fmaxf(lm, d2);
+                }
+                for (int o = 16; o > 0; o >>= 1) lm = fmaxf(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+            }
+            if (lane == 0) { S.wv[warp] = (double)r2m; S.wb[warp] = __float_as_int(lm); }
             __syncthreads();
+            float rm = 0.f, lmax = 0.f;
+            for (int w = 0; w < kBW; w++) {
+                rm = fmaxf(rm, (float)S.wv[w]);
+                lmax = fmaxf(lmax, __int_as_float((int)S.wb[w]));
+            }
+            S.fpr[0] = rm;        // identical in every thread (written redundantly)
+            S.fpr[1] = lmax;
         }
+        const float R = sqrtf(S.fpr[0]);
         const float lowb = S.fpr[1] * (1.0f - 1e-4f);
         // The outer points O = {q : (||x_q - c|| + R)^2 >= L}: both ends of any pair reaching L lie in O
         // (||x_a - x_b|| <= ||x_a - c|| + ||x_b - c|| <= ||x_a - c|| + R).  O in sample order.
@@ -1371,17 +1389,15 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
             A.nmean[(size_t)(c + 1) * rho + d] = S.c1[d];
         }
         A.nchild[v] = c;
-        __threadfence();
+        // st.release orders the records above before each state; the sync-word update (version + 1,
+        // in progress - 1, one atomic) is a release too, after the states
         st_rel(&A.nstate[c], ST_FREE);
         st_rel(&A.nstate[c + 1], ST_FREE);
         st_rel(&A.nstate[v], ST_DONE);
-        __threadfence();
         atomicAdd(&A.ctl[B_SPLITS], 1);
         atomicAdd(&A.ctl[B_ITERS], it + 1);
         if (Grp::kGrid) atomicAdd(&A.ctl[B_GRIDSPLITS], 1);
-        // termination protocol (claim_node): the version bump and the in-progress decrement are one
-        // atomic update of the (in progress, version) word
-        atomicAdd(syncword(A.ctl), (1ULL << 32) - 1ULL);
+        red_release_add64(syncword(A.ctl), (1ULL << 32) - 1ULL);
         trace_ev(A, 5, v, worker);
     }
 }
