@@ -140,6 +140,42 @@ HDF_DEV float lds_f(const float* p) {
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)));
     return v;
 }
+// Hot loops address shared memory through a 32-bit base taken once per loop (volatile: the compiler
+// keeps it in a register instead of re-deriving the generic pointer, S2R SR_CgaCtaId included, at
+// every access); ptxas folds the constant parts of base + offset into the LDS immediates.
+HDF_DEV uint32_t smem_pin(const void* p) {
+    uint32_t r;
+    asm volatile("{\n\t.reg .u64 t;\n\tcvta.to.shared.u64 t, %1;\n\tcvt.u32.u64 %0, t;\n\t}" : "=r"(r) : "l"(p));
+    return r;
+}
+HDF_DEV float lds_fa(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+HDF_DEV uint32_t lds_ua(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+HDF_DEV void sts_ua(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+// Side words of a pass (bit j of word j/32 = point j on side 1): this and the previous iteration's,
+// in shared memory (resident nodes) or global memory (streamed nodes).
+struct WordsSm {
+    uint32_t prev, cur;   // shared addresses
+    HDF_DEV uint32_t ld_prev(int i) const { return lds_ua(prev + 4u * i); }
+    HDF_DEV uint32_t ld_cur(int i) const { return lds_ua(cur + 4u * i); }
+    HDF_DEV void st_cur(int i, uint32_t v) const { sts_ua(cur + 4u * i, v); }
+    HDF_DEV WordsSm at(int w) const { return {prev + 4u * w, cur + 4u * w}; }
+};
+struct WordsGl {
+    const uint32_t* prev;
+    uint32_t* cur;
+    HDF_DEV uint32_t ld_prev(int i) const { return prev[i]; }
+    HDF_DEV uint32_t ld_cur(int i) const { return cur[i]; }
+    HDF_DEV void st_cur(int i, uint32_t v) const { cur[i] = v; }
+    HDF_DEV WordsGl at(int w) const { return {prev + w, cur + w}; }
+};
 HDF_DEV uint32_t lds_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)));
@@ -177,6 +213,30 @@ HDF_DEV bool cand_better(double v, long long a, double bv, long long ba) {
 
 // Warp reduce-scatter of 16 doubles in a fixed butterfly order (deterministic).  Afterwards the even
 // lane l holds the warp total of the returned value index.
+// Warp reduce-scatter of N (power of two, <= 32) doubles: returns the index of the total this lane
+// ends up holding in v[0]; the 32 / N lanes holding one index hold equal values (lane & (32/N - 1)
+// == 0 is one of them).  log2(N) halving steps, then log2(32 / N) butterfly steps.
+template <int N>
+HDF_DEV int warp_reduce_scatter(double (&v)[N]) {
+    const int lane = threadIdx.x & 31;
+    int idx = 0;
+#pragma unroll
+    for (int step = 0; (N >> step) > 1; step++) {
+        const int o = 16 >> step;
+        const int half = (N >> step) / 2;
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int j = 0; j < half; j++) {
+            const double send = upper ? v[j] : v[j + half];
+            const double keep = upper ? v[j + half] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+        idx += upper ? half : 0;
+    }
+#pragma unroll
+    for (int o = 32 / N / 2; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    return idx;
+}
 HDF_DEV int warp_reduce_scatter16(double (&v)[16]) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -525,11 +585,13 @@ HDF_DEV double local_sum(const Grp& g, SplitSm& S, int par, int v) {
     double x[kMaxC];
 #pragma unroll
     for (int q = 0; q < kMaxC; q++) x[q] = (q < g.size) ? g.peer(S, par, q, v) : 0.0;
-    double acc = 0.0;
+    // pairwise, in a fixed tree (the same in every CTA, so the totals are bit-identical)
 #pragma unroll
-    for (int q = 0; q < kMaxC; q++)
-        if (q < g.size) acc += x[q];
-    return acc;
+    for (int h = kMaxC / 2; h >= 1; h >>= 1) {
+#pragma unroll
+        for (int q = 0; q < h; q++) x[q] = x[2 * q] + x[2 * q + 1];
+    }
+    return x[0];
 }
 // ------------------------------------------------------------------------------- tile loads ---
 // Load `tn` points (rho floats each) starting at global `src` into the shared tile `dyn`: the 16-byte
@@ -702,18 +764,110 @@ HDF_DEV void set_lin(SplitSm& S, int rho) {
     }
 }
 
-template <int RHO, bool TOT>
-HDF_DEV void pass_small(const float* X, int tn, const uint32_t* prevW, uint32_t* curW, bool cmp, bool full,
+// Whole blocks of U * kBT points (no validity tests), the side words built straight from ballots:
+// wu = points inside the certification band (decided again in fp64, rare), wp = side-1 points.
+// CMP: compare with the previous pass's words; FULL: sums start from zero (every side-1 point
+// is added) instead of being updated by the points that moved.  Returns the first unprocessed point.
+template <int RHO, int U, bool TOT, bool CMP, bool FULL, class Words>
+HDF_DEV int pass_blocks(int j0, uint32_t xs, int tn, const Words& Wd, const SplitSm& S, const float (&wt)[RHO],
+                        const float (&mt)[RHO], float bound, double (&s1)[RHO], double (&st)[RHO], int& n1,
+                        int& chg) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (; j0 + U * kBT <= tn; j0 += U * kBT) {
+        float x[U][RHO];
+        uint32_t wp[U], wu[U];
+        uint32_t anyu = 0;
+#pragma unroll
+        for (int h = 0; h < U; h++) {
+            float D = 0.f;
+#pragma unroll
+            for (int d = 0; d < RHO; d++) {
+                x[h][d] = lds_fa(xs + 4u * (uint32_t)((j0 + h * kBT) * RHO + d));
+                D = fmaf(wt[d], fmaf(2.0f, x[h][d], -mt[d]), D);
+            }
+            wu[h] = __ballot_sync(0xffffffffu, !(fabsf(D) > bound));
+            wp[h] = __ballot_sync(0xffffffffu, D > 0.f);
+            anyu |= wu[h];
+        }
+        if (anyu) {
+#pragma unroll
+            for (int h = 0; h < U; h++) {
+                if (wu[h]) {
+                    bool s64 = false;
+                    if ((wu[h] >> lane) & 1u) {
+                        double dd0 = 0.0, dd1 = 0.0;
+#pragma unroll
+                        for (int d = 0; d < RHO; d++) {
+                            const double v = (double)x[h][d];
+                            dd0 = d2_rn(dd0, v, S.c0[d]);
+                            dd1 = d2_rn(dd1, v, S.c1[d]);
+                        }
+                        s64 = !(dd0 <= dd1);
+                    }
+                    wp[h] = (wp[h] & ~wu[h]) | (__ballot_sync(0xffffffffu, s64) & wu[h]);
+                }
+            }
+        }
+        uint32_t anym = 0, mk[U];
+#pragma unroll
+        for (int h = 0; h < U; h++) {
+            const int wi = (j0 >> 5) + h * kBW + warp;
+            if (lane == 0) Wd.st_cur(wi, wp[h]);
+            n1 += __popc(wp[h]);
+            if (CMP) {
+                const uint32_t c = wp[h] ^ Wd.ld_prev(wi);
+                chg += __popc(c);
+                mk[h] = FULL ? wp[h] : c;
+            } else {
+                mk[h] = wp[h];
+            }
+            anym |= mk[h];
+        }
+        if (anym) {
+#pragma unroll
+            for (int h = 0; h < U; h++) {
+                const double k = ((mk[h] >> lane) & 1u) ? (((wp[h] >> lane) & 1u) ? 1.0 : -1.0) : 0.0;
+#pragma unroll
+                for (int d = 0; d < RHO; d++) s1[d] = fma(k, (double)x[h][d], s1[d]);
+            }
+        }
+        if (TOT) {
+#pragma unroll
+            for (int d = 0; d < RHO; d++) {
+                double acc = 0.0;
+#pragma unroll
+                for (int h = 0; h < U; h++) acc += (double)x[h][d];
+                st[d] += acc;
+            }
+        }
+    }
+    return j0;
+}
+
+template <int RHO, bool TOT, class Words>
+HDF_DEV void pass_small(const float* X, int tn, const Words& Wd, bool cmp, bool full,
                         const SplitSm& S, double (&s1)[RHO], double (&st)[RHO], int& n1, int& chg) {
     // Incremental side-1 sums: s1 persists across the Lloyd iterations; a pass adds the points that
     // moved to side 1 and subtracts those that left it (full: s1 starts from 0 and every side-1 point
     // is added).  After the first iterations few points move, so the fp64 work nearly vanishes.
-    // U points per thread per step (points j0 + h kBT + tid) for instruction-level parallelism.
-    constexpr int U = 4;
+    // Whole blocks go through pass_blocks; the tail loop below handles the last partial block.
+    constexpr int U = 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     float wt[RHO], mt[RHO], bound;
     lin_consts<RHO>(S, wt, mt, bound);
-    for (int j0 = 0; j0 < tn; j0 += U * kBT) {
+    const uint32_t xs = smem_pin(X) + 4u * (uint32_t)(tid * RHO);
+    int jb;
+    if (TOT || !cmp) {
+        jb = pass_blocks<RHO, 4, TOT, false, true>(0, xs, tn, Wd, S, wt, mt, bound, s1, st, n1, chg);
+        jb = pass_blocks<RHO, 1, TOT, false, true>(jb, xs, tn, Wd, S, wt, mt, bound, s1, st, n1, chg);
+    } else if (!full) {
+        jb = pass_blocks<RHO, 4, TOT, true, false>(0, xs, tn, Wd, S, wt, mt, bound, s1, st, n1, chg);
+        jb = pass_blocks<RHO, 1, TOT, true, false>(jb, xs, tn, Wd, S, wt, mt, bound, s1, st, n1, chg);
+    } else {
+        jb = pass_blocks<RHO, 4, TOT, true, true>(0, xs, tn, Wd, S, wt, mt, bound, s1, st, n1, chg);
+        jb = pass_blocks<RHO, 1, TOT, true, true>(jb, xs, tn, Wd, S, wt, mt, bound, s1, st, n1, chg);
+    }
+    for (int j0 = jb; j0 < tn; j0 += U * kBT) {   // the ragged tail (< kBT points)
         float x[U][RHO];
         bool sd[U], cert[U];
         uint32_t pw[U];
@@ -722,13 +876,13 @@ HDF_DEV void pass_small(const float* X, int tn, const uint32_t* prevW, uint32_t*
         for (int h = 0; h < U; h++) {
             const int wi = (j0 >> 5) + h * kBW + warp;
             const bool has = j0 + h * kBT < tn;   // uniform
-            pw[h] = (cmp && has) ? prevW[wi] : 0u;
+            pw[h] = (cmp && has) ? Wd.ld_prev(wi) : 0u;
             const int j = j0 + h * kBT + tid;
             const bool ok = j < tn;
             float D = 0.f;
 #pragma unroll
             for (int d = 0; d < RHO; d++) {
-                x[h][d] = ok ? lds_f(X + (size_t)j * RHO + d) : 0.f;
+                x[h][d] = ok ? lds_fa(xs + 4u * (uint32_t)((j0 + h * kBT) * RHO + d)) : 0.f;
                 D = fmaf(wt[d], fmaf(2.0f, x[h][d], -mt[d]), D);
             }
             cert[h] = !ok || fabsf(D) > bound;
@@ -756,7 +910,7 @@ HDF_DEV void pass_small(const float* X, int tn, const uint32_t* prevW, uint32_t*
         for (int h = 0; h < U; h++) {
             const uint32_t w = __ballot_sync(0xffffffffu, sd[h]);
             const bool has = j0 + h * kBT < tn;
-            if (lane == 0 && has) curW[(j0 >> 5) + h * kBW + warp] = w;
+            if (lane == 0 && has) Wd.st_cur((j0 >> 5) + h * kBW + warp, w);
             if (cmp) chg += __popc(w ^ pw[h]);
             n1 += __popc(w);
             mk[h] = full ? w : (w ^ pw[h]);   // points whose sum term changes
@@ -783,20 +937,23 @@ HDF_DEV void pass_small(const float* X, int tn, const uint32_t* prevW, uint32_t*
 }
 
 // Generic rho: side phase (thread per point) ...
-HDF_DEV void pass_side_generic(const float* X, int tn, int rho, const uint32_t* prevW, uint32_t* curW, bool cmp,
+template <class Words>
+HDF_DEV void pass_side_generic(const float* X, int tn, int rho, const Words& Wd, bool cmp,
                                const SplitSm& S, int& n1, int& chg) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     float kd, kc;
     cert_consts(S, rho, kd, kc);
+    const uint32_t xs = smem_pin(X);
     for (int j0 = 0; j0 < tn; j0 += kBT) {
         const int j = j0 + tid;
         const bool ok = j < tn;
         int sd = 0;
         if (ok) {
             const float* x = X + (size_t)j * rho;
+            const uint32_t xa = xs + 4u * (uint32_t)(j * rho);
             float a0 = 0.f, a1 = 0.f;
             for (int d = 0; d < rho; d++) {
-                const float v = lds_f(x + d);
+                const float v = lds_fa(xa + 4u * d);
                 const float e0 = v - S.f0[d], e1 = v - S.f1[d];
                 a0 = fmaf(e0, e0, a0);
                 a1 = fmaf(e1, e1, a1);
@@ -806,8 +963,8 @@ HDF_DEV void pass_side_generic(const float* X, int tn, int rho, const uint32_t* 
         const uint32_t w = __ballot_sync(0xffffffffu, sd != 0);
         if (lane == 0) {
             const int wi = (j0 >> 5) + warp;
-            if (cmp) chg += __popc(w ^ prevW[wi]);
-            curW[wi] = w;
+            if (cmp) chg += __popc(w ^ Wd.ld_prev(wi));
+            Wd.st_cur(wi, w);
         }
         n1 += sd;
     }
@@ -815,11 +972,13 @@ HDF_DEV void pass_side_generic(const float* X, int tn, int rho, const uint32_t* 
 // ... then dimension-parallel sums: warp w owns dimensions w, w + 16, ... (<= 4 of them), lanes
 // stride over the tile's points (consecutive points per lane group, odd rho: conflict free).
 constexpr int kGenDims = (HDF_MAX_RHO + kBW - 1) / kBW;
-HDF_DEV void pass_sum_generic(const float* X, int tn, int rho, const uint32_t* curW, double (&a0)[kGenDims],
+template <class Words>
+HDF_DEV void pass_sum_generic(const float* X, int tn, int rho, const Words& Wd, double (&a0)[kGenDims],
                               double (&a1)[kGenDims]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t xs = smem_pin(X);
     for (int j0 = 0; j0 < tn; j0 += 32) {
-        const uint32_t w = curW[j0 >> 5];
+        const uint32_t w = Wd.ld_cur(j0 >> 5);
         const int j = j0 + lane;
         const bool ok = j < tn;
         const bool sd = (w >> lane) & 1u;
@@ -827,7 +986,7 @@ HDF_DEV void pass_sum_generic(const float* X, int tn, int rho, const uint32_t* c
         for (int q = 0; q < kGenDims; q++) {
             const int d = warp + kBW * q;
             if (d < rho && ok) {
-                const double v = (double)lds_f(X + (size_t)j * rho + d);
+                const double v = (double)lds_fa(xs + 4u * (uint32_t)(j * rho + d));
                 a0[q] += sd ? 0.0 : v;
                 a1[q] += sd ? v : 0.0;
             }
@@ -1057,26 +1216,30 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
 #pragma unroll
                     for (int q = 0; q < RH; q++) s1p[q] = 0.0;
                 }
-                for (int t0 = 0; t0 < np; t0 += A.cap) {
-                    const int tn = min(A.cap, np - t0);
-                    const float* T = resident ? X : load_tile(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
-                    if (tot)
-                        pass_small<RH, true>(T, tn, prevW + (t0 >> 5), curW + (t0 >> 5), it > 0, full, S, s1p, stp, n1,
-                                             chg);
-                    else
-                        pass_small<RH, false>(T, tn, prevW + (t0 >> 5), curW + (t0 >> 5), it > 0, full, S, s1p, stp,
-                                              n1, chg);
+                if (resident) {
+                    const WordsSm wd{smem_pin(prevW), smem_pin(curW)};
+                    if (tot) pass_small<RH, true>(X, np, wd, it > 0, full, S, s1p, stp, n1, chg);
+                    else pass_small<RH, false>(X, np, wd, it > 0, full, S, s1p, stp, n1, chg);
+                } else {
+                    for (int t0 = 0; t0 < np; t0 += A.cap) {
+                        const int tn = min(A.cap, np - t0);
+                        const float* T = load_tile(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
+                        const WordsGl wd = WordsGl{prevW, curW}.at(t0 >> 5);
+                        if (tot) pass_small<RH, true>(T, tn, wd, it > 0, full, S, s1p, stp, n1, chg);
+                        else pass_small<RH, false>(T, tn, wd, it > 0, full, S, s1p, stp, n1, chg);
+                    }
                 }
                 tick(0);
-                double vv[16];
+                constexpr int NR = (2 * RH + 2 <= 8) ? 8 : 16;
+                double vv[NR];
 #pragma unroll
-                for (int q = 0; q < 16; q++) vv[q] = 0.0;
+                for (int q = 0; q < NR; q++) vv[q] = 0.0;
 #pragma unroll
                 for (int q = 0; q < RH; q++) { vv[q] = tot ? stp[q] : 0.0; vv[RH + q] = s1p[q]; }
                 vv[2 * RH] = (lane == 0) ? (double)n1 : 0.0;     // ballot counts: lane 0's copy
                 vv[2 * RH + 1] = (lane == 0) ? (double)chg : 0.0;
-                const int vi = warp_reduce_scatter16(vv);
-                if ((lane & 1) == 0) S.red[warp * 16 + vi] = vv[0];
+                const int vi = warp_reduce_scatter<NR>(vv);
+                if ((lane & (32 / NR - 1)) == 0) S.red[warp * 16 + vi] = vv[0];
                 __syncthreads();
                 if constexpr (Grp::kLocal) {
                     // warp 0: the CTA's record, the exchange, the group totals and the new centres
@@ -1147,12 +1310,20 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
                 double s0[kGenDims], s1[kGenDims];
 #pragma unroll
                 for (int q = 0; q < kGenDims; q++) { s0[q] = 0.0; s1[q] = 0.0; }
-                for (int t0 = 0; t0 < np; t0 += A.cap) {
-                    const int tn = min(A.cap, np - t0);
-                    const float* T = resident ? X : load_tile(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
-                    pass_side_generic(T, tn, rho, prevW + (t0 >> 5), curW + (t0 >> 5), it > 0, S, n1, chg);
+                if (resident) {
+                    const WordsSm wd{smem_pin(prevW), smem_pin(curW)};
+                    pass_side_generic(X, np, rho, wd, it > 0, S, n1, chg);
                     __syncthreads();
-                    pass_sum_generic(T, tn, rho, curW + (t0 >> 5), s0, s1);
+                    pass_sum_generic(X, np, rho, wd, s0, s1);
+                } else {
+                    for (int t0 = 0; t0 < np; t0 += A.cap) {
+                        const int tn = min(A.cap, np - t0);
+                        const float* T = load_tile(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
+                        const WordsGl wd = WordsGl{prevW, curW}.at(t0 >> 5);
+                        pass_side_generic(T, tn, rho, wd, it > 0, S, n1, chg);
+                        __syncthreads();
+                        pass_sum_generic(T, tn, rho, wd, s0, s1);
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < kGenDims; q++) {
@@ -1289,6 +1460,7 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
         for (int t0 = 0; t0 < np; t0 += A.cap) {
             const int tn = min(A.cap, np - t0);
             const float* T = resident ? X : load_tile(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
+            const uint32_t Ts = smem_pin(T);
             const int nw = (tn + 31) >> 5;
             for (int w0 = 0; w0 < nw; w0 += kBT) {
                 // word prefix of side-0 counts for words [w0, w0 + kBT) of the tile
@@ -1325,12 +1497,12 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
                             const int jj = t0 + j;                                       // CTA-relative index
                             const int z0 = run0 + zb;                                    // side-0 before jj
                             const int dst = sd ? (m0 + pre1 + (jj - z0)) : (pre0 + z0);
-                            const float* x = T + (size_t)j * rho;
+                            const uint32_t xa = Ts + 4u * (uint32_t)(j * rho);
                             float* o = Po + (size_t)dst * rho;
                             const double* cc = sd ? S.c1 : S.c0;
                             double dd = 0.0;
                             for (int d = 0; d < rho; d++) {
-                                const float xv = lds_f(x + d);
+                                const float xv = lds_fa(xa + 4u * d);
                                 o[d] = xv;
                                 dd = d2_rn(dd, (double)xv, cc[d]);
                             }
@@ -1346,13 +1518,9 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
             }
         }
         // children's SSE over the group
-        double vv[16];
-#pragma unroll
-        for (int q = 0; q < 16; q++) vv[q] = 0.0;
-        vv[0] = se0;
-        vv[1] = se1;
-        const int vi = warp_reduce_scatter16(vv);
-        if ((lane & 1) == 0) S.red[warp * 16 + vi] = vv[0];
+        double vv[2] = {se0, se1};
+        const int vi = warp_reduce_scatter<2>(vv);
+        if ((lane & 15) == 0) S.red[warp * 16 + vi] = vv[0];
         __syncthreads();
         if (tid < 2) {
             double x = 0.0;
