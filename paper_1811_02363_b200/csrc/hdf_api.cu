@@ -132,7 +132,6 @@ hdf::BisectArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho,
     A.nbuf = cv.take<int>(A.maxn);
     A.nmean = cv.take<double>((size_t)A.maxn * rho);
     A.nfinal = cv.take<int>(A.maxn);
-    A.node_of = cv.take<int>((size_t)N);
     A.ctl = cv.take<int>(hdf::B_NUM);
     A.trace = cv.take<long long>(1 + 2 * hdf::kBisectTraceCap);
     A.ek = cv.take<double>(1);

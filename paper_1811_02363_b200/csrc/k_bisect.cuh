@@ -95,7 +95,6 @@ struct BisectArgs {
     int* nbuf;
     double* nmean;      // [maxn][rho]
     int* nfinal;        // [maxn] leaf id of the final leaf containing the node (labels)
-    int* node_of;       // [N] deepest computed node of each pixel (labels only)
     int* ctl;           // [B_NUM]
     long long* trace;   // [1 + 2 * kBisectTraceCap] (tag|node|worker, globaltimer), or null
     float* centres;     // [K][rho] out
@@ -643,51 +642,72 @@ HDF_DEV const float* load_tile(const float* src, int tn, int rho, float* dyn, Sp
 // (|d32 - d| <= (rho + 3) u d for fp32 inputs, u = 2^-24); pass 2 re-evaluates with the oracle's
 // fp64 sequence only the pairs with d32 >= M (1 - 8 (rho + 3) u), which contain every pair whose
 // fp64 value can be the row maximum.
-template <int RHO, class Base>
-HDF_DEV float pair_d32(const float* xa, const float* xb, int rho) {
-    float acc = 0.f;
-    if (RHO > 0) {
-#pragma unroll
-        for (int d = 0; d < (RHO > 0 ? RHO : 1); d++) {
-            const float t = xa[d] - xb[d];
-            acc = fmaf(t, t, acc);
-        }
-    } else {
-        for (int d = 0; d < rho; d++) {
-            const float t = xa[d] - xb[d];
-            acc = fmaf(t, t, acc);
-        }
+// Sample accessors: value d of sample q, from shared memory (rho <= kSampRho) or global memory.
+struct SampSm {
+    uint32_t base;   // shared address of the staged sample
+    int rs;          // row stride (floats)
+    HDF_DEV float operator()(int q, int d) const { return lds_fa(base + 4u * (uint32_t)(q * rs + d)); }
+    HDF_DEV void store(int q, int d, float v) const {
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(base + 4u * (uint32_t)(q * rs + d)), "f"(v) : "memory");
     }
-    return acc;
-}
-
-template <int RHO, class Base>
-HDF_DEV void row_farthest(int a, int sN, int rho, Base base, double& best, int& arg) {
+};
+struct SampGl {
+    const float* p;   // the node's first member
+    size_t rs;        // row stride (floats): stride * rho
+    HDF_DEV float operator()(int q, int d) const { return __ldcg(p + (size_t)q * rs + d); }
+    HDF_DEV void store(int, int, float) const {}
+};
+template <int RHO, bool IND, class Acc>
+HDF_DEV void row_farthest(int a, int nO, int rho, const Acc& ld, const short* fpo, double& best, int& arg) {
     // One pass: a lane keeps its running fp32 maximum M_l and re-evaluates in fp64 every pair whose
     // d32 >= M_l (1 - 8 (rho + 3) u) at the time it is seen -- a superset of the pairs that can be
-    // the lane's fp64 maximum, whose fp64 maximum is therefore exact.
+    // the lane's fp64 maximum, whose fp64 maximum is therefore exact.  Rows and columns are positions
+    // in the outer list: samples fpo[q] (IND) or the compacted copy's rows q.  A lane takes its
+    // columns four at a time (loads and fp32 distances in flight together), in ascending order.
     const int lane = threadIdx.x & 31;
     constexpr float u = 5.9604644775390625e-08f;
     constexpr int RR = RHO > 0 ? RHO : 1;
+    constexpr int UC = 4;
     const float shrink = 1.0f - 8.0f * (float)(rho + 3) * u;
+    const int qa = IND ? fpo[a] : a;
     float xr[RR];
-    const float* xa = base(a);
     if (RHO > 0) {
 #pragma unroll
-        for (int d = 0; d < RR; d++) xr[d] = xa[d];
+        for (int d = 0; d < RR; d++) xr[d] = ld(qa, d);
     }
-    const float* xav = RHO > 0 ? xr : xa;
     float mx = -1.0f;
     best = -1.0;
     arg = -1;
-    for (int q = a + 1 + lane; q < sN; q += 32) {
-        const float* xb = base(q);
-        const float d32 = pair_d32<RHO, Base>(xav, xb, rho);
-        if (d32 >= mx * shrink) {
-            mx = fmaxf(mx, d32);
-            double dd = 0.0;
-            for (int d = 0; d < rho; d++) dd = d2_rn(dd, (double)xa[d], (double)xb[d]);
-            if (dd > best) { best = dd; arg = q; }
+    for (int q0 = a + 1 + lane; q0 < nO; q0 += 32 * UC) {
+        float d32[UC];
+        int qb[UC];
+#pragma unroll
+        for (int c = 0; c < UC; c++) {
+            const int q = q0 + 32 * c;
+            qb[c] = (q < nO) ? (IND ? fpo[q] : q) : qa;
+            float acc = 0.f;
+            if (RHO > 0) {
+#pragma unroll
+                for (int d = 0; d < RR; d++) {
+                    const float t = xr[d] - ld(qb[c], d);
+                    acc = fmaf(t, t, acc);
+                }
+            } else {
+                for (int d = 0; d < rho; d++) {
+                    const float t = ld(qa, d) - ld(qb[c], d);
+                    acc = fmaf(t, t, acc);
+                }
+            }
+            d32[c] = (q < nO) ? acc : -2.0f;
+        }
+#pragma unroll
+        for (int c = 0; c < UC; c++) {
+            if (d32[c] >= mx * shrink) {
+                mx = fmaxf(mx, d32[c]);
+                double dd = 0.0;
+                for (int d = 0; d < rho; d++) dd = d2_rn(dd, (double)ld(qa, d), (double)ld(qb[c], d));
+                if (dd > best) { best = dd; arg = q0 + 32 * c; }
+            }
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -695,6 +715,153 @@ HDF_DEV void row_farthest(int a, int sN, int rho, Base base, double& best, int& 
         const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
         if (oa >= 0 && (arg < 0 || ob > best || (ob == best && oa < arg))) { best = ob; arg = oa; }
     }
+}
+
+// Farthest pair of the stride sample, exact and pruned (R3).  Row pruning: for any point c,
+// ||x_a - x_b|| <= ||x_a - c|| + R with R = max_b ||x_b - c||, so neither end of a pair reaching L (a
+// lower bound of the largest pair distance) lies outside O = {q : (||x_q - c|| + R)^2 >= L}; pairs
+// outside O are strictly below the maximum, so restricting rows and columns to O keeps the argmax and
+// its tie-breaking.  c = the node's mean (in S.fpc), L = the farthest partner of the sample point
+// farthest from c.  fp32 estimates carry 1e-4 relative margins (their errors are < 1e-5 for
+// rho <= 64).  Three barriers: the per-warp farthest-from-c records, the per-warp partner maxima,
+// then the compaction of O.  The CTA's best pair (over its rows) is left in S.outv[0..2].
+template <int RHO, bool CPT, class Acc, class Mark>
+HDF_DEV void sample_farthest_pair(const Acc& ld, int sN, int rho, int r, int C, SplitSm& S, Mark mark) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int RR = RHO > 0 ? RHO : 1;
+    float fc[RR];
+    if (RHO > 0) {
+#pragma unroll
+        for (int d = 0; d < RR; d++) fc[d] = S.fpc[d];
+    }
+    auto dist_c = [&](int q) {
+        float r2 = 0.f;
+        if (RHO > 0) {
+#pragma unroll
+            for (int d = 0; d < RR; d++) {
+                const float t = ld(q, d) - fc[d];
+                r2 = fmaf(t, t, r2);
+            }
+        } else {
+            for (int d = 0; d < rho; d++) {
+                const float t = ld(q, d) - S.fpc[d];
+                r2 = fmaf(t, t, r2);
+            }
+        }
+        return r2;
+    };
+    // (1) the point farthest from c: per thread (ascending q), per warp, then per CTA in every thread
+    float r2m = -1.f;
+    int rmi = 0;
+    for (int q = tid; q < sN; q += kBT) {
+        const float r2 = dist_c(q);
+        if (r2 > r2m) { r2m = r2; rmi = q; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float orr = __shfl_xor_sync(0xffffffffu, r2m, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, rmi, o);
+        if (orr > r2m || (orr == r2m && oi < rmi)) { r2m = orr; rmi = oi; }
+    }
+    if (lane == 0) { S.wv[warp] = (double)r2m; S.wa[warp] = rmi; }
+    __syncthreads();
+    mark(14);
+    float R2 = -1.f;
+    int istar = 0;
+#pragma unroll
+    for (int w = 0; w < kBW; w++) {
+        const float x = (float)S.wv[w];
+        const int i = (int)S.wa[w];
+        if (x > R2 || (x == R2 && i < istar)) { R2 = x; istar = i; }
+    }
+    // (2) L = max_q ||x_q - x_istar||^2
+    float xi[RR];
+    if (RHO > 0) {
+#pragma unroll
+        for (int d = 0; d < RR; d++) xi[d] = ld(istar, d);
+    }
+    float lm = 0.f;
+    for (int q = tid; q < sN; q += kBT) {
+        float d2 = 0.f;
+        if (RHO > 0) {
+#pragma unroll
+            for (int d = 0; d < RR; d++) {
+                const float t = ld(q, d) - xi[d];
+                d2 = fmaf(t, t, d2);
+            }
+        } else {
+            for (int d = 0; d < rho; d++) {
+                const float t = ld(q, d) - ld(istar, d);
+                d2 = fmaf(t, t, d2);
+            }
+        }
+        lm = fmaxf(lm, d2);
+    }
+    for (int o = 16; o > 0; o >>= 1) lm = fmaxf(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+    if (lane == 0) S.wb[warp] = __float_as_int(lm);
+    __syncthreads();
+    float L = 0.f;
+#pragma unroll
+    for (int w = 0; w < kBW; w++) L = fmaxf(L, __int_as_float((int)S.wb[w]));
+    mark(15);
+    const float R = sqrtf(fmaxf(R2, 0.f));
+    const float lowb = L * (1.0f - 1e-4f);
+    // (3) O in sample order: the sample indices in S.fpo and (CPT: a shared sample with compile-time
+    // rho) the coordinates compacted in place to the front of the sample.  A chunk reads all its
+    // samples before the barrier inside block_exscan and writes only below its own positions.
+    int nO = 0;
+    for (int q0 = 0; q0 < sN; q0 += kBT) {
+        const int q = q0 + tid;
+        bool in = false;
+        float xq[RR];
+        if (q < sN) {
+            float r2 = 0.f;
+            if (CPT) {
+#pragma unroll
+                for (int d = 0; d < RR; d++) {
+                    xq[d] = ld(q, d);
+                    const float t = xq[d] - fc[d];
+                    r2 = fmaf(t, t, r2);
+                }
+            } else {
+                r2 = dist_c(q);
+            }
+            const float ub = (sqrtf(r2) + R) * (1.0f + 1e-4f);
+            in = ub * ub >= lowb;
+        }
+        int tot;
+        const int pos = block_exscan(in ? 1 : 0, S.wsum, &tot);
+        if (in) {
+            S.fpo[nO + pos] = (short)q;
+            if (CPT) {
+#pragma unroll
+                for (int d = 0; d < RR; d++) ld.store(nO + pos, d, xq[d]);
+            }
+        }
+        nO += tot;
+    }
+    __syncthreads();
+    mark(16);
+    // (4) rows of O over the group's warps (rows ascend within a warp), then the CTA's best pair
+    double bv = -1.0;
+    long long ba = -1, bb = -1;
+    for (int ia = r + C * warp; ia < nO; ia += C * kBW) {
+        double best;
+        int arg;
+        row_farthest<RHO, !CPT>(ia, nO, rho, ld, S.fpo, best, arg);
+        if (arg >= 0 && (ba < 0 || best > bv)) { bv = best; ba = S.fpo[ia]; bb = S.fpo[arg]; }
+    }
+    if (lane == 0) { S.wv[warp] = bv; S.wa[warp] = ba; S.wb[warp] = bb; }
+    __syncthreads();
+    if (tid == 0) {
+        double bvv = -1.0;
+        long long ia = -1, ib = -1;
+        for (int w = 0; w < kBW; w++)
+            if (cand_better(S.wv[w], S.wa[w], bvv, ia)) { bvv = S.wv[w]; ia = S.wa[w]; ib = S.wb[w]; }
+        S.outv[0] = bvv;
+        S.outv[1] = (double)ia;
+        S.outv[2] = (double)ib;
+    }
+    __syncthreads();
 }
 
 // ------------------------------------------------------------------------------- the pass -----
@@ -773,6 +940,7 @@ HDF_DEV int pass_blocks(int j0, uint32_t xs, int tn, const Words& Wd, const Spli
                         const float (&mt)[RHO], float bound, double (&s1)[RHO], double (&st)[RHO], int& n1,
                         int& chg) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t cw = 0;
     for (; j0 + U * kBT <= tn; j0 += U * kBT) {
         float x[U][RHO];
         uint32_t wp[U], wu[U];
@@ -814,9 +982,9 @@ HDF_DEV int pass_blocks(int j0, uint32_t xs, int tn, const Words& Wd, const Spli
             const int wi = (j0 >> 5) + h * kBW + warp;
             if (lane == 0) Wd.st_cur(wi, wp[h]);
             n1 += __popc(wp[h]);
-            if (CMP) {
+            if (CMP) {   // only whether anything changed is used (convergence)
                 const uint32_t c = wp[h] ^ Wd.ld_prev(wi);
-                chg += __popc(c);
+                cw |= c;
                 mk[h] = FULL ? wp[h] : c;
             } else {
                 mk[h] = wp[h];
@@ -841,6 +1009,7 @@ HDF_DEV int pass_blocks(int j0, uint32_t xs, int tn, const Words& Wd, const Spli
             }
         }
     }
+    chg += cw != 0u;
     return j0;
 }
 
@@ -1057,111 +1226,13 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
         __syncthreads();
         if (lead) trace_ev(A, 7, v, worker);
     }
-    {
-        // Row pruning (exact): for any point c, ||x_a - x_b|| <= ||x_a - c|| + R with R = max_b ||x_b - c||,
-        // so row a cannot hold the maximum when (||x_a - c|| + R)^2 < L, L = a lower bound of the largest
-        // pair distance (here: the farthest partner of the point farthest from c).  fp32 estimates carry
-        // 1e-4 relative margins (their errors are < 1e-5 for rho <= 64); skipped rows hold only pairs
-        // strictly below the maximum, so the argmax and its tie-breaking are unchanged.
-        const float* sp = io.dynS;
-        auto sbase = [&](int q) { return insm ? sp + (size_t)q * rho : Pg + (size_t)q * stride * rho; };
-        // c = the node's mean (any point works; fp32), R = max ||x - c|| over the sample.  Every warp
-        // takes the point farthest from c among its share of the sample and scans all samples for that
-        // point's farthest partner: L = the largest of those pair distances (one barrier in all).
-        if (tid < rho) S.fpc[tid] = (float)__ldcg(&A.nmean[(size_t)v * rho + tid]);
-        __syncthreads();
-        {
-            float r2m = -1.f;
-            int rmi = 0;
-            for (int q = warp * 32 + lane; q < sN; q += kBT) {
-                const float* x = sbase(q);
-                float r2 = 0.f;
-                for (int d = 0; d < rho; d++) {
-                    const float t = x[d] - S.fpc[d];
-                    r2 = fmaf(t, t, r2);
-                }
-                if (r2 > r2m) { r2m = r2; rmi = q; }
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                const float orr = __shfl_xor_sync(0xffffffffu, r2m, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, rmi, o);
-                if (orr > r2m || (orr == r2m && oi < rmi)) { r2m = orr; rmi = oi; }
-            }
-            float lm = 0.f;
-            // (a sample in global memory is strided and wide: one warp's partner scan bounds L there)
-            if (r2m >= 0.f && (insm || warp == 0)) {
-                const float* xi = sbase(rmi);
-                for (int q = lane; q < sN; q += 32) {
-                    const float* x = sbase(q);
-                    float d2 = 0.f;
-                    for (int d = 0; d < rho; d++) {
-                        const float t = x[d] - xi[d];
-                        d2 = fmaf(t, t, d2);
-                    }
-                    lm = fmaxf(lm, d2);
-                }
-                for (int o = 16; o > 0; o >>= 1) lm = fmaxf(lm, __shfl_xor_sync(0xffffffffu, lm, o));
-            }
-            if (lane == 0) { S.wv[warp] = (double)r2m; S.wb[warp] = __float_as_int(lm); }
-            __syncthreads();
-            float rm = 0.f, lmax = 0.f;
-            for (int w = 0; w < kBW; w++) {
-                rm = fmaxf(rm, (float)S.wv[w]);
-                lmax = fmaxf(lmax, __int_as_float((int)S.wb[w]));
-            }
-            S.fpr[0] = rm;        // identical in every thread (written redundantly)
-            S.fpr[1] = lmax;
-        }
-        const float R = sqrtf(S.fpr[0]);
-        const float lowb = S.fpr[1] * (1.0f - 1e-4f);
-        // The outer points O = {q : (||x_q - c|| + R)^2 >= L}: both ends of any pair reaching L lie in O
-        // (||x_a - x_b|| <= ||x_a - c|| + ||x_b - c|| <= ||x_a - c|| + R).  O in sample order.
-        int nO = 0;
-        for (int q0 = 0; q0 < sN; q0 += kBT) {
-            const int q = q0 + tid;
-            bool in = false;
-            if (q < sN) {
-                const float* x = sbase(q);
-                float r2 = 0.f;
-                for (int d = 0; d < rho; d++) {
-                    const float t = x[d] - S.fpc[d];
-                    r2 = fmaf(t, t, r2);
-                }
-                const float ub = (sqrtf(r2) + R) * (1.0f + 1e-4f);
-                in = ub * ub >= lowb;
-            }
-            int tot;
-            const int pos = block_exscan(in ? 1 : 0, S.wsum, &tot);
-            if (in) S.fpo[nO + pos] = (short)q;
-            nO += tot;
-        }
-        __syncthreads();
-        double bv = -1.0;
-        long long ba = -1, bb = -1;
-        for (int ia = r + C * warp; ia < nO; ia += C * kBW) {   // rows ascend within the warp
-            double best;
-            int arg;
-            if (insm) {
-                row_farthest<RHO>(ia, nO, rho, [&](int q) { return sp + (size_t)S.fpo[q] * rho; }, best, arg);
-            } else {
-                row_farthest<RHO>(ia, nO, rho, [&](int q) { return Pg + (size_t)S.fpo[q] * stride * rho; }, best,
-                                  arg);
-            }
-            if (arg >= 0 && (ba < 0 || best > bv)) { bv = best; ba = S.fpo[ia]; bb = S.fpo[arg]; }
-        }
-        if (lane == 0) { S.wv[warp] = bv; S.wa[warp] = ba; S.wb[warp] = bb; }
-        __syncthreads();
-        if (tid == 0) {
-            double bvv = -1.0;
-            long long ia = -1, ib = -1;
-            for (int w = 0; w < kBW; w++)
-                if (cand_better(S.wv[w], S.wa[w], bvv, ia)) { bvv = S.wv[w]; ia = S.wa[w]; ib = S.wb[w]; }
-            S.outv[0] = bvv;
-            S.outv[1] = (double)ia;
-            S.outv[2] = (double)ib;
-        }
-        __syncthreads();
-    }
+    if (tid < rho) S.fpc[tid] = (float)__ldcg(&A.nmean[(size_t)v * rho + tid]);
+    __syncthreads();
+    auto mark = [&](int tag) {
+        if (lead) trace_ev(A, tag, v, worker);
+    };
+    if (insm) sample_farthest_pair<RHO, (RHO > 0)>(SampSm{smem_pin(io.dynS), rho}, sN, rho, r, C, S, mark);
+    else sample_farthest_pair<RHO, false>(SampGl{Pg, (size_t)stride * rho}, sN, rho, r, C, S, mark);
     if (lead) trace_ev(A, 8, v, worker);
     g.exchange(S, par, 3, XARGMAX);
     if (lead) trace_ev(A, 9, v, worker);
@@ -1173,7 +1244,7 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
     for (int f = tid; f < 2 * rho; f += kBT) {
         const int w = f / rho, d = f - w * rho;
         const long long q = S.lv[w];
-        const float x = insm ? io.dynS[q * rho + d] : __ldcg(Pg + (size_t)q * stride * rho + d);
+        const float x = __ldcg(Pg + (size_t)q * stride * rho + d);   // (the staged sample is compacted)
         (w ? S.c1 : S.c0)[d] = (double)x;
         (w ? S.f1 : S.f0)[d] = x;
     }
@@ -1186,7 +1257,8 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
 
     // ---- 3. Lloyd iterations (R4) ----
     // Record of a pass (per CTA): [0, rho) side-0 sums, [rho, 2 rho) side-1 sums, 2 rho: side-1 count,
-    // 2 rho + 1: changed sides.  Each value v is reduced by thread v and sent straight from it.
+    // 2 rho + 1: nonzero iff some side changed (a count of warps with changes).  Each value v is
+    // reduced by thread v and sent straight from it.
     int it = 0, fbw = 0, fpar = 0;
     bool conv = false;
     long long tph[4] = {0, 0, 0, 0};   // diagnostics (lead thread): pass, reduce, exchange, update
@@ -1509,7 +1581,6 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
                             if (sd) se1 += dd;
                             else se0 += dd;
                             Io[dst] = pix[u];
-                            if (A.labels) A.node_of[pix[u]] = cbase + sd;
                         }
                     }
                 }
@@ -1810,46 +1881,70 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
     }
     // ---- init: node table, root statistics (mean, SSE) in a fixed order ----
     for (long long i = gtid; i < A.maxn; i += gth) A.nstate[i] = ST_NONE;
-    if (A.labels)
-        for (long long i = gtid; i < A.N; i += gth) A.node_of[i] = 0;
     if (gtid < B_NUM) A.ctl[gtid] = (gtid == B_TRACE_N && A.trace) ? 1 : 0;
     const long long per = ((long long)A.N + G - 1) / G;
     const long long rb0 = min((long long)A.N, (long long)blockIdx.x * per), rb1 = min((long long)A.N, rb0 + per);
     double* rec0 = A.rec;
     double* rec1 = A.rec + (size_t)G * kRecV;
+    // Pass 1 over the CTA's contiguous range: per dimension the fp64 sum, max p_d and max -p_d
+    // (record: rec0 [0, rho) sums, [HDF_MAX_RHO, +rho) max p_d; rec1 [0, rho) max -p_d).
     for (int d0 = 0; d0 < rho; d0 += 8) {
-        double acc[16];
-        float mx[8];
+        constexpr int UP = 4;   // points per thread in flight
+        double acc[8];
+        float hi[8], nlo[8];
 #pragma unroll
-        for (int j = 0; j < 16; j++) acc[j] = 0.0;
+        for (int j = 0; j < 8; j++) { acc[j] = 0.0; hi[j] = -INFINITY; nlo[j] = -INFINITY; }
+        for (long long t0 = rb0 + tid; t0 < rb1; t0 += UP * kBT) {
+            float x[UP][8];
 #pragma unroll
-        for (int j = 0; j < 8; j++) mx[j] = 0.f;
-        for (long long t = rb0 + tid; t < rb1; t += kBT) {
+            for (int u = 0; u < UP; u++) {
+                const long long t = t0 + (long long)u * kBT;
 #pragma unroll
-            for (int j = 0; j < 8; j++)
-                if (d0 + j < rho) {
-                    const float x = __ldg(A.p + t * rho + d0 + j);
-                    acc[j] += (double)x;
-                    mx[j] = fmaxf(mx[j], fabsf(x));
+                for (int j = 0; j < 8; j++) x[u][j] = (t < rb1 && d0 + j < rho) ? __ldg(A.p + t * rho + d0 + j) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < UP; u++) {
+                if (t0 + (long long)u * kBT < rb1) {
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        acc[j] += (double)x[u][j];
+                        hi[j] = fmaxf(hi[j], x[u][j]);
+                        nlo[j] = fmaxf(nlo[j], -x[u][j]);
+                    }
                 }
+            }
         }
 #pragma unroll
         for (int j = 0; j < 8; j++)
-            for (int o = 16; o > 0; o >>= 1) mx[j] = fmaxf(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], o));
-        const int vi = warp_reduce_scatter16(acc);
-        if (((tid & 31) & 1) == 0) S.red[(tid >> 5) * 16 + vi] = acc[0];
+            for (int o = 16; o > 0; o >>= 1) {
+                hi[j] = fmaxf(hi[j], __shfl_xor_sync(0xffffffffu, hi[j], o));
+                nlo[j] = fmaxf(nlo[j], __shfl_xor_sync(0xffffffffu, nlo[j], o));
+            }
+        double av[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) av[j] = acc[j];
+        const int vi = warp_reduce_scatter<8>(av);
+        if ((tid & 3) == 0) S.red[(tid >> 5) * 16 + vi] = av[0];
         if ((tid & 31) == 0)
 #pragma unroll
-            for (int j = 0; j < 8; j++) S.red[(tid >> 5) * 16 + 8 + j] = (double)mx[j];
+            for (int j = 0; j < 4; j++) {   // hi and nlo packed as float pairs
+                S.red[(tid >> 5) * 16 + 8 + j] = __hiloint2double(__float_as_int(hi[2 * j + 1]), __float_as_int(hi[2 * j]));
+                S.red[(tid >> 5) * 16 + 12 + j] =
+                    __hiloint2double(__float_as_int(nlo[2 * j + 1]), __float_as_int(nlo[2 * j]));
+            }
         __syncthreads();
         if (tid < 8 && d0 + tid < rho) {
-            double s = 0.0, m = 0.0;
+            double sm = 0.0;
+            float h = -INFINITY, nl = -INFINITY;
             for (int w = 0; w < kBW; w++) {
-                s += S.red[w * 16 + tid];
-                m = fmax(m, S.red[w * 16 + 8 + tid]);
+                sm += S.red[w * 16 + tid];
+                const double hp = S.red[w * 16 + 8 + tid / 2], np = S.red[w * 16 + 12 + tid / 2];
+                h = fmaxf(h, __int_as_float((tid & 1) ? __double2hiint(hp) : __double2loint(hp)));
+                nl = fmaxf(nl, __int_as_float((tid & 1) ? __double2hiint(np) : __double2loint(np)));
             }
-            rec0[(size_t)blockIdx.x * kRecV + d0 + tid] = s;
-            rec0[(size_t)blockIdx.x * kRecV + HDF_MAX_RHO + d0 + tid] = m;   // max |p_d| of the block
+            rec0[(size_t)blockIdx.x * kRecV + d0 + tid] = sm;
+            rec0[(size_t)blockIdx.x * kRecV + HDF_MAX_RHO + d0 + tid] = (double)h;
+            rec1[(size_t)blockIdx.x * kRecV + d0 + tid] = (double)nl;
         }
         __syncthreads();
     }
@@ -1859,35 +1954,62 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
         A.ctl[B_NALLOC] = 1;
         A.ctl[B_TASK] = -1;
     }
-    for (int d = tid; d < rho; d += kBT) {
-        double s = 0.0;
-        for (int b = 0; b < G; b++) s += __ldcg(rec0 + (size_t)b * kRecV + d);
-        S.c0[d] = s / (double)A.N;
-        float m = 0.f;
-        for (int b = 0; b < G; b++) m = fmaxf(m, (float)__ldcg(rec0 + (size_t)b * kRecV + HDF_MAX_RHO + d));
-        S.xmax[d] = m;
-    }
-    __syncthreads();
+    // Every CTA gathers the G records, all loads in flight: quantity e (sum_d, max p_d, max -p_d) is
+    // reduced by one warp, lanes over blocks then a fixed butterfly (bit-identical in every CTA).
     {
-        double acc[16];
-#pragma unroll
-        for (int j = 0; j < 16; j++) acc[j] = 0.0;
-        for (long long t = rb0 + tid; t < rb1; t += kBT) acc[0] += dist_rn(A.p + t * rho, S.c0, rho);
-        const int vi = warp_reduce_scatter16(acc);
-        if (((tid & 31) & 1) == 0) S.red[(tid >> 5) * 16 + vi] = acc[0];
-        __syncthreads();
-        if (tid == 0) {
-            double s = 0.0;
-            for (int w = 0; w < kBW; w++) s += S.red[w * 16];
-            rec1[(size_t)blockIdx.x * kRecV] = s;
+        const int lane = tid & 31, warp = tid >> 5;
+        for (int e = warp; e < 3 * rho; e += kBW) {
+            const int kind = e / rho, d = e - kind * rho;
+            const double* src = (kind == 2) ? rec1 + d : rec0 + (kind == 1 ? HDF_MAX_RHO : 0) + d;
+            double v = (kind == 0) ? 0.0 : -INFINITY;
+            for (int b = lane; b < G; b += 32) {
+                const double x = __ldcg(src + (size_t)b * kRecV);
+                v = (kind == 0) ? v + x : fmax(v, x);
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double y = __shfl_xor_sync(0xffffffffu, v, o);
+                v = (kind == 0) ? v + y : fmax(v, y);
+            }
+            if (lane == 0) {
+                if (kind == 0) S.c0[d] = v / (double)A.N;
+                else if (kind == 1) S.c1[d] = v;     // max p_d (staged)
+                else S.tot[d] = v;                   // max -p_d (staged)
+            }
         }
     }
-    __threadfence();
-    grid.sync();
+    __syncthreads();
+    bool constant = true;
+    for (int d = 0; d < rho; d++) constant = constant && (S.c1[d] == -S.tot[d]);
+    __syncthreads();
+    for (int d = tid; d < rho; d += kBT) S.xmax[d] = (float)fmax(S.c1[d], S.tot[d]);
+    // The root's SSE is only compared with its descendants' (it is the largest unless the guide is
+    // constant, then 0) and enters E_K only when the root stays a leaf: a constant guide (0) or K = 1,
+    // where pass 2 computes it in a fixed order.
+    double root_sse = constant ? 0.0 : INFINITY;
+    if (A.K == 1 && !constant) {
+        __syncthreads();
+        double acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc[j] = 0.0;
+        for (long long t = rb0 + tid; t < rb1; t += kBT) acc[0] += dist_rn(A.p + t * rho, S.c0, rho);
+        const int vi = warp_reduce_scatter<8>(acc);
+        if ((tid & 3) == 0) S.red[(tid >> 5) * 16 + vi] = acc[0];
+        __syncthreads();
+        if (tid == 0) {
+            double sm = 0.0;
+            for (int w = 0; w < kBW; w++) sm += S.red[w * 16];
+            rec1[(size_t)blockIdx.x * kRecV + HDF_MAX_RHO + 8] = sm;
+        }
+        __threadfence();
+        grid.sync();
+        if (blockIdx.x == 0 && tid == 0) {
+            double sm = 0.0;
+            for (int b = 0; b < G; b++) sm += __ldcg(rec1 + (size_t)b * kRecV + HDF_MAX_RHO + 8);
+            root_sse = sm;
+        }
+    }
     if (blockIdx.x == 0 && tid == 0) {
-        double s = 0.0;
-        for (int b = 0; b < G; b++) s += __ldcg(rec1 + (size_t)b * kRecV);
-        A.nsse[0] = s;
+        A.nsse[0] = root_sse;
         A.nm[0] = A.N;
         A.nstart[0] = 0;
         A.nbuf[0] = kBufInput;
@@ -1907,7 +2029,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
     {
         GridGrp gg{(int)blockIdx.x, G, (int)cl.block_rank(), (int)cl.num_blocks(),
                    (int)(blockIdx.x / cl.num_blocks()), (int)(G / cl.num_blocks()), A.rec};
-        while (true) {
+        while (A.N > ccap) {   // (no node is larger than a cluster's capacity otherwise)
             if (blockIdx.x == 0 && tid < 32) {
                 const Claim c = claim_node(A, 1, ccap, 0);
                 if (tid == 0) {
@@ -1983,7 +2105,44 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
     __threadfence();
     grid.sync();
     if (A.labels) {
-        for (long long i = gtid; i < A.N; i += gth) A.labels[i] = __ldcg(&A.nfinal[__ldcg(&A.node_of[i])]);
+        // Pixel labels.  Every leaf of the computed tree (a node never split) holds its members at
+        // positions [nstart, nstart + nm) of buffer nbuf (no later partition writes there), and its
+        // label is nfinal.  A CTA walks a contiguous range of positions (index reads coalesced over
+        // the threads) and finds the leaf covering a position by descending from the root over the
+        // node table staged in shared memory, reusing it while the position stays inside.
+        const int n = min(__ldcg(&A.ctl[B_NALLOC]), A.maxn);
+        int* tst = reinterpret_cast<int*>(dsm);
+        int* tch = tst + n;
+        int* tsa = tch + n;
+        int* tnm = tsa + n;
+        int* tbf = tnm + n;
+        int* tfn = tbf + n;
+        for (int i = tid; i < n; i += kBT) {
+            tst[i] = __ldcg(&A.nstate[i]);
+            tch[i] = __ldcg(&A.nchild[i]);
+            tsa[i] = __ldcg(&A.nstart[i]);
+            tnm[i] = __ldcg(&A.nm[i]);
+            tbf[i] = __ldcg(&A.nbuf[i]);
+            tfn[i] = __ldcg(&A.nfinal[i]);
+        }
+        __syncthreads();
+        long long ls = 0, le = 0;
+        int lb = kBufInput, lf = 0;
+        for (long long j = rb0 + tid; j < rb1; j += kBT) {
+            if (j < ls || j >= le) {
+                int v = 0;
+                while (tst[v] == ST_DONE) {
+                    const int c = tch[v];
+                    v = (j < tsa[c + 1]) ? c : c + 1;
+                }
+                ls = tsa[v];
+                le = ls + tnm[v];
+                lb = tbf[v];
+                lf = tfn[v];
+            }
+            const long long pix = (lb == kBufInput) ? j : (long long)__ldcg(A.idx[lb] + j);
+            A.labels[pix] = lf;
+        }
     }
 }
 

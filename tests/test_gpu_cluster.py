@@ -101,3 +101,25 @@ def test_rho_31_and_6(hdf):
         cen_o, lab_o, _, ek_o = oracle.cluster(p, 12)
         cen_g, lab_g, info = hdf.cluster(_dev(p), 12, labels=True)
         assert abs(info.e_k - ek_o) <= 1e-6 * ek_o
+
+
+def test_constant_guide(hdf):
+    """A constant guide has one distinct vector: K = 1 gives it with E_K = 0, K > 1 is HDF_ERR_K (R5)."""
+    p = np.full((40, 56, 3), 17.25, np.float32)
+    cen, lab, info = hdf.cluster(_dev(p), 1, labels=True)
+    assert info.e_k == 0.0 and np.all(cen.cpu().numpy() == 17.25) and int(lab.max()) == 0
+    with pytest.raises(hdf.HdfKError) as e:
+        hdf.cluster(_dev(p), 4)
+    assert e.value.achievable == 1
+
+
+def test_root_split_of_two_values(hdf):
+    """Two distinct vectors, K = 2: the two leaves are exactly the two vectors (E_K = 0)."""
+    p = np.zeros((64, 64, 3), np.float32)
+    p[:, 20:] = (200.0, 10.0, 3.5)
+    cen, lab, info = hdf.cluster(_dev(p), 2, labels=True)
+    assert info.e_k == 0.0
+    got = sorted(map(tuple, cen.cpu().numpy().astype(np.float64)))
+    assert got == [(0.0, 0.0, 0.0), (200.0, 10.0, 3.5)]
+    lab = lab.cpu().numpy().reshape(64, 64)
+    assert len(np.unique(lab[:, :20])) == 1 and len(np.unique(lab[:, 20:])) == 1 and lab[0, 0] != lab[0, 30]

@@ -37,8 +37,8 @@ for name in sys.argv[1:]:
         byw = {}
         for w, t in sorted(tr, key=lambda x: x[1]):
             byw.setdefault(w >> 28, []).append((w & 0xFF, (w >> 8) & 0xFFFFF, (t - t0) / 1e3))
-        names = {1: "claim", 2: "start", 7: "sample", 8: "rows", 9: "sync", 10: "argmax", 3: "seeds", 4: "lloyd",
-                 11: "sse", 12: "xchg", 13: "scatter", 5: "publ"}
+        names = {1: "claim", 2: "start", 7: "sample", 14: "R", 15: "L", 16: "O", 8: "rows", 9: "sync", 10: "argmax", 3: "seeds", 4: "lloyd",
+                 11: "sse", 12: "part", 13: "ssex", 5: "publ"}
         rows = []
         for wk, evs in byw.items():
             cur = None
@@ -54,7 +54,7 @@ for name in sys.argv[1:]:
                     cur["t"][tag] = t
         for rw in sorted(rows, key=lambda r: r["t"][2]):
             tt = rw["t"]
-            seq = [2, 7, 8, 9, 10, 3, 4, 11, 12, 13, 5]
+            seq = [2, 7, 14, 15, 16, 8, 9, 10, 3, 4, 11, 12, 13, 5]
             parts = []
             prev = tt[2]
             for tag in seq[1:]:
