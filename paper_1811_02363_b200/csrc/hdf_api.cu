@@ -135,6 +135,7 @@ hdf::BisectArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho,
     A.ctl = cv.take<int>(hdf::B_NUM);
     A.trace = cv.take<long long>(1 + 2 * hdf::kBisectTraceCap);
     A.ek = cv.take<double>(1);
+    A.xw = cv.take<unsigned long long>((size_t)2 * kBisectMaxGrid * hdf::kRecV * 2);
     return A;
 }
 
@@ -289,8 +290,12 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
         info->tile_points = sh.cap;
         info->e_k = ek;
         if (info->status == HDF_ERR_CUDA)
-            return fail(HDF_ERR_CUDA, "clustering kernel: internal error (abort %d, nodes %d, splits %d, not done %d)",
-                        ctrl[hdf::B_ABORT], ctrl[hdf::B_NALLOC], ctrl[hdf::B_SPLITS], ctrl[hdf::B_NOTDONE]);
+            return fail(HDF_ERR_CUDA,
+                        "clustering kernel: internal error (abort %d, nodes %d, splits %d, not done %d, diag %d %d %d %d "
+                        "%d %d)",
+                        ctrl[hdf::B_ABORT], ctrl[hdf::B_NALLOC], ctrl[hdf::B_SPLITS], ctrl[hdf::B_NOTDONE],
+                        ctrl[hdf::B_DIAG0], ctrl[hdf::B_DIAG1], ctrl[hdf::B_DIAG2], ctrl[hdf::B_DIAG3],
+                        ctrl[hdf::B_DIAG4], ctrl[hdf::B_DIAG5]);
         if (info->status == HDF_ERR_K)
             return fail(HDF_ERR_K, "K=%d exceeds the number of distinct guide vectors (%d)", K, info->achievable_k);
     }

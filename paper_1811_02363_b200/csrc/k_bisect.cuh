@@ -68,6 +68,7 @@ enum {
     B_TRACE_N,     // trace events recorded
     B_ABORT,       // internal error: 1 node table overflow, 2 cluster range not resident (never expected)
     B_NOTDONE,     // diagnostics: split-set nodes without a computed split (never expected)
+    B_DIAG0, B_DIAG1, B_DIAG2, B_DIAG3, B_DIAG4, B_DIAG5,   // diagnostics (grid exchange timeouts)
     B_NUM
 };
 enum { ST_FREE = 0, ST_CLAIMED = 1, ST_DONE = 2, ST_NONE = 3 };
@@ -97,6 +98,7 @@ struct BisectArgs {
     int* nfinal;        // [maxn] leaf id of the final leaf containing the node (labels)
     int* ctl;           // [B_NUM]
     long long* trace;   // [1 + 2 * kBisectTraceCap] (tag|node|worker, globaltimer), or null
+    unsigned long long* xw;   // grid exchange: [2][clusters][2 kRecV] tagged record words (seq << 32 | half)
     float* centres;     // [K][rho] out
     int* labels;        // [N] out, or null
     double* ek;         // out
@@ -292,6 +294,7 @@ struct SplitSm {
             double gb[kGB];                     // staged peer records (pull / grid exchanges)
         };
     };
+    double grx[2][16][16];                      // grid mode: the cluster's CTA records, at the leader
     double red[kBW * 16];
     double wv[kBW];
     long long wa[kBW], wb[kBW];
@@ -307,6 +310,7 @@ struct SplitSm {
     long long lv[4];
     uint64_t bar;                               // TMA mbarrier
     uint64_t xbar[2];                           // push-exchange mbarriers (by parity)
+    uint64_t gbar[2];                           // grid mode: the cluster leader's record mbarriers
     uint32_t tma_phase;
     int task, cbase;
 };
@@ -351,52 +355,122 @@ enum { XSUM = 0, XARGMAX = 1 };
 // cluster record to global memory, one grid barrier, and every CTA reads the (few) cluster records.
 // Record-level accessors (nrec / rec) therefore see cluster records; the order of every sum is
 // fixed (clusters in order, CTAs in rank order inside a cluster), so all CTAs agree bit for bit.
+// Grid mode: the group is the whole grid.  Exchange: every CTA pushes its record to its cluster's
+// leader (st.async + mbarrier; a DSMEM pull for records longer than kPushV), the leader combines the
+// cluster's records in a fixed order and stores the cluster record to global memory as tagged 64-bit
+// words (exchange number << 32 | one 32-bit half of a value); every CTA reads the cluster records by
+// polling those words until the tags match.  No grid barrier: each word validates itself, and the
+// two parities alternate, so a slot is rewritten only after every CTA has read it (a CTA's next
+// record, which the next-but-one exchange waits for, follows its reads).
 struct GridGrp {
     int rank, size;           // CTA rank / count in the grid
     int crank, csize, cid;    // rank in the cluster, cluster size, cluster index
     int ncl;                  // clusters in the grid
-    double* rec;              // [2][ncl][kRecV] cluster records
+    unsigned long long* xw;   // [2][ncl][2 kRecV] tagged words
+    int* ctl;
+    uint32_t seq = 0;         // exchanges so far (the same in every CTA)
+    uint32_t sq[2] = {0, 0};  // exchange number held by each parity's slots
+    uint32_t gph = 0;         // phase bits of S.gbar (leader)
+    uint32_t pushed = 0;      // bit par: that exchange went through the push buffer
     static constexpr bool kGrid = true, kLocal = false;
     HDF_DEV void sync() { cg::this_grid().sync(); }
+    HDF_DEV unsigned long long* slot(int par, int q, int v) const {
+        return xw + (((size_t)par * ncl + q) * kRecV + v) * 2;
+    }
     HDF_DEV void exchange(SplitSm& S, int par, int nv, int kind = XSUM) {
         cg::cluster_group cl = cg::this_cluster();
-        for (int v = threadIdx.x; v < nv; v += kBT) S.rx[par][v] = S.outv[v];
-        cl.sync();
-        if (crank == 0) {
-            double* rp = rec + ((size_t)par * ncl + cid) * kRecV;
-            if (kind == XSUM) {
-                for (int v = threadIdx.x; v < nv; v += kBT) {
-                    double acc = 0.0;
-                    for (int q = 0; q < csize; q++) acc += cl.map_shared_rank(&S.rx[par][0], q)[v];
-                    rp[v] = acc;
-                }
-            } else if (threadIdx.x == 0) {
-                double bvv = -1.0;
-                long long ia = -1, ib = -1;
-                for (int q = 0; q < csize; q++) {
-                    const double* y = cl.map_shared_rank(&S.rx[par][0], q);
-                    const long long qa = (long long)y[1], qb = (long long)y[2];
-                    if (cand_better(y[0], qa, bvv, ia)) { bvv = y[0]; ia = qa; ib = qb; }
-                }
-                rp[0] = bvv;
-                rp[1] = (double)ia;
-                rp[2] = (double)ib;
+        const int tid = threadIdx.x;
+        sq[par] = ++seq;
+        const bool push = nv <= kPushV;
+        pushed = push ? (pushed | (1u << par)) : (pushed & ~(1u << par));
+        if (push) {
+            if (crank == 0 && tid == 0) mbar_arrive_expect_tx(&S.gbar[par], (uint32_t)(csize * nv * 8));
+            if (tid < nv)
+                st_async_f64(mapa_u32(smem_u32(&S.grx[par][crank][tid]), 0), S.outv[tid],
+                             mapa_u32(smem_u32(&S.gbar[par]), 0));
+            if (crank == 0) {
+                mbar_wait_cluster(&S.gbar[par], (gph >> par) & 1u);
+                gph ^= 1u << par;
             }
+        } else {
+            for (int v = tid; v < nv; v += kBT) S.rx[par][v] = S.outv[v];
+            cl.sync();
         }
-        __threadfence();
-        cg::this_grid().sync();
+        if (crank != 0) {
+            if (!push) cl.sync();   // the leader reads this CTA's posted record in between
+            return;
+        }
+        const uint64_t tag = (uint64_t)seq << 32;
+        auto put = [&](int v, double x) {
+            const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+            unsigned long long* w = slot(par, cid, v);
+            __stcg(w, tag | (b & 0xffffffffull));
+            __stcg(w + 1, tag | (b >> 32));
+        };
+        auto rec = [&](int q, int v) -> double {
+            return push ? S.grx[par][q][v] : cl.map_shared_rank(&S.rx[par][0], q)[v];
+        };
+        if (kind == XSUM) {
+            for (int v = tid; v < nv; v += kBT) {
+                double x[kMaxC];
+#pragma unroll
+                for (int q = 0; q < kMaxC; q++) x[q] = (q < csize) ? rec(q, v) : 0.0;
+#pragma unroll
+                for (int h = kMaxC / 2; h >= 1; h >>= 1) {
+#pragma unroll
+                    for (int q = 0; q < h; q++) x[q] = x[2 * q] + x[2 * q + 1];
+                }
+                put(v, x[0]);
+            }
+        } else if (tid == 0) {
+            double bvv = -1.0;
+            long long ia = -1, ib = -1;
+            for (int q = 0; q < csize; q++) {
+                const double y0 = rec(q, 0);
+                const long long qa = (long long)rec(q, 1), qb = (long long)rec(q, 2);
+                if (cand_better(y0, qa, bvv, ia)) { bvv = y0; ia = qa; ib = qb; }
+            }
+            put(0, bvv);
+            put(1, (double)ia);
+            put(2, (double)ib);
+        }
+        if (!push) cl.sync();   // the peers' rx stay in place until the leader has read them
     }
     HDF_DEV int nrec() const { return ncl; }
     HDF_DEV double peer(SplitSm&, int par, int q, int v) const {
-        return __ldcg(rec + ((size_t)par * ncl + q) * kRecV + v);
+        const unsigned long long* w = slot(par, q, v);
+        const uint32_t want = sq[par];
+        unsigned long long lo, hi;
+        long long spins = 0;
+        do {
+            lo = __ldcv(w);
+            hi = __ldcv(w + 1);
+            if (++spins > (1LL << 22)) {
+                if (atomicCAS(&ctl[B_ABORT], 0, 7) == 0) {
+                    ctl[B_DIAG0] = (int)want;
+                    ctl[B_DIAG1] = (int)(lo >> 32);
+                    ctl[B_DIAG2] = (int)(hi >> 32);
+                    ctl[B_DIAG3] = par * 100000 + q * 1000 + v;
+                    ctl[B_DIAG4] = rank;
+                    ctl[B_DIAG5] = (int)seq;
+                }
+                break;
+            }
+        } while ((uint32_t)(lo >> 32) != want || (uint32_t)(hi >> 32) != want);
+        return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
     }
     // sum of value v over the CTAs of lower grid rank (clusters before this one, then the CTAs of
-    // this cluster before this CTA); the cluster-local records of parity par are still in place
+    // this cluster before this CTA, from the leader's push buffer or the peers' posted records)
     HDF_DEV double prefix(SplitSm& S, int par, int v) const {
         double acc = 0.0;
-        for (int c = 0; c < cid; c++) acc += __ldcg(rec + ((size_t)par * ncl + c) * kRecV + v);
+        for (int c = 0; c < cid; c++) acc += peer(S, par, c, v);
         cg::cluster_group cl = cg::this_cluster();
-        for (int q = 0; q < crank; q++) acc += cl.map_shared_rank(&S.rx[par][0], q)[v];
+        if ((pushed >> par) & 1u) {
+            const double* lr = cl.map_shared_rank(&S.grx[par][0][0], 0);
+            for (int q = 0; q < crank; q++) acc += lr[q * kPushV + v];
+        } else {
+            for (int q = 0; q < crank; q++) acc += cl.map_shared_rank(&S.rx[par][0], q)[v];
+        }
         return acc;
     }
 };
@@ -1870,6 +1944,8 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
         mbar_init(&S.bar, 1);
         mbar_init(&S.xbar[0], 1);
         mbar_init(&S.xbar[1], 1);
+        mbar_init(&S.gbar[0], 1);
+        mbar_init(&S.gbar[1], 1);
         fence_barrier_init();
         S.tma_phase = 0;
     }
@@ -1881,6 +1957,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
     }
     // ---- init: node table, root statistics (mean, SSE) in a fixed order ----
     for (long long i = gtid; i < A.maxn; i += gth) A.nstate[i] = ST_NONE;
+    for (long long i = gtid; i < (long long)2 * G * kRecV * 2; i += gth) A.xw[i] = 0ull;
     if (gtid < B_NUM) A.ctl[gtid] = (gtid == B_TRACE_N && A.trace) ? 1 : 0;
     const long long per = ((long long)A.N + G - 1) / G;
     const long long rb0 = min((long long)A.N, (long long)blockIdx.x * per), rb1 = min((long long)A.N, rb0 + per);
@@ -2028,7 +2105,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
     const long long ccap = min(A.ccap, (long long)cl.num_blocks() * A.cap);
     {
         GridGrp gg{(int)blockIdx.x, G, (int)cl.block_rank(), (int)cl.num_blocks(),
-                   (int)(blockIdx.x / cl.num_blocks()), (int)(G / cl.num_blocks()), A.rec};
+                   (int)(blockIdx.x / cl.num_blocks()), (int)(G / cl.num_blocks()), A.xw, A.ctl};
         while (A.N > ccap) {   // (no node is larger than a cluster's capacity otherwise)
             if (blockIdx.x == 0 && tid < 32) {
                 const Claim c = claim_node(A, 1, ccap, 0);
