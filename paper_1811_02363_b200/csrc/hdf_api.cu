@@ -252,9 +252,15 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
         const char* e = getenv("HDF_BISECT_TRACE");
         if (!(e && atoi(e) != 0)) A.trace = nullptr;
     }
-    if (const char* e = getenv("HDF_BISECT_GRID_ABOVE")) A.ccap = std::min<long long>(A.ccap, atoll(e));
+    A.gabove = A.ccap;
+    if (const char* e = getenv("HDF_BISECT_GRID_ABOVE")) {   // may lower (cluster capacity too) or raise it
+        A.gabove = std::max<long long>(1, atoll(e));
+        A.ccap = std::min<long long>(A.ccap, A.gabove);
+    }
     A.ctamax = std::min<long long>(A.cap, 2048);   // smaller nodes: one CTA each (measured best on c2b)
     if (const char* e = getenv("HDF_BISECT_CTA_MAX")) A.ctamax = std::min<long long>(A.cap, atoll(e));
+    A.qmax = 0;   // groups of 4 CTAs for nodes of at most qmax points (cluster batches; off: measured slower)
+    if (const char* e = getenv("HDF_BISECT_QUAD_MAX")) A.qmax = std::min<long long>(4LL * A.cap, atoll(e));
     {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[2];

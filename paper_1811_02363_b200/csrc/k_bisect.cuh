@@ -80,7 +80,9 @@ struct BisectArgs {
     int cap;            // points per CTA tile (multiple of kBT)
     int wcap;           // side words per CTA in the global scratch (streamed ranges)
     long long ccap;     // points a cluster keeps resident (C * cap)
-    long long ctamax;   // nodes larger than this go to cluster workers (<= cap)
+    long long gabove;   // nodes larger than this are split by the whole grid (>= ccap: clusters stream)
+    long long ctamax;   // nodes of at most this many points go to single CTAs (<= cap)
+    long long qmax;     // nodes of at most this many points go to groups of 4 CTAs (<= 4 cap)
     const float* pts[3];   // ping-pong leaf storage; pts[2] = p
     float* ptsw[2];
     int* idx[2];
@@ -311,6 +313,9 @@ struct SplitSm {
     uint64_t bar;                               // TMA mbarrier
     uint64_t xbar[2];                           // push-exchange mbarriers (by parity)
     uint64_t gbar[2];                           // grid mode: the cluster leader's record mbarriers
+    uint64_t bbar;                              // group broadcast mbarrier (PushGrp::bcast)
+    int2 bcv;                                   // group broadcast value
+    int btask[16], bcb[16], bn, bgran;          // a cluster batch: tasks of its groups, count, group size
     uint32_t tma_phase;
     int task, cbase;
 };
@@ -493,16 +498,17 @@ struct ClusterGrp {
 };
 struct PushGrp {
     int rank, size;
-    uint32_t ph;   // phase bits of S.xbar[0..1] (every thread keeps its own copy)
+    uint32_t ph;    // phase bits of S.xbar[0..1] (every thread keeps its own copy)
+    int base = 0;   // cluster rank of group rank 0 (a group is `size` consecutive CTAs of a cluster)
     static constexpr bool kGrid = false, kLocal = true;
-    HDF_DEV void sync() { cg::this_cluster().sync(); }
     HDF_DEV int nrec() const { return size; }
     HDF_DEV void exchange(SplitSm& S, int par, int nv, int = XSUM) {
         const int tid = threadIdx.x;
         if (tid == 0) mbar_arrive_expect_tx(&S.xbar[par], (uint32_t)(size * nv * 8));
         for (int t = tid; t < size * nv; t += kBT) {
             const int q = t / nv, v = t - q * nv;
-            st_async_f64(mapa_u32(smem_u32(&S.rxb[par][rank][v]), q), S.outv[v], mapa_u32(smem_u32(&S.xbar[par]), q));
+            st_async_f64(mapa_u32(smem_u32(&S.rxb[par][rank][v]), base + q), S.outv[v],
+                         mapa_u32(smem_u32(&S.xbar[par]), base + q));
         }
         mbar_wait_cluster(&S.xbar[par], (ph >> par) & 1u);
         ph ^= 1u << par;
@@ -511,12 +517,28 @@ struct PushGrp {
     // push one value of this CTA's record to every CTA of the cluster (itself included)
     HDF_DEV void send(SplitSm& S, int par, int v, double x) {
         const uint32_t la = smem_u32(&S.rxb[par][rank][v]), lb = smem_u32(&S.xbar[par]);
-        for (int q = 0; q < size; q++) st_async_f64(mapa_u32(la, q), x, mapa_u32(lb, q));
+        for (int q = 0; q < size; q++) st_async_f64(mapa_u32(la, base + q), x, mapa_u32(lb, base + q));
     }
     HDF_DEV void wait(SplitSm& S, int par, int nv) {
         if (threadIdx.x == 0) mbar_arrive_expect_tx(&S.xbar[par], (uint32_t)(size * nv * 8));
         mbar_wait_cluster(&S.xbar[par], (ph >> par) & 1u);
         ph ^= 1u << par;
+    }
+    // group rank 0's (a, b) to every CTA of the group (its own buffer and mbarrier, phase bit 2 of ph);
+    // rank 0 calls it with its warp-0 values, every thread returns them
+    HDF_DEV int2 bcast(SplitSm& S, int a, int b) {
+        const int tid = threadIdx.x;
+        if (tid == 0) mbar_arrive_expect_tx(&S.bbar, 8u);
+        if (rank == 0 && tid < size) {
+            const uint32_t la = smem_u32(&S.bcv), lb = smem_u32(&S.bbar);
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.s32 [%0], {%1, %2}, [%3];" ::"r"(
+                             mapa_u32(la, base + tid)),
+                         "r"(a), "r"(b), "r"(mapa_u32(lb, base + tid))
+                         : "memory");
+        }
+        mbar_wait_cluster(&S.bbar, (ph >> 2) & 1u);
+        ph ^= 4u;
+        return make_int2(S.bcv.x, S.bcv.y);
     }
     // only warp 0 waits (the other warps keep their phase bits in step)
     HDF_DEV void wait_warp0(SplitSm& S, int par, int nv) {
@@ -1255,9 +1277,9 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
     const int a = (int)((long long)m * r / C), e = (int)((long long)m * (r + 1) / C), np = e - a;
     const float* Pg = A.pts[buf] + (size_t)start * rho;   // the node's points
     const bool resident = (m + C - 1) / C <= A.cap;      // uniform over the group (np <= ceil(m / C))
-    // Grid mode splits every claimable node larger than a cluster's capacity and cluster mode every
-    // node larger than one CTA's, so only grid mode ever streams; guard the invariant.
-    if (!Grp::kGrid && !resident) {
+    // Nodes larger than the group's shared memory stream their points tile by tile (grid mode, and
+    // cluster mode up to gabove); the side words then live in the CTA's global scratch (guarded).
+    if (!resident && (m + C - 1) / C > 32LL * (A.wcap - 2)) {
         if (tid == 0) atomicExch(&A.ctl[B_ABORT], 2);
         return;
     }
@@ -1662,6 +1684,9 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
                 __syncthreads();
             }
         }
+        // the scatter is made visible before the SSE records are sent: the group leader publishes the
+        // children once it has every record (no separate barrier for push groups)
+        __threadfence();
         // children's SSE over the group
         double vv[2] = {se0, se1};
         const int vi = warp_reduce_scatter<2>(vv);
@@ -1680,8 +1705,7 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
     }
 
     if (lead) trace_ev(A, 13, v, worker);
-    __threadfence();
-    g.sync();   // the whole group's scatter is complete and visible
+    if constexpr (!Grp::kLocal) g.sync();   // grid / pull groups: the whole group's scatter is visible
     // ---- 6. publish the children ----
     if (lead) {
         const int c = cbase;
@@ -1712,20 +1736,21 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
         if (Grp::kGrid) atomicAdd(&A.ctl[B_GRIDSPLITS], 1);
         red_release_add64(syncword(A.ctl), (1ULL << 32) - 1ULL);
         trace_ev(A, 5, v, worker);
+        trace_ev(A, 17, c, v);   // children c, c + 1 of v (the worker field carries the parent)
     }
 }
 
 // ------------------------------------------------------------------------------- the claim ----
 // Warp-cooperative.  Chooses the FREE node of largest SSE (ties -> lowest id) with SSE > 0 and >= 2
 // members, and claims it if fewer than K-1 published nodes precede it in (SSE desc, id asc) order.
-// Only nodes larger than `bigcap` points are considered.  mode 1 (grid phase, a single claimer):
-// returns -1 when nothing is claimable.  mode 2 (cluster / CTA phases): when nothing is claimable,
+// Only nodes with bigcap < m <= maxm points are considered.  mode 1 (grid phase, a single claimer)
+// and mode 3 (a group's follow-up claim inside a cluster batch): return -1 when nothing is claimable.  mode 2 (cluster / CTA phases): when nothing is claimable,
 // waits until a publication changes the table; returns -1 once nothing is claimable and no split is
 // in progress.
 struct Claim {
     int task, cbase;
 };
-HDF_DEV Claim claim_node(const BisectArgs& A, int mode, long long bigcap, int wid) {
+HDF_DEV Claim claim_node(const BisectArgs& A, int mode, long long bigcap, int wid, long long maxm = LLONG_MAX) {
     const int lane = threadIdx.x & 31;
     int backoff = 16;
     while (true) {
@@ -1753,7 +1778,10 @@ HDF_DEV Claim claim_node(const BisectArgs& A, int mode, long long bigcap, int wi
         for (int u = 0; u < kScan; u++) {
             const int i = lane + 32 * u;
             ssev[u] = (stv[u] != ST_NONE) ? __ldcg(&A.nsse[i]) : -1.0;
-            if (stv[u] == ST_FREE && ssev[u] > 0.0 && __ldcg(&A.nm[i]) >= mmin) elig |= 1u << u;
+            if (stv[u] == ST_FREE && ssev[u] > 0.0) {
+                const int mi = __ldcg(&A.nm[i]);
+                if (mi >= mmin && mi <= maxm) elig |= 1u << u;
+            }
         }
         // Candidates in (SSE desc, id asc) order.  Idle workers start at different ranks of that order
         // (wid modulo the number of candidates, at most 8 deep) so that they do not all race for the
@@ -1814,7 +1842,7 @@ HDF_DEV Claim claim_node(const BisectArgs& A, int mode, long long bigcap, int wi
             }
             if (!skipped) break;
         }
-        if (mode == 1) return {-1, 0};
+        if (mode != 2) return {-1, 0};   // modes 1, 3: no waiting
         if (lost) continue;   // lost races: rescan at once
         int done = 0;
         if (lane == 0) {
@@ -1946,6 +1974,7 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
         mbar_init(&S.xbar[1], 1);
         mbar_init(&S.gbar[0], 1);
         mbar_init(&S.gbar[1], 1);
+        mbar_init(&S.bbar, 1);
         fence_barrier_init();
         S.tma_phase = 0;
     }
@@ -2103,12 +2132,14 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
     // ---- phase 1: nodes too large for one cluster, split by the whole grid ----
     cg::cluster_group cl = cg::this_cluster();
     const long long ccap = min(A.ccap, (long long)cl.num_blocks() * A.cap);
+    // grid mode above gabove; a cluster streams at most its CTAs' side-word scratch
+    const long long gab = max(ccap, min(A.gabove, (long long)cl.num_blocks() * 32LL * (A.wcap - 2)));
     {
         GridGrp gg{(int)blockIdx.x, G, (int)cl.block_rank(), (int)cl.num_blocks(),
                    (int)(blockIdx.x / cl.num_blocks()), (int)(G / cl.num_blocks()), A.xw, A.ctl};
-        while (A.N > ccap) {   // (no node is larger than a cluster's capacity otherwise)
+        while (A.N > gab) {   // (no node needs the grid otherwise)
             if (blockIdx.x == 0 && tid < 32) {
-                const Claim c = claim_node(A, 1, ccap, 0);
+                const Claim c = claim_node(A, 1, gab, 0);
                 if (tid == 0) {
                     A.ctl[B_TASK] = c.task;
                     A.ctl[B_TASKC] = c.cbase;
@@ -2144,8 +2175,81 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
             }
         };
         if (RHO > 0) {
-            PushGrp g{(int)cl.block_rank(), (int)cl.num_blocks(), 0u};
-            run(g);
+            // Cluster batches.  The cluster's rank 0 claims the best node; a node of at most qmax points
+            // turns the cluster into groups of 4 CTAs (at most ctamax points: single CTAs) for this
+            // batch, and rank 0 claims up to one node per group (no waiting).  A group that finishes
+            // its node claims another one of at most its size limit (no waiting) and stops when there
+            // is none; the cluster regroups when every group has stopped.
+            const int cdim = (int)cl.num_blocks(), crank = (int)cl.block_rank();
+            uint32_t ph = 0;
+            while (true) {
+                if (crank == 0 && tid < 32) {
+                    if (tid == 0) trace_ev(A, 1, 0, worker);
+                    const Claim c0 = claim_node(A, 2, 1, worker * 16);
+                    int gsz = cdim, nt = 0;
+                    int tk[16], cb[16];
+                    if (c0.task >= 0) {
+                        const int m0 = __ldcg(&A.nm[c0.task]);
+                        if (m0 <= A.ctamax) gsz = 1;
+                        else if (m0 <= A.qmax && cdim >= 4) gsz = 4;
+                        tk[0] = c0.task;
+                        cb[0] = c0.cbase;
+                        nt = 1;
+                        const long long lim = gsz == 1 ? A.ctamax : A.qmax;
+                        for (int q = 1; q < cdim / gsz; q++) {
+                            const Claim c = claim_node(A, 3, 1, worker * 16 + q, lim);
+                            if (c.task < 0) break;
+                            tk[q] = c.task;
+                            cb[q] = c.cbase;
+                            nt++;
+                        }
+                    } else {
+                        tk[0] = -1;
+                        cb[0] = 0;
+                    }
+                    // to every CTA of the cluster
+                    for (int r = 0; r < cdim; r++) {
+                        SplitSm* R = cl.map_shared_rank(&S, r);
+                        if (tid == 0) { R->bn = nt; R->bgran = gsz; }
+                        if (tid < 16) {
+                            R->btask[tid] = (tid < nt) ? tk[tid] : -1;
+                            R->bcb[tid] = (tid < nt) ? cb[tid] : 0;
+                        }
+                    }
+                }
+                cl.sync();
+                const int gsz = S.bgran, gi = crank / gsz;
+                int task = S.btask[gi], cbt = S.bcb[gi];
+                const bool done = S.btask[0] < 0;
+                if (done) break;
+                PushGrp g{crank - gi * gsz, gsz, ph, gi * gsz};
+                const long long lim = gsz == 1 ? A.ctamax : A.qmax;
+                while (task >= 0) {
+                    split_node<RHO>(A, g, S, io, task, cbt, worker * 16 + gi);
+                    if (gsz == cdim) break;   // a whole-cluster node: back to the batch level
+                    int nt = -1, nc = 0;
+                    if (g.rank == 0 && tid < 32) {
+                        const Claim c = claim_node(A, 3, 1, worker * 16 + gi, lim);
+                        nt = c.task;
+                        nc = c.cbase;
+                    }
+                    if (gsz == 1) {
+                        if (tid == 0) { S.task = nt; S.cbase = nc; }
+                        __syncthreads();
+                        task = S.task;
+                        cbt = S.cbase;
+                        __syncthreads();
+                    } else {
+                        nt = __shfl_sync(0xffffffffu, nt, 0);
+                        nc = __shfl_sync(0xffffffffu, nc, 0);
+                        const int2 tc = g.bcast(S, nt, nc);   // (rank 0: lanes < gsz hold the values)
+                        task = tc.x;
+                        cbt = tc.y;
+                    }
+                }
+                ph = g.ph;
+                cl.sync();   // the batch ends when every group has stopped
+            }
         } else {
             ClusterGrp g{(int)cl.block_rank(), (int)cl.num_blocks()};
             run(g);

@@ -52,6 +52,34 @@ for name in sys.argv[1:]:
                     cur.setdefault("ph", [0, 0, 0, 0])[tag - 20] = node / 10.0
                 elif cur is not None and tag in names:
                     cur["t"][tag] = t
+        # critical path: parent links from the tag-17 events, chain ending at the last publication
+        parent = {}
+        for w, t in tr:
+            if (w & 0xFF) == 17:
+                c, pnode = (w >> 8) & 0xFFFFF, (w >> 28) & 0xFFF
+                parent[c] = pnode
+                parent[c + 1] = pnode
+        byn = {r["node"]: r for r in rows if 5 in r["t"]}
+        if byn:
+            last = max(byn.values(), key=lambda r: r["t"][5])
+            chain, v = [], last["node"]
+            while v in byn:
+                chain.append(byn[v])
+                v = parent.get(v, -1)
+            chain.reverse()
+            tot_l = sum(r["t"].get(4, 0) - r["t"].get(3, 0) for r in chain)
+            tot_s = sum(r["t"][5] - r["t"][2] for r in chain)
+            gaps = sum(b["t"][2] - a["t"][5] for a, b in zip(chain, chain[1:]))
+            print(f"   critical chain: {len(chain)} splits, {tot_s:.1f} us in splits ({tot_l:.1f} Lloyd, "
+                  f"{sum(r['it'] for r in chain)} iterations), {gaps:.1f} us waiting between them; nodes "
+                  + " ".join(str(r["node"]) for r in chain))
+            for a, b in zip(chain, chain[1:]):
+                t0, t1 = a["t"][5], b["t"][2]
+                if t1 - t0 < 3:
+                    continue
+                busy = [f"w{r['w']}:n{r['node']}[{r['t'][2]:.0f}-{r['t'].get(5, 0):.0f}]" for r in rows
+                        if r["t"][2] < t1 and r["t"].get(5, 1e9) > t0]
+                print(f"     gap {t1 - t0:5.1f} us before node {b['node']} (ready {t0:.1f}): " + " ".join(busy))
         for rw in sorted(rows, key=lambda r: r["t"][2]):
             tt = rw["t"]
             seq = [2, 7, 14, 15, 16, 8, 9, 10, 3, 4, 11, 12, 13, 5]
