@@ -475,6 +475,27 @@ int side_stream(SideStream* out) {
     return HDF_OK;
 }
 
+using CoefKernel = void (*)(const hdf::CoefParams);
+template <int NT>
+CoefKernel coeffs_mma_rho(int rho) {
+    if (rho == 3) return hdf::k_coeffs_mma<NT, 3>;
+    if (rho == 6) return hdf::k_coeffs_mma<NT, 6>;
+    return hdf::k_coeffs_mma<NT, 0>;
+}
+CoefKernel coeffs_mma_kernel(int nt, int rho) {
+    switch (nt) {
+        case 1: return coeffs_mma_rho<1>(rho);
+        case 2: return coeffs_mma_rho<2>(rho);
+        case 3: return coeffs_mma_rho<3>(rho);
+        case 4: return coeffs_mma_rho<4>(rho);
+        case 5: return coeffs_mma_rho<5>(rho);
+        case 6: return coeffs_mma_rho<6>(rho);
+        case 7: return coeffs_mma_rho<7>(rho);
+        case 8: return coeffs_mma_rho<8>(rho);
+        default: return nullptr;
+    }
+}
+
 int nsm_of_device() {
     int dev = 0, nsm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -597,12 +618,27 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         const long long npix = (long long)H * W;
         const unsigned nblk = (unsigned)((npix + hdf::kCoefPix - 1) / hdf::kCoefPix);
         void (*kt)(const hdf::CoefParams) = nullptr;
+        void (*km)(const hdf::CoefParams) = nullptr;
+        km = coeffs_mma_kernel((K + 7) / 8, rho);   // tensor cores (3xTF32), K <= 64 padded to 8 NT
+        if (const char* e = getenv("HDF_COEFFS_FMA")) {   // diagnostics: the CUDA-core kernel instead
+            if (atoi(e)) km = nullptr;
+        }
         if (K == 8) kt = hdf::k_coeffs_t<8>;
         else if (K == 16) kt = hdf::k_coeffs_t<16>;
         else if (K == 32) kt = hdf::k_coeffs_t<32>;
         else if (K == 64) kt = hdf::k_coeffs_t<64>;
         ProfScope prof(HDF_STAGE_COEFFS, st);
-        if (kt) {   // compile-time K: b in registers, broadcast A^+ rows
+        if (km) {
+            const int nt = (K + 7) / 8;
+            const size_t smem = sizeof(float) * ((size_t)2 * nt * nt * 2 * 32 + (size_t)8 * nt * rho);
+            HDF_CUDA(cudaFuncSetAttribute(km, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const long long ntile = (npix + 15) / 16;
+            const long long want = (ntile + 7) / 8;
+            int per_sm = 1;   // resident blocks per SM: a persistent grid (A^+ staged once per block)
+            HDF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, km, hdf::kCoefMmaThreads, smem));
+            const unsigned nb = (unsigned)std::min<long long>(want, (long long)nsm * std::max(per_sm, 1));
+            km<<<nb, hdf::kCoefMmaThreads, smem, st>>>(cp);
+        } else if (kt) {   // compile-time K: b in registers, broadcast A^+ rows
             const size_t smem = sizeof(float) * ((size_t)K * K + (size_t)K * rho);
             HDF_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             kt<<<nblk, hdf::kCoefPix, smem, st>>>(cp);

@@ -311,4 +311,143 @@ __global__ void __launch_bounds__(kCoefPix) k_coeffs_t(const CoefParams P) {
     }
 }
 
+// ---------------------------------------------------------------------------------------------------
+// c(i) = A^+ b(i) on the tensor cores (K = 8 NT <= 64, zero-padded): the pixels' b vectors times
+// A^+ is a [pixels x K] x [K x K] contraction.  mma.sync m16n8k8 TF32 with the 3xTF32 split
+// (x = hi + lo, both TF32; hi*hi + hi*lo + lo*hi, fp32 accumulation) keeps fp32-level accuracy.
+// (The split: tf32_hi / tf32_lo.)  A warp takes 16 consecutive pixels per step: lane (g, t) (g = lane / 4, t = lane % 4) computes
+// b for pixels g, g + 8 and centres 8s + t, 8s + t + 4 -- exactly its A-fragment -- so every b is
+// evaluated once; the A^+ fragments (hi and lo, per (n-tile j, k-step s)) are staged in shared
+// memory in lane order (one LDS.64 each).
+constexpr int kCoefMmaThreads = 256;
+// TF32 split without cvt (which is emulated): hi = x with the low 13 mantissa bits cleared (exact in
+// TF32), lo = x - hi (exact in fp32); the tensor core reads lo's top 19 bits, so lo carries x to
+// within 2^-21 relative.  Finite inputs only.
+HDF_DEV uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
+HDF_DEV uint32_t tf32_lo(float x, uint32_t hi) { return __float_as_uint(x - __uint_as_float(hi)); }
+HDF_DEV void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+template <int NT, int RHO>   // RHO > 0: compile-time guide dimension, 0: runtime
+__global__ void __launch_bounds__(kCoefMmaThreads) k_coeffs_mma(const CoefParams P) {
+    extern __shared__ __align__(16) float smq[];
+    constexpr int K8 = 8 * NT;
+    constexpr int RR = RHO > 0 ? RHO : 1;
+    const int K = P.K, rho = RHO > 0 ? RHO : P.rho;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    uint2* Afr = reinterpret_cast<uint2*>(smq);             // [NT][NT][2 (hi, lo)][32]
+    float* mus = smq + 2 * (NT * NT * 2 * 32);              // [K8][rho], rows >= K zero
+    for (int e = tid; e < NT * NT * 32; e += kCoefMmaThreads) {
+        const int ln = e & 31, js = e >> 5, j = js / NT, sk = js - j * NT;
+        const int gg = ln >> 2, tt = ln & 3;
+        const int k = 8 * j + gg, l0 = 8 * sk + tt, l1 = l0 + 4;
+        const float a0 = (k < K && l0 < K) ? P.Ap32[k * K + l0] : 0.f;
+        const float a1 = (k < K && l1 < K) ? P.Ap32[k * K + l1] : 0.f;
+        const uint32_t h0 = tf32_hi(a0), h1 = tf32_hi(a1);
+        const uint32_t q0 = tf32_lo(a0, h0), q1 = tf32_lo(a1, h1);
+        Afr[(js * 2 + 0) * 32 + ln] = make_uint2(h0, h1);
+        Afr[(js * 2 + 1) * 32 + ln] = make_uint2(q0, q1);
+    }
+    for (int e = tid; e < K8 * rho; e += kCoefMmaThreads) mus[e] = (e < K * rho) ? P.centres[e] : 0.f;
+    __syncthreads();
+    const float c2 = P.neg_inv2sr2 * 1.4426950408889634f;
+    const long long npix = (long long)P.H * P.W;
+    const long long ntile = (npix + 15) / 16;
+    const long long tstep = (long long)gridDim.x * (kCoefMmaThreads / 32);
+    // compile-time rho: the next tile's guide values are loaded while this tile is computed
+    float xn0[RR], xn1[RR];
+    auto load_x = [&](long long tile) {
+        const long long j0 = tile * 16 + g, j1 = j0 + 8;
+        const float* q0 = P.p + (j0 < npix ? j0 : 0) * rho;
+        const float* q1 = P.p + (j1 < npix ? j1 : 0) * rho;
+#pragma unroll
+        for (int d = 0; d < RR; d++) {
+            xn0[d] = __ldg(q0 + d);
+            xn1[d] = __ldg(q1 + d);
+        }
+    };
+    const long long tile0 = (long long)blockIdx.x * (kCoefMmaThreads / 32) + warp;
+    if (RHO > 0 && tile0 < ntile) load_x(tile0);
+    for (long long tile = tile0; tile < ntile; tile += tstep) {
+        const long long i0 = tile * 16 + g, i1 = i0 + 8;
+        const bool v0 = i0 < npix, v1 = i1 < npix;
+        const float* p0 = P.p + (v0 ? i0 : 0) * rho;
+        const float* p1 = P.p + (v1 ? i1 : 0) * rho;
+        float x0[RR], x1[RR];
+        if (RHO > 0) {
+#pragma unroll
+            for (int d = 0; d < RR; d++) {
+                x0[d] = xn0[d];
+                x1[d] = xn1[d];
+            }
+            if (tile + tstep < ntile) load_x(tile + tstep);
+        }
+        auto bval = [&](int which, int l) {
+            const float* mu = mus + l * rho;
+            float d2 = 0.f;
+            if (RHO > 0) {
+#pragma unroll
+                for (int d = 0; d < RR; d++) {
+                    const float u = (which ? x1[d] : x0[d]) - mu[d];
+                    d2 = fmaf(u, u, d2);
+                }
+            } else {
+                const float* pp = which ? p1 : p0;
+                for (int d = 0; d < rho; d++) {
+                    const float u = __ldg(pp + d) - mu[d];
+                    d2 = fmaf(u, u, d2);
+                }
+            }
+            float y;
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d2 * c2));
+            return y;
+        };
+        float acc[NT][4];
+#pragma unroll
+        for (int j = 0; j < NT; j++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[j][q] = 0.f;
+#pragma unroll
+        for (int sk = 0; sk < NT; sk++) {
+            const float b[4] = {bval(0, 8 * sk + t), bval(1, 8 * sk + t), bval(0, 8 * sk + t + 4),
+                                bval(1, 8 * sk + t + 4)};
+            uint32_t ah[4], al[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                ah[q] = tf32_hi(b[q]);
+                al[q] = tf32_lo(b[q], ah[q]);
+            }
+#pragma unroll
+            for (int j = 0; j < NT; j++) {
+                const uint2 bh = Afr[((j * NT + sk) * 2 + 0) * 32 + lane];
+                const uint2 bl = Afr[((j * NT + sk) * 2 + 1) * 32 + lane];
+                mma_tf32(acc[j], al, bh.x, bh.y);
+                mma_tf32(acc[j], ah, bl.x, bl.y);
+                mma_tf32(acc[j], ah, bh.x, bh.y);
+            }
+        }
+        // lane (g, t) holds C[g][8j + 2t + {0, 1}] and C[g + 8][8j + 2t + {0, 1}]
+        const int y0 = v0 ? (int)(i0 / P.W) : 0, y1 = v1 ? (int)(i1 / P.W) : 0;
+        float* o0 = P.cpl + (long long)y0 * P.Wp + (i0 - (long long)y0 * P.W);
+        float* o1 = P.cpl + (long long)y1 * P.Wp + (i1 - (long long)y1 * P.W);
+#pragma unroll
+        for (int j = 0; j < NT; j++) {
+            const int k = 8 * j + 2 * t;
+            if (k < K) {
+                if (v0) o0[(long long)k * P.cstride] = acc[j][0];
+                if (v1) o1[(long long)k * P.cstride] = acc[j][2];
+            }
+            if (k + 1 < K) {
+                if (v0) o0[(long long)(k + 1) * P.cstride] = acc[j][1];
+                if (v1) o1[(long long)(k + 1) * P.cstride] = acc[j][3];
+            }
+        }
+    }
+}
+
 }  // namespace hdf

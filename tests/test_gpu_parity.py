@@ -83,6 +83,9 @@ def test_parity_full_size(hdf, name):
     ("c2a", 200, 333, 16),
     ("c3", 97, 129, 7),         # n = 31
     ("c4", 150, 173, 32),       # box, rho != n, flagged pixels
+    ("c2a", 96, 130, 40),       # K = 40: five 8-wide tensor-core tiles
+    ("c2a", 64, 200, 64),       # K = 64: the largest tensor-core coefficient kernel
+    ("c4", 70, 90, 12),         # rho = 6, K padded to 16
 ])
 def test_parity_ragged(hdf, name, H, W, K):
     _parity_case(hdf, name, H, W, K)
