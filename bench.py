@@ -114,7 +114,7 @@ def stage_work(cfg, K: int, H: int, W: int):
         "vpass": {"bytes": 4 * npx * (n_in + planes), "fma": npx * (planes * taps + K * (rho + 1 + n))},
         "hpass": {"bytes": 4 * npx * (planes + n),
                   "fma": npx * (planes * (taps if cfg.kind == "gaussian" else 4) + planes + n)},
-        "coeffs": {"bytes": 4 * npx * rho, "fma": npx * (K * K + K * (rho + 1))},
+        "coeffs": {"bytes": 4 * npx * rho, "fma": npx * (K * K + K * (rho + 1)), "mma_flop": 2 * npx * K * K},
         "filter": {"bytes": 4 * npx * (n_in + 2 * planes + n)},        # SURVEY 8(d) B_req
     }
 
@@ -221,7 +221,10 @@ def run_ours(args, rank: int, world: int, dist):
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
 
     # dram bytes per launch from the committed ncu --set full capture of this workload (profiles/), if any
-    kname = {"vpass": "k_range_vpass", "hpass": "k_hpass_combine", "coeffs": "k_coeffs_t"}
+    kname = {"vpass": "k_range_vpass", "hpass": "k_hpass_combine", "coeffs": "k_coeffs_mma"}
+    # tensor-core peak for the coefficient contraction (TF32): the measured bf16 peak x the nominal
+    # dense TF32 / bf16 ratio (1.1 / 2.25 PFLOP/s, B200_PROFILING.md)
+    tf32_peak = peaks.get("bf16_tflops", 2250.0) * (1.1 / 2.25) * 1e12
     traffic = {}
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")))
@@ -236,7 +239,20 @@ def run_ours(args, rank: int, world: int, dist):
         fma_s = work[name]["fma"] / t
         t_hbm = work[name]["bytes"] / (hbm_peak * 1e9)
         t_alu = work[name]["fma"] / fma_peak(sm_mhz, nsm)
-        if t_alu > t_hbm:
+        if name == "coeffs" and K <= 64:   # k_coeffs_mma: mma.sync TF32 (3xTF32 split)
+            fl = work[name]["mma_flop"] / t
+            t_tc = work[name]["mma_flop"] / tf32_peak
+            if t_tc >= t_hbm:
+                r = {"bound": "tensor", "achieved": round(fl / 1e12, 3), "peak": round(tf32_peak / 1e12, 1),
+                     "unit": "TFLOP/s (tf32)", "frac": round(fl / tf32_peak, 4),
+                     "peak_basis": "MEASURED_PEAKS bf16_tflops x 1.1/2.25 (nominal dense tf32/bf16); "
+                                   "algorithmic 2 K^2 flop/px, the 3xTF32 split issues 3x that",
+                     "hbm_achieved_gbs": round(hbm_gbs, 1), "hbm_frac": round(hbm_gbs / hbm_peak, 4)}
+            else:
+                r = {"bound": "hbm", "achieved": round(hbm_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(hbm_gbs / hbm_peak, 4), "peak_basis": "measured copy (MEASURED_PEAKS.json hbm_gbs)",
+                     "tc_achieved_tflops": round(fl / 1e12, 3)}
+        elif t_alu > t_hbm:
             r = {"bound": "alu", "achieved": round(fma_s / 1e12, 3), "peak": round(fma_peak(sm_mhz, nsm) / 1e12, 3),
                  "unit": "TFMA/s (fp32)", "frac": round(fma_s / fma_peak(sm_mhz, nsm), 4),
                  "peak_basis": f"{nsm} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (median SM clock in the timed region)",
@@ -255,12 +271,21 @@ def run_ours(args, rank: int, world: int, dist):
     if dom in work:
         roof = kernel_roof(dom)
     else:
-        # the clustering kernel: a dependent chain of Lloyd iterations and grid / cluster barriers, bound
-        # by synchronisation latency rather than by HBM or the FP32 pipe
-        roof = {"bound": "latency", "kernel": dom, "achieved": None, "peak": None, "unit": None, "frac": None,
-                "traffic": None, "ms_per_launch": round(per_launch[dom], 4),
-                "note": "dependent chain of 2-means iterations (exact bisecting K-means); see filter_roofline "
-                        "for the dominant filter kernel"}
+        # The clustering kernel against the HBM roof: its algorithmic bytes are the K-1 splits of the
+        # procedure, each reading the node's members once per Lloyd pass, then once more and writing
+        # them (coordinates + index) for the partition.  It is bound by the latency
+        # of its dependent chain of passes and exchanges, not by bandwidth, hence the low fraction.
+        _, _, info = hdf.cluster(pd, K)
+        cb = 4 * cfg.rho * (info.point_passes + info.points_split) + 4 * (cfg.rho + 1) * info.points_split
+        t = per_launch[dom] * 1e-3
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(cb / t / 1e9, 1), "peak": hbm_peak,
+                "unit": "GB/s", "frac": round(cb / t / 1e9 / hbm_peak, 4),
+                "traffic": traffic.get("k_bisect", {}).get("dram_bytes"),   # (ncu runs it without clusters)
+                "ms_per_launch": round(per_launch[dom], 4), "algorithmic_bytes": int(cb),
+                "peak_basis": "measured copy (MEASURED_PEAKS.json hbm_gbs)",
+                "note": "exact bisecting K-means: a dependent chain of 2-means passes and group exchanges "
+                        f"({info.point_passes} member-passes over the {K - 1} splits); latency-bound, see "
+                        "filter_roofline for the dominant filter kernel"}
     # the filter stage: pinv runs on a side stream concurrently with the column pass (not on the path)
     t_filter = sum(per_launch[k] for k in ("coeffs", "vpass", "hpass", "fallback")) * 1e-3
     filt = {"ms": round(t_filter * 1e3, 4), "B_req_bytes": work["filter"]["bytes"],

@@ -79,6 +79,8 @@ typedef struct {
     int32_t tile_points;     /* guide vectors a CTA keeps resident in shared memory                */
     int32_t launch_ctas;     /* CTAs of the cooperative launch                                      */
     int32_t cluster_ctas;    /* CTAs per thread-block cluster (one worker)                          */
+    int64_t point_passes;    /* sum over the K-1 splits of the procedure: members x Lloyd passes    */
+    int64_t points_split;    /* sum over the K-1 splits of the procedure: members                   */
 } hdf_cluster_info;
 
 /* Device workspace (bytes) for hdf_cluster on an H x W guide of dimension rho. */

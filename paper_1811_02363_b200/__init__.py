@@ -46,7 +46,8 @@ class HdfKError(HdfError):
 class ClusterInfo(C.Structure):
     _fields_ = [("status", C.c_int32), ("achievable_k", C.c_int32), ("splits_computed", C.c_int32),
                 ("lloyd_iters", C.c_int32), ("e_k", C.c_double), ("grid_splits", C.c_int32),
-                ("tile_points", C.c_int32), ("launch_ctas", C.c_int32), ("cluster_ctas", C.c_int32)]
+                ("tile_points", C.c_int32), ("launch_ctas", C.c_int32), ("cluster_ctas", C.c_int32),
+                ("point_passes", C.c_int64), ("points_split", C.c_int64)]
 
 
 _lib = None

@@ -130,6 +130,7 @@ hdf::BisectArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho,
     A.nparent = cv.take<int>(A.maxn);
     A.nchild = cv.take<int>(A.maxn);
     A.nbuf = cv.take<int>(A.maxn);
+    A.nit = cv.take<int>(A.maxn);
     A.nmean = cv.take<double>((size_t)A.maxn * rho);
     A.nfinal = cv.take<int>(A.maxn);
     A.ctl = cv.take<int>(hdf::B_NUM);
@@ -293,6 +294,13 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
         info->splits_computed = ctrl[hdf::B_SPLITS];
         info->lloyd_iters = ctrl[hdf::B_ITERS];
         info->grid_splits = ctrl[hdf::B_GRIDSPLITS];
+        {
+            unsigned long long pp, pm;
+            memcpy(&pp, &ctrl[hdf::B_PTPASS], 8);
+            memcpy(&pm, &ctrl[hdf::B_PTSPLIT], 8);
+            info->point_passes = (int64_t)pp;
+            info->points_split = (int64_t)pm;
+        }
         info->tile_points = sh.cap;
         info->e_k = ek;
         if (info->status == HDF_ERR_CUDA)

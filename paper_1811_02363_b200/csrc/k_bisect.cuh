@@ -69,6 +69,9 @@ enum {
     B_ABORT,       // internal error: 1 node table overflow, 2 cluster range not resident (never expected)
     B_NOTDONE,     // diagnostics: split-set nodes without a computed split (never expected)
     B_DIAG0, B_DIAG1, B_DIAG2, B_DIAG3, B_DIAG4, B_DIAG5,   // diagnostics (grid exchange timeouts)
+    B_PAD,
+    B_PTPASS, B_PTPASS_HI,     // u64: sum over the K-1 split nodes of m * (Lloyd passes) (8-byte aligned)
+    B_PTSPLIT, B_PTSPLIT_HI,   // u64: sum over the K-1 split nodes of m
     B_NUM
 };
 enum { ST_FREE = 0, ST_CLAIMED = 1, ST_DONE = 2, ST_NONE = 3 };
@@ -96,6 +99,7 @@ struct BisectArgs {
     int* nparent;
     int* nchild;
     int* nbuf;
+    int* nit;           // Lloyd passes of each computed split
     double* nmean;      // [maxn][rho]
     int* nfinal;        // [maxn] leaf id of the final leaf containing the node (labels)
     int* ctl;           // [B_NUM]
@@ -388,7 +392,10 @@ struct GridGrp {
         sq[par] = ++seq;
         const bool push = nv <= kPushV;
         pushed = push ? (pushed | (1u << par)) : (pushed & ~(1u << par));
-        if (push) {
+        if (push && csize == 1) {   // no cluster (e.g. a launch without the cluster attribute)
+            if (tid < nv) S.grx[par][0][tid] = S.outv[tid];
+            __syncthreads();
+        } else if (push) {
             if (crank == 0 && tid == 0) mbar_arrive_expect_tx(&S.gbar[par], (uint32_t)(csize * nv * 8));
             if (tid < nv)
                 st_async_f64(mapa_u32(smem_u32(&S.grx[par][crank][tid]), 0), S.outv[tid],
@@ -1726,6 +1733,7 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
             A.nmean[(size_t)(c + 1) * rho + d] = S.c1[d];
         }
         A.nchild[v] = c;
+        A.nit[v] = it + 1;
         // st.release orders the records above before each state; the sync-word update (version + 1,
         // in progress - 1, one atomic) is a release too, after the states
         st_rel(&A.nstate[c], ST_FREE);
@@ -1909,6 +1917,17 @@ HDF_DEV void finalise(const BisectArgs& A, unsigned char* dyn) {
     }
     __syncthreads();
     const int nS = s_cnt[0];
+    if (tid == 0) {   // the split set's algorithmic work (bench roofline): sum m * passes, sum m
+        unsigned long long pp = 0, pm = 0;
+        for (int i = 0; i < n; i++)
+            if (inS[i]) {
+                const unsigned long long mi = (unsigned long long)__ldcg(&A.nm[i]);
+                pp += mi * (unsigned long long)__ldcg(&A.nit[i]);
+                pm += mi;
+            }
+        *reinterpret_cast<unsigned long long*>(&A.ctl[B_PTPASS]) = pp;
+        *reinterpret_cast<unsigned long long*>(&A.ctl[B_PTSPLIT]) = pm;
+    }
     // final leaves: the root if nothing is split, else children of split nodes that are not split
     for (int i = tid; i < n; i += kBT) {
         int f = -1;

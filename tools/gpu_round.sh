@@ -11,4 +11,4 @@ timeout 900 python bench.py --all --steps 10 --no-cpu-baseline > gpurun_out/benc
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/ncu_plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo launches rc=$?
-ncu --set full --clock-control none --import-source on -k regex:"k_range_vpass|k_hpass_combine|k_coeffs" -s 3 -c 3 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo full rc=$?
+ncu --set full --clock-control none --import-source on -k regex:"k_range_vpass|k_hpass_combine|k_coeffs_mma|k_bisect" -s 4 -c 4 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo full rc=$?

@@ -42,6 +42,8 @@ METRICS = [
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma pipe %"),
     ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "fma inst %"),
     ("sm__instruction_throughput.avg.pct_of_peak_sustained_active", "issue %"),
+    ("sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active", "hmma inst %"),
+    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy %"),
     ("launch__registers_per_thread", "regs"),
     ("launch__shared_mem_per_block_dynamic", "dyn smem"),
