@@ -145,8 +145,14 @@ def run_ours(args, rank: int, world: int, dist):
     kw = dict(kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r, K=K, tau=0.5,
               out=g, ws=ws)
 
-    def step():
-        hdf.filter(fd, pd, **kw)        # centres=None: clustering runs inside the call
+    if args.variant == "hard":       # hard-assignment variant: one-hot coefficients, no A^+
+        kwh = {k: v for k, v in kw.items() if k != "tau"}
+
+        def step():
+            hdf.filter_hard(fd, None if cfg.bilateral else pd, **kwh)
+    else:
+        def step():
+            hdf.filter(fd, pd, **kw)        # centres=None: clustering runs inside the call
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
@@ -297,7 +303,9 @@ def run_ours(args, rank: int, world: int, dist):
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, SURVEY 8(d) generators)",
-        "config": workload_config(args.config, world),
+        "config": dict(workload_config(args.config, world),
+                       **({"variant": "hard (one-hot coefficients, P:341-357); e2e is the soft path's"}
+                          if args.variant == "hard" else {})),
         "stages_ms_per_step": {k: round(ms / args.steps, 4) for k, (ms, n) in prof.items() if n},
         "filter": filt, "roofline": roof, "filter_roofline": filter_roof, "gpu_launches": launches, "clocks": clk,
         "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -389,6 +397,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--all", action="store_true", help="one line per config (exploration)")
+    ap.add_argument("--variant", default="soft", choices=["soft", "hard"],
+                    help="hard: the hard-assignment variant (exploration; not the headline)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 

@@ -141,6 +141,20 @@ int hdf_filter(const float *f, int n, const float *p, int rho, int H, int W, int
                int radius, float sigma_r, int K, const float *centres, float tau, float *g,
                int32_t *n_flagged_host, void *ws, size_t ws_bytes, void *stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * hdf_filter_hard -- the hard-assignment variant (coeffICIP)/(HDapprox2): every pixel keeps
+ * only its own cluster's term, g(i) = v_s(i) / r_s(i) with s = label(i) (no pseudo-inverse, no
+ * fallback: r_s(i) >= omega(0) phi(p(i) - mu_s) > 0).  Theorem 1 bounds its error
+ * against the exact filter by C L^2 n |W|^2 E_K.
+ *   centres, labels  [K][rho] float32 and [H][W] int32 (values in [0, K)), device: both given (e.g.
+ *                    from hdf_cluster) or both NULL (clustering runs inside the call, labels kept in
+ *                    the workspace); HDF_ERR_ARG otherwise
+ *   other arguments, workspace (hdf_filter_workspace_bytes) and errors as hdf_filter; asynchronous.
+ */
+int hdf_filter_hard(const float *f, int n, const float *p, int rho, int H, int W, int kind, float sigma_s,
+                    int radius, float sigma_r, int K, const float *centres, const int32_t *labels, float *g,
+                    void *ws, size_t ws_bytes, void *stream);
+
 /*
  * hdf_filter_host -- the whole hot path end to end from HOST buffers: copies f and p to the device
  * workspace, clusters, filters, and copies g back, all on `stream`, then synchronises it.

@@ -26,7 +26,8 @@ MAX_K, MAX_RHO, MAX_N, MAX_RADIUS = 128, 64, 64, 32
 
 # every symbol include/hdf.h declares (checked by the CPU tests)
 EXPORTS = ("hdf_version", "hdf_last_error", "hdf_cluster_workspace_bytes", "hdf_cluster",
-           "hdf_filter_workspace_bytes", "hdf_filter", "hdf_filter_host_workspace_bytes", "hdf_filter_host",
+           "hdf_filter_workspace_bytes", "hdf_filter", "hdf_filter_hard", "hdf_filter_host_workspace_bytes",
+           "hdf_filter_host",
            "hdf_profile_enable", "hdf_profile_collect", "hdf_cluster_trace")
 STAGES = ("cluster", "pinv", "coeffs", "vpass", "hpass", "fallback", "h2d", "d2h")
 
@@ -72,6 +73,8 @@ def lib():
         L.hdf_filter_workspace_bytes.restype = sz
         L.hdf_filter.argtypes = [vp, i, vp, i, i, i, i, f, i, f, i, vp, f, vp, C.POINTER(C.c_int32), vp, sz, vp]
         L.hdf_filter.restype = i
+        L.hdf_filter_hard.argtypes = [vp, i, vp, i, i, i, i, f, i, f, i, vp, vp, vp, vp, sz, vp]
+        L.hdf_filter_hard.restype = i
         L.hdf_filter_host_workspace_bytes.argtypes = [i, i, i, i, i, i, f, i]
         L.hdf_filter_host_workspace_bytes.restype = sz
         L.hdf_filter_host.argtypes = [vp, i, vp, i, i, i, i, f, i, f, i, f, vp, vp, C.POINTER(C.c_int32),
@@ -204,6 +207,45 @@ def filter(f: torch.Tensor, p: torch.Tensor | None = None, *, kind: str = "gauss
     if st not in (OK, WARN_ILLCOND):
         _raise(st)
     return FilterResult(g, nfl.value if count_flagged else None, st)
+
+
+def filter_hard(f: torch.Tensor, p: torch.Tensor | None = None, *, kind: str = "gaussian", sigma_s: float = 1.0,
+                radius: int = -1, sigma_r: float = 1.0, K: int = 16, centres: torch.Tensor | None = None,
+                labels: torch.Tensor | None = None, out: torch.Tensor | None = None, ws: Workspace | None = None,
+                stream=None) -> torch.Tensor:
+    """Hard-assignment variant (coeffICIP)/(HDapprox2): g(i) = v_s(i) / r_s(i), s = label(i).
+
+    centres [K,rho] and labels [H,W] int32 (e.g. from cluster(..., labels=True)) together, or neither
+    (the library clusters p first)."""
+    f = _dev_f32(f, "f")
+    if p is None:
+        p = f
+    p = _dev_f32(p, "p")
+    H, W, n = _hwc(f, "f")
+    Hp, Wp, rho = _hwc(p, "p")
+    if (Hp, Wp) != (H, W):
+        raise ValueError("f and p must have the same H, W")
+    if (centres is None) != (labels is None):
+        raise ValueError("pass both centres and labels, or neither")
+    if centres is not None:
+        centres = _dev_f32(centres, "centres")
+        if centres.dim() != 2 or centres.shape[1] != rho:
+            raise ValueError("centres must be [K, rho]")
+        K = centres.shape[0]
+        if not (labels.is_cuda and labels.dtype == torch.int32 and labels.is_contiguous()
+                and labels.numel() == H * W):
+            raise TypeError("labels must be a contiguous int32 CUDA tensor of H*W elements")
+    g = out if out is not None else torch.empty((H, W, n), dtype=torch.float32, device=f.device)
+    g = _dev_f32(g, "out")
+    need = filter_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius)
+    wsb = (ws or _default_ws).get(need, f.device)
+    st = lib().hdf_filter_hard(f.data_ptr(), n, p.data_ptr(), rho, H, W, KIND[kind], float(sigma_s), int(radius),
+                               float(sigma_r), int(K), centres.data_ptr() if centres is not None else None,
+                               labels.data_ptr() if labels is not None else None, g.data_ptr(), wsb.data_ptr(),
+                               wsb.numel(), _stream_ptr(stream))
+    if st != OK:
+        _raise(st)
+    return g
 
 
 def filter_host(f_host: torch.Tensor, p_host: torch.Tensor | None = None, *, kind: str = "gaussian",

@@ -401,6 +401,7 @@ struct FilterWS {
     int* status;
     int* flag_count;
     int* flag_list;
+    int* labels;      // internal labels (hard variant, when the caller passes NULL)
     float* centres;   // internal centres (when the caller passes NULL)
     void* cluster_ws;
 };
@@ -416,6 +417,7 @@ FilterWS carve_filter(Carver& cv, int H, int W, int n, int rho, int K, int Wp, b
     w.status = cv.take<int>(4);
     w.flag_count = w.status + 1;
     w.flag_list = cv.take<int>((size_t)H * W);
+    w.labels = cv.take<int>((size_t)H * W);
     w.centres = cv.take<float>((size_t)K * rho);
     w.cluster_ws = nullptr;
     if (with_cluster) {
@@ -522,9 +524,11 @@ void fill_taps(float* taps, int kind, float sigma_s, int R, int Rp) {
     }
 }
 
+// hard: the hard-assignment variant: c = one-hot(label), no A^+, no fallback (tau = 0).
+// hard_labels: the caller's labels (with its centres), or NULL to cluster here (labels in the workspace).
 int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int kind, float sigma_s, int radius,
                float sigma_r, int K, const float* centres, float tau, float* g, int32_t* n_flagged_host, void* ws,
-               size_t ws_bytes, cudaStream_t st) {
+               size_t ws_bytes, cudaStream_t st, bool hard = false, const int32_t* hard_labels = nullptr) {
     int rc = check_common(H, W, rho, K);
     if (rc) return rc;
     if (!f || !p || !g || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
@@ -544,11 +548,14 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     FilterWS w = carve_filter(cv, H, W, n, rho, K, F.Wp, true);
     const float neg_inv2sr2 = (float)(-1.0 / (2.0 * (double)sigma_r * (double)sigma_r));
 
+    if (hard) tau = 0.5f;   // small r_s(i): the direct window sum with mu_s (k_fallback, hard mode)
     // step 1 (optional): cluster the guide inside this call
     if (!centres) {
-        rc = launch_cluster(p, H, W, rho, K, w.centres, nullptr, nullptr, w.cluster_ws, st);
+        int32_t* lab = hard ? w.labels : nullptr;
+        rc = launch_cluster(p, H, W, rho, K, w.centres, lab, nullptr, w.cluster_ws, st);
         if (rc) return rc;
         centres = w.centres;
+        if (hard) hard_labels = lab;
     }
     // step 2: A and A^+ (one CTA, fp64) on the side stream, concurrent with the column pass
     SideStream ss;
@@ -556,7 +563,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     if (rc) return rc;
     HDF_CUDA(cudaEventRecord(ss.fork, st));
     HDF_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
-    {
+    if (!hard) {
         hdf::PinvOut po{w.Ap32, w.Ap64, w.status, w.Vscratch};
         const size_t smem = hdf::pinv_smem_bytes(K);
         HDF_CUDA(cudaFuncSetAttribute(hdf::k_gram_pinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -567,6 +574,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     }
     HDF_CUDA(cudaEventRecord(ss.join, ss.s));
     HDF_CUDA(cudaMemsetAsync(w.flag_count, 0, sizeof(int), st));
+    if (hard) HDF_CUDA(cudaMemsetAsync(w.status, 0, sizeof(int), st));
     float taps[hdf::kMaxTaps];
     fill_taps(taps, kind, sigma_s, F.R, F.Rp);
     // F1: range weights + column pass
@@ -636,7 +644,11 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         else if (K == 32) kt = hdf::k_coeffs_t<32>;
         else if (K == 64) kt = hdf::k_coeffs_t<64>;
         ProfScope prof(HDF_STAGE_COEFFS, st);
-        if (km) {
+        if (hard) {
+            const long long ntot = npix;
+            const unsigned nb = (unsigned)std::min<long long>((ntot + 255) / 256, (long long)nsm * 16);
+            hdf::k_coeffs_onehot<<<nb, 256, 0, st>>>(hard_labels, w.cpl, (long long)H * F.Wp, H, W, F.Wp, K);
+        } else if (km) {
             const int nt = (K + 7) / 8;
             const size_t smem = sizeof(float) * ((size_t)2 * nt * nt * 2 * 32 + (size_t)8 * nt * rho);
             HDF_CUDA(cudaFuncSetAttribute(km, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -702,6 +714,8 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         fb.W = W;
         fb.R = F.R;
         fb.neg_inv2sr2 = neg_inv2sr2;
+        fb.mu = hard ? centres : nullptr;
+        fb.labels = hard ? hard_labels : nullptr;
         float t2[hdf::kMaxTaps];
         fill_taps(t2, kind, sigma_s, F.R, F.R);
         memcpy(fb.taps, t2, sizeof(t2));
@@ -846,6 +860,17 @@ int hdf_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     g_err.clear();
     return run_filter(f, n, p, rho, H, W, kind, sigma_s, radius, sigma_r, K, centres, tau, g, n_flagged_host, ws,
                       ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int hdf_filter_hard(const float* f, int n, const float* p, int rho, int H, int W, int kind, float sigma_s, int radius,
+                    float sigma_r, int K, const float* centres, const int32_t* labels, float* g, void* ws,
+                    size_t ws_bytes, void* stream) {
+    g_err.clear();
+    if ((centres == nullptr) != (labels == nullptr))
+        return fail(HDF_ERR_ARG, "hdf_filter_hard: pass both centres and labels, or neither");
+    if (labels && misaligned(labels)) return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
+    return run_filter(f, n, p, rho, H, W, kind, sigma_s, radius, sigma_r, K, centres, 0.f, g, nullptr, ws, ws_bytes,
+                      static_cast<cudaStream_t>(stream), true, labels);
 }
 
 size_t hdf_filter_host_workspace_bytes(int H, int W, int n, int rho, int K, int kind, float sigma_s, int radius) {

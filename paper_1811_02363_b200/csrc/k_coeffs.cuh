@@ -450,4 +450,17 @@ __global__ void __launch_bounds__(kCoefMmaThreads) k_coeffs_mma(const CoefParams
     }
 }
 
+// Hard-assignment variant (coeffICIP)/(HDapprox2): c(i) = one-hot(label(i)), so the row
+// pass's combine gives g(i) = v_s(i) / r_s(i), s = label(i).  Plane k, row y, column x.
+__global__ void __launch_bounds__(256) k_coeffs_onehot(const int32_t* labels, float* cpl, long long cstride, int H,
+                                                       int W, int Wp, int K) {
+    const long long npix = (long long)H * W;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < npix; i += (long long)gridDim.x * blockDim.x) {
+        const int y = (int)(i / W), x = (int)(i - (long long)y * W);
+        const int s = __ldg(labels + i);
+        float* o = cpl + (long long)y * Wp + x;
+        for (int k = 0; k < K; k++) o[(long long)k * cstride] = (k == s) ? 1.f : 0.f;
+    }
+}
+
 }  // namespace hdf

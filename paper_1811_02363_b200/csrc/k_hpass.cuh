@@ -214,6 +214,8 @@ struct FBParams {
     int n, rho, H, W, R;
     float neg_inv2sr2;
     float taps[kMaxTaps];
+    const float* mu;           // hard variant: centres [K][rho] and labels [H*W]: the range kernel is
+    const int32_t* labels;     // phi(p(j) - mu_{label(i)}); NULL: phi(p(j) - p(i))
 };
 
 static __global__ void __launch_bounds__(256) k_fallback(const __grid_constant__ FBParams P) {
@@ -225,7 +227,26 @@ static __global__ void __launch_bounds__(256) k_fallback(const __grid_constant__
     for (int t = gw; t < cnt; t += nw) {
         const int i = P.flag_list[t];
         const int y = i / P.W, x = i % P.W;
-        const float* pi = P.p + (long long)i * P.rho;
+        const float* pi = P.labels ? P.mu + (long long)__ldg(P.labels + i) * P.rho : P.p + (long long)i * P.rho;
+        // hard variant: the window's weights are scaled by exp(-d2min / (2 sr^2)) (the ratio is
+        // unchanged) so that a window far from its centre does not underflow
+        float dmin = 0.f;
+        if (P.labels) {
+            dmin = INFINITY;
+            for (int e = lane; e < win; e += 32) {
+                const int ty = e / side - P.R, tx = e % side - P.R;
+                const int yy = y - ty, xx = x - tx;
+                if (yy < 0 || yy >= P.H || xx < 0 || xx >= P.W) continue;
+                const float* pj = P.p + ((long long)yy * P.W + xx) * P.rho;
+                float d2 = 0.f;
+                for (int d = 0; d < P.rho; d++) {
+                    const float dd = pj[d] - pi[d];
+                    d2 = fmaf(dd, dd, d2);
+                }
+                dmin = fminf(dmin, d2);
+            }
+            for (int o = 16; o > 0; o >>= 1) dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+        }
         for (int c0 = 0; c0 < P.n; c0 += 8) {
             float num[8];
             float den = 0.f;
@@ -242,7 +263,7 @@ static __global__ void __launch_bounds__(256) k_fallback(const __grid_constant__
                     float dd = pj[d] - pi[d];
                     d2 = fmaf(dd, dd, d2);
                 }
-                const float wt = P.taps[ty + P.R] * P.taps[tx + P.R] * expf(d2 * P.neg_inv2sr2);
+                const float wt = P.taps[ty + P.R] * P.taps[tx + P.R] * expf((d2 - dmin) * P.neg_inv2sr2);
                 den += wt;
 #pragma unroll
                 for (int u = 0; u < 8; u++)

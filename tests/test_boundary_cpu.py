@@ -25,7 +25,7 @@ def lib():
 
 def test_header_declares_the_entry_points():
     names = _declared()
-    for want in ("hdf_cluster", "hdf_filter", "hdf_filter_host", "hdf_last_error"):
+    for want in ("hdf_cluster", "hdf_filter", "hdf_filter_hard", "hdf_filter_host", "hdf_last_error"):
         assert want in names
 
 
@@ -54,6 +54,9 @@ def test_argument_errors_before_any_launch(lib):
     assert st == hdf.ERR_ARG and b"NULL" in lib.hdf_last_error()
     st = lib.hdf_cluster(None, 8, 8, 3, 0, None, None, None, None, 0, None)
     assert st == hdf.ERR_ARG
+    # hard variant: centres without labels (or the reverse) is an argument error
+    st = lib.hdf_filter_hard(None, 3, None, 3, 8, 8, 0, 1.0, -1, 1.0, 2, C.c_void_p(16), None, None, None, 0, None)
+    assert st == hdf.ERR_ARG and b"both" in lib.hdf_last_error()
     st = lib.hdf_cluster(None, 8, 8, 3, hdf.MAX_K + 1, None, None, None, None, 0, None)
     assert st == hdf.ERR_ARG
 

@@ -231,3 +231,37 @@ def test_cluster_k_too_large(hdf):
     with pytest.raises(hdf.HdfKError) as e:
         hdf.cluster(_dev(p), 7)
     assert e.value.achievable == 5
+
+
+# ------------------------------------------------------- hard-assignment variant (NEXT #2) --------
+@pytest.mark.parametrize("name,H,W,K", [("c1", None, None, 8), ("c2a", 200, 333, 16), ("c4", 150, 173, 32),
+                                        ("c3", 97, 129, 7)])
+def test_parity_hard_variant(hdf, name, H, W, K):
+    """hdf_filter_hard against oracle.filter_hard on the oracle's centres and labels."""
+    cfg, f, p = synth.make(name, H, W)
+    K = K or cfg.K
+    cen, lab, _, _ = oracle.cluster(p, K)
+    g_ref = oracle.filter_hard(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, cen, lab, r=cfg.radius)
+    fd = _dev(f)
+    pd = fd if cfg.bilateral else _dev(p)
+    labd = torch.from_numpy(np.ascontiguousarray(lab.reshape(f.shape[0], f.shape[1]), dtype=np.int32)).cuda()
+    g = hdf.filter_hard(fd, None if cfg.bilateral else pd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius,
+                        sigma_r=cfg.sigma_r, centres=_dev(cen.astype(np.float32)), labels=labd)
+    d = np.abs(g.cpu().numpy().astype(np.float64) - g_ref) * (255.0 / cfg.R_range)
+    assert d.max() <= 1e-2 and d.mean() <= 1e-3, (d.max(), d.mean())
+
+
+def test_hard_variant_clusters_inside_and_obeys_theorem1(hdf):
+    """Centres and labels computed inside the call; the result obeys Theorem 1 (the P11
+    pin's form): sum ||g_hard - g||^2 <= C L^2 n |W|^2 E_K, C = 2 sqrt(R)/(omega(0) phi(0)) with R the
+    intensity range, L = e^{-1/2}/sigma_r, |W| = (2 r + 1)^2 window pixels."""
+    cfg, f, p = synth.make("c1")
+    fd = _dev(f)
+    g = hdf.filter_hard(fd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r, K=cfg.K)
+    _, _, info = hdf.cluster(fd, cfg.K)
+    gb, _ = oracle.bruteforce(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, r=cfg.radius)
+    lhs = ((g.cpu().numpy().astype(np.float64) - gb) ** 2).sum()
+    C = 2.0 * np.sqrt(cfg.R_range) / 1.0
+    L = np.exp(-0.5) / cfg.sigma_r
+    rhs = C * L * L * f.shape[2] * ((2 * cfg.radius + 1) ** 2) ** 2 * info.e_k
+    assert 0.0 < lhs <= rhs
