@@ -1147,7 +1147,8 @@ HDF_DEV void pass_small(const float* X, int tn, const Words& Wd, bool cmp, bool 
 #pragma unroll
         for (int h = 0; h < U; h++) {
             const int wi = (j0 >> 5) + h * kBW + warp;
-            const bool has = j0 + h * kBT < tn;   // uniform
+            // (per warp: a word past the range may belong to the next streamed tile -- never touch it)
+            const bool has = j0 + h * kBT + warp * 32 < tn;
             pw[h] = (cmp && has) ? Wd.ld_prev(wi) : 0u;
             const int j = j0 + h * kBT + tid;
             const bool ok = j < tn;
@@ -1181,9 +1182,9 @@ HDF_DEV void pass_small(const float* X, int tn, const Words& Wd, bool cmp, bool 
 #pragma unroll
         for (int h = 0; h < U; h++) {
             const uint32_t w = __ballot_sync(0xffffffffu, sd[h]);
-            const bool has = j0 + h * kBT < tn;
+            const bool has = j0 + h * kBT + warp * 32 < tn;
             if (lane == 0 && has) Wd.st_cur((j0 >> 5) + h * kBW + warp, w);
-            if (cmp) chg += __popc(w ^ pw[h]);
+            if (cmp && has) chg += __popc(w ^ pw[h]);
             n1 += __popc(w);
             mk[h] = full ? w : (w ^ pw[h]);   // points whose sum term changes
             anym |= mk[h];
@@ -1233,7 +1234,7 @@ HDF_DEV void pass_side_generic(const float* X, int tn, int rho, const Words& Wd,
             sd = side_of(x, rho, a0, a1, kd, kc, S);
         }
         const uint32_t w = __ballot_sync(0xffffffffu, sd != 0);
-        if (lane == 0) {
+        if (lane == 0 && j0 + warp * 32 < tn) {   // (words past the range: the next tile's)
             const int wi = (j0 >> 5) + warp;
             if (cmp) chg += __popc(w ^ Wd.ld_prev(wi));
             Wd.st_cur(wi, w);
