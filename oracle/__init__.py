@@ -12,6 +12,7 @@ Functions follow PAPER.md (see the C file for per-function citations):
   bruteforce     (num)/(den), window clipped to Omega (R8)
   nystrom        Appendix A identity written as a direct window sum
   filter_hard    hard-assignment variant (coeffICIP)/(HDapprox2)
+  pca_guide      PCA-NLM patch guide (reading R11), numpy fp64
   conv2          omega * x with the clipped window
   mse, psnr      (rmse), intensities normalised by R
 """
@@ -292,3 +293,34 @@ def mse(a, b, R: float = 1.0) -> float:
 def psnr(a, b, R: float = 1.0) -> float:
     m = mse(a, b, R)
     return float("inf") if m == 0.0 else float(-10.0 * np.log10(m))
+
+
+# ------------------------------------------------------------------ PCA-NLM patch guide ----------
+def pca_guide(img, m: int = 3, dim: int = 6):
+    """NLM guide (reading R11): p(i) = the m x m patch of img around i (all n channels,
+    rho = n m^2 values in (channel, dy, dx) order; replicate borders), mean-centred over all pixels
+    and projected on the `dim` leading eigenvectors of the patch covariance (PCA-NLM).
+    Eigenvectors in descending eigenvalue order, each signed so that its entry of largest magnitude
+    is positive.  fp64.  Returns (guide [H, W, dim], basis [n m^2, dim], mean [n m^2], eigenvalues)."""
+    x = _d(img)
+    H, W, n = x.shape
+    r = m // 2
+    cols = []
+    for c in range(n):
+        for dy in range(-r, r + 1):
+            for dx in range(-r, r + 1):
+                yy = np.clip(np.arange(H) + dy, 0, H - 1)
+                xx = np.clip(np.arange(W) + dx, 0, W - 1)
+                cols.append(x[yy][:, xx, c])
+    P = np.stack(cols, axis=-1).reshape(H * W, n * m * m)
+    mean = P.mean(axis=0)
+    Pc = P - mean
+    C = (Pc.T @ Pc) / P.shape[0]
+    evals, evecs = np.linalg.eigh(C)
+    order = np.argsort(-evals, kind="stable")[:dim]
+    B = evecs[:, order].copy()
+    for j in range(dim):
+        k = int(np.argmax(np.abs(B[:, j])))
+        if B[k, j] < 0:
+            B[:, j] = -B[:, j]
+    return (Pc @ B).reshape(H, W, dim), B, mean, evals[order]

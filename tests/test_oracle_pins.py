@@ -403,3 +403,48 @@ def test_p13_thread_count_independent():
         env = dict(os.environ, OMP_NUM_THREADS=t, PYTHONPATH=root)
         outs.add(subprocess.check_output([sys.executable, "-c", code], env=env, cwd=root).strip())
     assert len(outs) == 1
+
+
+# ------------------------------------------------------- PCA-NLM patch guide (NEXT #3) -----------
+def _patch_bruteforce(img, i, j, m):
+    """The patch of pixel (i, j) written out: channel-major, rows then columns, replicate borders."""
+    H, W, n = img.shape
+    r = m // 2
+    return np.array([img[min(max(i + dy, 0), H - 1), min(max(j + dx, 0), W - 1), c]
+                     for c in range(n) for dy in range(-r, r + 1) for dx in range(-r, r + 1)])
+
+
+def test_pca_guide_full_rank_reconstructs_patches():
+    """With dim = n m^2 the projection is invertible: guide @ B^T + mean gives back every patch, which
+    is checked against patches written out pixel by pixel (order, borders, centring)."""
+    rng = np.random.default_rng(7)
+    img = rng.uniform(0, 255, (6, 7, 2))
+    g, B, mu, ev = oracle.pca_guide(img, 3, 18)
+    rec = g.reshape(-1, 18) @ B.T + mu
+    for (i, j) in [(0, 0), (0, 6), (5, 0), (5, 6), (2, 3), (3, 1)]:
+        assert np.allclose(rec[i * 7 + j], _patch_bruteforce(img, i, j, 3), atol=1e-9)
+
+
+def test_pca_guide_matches_svd_and_is_orthonormal():
+    """Independent route: the right singular vectors of the centred patch matrix (SVD) span the same
+    leading directions with eigenvalues s^2 / N; the basis is orthonormal, sorted, sign-normalised."""
+    rng = np.random.default_rng(8)
+    img = rng.uniform(0, 1, (12, 10, 3))
+    g, B, mu, ev = oracle.pca_guide(img, 3, 6)
+    P = np.stack([_patch_bruteforce(img, i, j, 3) for i in range(12) for j in range(10)])
+    Pc = P - P.mean(0)
+    U, s, Vt = np.linalg.svd(Pc, full_matrices=False)
+    assert np.allclose(ev, (s[:6] ** 2) / P.shape[0], rtol=1e-10)
+    for k in range(6):
+        v = Vt[k] * np.sign(Vt[k][np.argmax(np.abs(Vt[k]))])
+        assert np.allclose(B[:, k], v, atol=1e-8)
+    assert np.allclose(B.T @ B, np.eye(6), atol=1e-12)
+    assert all(ev[k] >= ev[k + 1] for k in range(5))
+    assert all(B[np.argmax(np.abs(B[:, k])), k] > 0 for k in range(6))
+    cov = g.reshape(-1, 6).T @ g.reshape(-1, 6) / P.shape[0]
+    assert np.allclose(cov, np.diag(ev), atol=1e-9 * ev[0])
+
+
+def test_pca_guide_constant_image_is_zero():
+    g, B, mu, ev = oracle.pca_guide(np.full((5, 6, 3), 42.0), 3, 4)
+    assert np.all(g == 0.0) and np.allclose(mu, 42.0)
