@@ -142,6 +142,24 @@ int hdf_filter(const float *f, int n, const float *p, int rho, int H, int W, int
                int32_t *n_flagged_host, void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * hdf_pca_guide -- PCA-NLM guide on the GPU (reading R11).
+ *   p(i) = the m x m patch of f around i, all n channels (D = n m^2 values, channel-major then rows
+ *   then columns; replicate borders), minus the mean patch, projected on the `dim` leading
+ *   eigenvectors of the patch covariance (fp64 moments and Jacobi eigen-decomposition; descending
+ *   eigenvalues; each eigenvector signed so that its entry of largest magnitude is positive).
+ *   f          [H][W][n] float32, device (read only)
+ *   m          odd patch side; D = n m^2 <= 64
+ *   dim        1 <= dim <= min(D, 32)
+ *   p          [H][W][dim] float32, device, out: the guide (usable as hdf_filter's p)
+ *   basis_out  [dim][D] float32, device, out (or NULL): the projection basis
+ *   ws         device workspace of at least hdf_pca_guide_workspace_bytes(H, W, n, m, dim)
+ * Errors: HDF_ERR_ARG (sizes, NULL, alignment), HDF_ERR_WORKSPACE; asynchronous on `stream`.
+ */
+size_t hdf_pca_guide_workspace_bytes(int H, int W, int n, int m, int dim);
+int hdf_pca_guide(const float *f, int H, int W, int n, int m, int dim, float *p, float *basis_out, void *ws,
+                  size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------------
  * hdf_filter_hard -- the hard-assignment variant (coeffICIP)/(HDapprox2): every pixel keeps
  * only its own cluster's term, g(i) = v_s(i) / r_s(i) with s = label(i) (no pseudo-inverse, no
  * fallback: r_s(i) >= omega(0) phi(p(i) - mu_s) > 0).  Theorem 1 bounds its error

@@ -27,7 +27,7 @@ MAX_K, MAX_RHO, MAX_N, MAX_RADIUS = 128, 64, 64, 32
 # every symbol include/hdf.h declares (checked by the CPU tests)
 EXPORTS = ("hdf_version", "hdf_last_error", "hdf_cluster_workspace_bytes", "hdf_cluster",
            "hdf_filter_workspace_bytes", "hdf_filter", "hdf_filter_hard", "hdf_filter_host_workspace_bytes",
-           "hdf_filter_host",
+           "hdf_filter_host", "hdf_pca_guide_workspace_bytes", "hdf_pca_guide",
            "hdf_profile_enable", "hdf_profile_collect", "hdf_cluster_trace")
 STAGES = ("cluster", "pinv", "coeffs", "vpass", "hpass", "fallback", "h2d", "d2h")
 
@@ -73,6 +73,10 @@ def lib():
         L.hdf_filter_workspace_bytes.restype = sz
         L.hdf_filter.argtypes = [vp, i, vp, i, i, i, i, f, i, f, i, vp, f, vp, C.POINTER(C.c_int32), vp, sz, vp]
         L.hdf_filter.restype = i
+        L.hdf_pca_guide_workspace_bytes.argtypes = [i, i, i, i, i]
+        L.hdf_pca_guide_workspace_bytes.restype = sz
+        L.hdf_pca_guide.argtypes = [vp, i, i, i, i, i, vp, vp, vp, sz, vp]
+        L.hdf_pca_guide.restype = i
         L.hdf_filter_hard.argtypes = [vp, i, vp, i, i, i, i, f, i, f, i, vp, vp, vp, vp, sz, vp]
         L.hdf_filter_hard.restype = i
         L.hdf_filter_host_workspace_bytes.argtypes = [i, i, i, i, i, i, f, i]
@@ -246,6 +250,24 @@ def filter_hard(f: torch.Tensor, p: torch.Tensor | None = None, *, kind: str = "
     if st != OK:
         _raise(st)
     return g
+
+
+def pca_guide(f: torch.Tensor, m: int = 3, dim: int = 6, *, basis: bool = False, ws: Workspace | None = None,
+              stream=None):
+    """PCA-NLM guide: m x m x n patches of f projected on the `dim` leading eigenvectors of
+    their covariance.  Returns the guide [H, W, dim] (and the basis [dim, n m^2] with basis=True)."""
+    f = _dev_f32(f, "f")
+    H, W, n = _hwc(f, "f")
+    p = torch.empty((H, W, dim), dtype=torch.float32, device=f.device)
+    B = torch.empty((dim, n * m * m), dtype=torch.float32, device=f.device) if basis else None
+    need = int(lib().hdf_pca_guide_workspace_bytes(H, W, n, int(m), int(dim)))
+    wsb = (ws or _default_ws).get(max(need, 256), f.device)
+    st = lib().hdf_pca_guide(f.data_ptr(), H, W, n, int(m), int(dim), p.data_ptr(),
+                             B.data_ptr() if B is not None else None, wsb.data_ptr(), wsb.numel(),
+                             _stream_ptr(stream))
+    if st != OK:
+        _raise(st)
+    return (p, B) if basis else p
 
 
 def filter_host(f_host: torch.Tensor, p_host: torch.Tensor | None = None, *, kind: str = "gaussian",

@@ -15,6 +15,7 @@
 #include "hdf_dispatch.h"
 #include "k_bisect.cuh"
 #include "k_coeffs.cuh"
+#include "k_guide.cuh"
 
 namespace {
 
@@ -871,6 +872,57 @@ int hdf_filter_hard(const float* f, int n, const float* p, int rho, int H, int W
     if (labels && misaligned(labels)) return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
     return run_filter(f, n, p, rho, H, W, kind, sigma_s, radius, sigma_r, K, centres, 0.f, g, nullptr, ws, ws_bytes,
                       static_cast<cudaStream_t>(stream), true, labels);
+}
+
+// ------------------------------------------------------------------ PCA-NLM guide (NEXT #3) ----
+size_t hdf_pca_guide_workspace_bytes(int H, int W, int n, int m, int dim) {
+    if (H < 1 || W < 1 || n < 1 || m < 1 || dim < 1) return 0;
+    const int D = n * m * m;
+    if (D > hdf::kPcaMaxD) return 0;
+    Carver cv(nullptr);
+    cv.take<double>((size_t)hdf::kPcaGrid * (D + D * (D + 1) / 2));
+    cv.take<float>((size_t)hdf::kPcaMaxDim * D);
+    cv.take<float>((size_t)D);
+    cv.take<double>((size_t)hdf::kPcaMaxDim);
+    return cv.off + 256;
+}
+
+int hdf_pca_guide(const float* f, int H, int W, int n, int m, int dim, float* p, float* basis_out, void* ws,
+                  size_t ws_bytes, void* stream) {
+    g_err.clear();
+    if (!f || !p || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
+    if (H < 1 || W < 1 || n < 1) return fail(HDF_ERR_ARG, "H, W, n must be >= 1");
+    if (m < 1 || m % 2 == 0) return fail(HDF_ERR_ARG, "patch side m must be odd and >= 1 (got %d)", m);
+    const int D = n * m * m;
+    if (D > hdf::kPcaMaxD) return fail(HDF_ERR_ARG, "patch dimension n m^2 = %d exceeds %d", D, hdf::kPcaMaxD);
+    if (dim < 1 || dim > D || dim > hdf::kPcaMaxDim)
+        return fail(HDF_ERR_ARG, "dim must be in [1, min(n m^2, %d)] (got %d)", hdf::kPcaMaxDim, dim);
+    if (misaligned(f) || misaligned(p) || misaligned(ws)) return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
+    const size_t need = hdf_pca_guide_workspace_bytes(H, W, n, m, dim);
+    if (ws_bytes < need) return fail(HDF_ERR_WORKSPACE, "workspace %zu < required %zu bytes", ws_bytes, need);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Carver cv(ws);
+    double* part = cv.take<double>((size_t)hdf::kPcaGrid * (D + D * (D + 1) / 2));
+    hdf::PcaOut po;
+    po.basis = cv.take<float>((size_t)hdf::kPcaMaxDim * D);
+    po.mean = cv.take<float>((size_t)D);
+    po.evals = cv.take<double>((size_t)hdf::kPcaMaxDim);
+    const long long N = (long long)H * W;
+    hdf::k_pca_moments<<<hdf::kPcaGrid, hdf::kPcaThreads, 0, st>>>(f, H, W, n, m, part);
+    HDF_CUDA(cudaGetLastError());
+    HDF_CUDA(cudaFuncSetAttribute(hdf::k_pca_eig, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)hdf::pca_eig_smem()));
+    hdf::k_pca_eig<<<1, hdf::kPcaThreads, hdf::pca_eig_smem(), st>>>(part, hdf::kPcaGrid, D, dim, N, po);
+    HDF_CUDA(cudaGetLastError());
+    const unsigned nb = (unsigned)std::min<long long>((N + hdf::kPcaThreads - 1) / hdf::kPcaThreads, 148LL * 8);
+    if (dim <= 8) hdf::k_pca_project<8><<<nb, hdf::kPcaThreads, 0, st>>>(f, H, W, n, m, dim, po.basis, po.mean, p);
+    else if (dim <= 16)
+        hdf::k_pca_project<16><<<nb, hdf::kPcaThreads, 0, st>>>(f, H, W, n, m, dim, po.basis, po.mean, p);
+    else hdf::k_pca_project<32><<<nb, hdf::kPcaThreads, 0, st>>>(f, H, W, n, m, dim, po.basis, po.mean, p);
+    HDF_CUDA(cudaGetLastError());
+    if (basis_out)
+        HDF_CUDA(cudaMemcpyAsync(basis_out, po.basis, sizeof(float) * (size_t)dim * D, cudaMemcpyDeviceToDevice, st));
+    return HDF_OK;
 }
 
 size_t hdf_filter_host_workspace_bytes(int H, int W, int n, int rho, int K, int kind, float sigma_s, int radius) {

@@ -57,6 +57,12 @@ def test_argument_errors_before_any_launch(lib):
     # hard variant: centres without labels (or the reverse) is an argument error
     st = lib.hdf_filter_hard(None, 3, None, 3, 8, 8, 0, 1.0, -1, 1.0, 2, C.c_void_p(16), None, None, None, 0, None)
     assert st == hdf.ERR_ARG and b"both" in lib.hdf_last_error()
+    # PCA guide: even patch side, too many dimensions
+    st = lib.hdf_pca_guide(C.c_void_p(16), 8, 8, 3, 2, 2, C.c_void_p(16), None, C.c_void_p(16), 1 << 20, None)
+    assert st == hdf.ERR_ARG and b"odd" in lib.hdf_last_error()
+    st = lib.hdf_pca_guide(C.c_void_p(16), 8, 8, 3, 5, 6, C.c_void_p(16), None, C.c_void_p(16), 1 << 20, None)
+    assert st == hdf.ERR_ARG   # 3 * 25 = 75 > 64
+    assert hdf.lib().hdf_pca_guide_workspace_bytes(8, 8, 3, 3, 6) > 0
     st = lib.hdf_cluster(None, 8, 8, 3, hdf.MAX_K + 1, None, None, None, None, 0, None)
     assert st == hdf.ERR_ARG
 

@@ -265,3 +265,33 @@ def test_hard_variant_clusters_inside_and_obeys_theorem1(hdf):
     L = np.exp(-0.5) / cfg.sigma_r
     rhs = C * L * L * f.shape[2] * ((2 * cfg.radius + 1) ** 2) ** 2 * info.e_k
     assert 0.0 < lhs <= rhs
+
+
+# ------------------------------------------------------- PCA-NLM guide on the GPU (NEXT #3) ------
+@pytest.mark.parametrize("H,W,n,m,dim,seed", [(64, 80, 3, 3, 6, 1), (97, 61, 1, 5, 4, 2), (40, 50, 3, 1, 3, 3),
+                                              (128, 128, 2, 5, 12, 4)])
+def test_pca_guide_matches_oracle(hdf, H, W, n, m, dim, seed):
+    """hdf_pca_guide against oracle.pca_guide: fp64 moments and eigenvectors on both
+    sides (summation order differs), fp32 projection on the GPU."""
+    rng = np.random.default_rng(seed)
+    img = np.clip(rng.normal(120, 60, (H, W, n)), 0, 255).astype(np.float32)
+    img[: H // 2] *= 0.5                                    # some structure
+    g_ref, B_ref, mu_ref, ev = oracle.pca_guide(img, m, dim)
+    g, B = hdf.pca_guide(_dev(img), m, dim, basis=True)
+    assert np.allclose(B.cpu().numpy(), B_ref.T, atol=1e-5)
+    scale = np.abs(g_ref).max()
+    assert np.abs(g.cpu().numpy() - g_ref).max() <= 2e-5 * scale
+
+
+def test_pca_guide_feeds_the_nlm_filter(hdf):
+    """C4 with the guide built on the GPU: the filter on that guide matches the oracle filter on the
+    same guide (the parity bar of the main path)."""
+    cfg, f, _ = synth.make("c4", 120, 150)
+    fd = _dev(f)
+    pd = hdf.pca_guide(fd, 3, 6)
+    p = pd.cpu().numpy()
+    cen, _, _, _ = oracle.cluster(p, cfg.K)
+    mu32 = cen.astype(np.float32)
+    g_o, eta, fl, nf = oracle.filter(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, mu32, r=cfg.radius, tau=0.5)
+    g_g, nfg = _run_gpu(hdf, f, p, cfg, mu32, 0.5)
+    _compare(g_g, g_o, eta, fl, 0.5, 255.0 / cfg.R_range, nfg)
