@@ -138,6 +138,7 @@ hdf::BisectArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho,
     A.trace = cv.take<long long>(1 + 2 * hdf::kBisectTraceCap);
     A.ek = cv.take<double>(1);
     A.xw = cv.take<unsigned long long>((size_t)2 * kBisectMaxGrid * hdf::kRecV * 2);
+    A.teams = cv.take<int>((size_t)hdf::kTeamMax * 5 + kBisectMaxGrid);
     return A;
 }
 

@@ -76,6 +76,7 @@ enum {
 };
 enum { ST_FREE = 0, ST_CLAIMED = 1, ST_DONE = 2, ST_NONE = 3 };
 constexpr int kBufInput = 2;        // node buffer 2 = the caller's p (root only), identity index
+constexpr int kTeamMax = 16;        // grid-mode teams per round
 
 struct BisectArgs {
     const float* p;
@@ -105,6 +106,8 @@ struct BisectArgs {
     int* ctl;           // [B_NUM]
     long long* trace;   // [1 + 2 * kBisectTraceCap] (tag|node|worker, globaltimer), or null
     unsigned long long* xw;   // grid exchange: [2][clusters][2 kRecV] tagged record words (seq << 32 | half)
+    int* teams;         // grid-mode round: [kTeamMax][5] (node, cbase, first cluster, clusters, -), then
+                        // [clusters] the team of each cluster
     float* centres;     // [K][rho] out
     int* labels;        // [N] out, or null
     double* ek;         // out
@@ -372,24 +375,27 @@ enum { XSUM = 0, XARGMAX = 1 };
 // two parities alternate, so a slot is rewritten only after every CTA has read it (a CTA's next
 // record, which the next-but-one exchange waits for, follows its reads).
 struct GridGrp {
-    int rank, size;           // CTA rank / count in the grid
-    int crank, csize, cid;    // rank in the cluster, cluster size, cluster index
-    int ncl;                  // clusters in the grid
-    unsigned long long* xw;   // [2][ncl][2 kRecV] tagged words
+    int rank, size;           // CTA rank / count in the team
+    int crank, csize, cid;    // rank in the cluster, cluster size, cluster index (in the grid)
+    int ncl;                  // clusters in the team: [c0, c0 + ncl)
+    unsigned long long* xw;   // [2][nclg][2 kRecV] tagged words (slots by grid cluster index)
     int* ctl;
-    uint32_t seq = 0;         // exchanges so far (the same in every CTA)
-    uint32_t sq[2] = {0, 0};  // exchange number held by each parity's slots
+    int c0 = 0;               // the team's first cluster
+    int nclg = 0;             // clusters in the grid (slot stride)
+    uint32_t tagbase = 0;     // team id << 16 (unique per team formation: stale slots never match)
+    uint32_t seq = 0;         // exchanges so far (the same in every CTA of the team)
+    uint32_t sq[2] = {0, 0};  // tag held by each parity's slots
     uint32_t gph = 0;         // phase bits of S.gbar (leader)
     uint32_t pushed = 0;      // bit par: that exchange went through the push buffer
     static constexpr bool kGrid = true, kLocal = false;
     HDF_DEV void sync() { cg::this_grid().sync(); }
-    HDF_DEV unsigned long long* slot(int par, int q, int v) const {
-        return xw + (((size_t)par * ncl + q) * kRecV + v) * 2;
+    HDF_DEV unsigned long long* slot(int par, int q, int v) const {   // q: team cluster index
+        return xw + (((size_t)par * nclg + c0 + q) * kRecV + v) * 2;
     }
     HDF_DEV void exchange(SplitSm& S, int par, int nv, int kind = XSUM) {
         cg::cluster_group cl = cg::this_cluster();
         const int tid = threadIdx.x;
-        sq[par] = ++seq;
+        sq[par] = tagbase | (++seq & 0xffffu);
         const bool push = nv <= kPushV;
         pushed = push ? (pushed | (1u << par)) : (pushed & ~(1u << par));
         if (push && csize == 1) {   // no cluster (e.g. a launch without the cluster attribute)
@@ -412,10 +418,10 @@ struct GridGrp {
             if (!push) cl.sync();   // the leader reads this CTA's posted record in between
             return;
         }
-        const uint64_t tag = (uint64_t)seq << 32;
+        const uint64_t tag = (uint64_t)sq[par] << 32;
         auto put = [&](int v, double x) {
             const unsigned long long b = (unsigned long long)__double_as_longlong(x);
-            unsigned long long* w = slot(par, cid, v);
+            unsigned long long* w = slot(par, cid - c0, v);
             __stcg(w, tag | (b & 0xffffffffull));
             __stcg(w + 1, tag | (b >> 32));
         };
@@ -464,7 +470,7 @@ struct GridGrp {
                     ctl[B_DIAG2] = (int)(hi >> 32);
                     ctl[B_DIAG3] = par * 100000 + q * 1000 + v;
                     ctl[B_DIAG4] = rank;
-                    ctl[B_DIAG5] = (int)seq;
+                    ctl[B_DIAG5] = (int)sq[par ^ 1];
                 }
                 break;
             }
@@ -475,7 +481,7 @@ struct GridGrp {
     // this cluster before this CTA, from the leader's push buffer or the peers' posted records)
     HDF_DEV double prefix(SplitSm& S, int par, int v) const {
         double acc = 0.0;
-        for (int c = 0; c < cid; c++) acc += peer(S, par, c, v);
+        for (int c = 0; c < cid - c0; c++) acc += peer(S, par, c, v);
         cg::cluster_group cl = cg::this_cluster();
         if ((pushed >> par) & 1u) {
             const double* lr = cl.map_shared_rank(&S.grx[par][0][0], 0);
@@ -1713,7 +1719,9 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
     }
 
     if (lead) trace_ev(A, 13, v, worker);
-    if constexpr (!Grp::kLocal) g.sync();   // grid / pull groups: the whole group's scatter is visible
+    // Pull groups (ClusterGrp) still need a barrier; push and grid groups' SSE exchange has already
+    // delivered every CTA's record, sent after its fence, to the lead.
+    if constexpr (!Grp::kLocal && !Grp::kGrid) g.sync();
     // ---- 6. publish the children ----
     if (lead) {
         const int c = cbase;
@@ -2155,22 +2163,62 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
     // grid mode above gabove; a cluster streams at most its CTAs' side-word scratch
     const long long gab = max(ccap, min(A.gabove, (long long)cl.num_blocks() * 32LL * (A.wcap - 2)));
     {
-        GridGrp gg{(int)blockIdx.x, G, (int)cl.block_rank(), (int)cl.num_blocks(),
-                   (int)(blockIdx.x / cl.num_blocks()), (int)(G / cl.num_blocks()), A.xw, A.ctl};
+        // Rounds: block 0 claims every claimable node larger than gab (best first) and gives each a
+        // team of consecutive clusters, in proportion to its size (at least one); the teams split
+        // their nodes concurrently (tagged-word exchanges inside the team), then the grid syncs.
+        const int nclg = G / (int)cl.num_blocks(), cidg = (int)(blockIdx.x / cl.num_blocks());
+        int round = 0;
+        uint32_t gph = 0;   // phase bits of this CTA's S.gbar, carried across rounds (the barriers persist)
         while (A.N > gab) {   // (no node needs the grid otherwise)
             if (blockIdx.x == 0 && tid < 32) {
-                const Claim c = claim_node(A, 1, gab, 0);
+                // The best node first; then only nodes that fit resident in the clusters still free
+                // (a streamed node is bandwidth-bound: splitting the grid would only slow it down).
+                // Each team gets the clusters its node needs resident; the rest go round robin.
+                int nt = 0, need = 0;
+                int tk[kTeamMax], tcb[kTeamMax], tcl[kTeamMax];
+                while (nt < min(nclg, kTeamMax) && need < nclg) {
+                    const long long lim = nt == 0 ? LLONG_MAX : (long long)(nclg - need) * ccap;
+                    const Claim c = claim_node(A, 1, gab, 0, lim);
+                    if (c.task < 0) break;
+                    const long long mi = __ldcg(&A.nm[c.task]);
+                    tk[nt] = c.task;
+                    tcb[nt] = c.cbase;
+                    tcl[nt] = (int)min((long long)nclg, (mi + ccap - 1) / ccap);
+                    need += tcl[nt];
+                    nt++;
+                }
                 if (tid == 0) {
-                    A.ctl[B_TASK] = c.task;
-                    A.ctl[B_TASKC] = c.cbase;
+                    int used = 0;
+                    for (int i = 0; i < nt; i++) used += tcl[i];
+                    for (int i = 0; used < nclg && nt > 0; i = (i + 1) % nt, used++) tcl[i]++;
+                    int c = 0;
+                    for (int i = 0; i < nt; i++) {
+                        A.teams[i * 5 + 0] = tk[i];
+                        A.teams[i * 5 + 1] = tcb[i];
+                        A.teams[i * 5 + 2] = c;
+                        A.teams[i * 5 + 3] = tcl[i];
+                        for (int q = 0; q < tcl[i]; q++) A.teams[kTeamMax * 5 + c + q] = i;
+                        c += tcl[i];
+                    }
+                    A.ctl[B_TASK] = nt;
                     __threadfence();
                 }
             }
             grid.sync();
-            const int task = __ldcg(&A.ctl[B_TASK]);
-            const int cb = __ldcg(&A.ctl[B_TASKC]);
-            if (task < 0) break;
-            split_node<RHO>(A, gg, S, io, task, cb, -1);
+            const int nt = __ldcg(&A.ctl[B_TASK]);
+            if (nt <= 0) break;
+            const int ti = __ldcg(&A.teams[kTeamMax * 5 + cidg]);
+            const int task = __ldcg(&A.teams[ti * 5 + 0]), cb = __ldcg(&A.teams[ti * 5 + 1]);
+            const int tc0 = __ldcg(&A.teams[ti * 5 + 2]), tn = __ldcg(&A.teams[ti * 5 + 3]);
+            GridGrp gg{(cidg - tc0) * (int)cl.num_blocks() + (int)cl.block_rank(), tn * (int)cl.num_blocks(),
+                       (int)cl.block_rank(), (int)cl.num_blocks(), cidg, tn, A.xw, A.ctl};
+            gg.c0 = tc0;
+            gg.nclg = nclg;
+            gg.tagbase = (uint32_t)(round * kTeamMax + ti + 1) << 16;   // unique per team formation
+            gg.gph = gph;
+            split_node<RHO>(A, gg, S, io, task, cb, -1 - ti);
+            gph = gg.gph;
+            round++;
             grid.sync();
         }
     }
