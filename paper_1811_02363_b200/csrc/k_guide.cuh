@@ -104,13 +104,14 @@ struct PcaOut {
 };
 
 // One CTA of kPcaThreads threads.  Dynamic shared memory (pca_eig_smem): C [D][D], V [D][D], mean (fp64).
-constexpr size_t pca_eig_smem() { return sizeof(double) * (2 * kPcaMaxD * kPcaMaxD + kPcaMaxD); }
+constexpr int kPcaLd = kPcaMaxD + 1;   // row stride of C and V (odd: column walks hit distinct banks)
+constexpr size_t pca_eig_smem() { return sizeof(double) * (2 * kPcaMaxD * kPcaLd + kPcaMaxD); }
 __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int G, int D, int dim, long long N,
                                                          PcaOut out) {
     extern __shared__ __align__(16) double pca_sm[];
     double* C = pca_sm;
-    double* V = C + kPcaMaxD * kPcaMaxD;
-    double* mu = V + kPcaMaxD * kPcaMaxD;
+    double* V = C + kPcaMaxD * kPcaLd;
+    double* mu = V + kPcaMaxD * kPcaLd;
     __shared__ int sel[kPcaMaxDim];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int E = pca_nent(D);
@@ -126,18 +127,18 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
         } else {
             int r = e - D, a = 0;
             while (r >= D - a) { r -= D - a; a++; }
-            C[a * kPcaMaxD + a + r] = s / (double)N;   // E[x_a x_b], b = a + r
+            C[a * kPcaLd + a + r] = s / (double)N;   // E[x_a x_b], b = a + r
         }
     }
     __syncthreads();
     for (int e = tid; e < D * D; e += kPcaThreads) {
         const int a = e / D, b = e - a * D;
         if (a <= b) {
-            const double c = C[a * kPcaMaxD + b] - mu[a] * mu[b];
-            C[a * kPcaMaxD + b] = c;
-            if (a != b) C[b * kPcaMaxD + a] = c;
+            const double c = C[a * kPcaLd + b] - mu[a] * mu[b];
+            C[a * kPcaLd + b] = c;
+            if (a != b) C[b * kPcaLd + a] = c;
         }
-        V[a * kPcaMaxD + b] = (a == b) ? 1.0 : 0.0;
+        V[a * kPcaLd + b] = (a == b) ? 1.0 : 0.0;
     }
     __syncthreads();
     // Parallel (round-robin) Jacobi: each step rotates D'/2 disjoint pairs at once (D' = D rounded up
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
             double off = 0.0, fro = 0.0;
             for (int e = lane; e < D * D; e += 32) {
                 const int a = e / D, b = e - a * D;
-                const double v = C[a * kPcaMaxD + b];
+                const double v = C[a * kPcaLd + b];
                 fro += v * v;
                 if (a != b) off += v * v;
             }
@@ -174,12 +175,19 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
                 if (p > q) { const int t = p; p = q; q = t; }
                 double c = 1.0, sn = 0.0;
                 if (q < D) {
-                    const double apq = C[p * kPcaMaxD + q];
+                    const double apq = C[p * kPcaLd + q];
                     if (apq != 0.0) {
-                        const double tau = (C[q * kPcaMaxD + q] - C[p * kPcaMaxD + p]) / (2.0 * apq);
-                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                        c = 1.0 / sqrt(1.0 + t * t);
-                        sn = t * c;
+                        // the angle in fp32 (an inexact angle only slows the last sweeps down), the
+                        // rotation itself in fp64 and exactly orthogonal to rounding: c from one Newton
+                        // step of 1/sqrt(1 + t^2) seeded in fp32, s = t c
+                        const float tau = (float)((C[q * kPcaLd + q] - C[p * kPcaLd + p]) / (2.0 * apq));
+                        const float tf = copysignf(1.0f, tau) / (fabsf(tau) + sqrtf(fmaf(tau, tau, 1.0f)));
+                        const double t = (double)tf, u = fma(t, t, 1.0);
+                        double r = (double)rsqrtf((float)u);
+                        r = r * fma(-0.5 * u, r * r, 1.5);
+                        r = r * fma(-0.5 * u, r * r, 1.5);
+                        c = r;
+                        sn = t * r;
                     }
                 }
                 rc[i] = c;
@@ -192,12 +200,12 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
                 if (p > q) { const int t = p; p = q; q = t; }
                 if (q >= D || rs[i] == 0.0) continue;
                 const double c = rc[i], sn = rs[i];
-                const double akp = C[k * kPcaMaxD + p], akq = C[k * kPcaMaxD + q];
-                C[k * kPcaMaxD + p] = c * akp - sn * akq;
-                C[k * kPcaMaxD + q] = sn * akp + c * akq;
-                const double vkp = V[k * kPcaMaxD + p], vkq = V[k * kPcaMaxD + q];
-                V[k * kPcaMaxD + p] = c * vkp - sn * vkq;
-                V[k * kPcaMaxD + q] = sn * vkp + c * vkq;
+                const double akp = C[k * kPcaLd + p], akq = C[k * kPcaLd + q];
+                C[k * kPcaLd + p] = c * akp - sn * akq;
+                C[k * kPcaLd + q] = sn * akp + c * akq;
+                const double vkp = V[k * kPcaLd + p], vkq = V[k * kPcaLd + q];
+                V[k * kPcaLd + p] = c * vkp - sn * vkq;
+                V[k * kPcaLd + q] = sn * vkp + c * vkq;
             }
             __syncthreads();
             for (int e = tid; e < np * D; e += kPcaThreads) {   // rows p, q (all columns k)
@@ -206,9 +214,9 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
                 if (p > q) { const int t = p; p = q; q = t; }
                 if (q >= D || rs[i] == 0.0) continue;
                 const double c = rc[i], sn = rs[i];
-                const double apk = C[p * kPcaMaxD + k], aqk = C[q * kPcaMaxD + k];
-                C[p * kPcaMaxD + k] = c * apk - sn * aqk;
-                C[q * kPcaMaxD + k] = sn * apk + c * aqk;
+                const double apk = C[p * kPcaLd + k], aqk = C[q * kPcaLd + k];
+                C[p * kPcaLd + k] = c * apk - sn * aqk;
+                C[q * kPcaLd + k] = sn * apk + c * aqk;
             }
             __syncthreads();
         }
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
             for (int j = 0; j < dim; j++) {
                 int bi = -1;
                 for (int k = 0; k < D; k++)
-                    if (!((used >> k) & 1ull) && (bi < 0 || C[k * kPcaMaxD + k] > C[bi * kPcaMaxD + bi])) bi = k;
+                    if (!((used >> k) & 1ull) && (bi < 0 || C[k * kPcaLd + k] > C[bi * kPcaLd + bi])) bi = k;
                 used |= 1ull << bi;
                 sel[j] = bi;
             }
@@ -234,7 +242,7 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
         double best = -1.0, val = 0.0;
         int bk = D;
         for (int k = lane; k < D; k += 32) {
-            const double v = V[k * kPcaMaxD + col];
+            const double v = V[k * kPcaLd + col];
             if (fabs(v) > best) { best = fabs(v); val = v; bk = k; }
         }
         for (int o = 16; o > 0; o >>= 1) {
@@ -244,8 +252,8 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
             if (ob > best || (ob == best && ok < bk)) { best = ob; val = ov; bk = ok; }
         }
         const double sg = val < 0.0 ? -1.0 : 1.0;
-        for (int k = lane; k < D; k += 32) out.basis[j * D + k] = (float)(sg * V[k * kPcaMaxD + col]);
-        if (lane == 0) out.evals[j] = C[col * kPcaMaxD + col];
+        for (int k = lane; k < D; k += 32) out.basis[j * D + k] = (float)(sg * V[k * kPcaLd + col]);
+        if (lane == 0) out.evals[j] = C[col * kPcaLd + col];
     }
     for (int d = tid; d < D; d += kPcaThreads) out.mean[d] = (float)mu[d];
 }
