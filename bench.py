@@ -145,7 +145,16 @@ def run_ours(args, rank: int, world: int, dist):
     kw = dict(kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r, K=K, tau=0.5,
               out=g, ws=ws)
 
-    if args.variant == "hard":       # hard-assignment variant: one-hot coefficients, no A^+
+    if args.strips and world > 1:   # one image over the ranks in row strips (NEXT #4; strong scaling)
+        from paper_1811_02363_b200 import strips as _strips
+        fd = torch.from_numpy(synth.make(args.config)[1]).to(dev)
+        pd = fd if cfg.bilateral else torch.from_numpy(synth.make(args.config)[2]).to(dev)
+        H, W = fd.shape[:2]
+
+        def step():
+            _strips.filter_strips(fd, None if cfg.bilateral else pd, kind=cfg.kind, sigma_s=cfg.sigma_s,
+                                  radius=cfg.radius, sigma_r=cfg.sigma_r, K=K, tau=0.5, gather=False, dist=dist)
+    elif args.variant == "hard":     # hard-assignment variant: one-hot coefficients, no A^+
         kwh = {k: v for k, v in kw.items() if k != "tau"}
 
         def step():
@@ -189,7 +198,7 @@ def run_ours(args, rank: int, world: int, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
     ms_step = t_ms / args.steps
-    value = world * H * W / (ms_step * 1e-3) / 1e6
+    value = (1 if (args.strips and world > 1) else world) * H * W / (ms_step * 1e-3) / 1e6
 
     # ---- end to end through the public host API: H2D + cluster + filter + D2H each step ----
     fh = torch.from_numpy(f).pin_memory()
@@ -301,7 +310,8 @@ def run_ours(args, rank: int, world: int, dist):
     launches = sum(n for k, (ms, n) in kern.items())
     return {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "strong" if (args.strips and world > 1) else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, SURVEY 8(d) generators)",
         "config": dict(workload_config(args.config, world),
                        **({"variant": "hard (one-hot coefficients, P:341-357); e2e is the soft path's"}
@@ -397,6 +407,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--all", action="store_true", help="one line per config (exploration)")
+    ap.add_argument("--strips", action="store_true",
+                    help="N > 1: one image in row strips over the ranks (strong scaling, exploration)")
     ap.add_argument("--variant", default="soft", choices=["soft", "hard"],
                     help="hard: the hard-assignment variant (exploration; not the headline)")
     args = ap.parse_args()

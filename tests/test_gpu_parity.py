@@ -295,3 +295,27 @@ def test_pca_guide_feeds_the_nlm_filter(hdf):
     g_o, eta, fl, nf = oracle.filter(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, mu32, r=cfg.radius, tau=0.5)
     g_g, nfg = _run_gpu(hdf, f, p, cfg, mu32, 0.5)
     _compare(g_g, g_o, eta, fl, 0.5, 255.0 / cfg.R_range, nfg)
+
+
+# ------------------------------------------------------- row strips (NEXT #4) on one GPU ----------
+@pytest.mark.parametrize("name,H,W,world", [("c2a", 200, 160, 3), ("c4", 150, 120, 4), ("c1", None, None, 2)])
+def test_row_strips_match_the_whole_image(hdf, name, H, W, world):
+    """Each strip (with its R-row halo) filtered by the CUDA path with the whole image's centres and
+    stitched: the same as filtering the whole image (strip borders are never image borders)."""
+    from paper_1811_02363_b200 import strips
+    cfg, f, p = synth.make(name, H, W)
+    fd = _dev(f)
+    pd = fd if cfg.bilateral else _dev(p)
+    cen, _, _ = hdf.cluster(pd, cfg.K)
+    full = hdf.filter(fd, pd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                      centres=cen, tau=0.5).g
+    R = strips.radius_of(cfg.kind, cfg.sigma_s, cfg.radius)
+    parts = []
+    for y0, y1, h0, h1 in strips.strip_bounds(f.shape[0], world, R):
+        fs = fd[h0:h1].contiguous()
+        ps = fs if cfg.bilateral else pd[h0:h1].contiguous()
+        g = hdf.filter(fs, ps, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=R, sigma_r=cfg.sigma_r, centres=cen,
+                       tau=0.5).g
+        parts.append(g[y0 - h0:y1 - h0])
+    got = torch.cat(parts, 0)
+    assert torch.allclose(got, full, rtol=0, atol=1e-5 * cfg.R_range)
