@@ -2323,12 +2323,15 @@ __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ Bisec
             run(g);
         }
     }
-    __threadfence();
-    grid.sync();
-
+    // ---- phase 3: every CTA is a worker (only needed when phase 2 left small nodes: rho > 7, or no
+    //      thread-block clusters); with cluster batches phase 2 has split every node already ----
+    const bool phase3 = !(RHO > 0 && cl.num_blocks() > 1);
+    if (phase3) {
+        __threadfence();
+        grid.sync();
+    }
     if (b0) trace_ev(A, 33, 0, 0);
-    // ---- phase 3: every CTA is a worker ----
-    {
+    if (phase3) {
         CtaGrp g;
         const int worker = 1000 + blockIdx.x;
         while (true) {
