@@ -1926,16 +1926,22 @@ HDF_DEV void finalise(const BisectArgs& A, unsigned char* dyn) {
     }
     __syncthreads();
     const int nS = s_cnt[0];
-    if (tid == 0) {   // the split set's algorithmic work (bench roofline): sum m * passes, sum m
+    if (tid < 32) {   // the split set's algorithmic work (bench roofline): sum m * passes, sum m
         unsigned long long pp = 0, pm = 0;
-        for (int i = 0; i < n; i++)
+        for (int i = tid; i < n; i += 32)
             if (inS[i]) {
                 const unsigned long long mi = (unsigned long long)__ldcg(&A.nm[i]);
                 pp += mi * (unsigned long long)__ldcg(&A.nit[i]);
                 pm += mi;
             }
-        *reinterpret_cast<unsigned long long*>(&A.ctl[B_PTPASS]) = pp;
-        *reinterpret_cast<unsigned long long*>(&A.ctl[B_PTSPLIT]) = pm;
+        for (int o = 16; o > 0; o >>= 1) {
+            pp += __shfl_xor_sync(0xffffffffu, pp, o);
+            pm += __shfl_xor_sync(0xffffffffu, pm, o);
+        }
+        if (tid == 0) {
+            *reinterpret_cast<unsigned long long*>(&A.ctl[B_PTPASS]) = pp;
+            *reinterpret_cast<unsigned long long*>(&A.ctl[B_PTSPLIT]) = pm;
+        }
     }
     // final leaves: the root if nothing is split, else children of split nodes that are not split
     for (int i = tid; i < n; i += kBT) {
