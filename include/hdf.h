@@ -127,6 +127,10 @@ size_t hdf_filter_workspace_bytes(int H, int W, int n, int rho, int K, int kind,
  *            box; 0 <= S <= HDF_MAX_RADIUS
  *   sigma_r  range sigma (> 0), phi(x) = exp(-||x||^2 / 2 sigma_r^2)
  *   K        number of centres, 1 <= K <= HDF_MAX_K
+ *   Working-set limit: the column pass keeps 2 J rows of (rho, or rho + n when f is not p) floats for
+ *   32 columns in shared memory (J = rows per step, 2..16 with the radius), so large rho + n need a
+ *   small radius (e.g. rho + n = 67 works up to radius 2, rho + n = 6 up to 32); beyond that the call
+ *   returns HDF_ERR_ARG before launching anything.
  *   centres  [K][rho] float32, device; NULL -> hdf_cluster is run first inside this call (then
  *            ws must also hold the clustering workspace, which hdf_filter_workspace_bytes includes)
  *   tau      degenerate-normaliser threshold (R9); 0 disables the rule; callers pass 0.5

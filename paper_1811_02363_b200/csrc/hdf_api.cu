@@ -104,7 +104,9 @@ struct ProfScope {
 // and its pixel index, grid-mode side words and exchange records, the node table.
 constexpr int kBisectMaxGrid = 256;     // upper bound of the cooperative grid (records, side words)
 constexpr int kBisectMinGrid = 32;      // the launch never uses fewer CTAs (streamed ranges <= N / 32)
-int bisect_maxn(int K) { (void)K; return 512; }   // claim scans hold 512 nodes in registers (16 per lane)
+// Node table: the K-1 splits need 2K-1 nodes; speculative splits need room too.  Claim scans hold
+// the table in registers (16 or 32 entries per lane).
+int bisect_maxn(int K) { return K > 64 ? 1024 : 512; }
 
 hdf::BisectArgs carve_cluster(Carver& cv, const float* p, int H, int W, int rho, int K) {
     const long long N = (long long)H * W;
@@ -384,14 +386,32 @@ int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, F
     F.planes_bytes = round_up(F.Lbox * F.RR * NP * 4, 128);
     F.stage_bytes = F.planes_bytes + round_up(hdf::kCoefBox * F.RR * 4, 128);
     const int fixed = 128 + round_up(F.RR * hdf::kHTW * 4, 128) + 128;
-    const int budget = 200 * 1024;
+    int optin = 227 * 1024;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    }
+    const int budget = std::min(200 * 1024, optin - 2048);   // (large n and R: up to the opt-in limit)
     F.NS = std::min(4, (budget - fixed) / F.stage_bytes);
+    if (F.NS < 2) F.NS = std::min(2, (optin - 2048 - fixed) / F.stage_bytes);
     if (F.NS < 2) return fail(HDF_ERR_ARG, "tile does not fit shared memory (n=%d, R=%d)", n, radius);
     F.hl.grid = dim3((W + hdf::kHTW - 1) / hdf::kHTW, (H + F.RR - 1) / F.RR);
     F.hl.threads = 32 * (F.NWC + 1);
     F.hl.smem = fixed + (size_t)F.NS * F.stage_bytes;
     F.hl.maxjp = maxjp;
     return HDF_OK;
+}
+
+// Dynamic shared memory of k_range_vpass: the centres of its plane group, two buffers of J raw rows
+// (rho, or rho + n floats per pixel when f is not p) and two of J range-weight rows.
+size_t vpass_smem(const FilterPlan& F, int rho, int n, bool f_is_p) {
+    const int J = hdf::vpass_j(F.Rp);
+    const int RW = f_is_p ? rho : rho + n;
+    const size_t mus_len = (size_t)round_up(hdf::vfir_nkmax(F.NP, F.Pg) * rho, 4);
+    const size_t raw_len = (size_t)round_up(J * hdf::kVTX * RW, 4);
+    const size_t zs_len = (size_t)J * F.Pg * hdf::kVTX;
+    return sizeof(float) * (mus_len + 2 * raw_len + 2 * zs_len);
 }
 
 struct FilterWS {
@@ -546,6 +566,19 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     if (rc) return rc;
     const size_t need = hdf_filter_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
     if (ws_bytes < need) return fail(HDF_ERR_WORKSPACE, "workspace %zu < required %zu bytes", ws_bytes, need);
+    // the column pass keeps J raw rows (rho or rho + n floats per pixel, double buffered) and J range-
+    // weight rows of its plane group in shared memory: checked before anything is enqueued
+    const size_t vsmem = vpass_smem(F, rho, n, f == p);
+    {
+        int dev = 0, optin = 0;
+        HDF_CUDA(cudaGetDevice(&dev));
+        HDF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        if (vsmem > (size_t)optin)
+            return fail(HDF_ERR_ARG,
+                        "the column pass needs %zu bytes of shared memory (rho %d, n %d, radius %d) > %d: reduce "
+                        "rho + n or the radius",
+                        vsmem, rho, n, F.Rp, optin);
+    }
     Carver cv(ws);
     FilterWS w = carve_filter(cv, H, W, n, rho, K, F.Wp, true);
     const float neg_inv2sr2 = (float)(-1.0 / (2.0 * (double)sigma_r * (double)sigma_r));
@@ -607,14 +640,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         }
         for (int t = 0; t < 2 * HDF_MAX_RADIUS + 1; t++) vp.tws[t] = (t <= 2 * F.Rp) ? taps[t] : 0.f;
         hdf::VLaunch vl = F.vl;
-        {
-            const int J = hdf::vpass_j(F.Rp);
-            const int RW = vp.f_is_p ? rho : rho + n;
-            const size_t mus_len = (size_t)round_up(hdf::vfir_nkmax(F.NP, F.Pg) * rho, 4);
-            const size_t raw_len = (size_t)round_up(J * hdf::kVTX * RW, 4);
-            const size_t zs_len = (size_t)J * F.Pg * hdf::kVTX;
-            vl.smem = sizeof(float) * (mus_len + 2 * raw_len + 2 * zs_len);
-        }
+        vl.smem = vsmem;
         ProfScope prof(HDF_STAGE_VPASS, st);
         HDF_CUDA(hdf::launch_vpass(F.Rp, F.box, vl, st, vp));
     }

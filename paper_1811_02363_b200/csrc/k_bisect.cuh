@@ -1767,7 +1767,8 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
 struct Claim {
     int task, cbase;
 };
-HDF_DEV Claim claim_node(const BisectArgs& A, int mode, long long bigcap, int wid, long long maxm = LLONG_MAX) {
+template <int kScan>   // node-table entries per lane: the table holds 32 kScan nodes
+HDF_DEV Claim claim_node_t(const BisectArgs& A, int mode, long long bigcap, int wid, long long maxm) {
     const int lane = threadIdx.x & 31;
     int backoff = 16;
     while (true) {
@@ -1781,7 +1782,6 @@ HDF_DEV Claim claim_node(const BisectArgs& A, int mode, long long bigcap, int wi
         n = min(__shfl_sync(0xffffffffu, n, 0), A.maxn);
         const long long mmin = max(bigcap + 1, 2LL);
         // states (relaxed, all in flight), then one acquire fence before the fields they publish
-        constexpr int kScan = 16;
         int stv[kScan];
 #pragma unroll
         for (int u = 0; u < kScan; u++) {
@@ -1878,6 +1878,10 @@ HDF_DEV Claim claim_node(const BisectArgs& A, int mode, long long bigcap, int wi
         }
         __syncwarp();
     }
+}
+
+HDF_DEV Claim claim_node(const BisectArgs& A, int mode, long long bigcap, int wid, long long maxm = LLONG_MAX) {
+    return A.maxn > 512 ? claim_node_t<32>(A, mode, bigcap, wid, maxm) : claim_node_t<16>(A, mode, bigcap, wid, maxm);
 }
 
 // ------------------------------------------------------------------------------ finalisation --

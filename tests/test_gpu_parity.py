@@ -319,3 +319,49 @@ def test_row_strips_match_the_whole_image(hdf, name, H, W, world):
         parts.append(g[y0 - h0:y1 - h0])
     got = torch.cat(parts, 0)
     assert torch.allclose(got, full, rtol=0, atol=1e-5 * cfg.R_range)
+
+
+# ------------------------------------------------------- the ABI's maximum sizes ------------------
+def _limits_case(hdf, K, rho, n, R, s, sr, seed):
+    rng = np.random.default_rng(seed)
+    H, W = 70, 90
+    base = rng.uniform(0, 1, (8, 8, rho))
+    p = np.kron(base, np.ones((9, 12, 1)))[:H, :W] + rng.normal(0, 0.02, (H, W, rho))
+    p = np.clip(p, 0, 1).astype(np.float32)
+    f = rng.uniform(0, 1, (H, W, n)).astype(np.float32)
+    cen, _, _, _ = oracle.cluster(p, K)
+    mu32 = cen.astype(np.float32)
+    g_o, eta, fl, nf = oracle.filter(f, p, "gaussian", s, sr, mu32, r=R, tau=0.5)
+    res = hdf.filter(_dev(f), _dev(p), kind="gaussian", sigma_s=s, radius=R, sigma_r=sr,
+                     centres=_dev(mu32), tau=0.5, count_flagged=True)
+    _compare(res.g.cpu().numpy().astype(np.float64), g_o, eta, fl, 0.5, 255.0, res.n_flagged)
+
+
+@pytest.mark.parametrize("K,rho,n,R", [(128, 64, 3, 9),     # HDF_MAX_K, HDF_MAX_RHO
+                                       (8, 3, 64, 2),       # HDF_MAX_N channels (small radius: J rows of rho + n)
+                                       (16, 3, 3, 32),      # HDF_MAX_RADIUS
+                                       (100, 8, 8, 15)])    # K off the compiled sizes (generic kernels)
+def test_parity_at_the_limits(hdf, K, rho, n, R):
+    """The ABI's maximum K, rho, n and radius (not all at once: the column pass's working set is
+    rho + n floats per pixel for J rows in shared memory)."""
+    _limits_case(hdf, K, rho, n, R, s=max(1.0, R / 3.0), sr=0.6, seed=K + rho + n + R)
+
+
+def test_working_set_too_large_is_an_argument_error(hdf):
+    """rho + n = 128 with radius 32 does not fit the column pass: HDF_ERR_ARG before any launch."""
+    f = torch.zeros((16, 16, 64), device="cuda")
+    p = torch.zeros((16, 16, 64), device="cuda")
+    with pytest.raises(hdf.HdfError) as e:
+        hdf.filter(f, p, kind="gaussian", sigma_s=10.0, radius=32, sigma_r=1.0, K=4,
+                   centres=torch.zeros((4, 64), device="cuda"))
+    assert e.value.status == hdf.ERR_ARG and "shared memory" in str(e.value)
+
+
+def test_cluster_k128_rho64_matches_oracle(hdf):
+    """Bisecting K-means at K = 128 on a 64-dimensional guide: the same E_K as the oracle."""
+    rng = np.random.default_rng(12)
+    p = rng.uniform(0, 1, (60, 70, 64)).astype(np.float32)
+    cen_o, lab_o, _, ek_o = oracle.cluster(p, 128)
+    cen_g, lab_g, info = hdf.cluster(_dev(p), 128, labels=True)
+    assert abs(info.e_k - ek_o) <= 1e-9 * ek_o
+    assert np.array_equal(lab_g.cpu().numpy().reshape(-1), lab_o)
