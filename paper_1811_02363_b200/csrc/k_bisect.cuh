@@ -711,6 +711,7 @@ struct TileLd {
     uint32_t body;
 };
 HDF_DEV TileLd tile_issue(const float* src, int tn, int rho, float* dyn, SplitSm& S) {
+    uint64_t* bar = &S.bar;
     const uintptr_t s = reinterpret_cast<uintptr_t>(src);
     const int delta = (int)((s & 15u) >> 2);
     const uintptr_t s0 = s - 4u * (uintptr_t)delta;
@@ -720,10 +721,10 @@ HDF_DEV TileLd tile_issue(const float* src, int tn, int rho, float* dyn, SplitSm
     __syncthreads();   // the previous tile is fully consumed
     if (threadIdx.x == 0 && body > 0) {
         fence_proxy_async();
-        mbar_arrive_expect_tx(&S.bar, body);
+        mbar_arrive_expect_tx(bar, body);
         for (uint32_t off = 0; off < body; off += 32768u)
             bulk_g2s(reinterpret_cast<char*>(dyn) + off, reinterpret_cast<const char*>(s0) + off,
-                     min(32768u, body - off), &S.bar);
+                     min(32768u, body - off), bar);
     }
     const uintptr_t tb = body > 0 ? body_end : s0;   // tail floats [tb, end)
     const int tail = (int)((end - tb) >> 2);
@@ -1403,12 +1404,19 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
                     if (tot) pass_small<RH, true>(X, np, wd, it > 0, full, S, s1p, stp, n1, chg);
                     else pass_small<RH, false>(X, np, wd, it > 0, full, S, s1p, stp, n1, chg);
                 } else {
+                    // streamed: the tile's side words are staged in the (otherwise idle) shared word
+                    // buffers, the previous ones loaded while the tile's TMA is in flight
+                    const WordsSm wd{smem_pin(io.dynW), smem_pin(io.dynW + wsm)};
                     for (int t0 = 0; t0 < np; t0 += A.cap) {
-                        const int tn = min(A.cap, np - t0);
-                        const float* T = load_tile(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
-                        const WordsGl wd = WordsGl{prevW, curW}.at(t0 >> 5);
-                        if (tot) pass_small<RH, true>(T, tn, wd, it > 0, full, S, s1p, stp, n1, chg);
-                        else pass_small<RH, false>(T, tn, wd, it > 0, full, S, s1p, stp, n1, chg);
+                        const int tn = min(A.cap, np - t0), nw = (tn + 31) >> 5;
+                        const TileLd tl = tile_issue(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
+                        if (it > 0)
+                            for (int i = tid; i < nw; i += kBT) io.dynW[i] = __ldcg(prevW + (t0 >> 5) + i);
+                        tile_wait(S, tl);
+                        if (tot) pass_small<RH, true>(tl.ptr, tn, wd, it > 0, full, S, s1p, stp, n1, chg);
+                        else pass_small<RH, false>(tl.ptr, tn, wd, it > 0, full, S, s1p, stp, n1, chg);
+                        __syncthreads();
+                        for (int i = tid; i < nw; i += kBT) curW[(t0 >> 5) + i] = io.dynW[wsm + i];
                     }
                 }
                 tick(0);
@@ -1498,13 +1506,18 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
                     __syncthreads();
                     pass_sum_generic(X, np, rho, wd, s0, s1);
                 } else {
+                    const WordsSm wd{smem_pin(io.dynW), smem_pin(io.dynW + wsm)};   // (staged, as above)
                     for (int t0 = 0; t0 < np; t0 += A.cap) {
-                        const int tn = min(A.cap, np - t0);
-                        const float* T = load_tile(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
-                        const WordsGl wd = WordsGl{prevW, curW}.at(t0 >> 5);
-                        pass_side_generic(T, tn, rho, wd, it > 0, S, n1, chg);
+                        const int tn = min(A.cap, np - t0), nw = (tn + 31) >> 5;
+                        const TileLd tl = tile_issue(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
+                        if (it > 0)
+                            for (int i = tid; i < nw; i += kBT) io.dynW[i] = __ldcg(prevW + (t0 >> 5) + i);
+                        tile_wait(S, tl);
+                        pass_side_generic(tl.ptr, tn, rho, wd, it > 0, S, n1, chg);
                         __syncthreads();
-                        pass_sum_generic(T, tn, rho, wd, s0, s1);
+                        pass_sum_generic(tl.ptr, tn, rho, wd, s0, s1);
+                        __syncthreads();
+                        for (int i = tid; i < nw; i += kBT) curW[(t0 >> 5) + i] = io.dynW[wsm + i];
                     }
                 }
 #pragma unroll
