@@ -1654,9 +1654,17 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
         int run0 = 0;
         for (int t0 = 0; t0 < np; t0 += A.cap) {
             const int tn = min(A.cap, np - t0);
-            const float* T = resident ? X : load_tile(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
-            const uint32_t Ts = smem_pin(T);
+            const uint32_t* FWt = FW + (t0 >> 5);   // the tile's final side words
+            const float* T = X;
             const int nw = (tn + 31) >> 5;
+            if (!resident) {   // streamed: the words staged in shared memory under the tile's TMA
+                const TileLd tl = tile_issue(Pg + (size_t)(a + t0) * rho, tn, rho, io.dynX, S);
+                for (int i = tid; i < nw; i += kBT) io.dynW[i] = __ldcg(FWt + i);
+                tile_wait(S, tl);
+                T = tl.ptr;
+                FWt = io.dynW;
+            }
+            const uint32_t Ts = smem_pin(T);
             for (int w0 = 0; w0 < nw; w0 += kBT) {
                 // word prefix of side-0 counts for words [w0, w0 + kBT) of the tile
                 const int wi = w0 + tid;
@@ -1664,7 +1672,7 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
                 if (wi < nw) {
                     const int nb = min(32, tn - wi * 32);
                     const uint32_t valid = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
-                    z = __popc(~FW[(t0 >> 5) + wi] & valid);
+                    z = __popc(~FWt[wi] & valid);
                 }
                 int ztot;
                 const int zp = block_exscan(z, S.wsum, &ztot);
@@ -1685,7 +1693,7 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
                         if (j0 >= jhi) break;
                         const int j = j0 + tid;
                         const int wl = ((j0 - jlo) >> 5) + warp;
-                        const uint32_t w = FW[((t0 + j0) >> 5) + warp];
+                        const uint32_t w = FWt[(j0 >> 5) + warp];
                         if (j < jhi) {
                             const int sd = (w >> lane) & 1u;
                             const int zb = S.wp[wl] + __popc(~w & ((1u << lane) - 1u));   // side-0 before j (chunk)
