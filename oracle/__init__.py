@@ -13,12 +13,16 @@ Functions follow PAPER.md (see the C file for per-function citations):
   nystrom        Appendix A identity written as a direct window sum
   filter_hard    hard-assignment variant (coeffICIP)/(HDapprox2)
   pca_guide      PCA-NLM patch guide (reading R11), numpy fp64
+  young_coeffs, young1d, young2d, filter_iir
+                 Young's O(1) recursive Gaussian (the reference the paper cites) and
+                 Algorithm 1 with it in place of the FIR (NEXT #1; readings R12), numpy fp64
   conv2          omega * x with the clipped window
   mse, psnr      (rmse), intensities normalised by R
 """
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 import threading
@@ -324,3 +328,77 @@ def pca_guide(img, m: int = 3, dim: int = 6):
         if B[k, j] < 0:
             B[:, j] = -B[:, j]
     return (Pc @ B).reshape(H, W, dim), B, mean, evals[order]
+
+
+# ---------------------------------------------------------------- recursive Gaussian (NEXT #1) --
+def young_coeffs(sigma_s: float):
+    """Young & van Vliet's recursive Gaussian, the O(1) convolution the paper uses for the Gaussian
+    steps: q from sigma (two ranges), the third-order recursion's b0..b3 and the input
+    gain B = 1 - (b1 + b2 + b3) / b0 (unit DC gain per pass).  Returns (B, b1/b0, b2/b0, b3/b0).
+    Reading R12: sigma_s >= 0.5 (the range the q formula is given for)."""
+    s = float(sigma_s)
+    if s < 0.5:
+        raise ValueError("the recursive Gaussian needs sigma_s >= 0.5")
+    q = 0.98711 * s - 0.96330 if s >= 2.5 else 3.97156 - 4.14554 * math.sqrt(1.0 - 0.26891 * s)
+    b0 = 1.57825 + 2.44413 * q + 1.4281 * q * q + 0.422205 * q ** 3
+    b1 = 2.44413 * q + 2.85619 * q * q + 1.26661 * q ** 3
+    b2 = -(1.4281 * q * q + 1.26661 * q ** 3)
+    b3 = 0.422205 * q ** 3
+    return 1.0 - (b1 + b2 + b3) / b0, b1 / b0, b2 / b0, b3 / b0
+
+
+def young1d(x, sigma_s: float, axis: int = 0) -> np.ndarray:
+    """One axis of the recursive Gaussian, readings R12: the causal pass
+    w[t] = G B x[t] + a1 w[t-1] + a2 w[t-2] + a3 w[t-3], then the anti-causal pass
+    y[t] = B w[t] + a1 y[t+1] + a2 y[t+2] + a3 y[t+3], on the signal extended by zeros outside the image
+    (the signal is 0 outside Omega, as under the FIR's clipped window; written out as zero padding past
+    the end, long enough for the tails to vanish) and G = sqrt(2 pi) sigma_s, so that the response
+    peaks near 1 like the unnormalised FIR taps exp(-t^2 / 2 sigma^2) (omega(0) = 1 for rule R9)."""
+    B, a1, a2, a3 = young_coeffs(sigma_s)
+    G = math.sqrt(2.0 * math.pi) * float(sigma_s)
+    x = np.moveaxis(np.asarray(x, dtype=np.float64), axis, 0)
+    N = x.shape[0]
+    L = int(60.0 * float(sigma_s)) + 100           # zero padding after the end: the tails fall below 1e-16
+    M = N + L
+    xp = np.zeros((M,) + x.shape[1:])
+    xp[:N] = x
+    w = np.zeros((M + 3,) + x.shape[1:])          # w[t + 3] = w_t; w_-1..w_-3 = 0 (rest before the start)
+    for t in range(M):
+        w[t + 3] = G * B * xp[t] + a1 * w[t + 2] + a2 * w[t + 1] + a3 * w[t]
+    y = np.zeros((M + 3,) + x.shape[1:])          # y[t] = y_t; at rest L samples past the end
+    for t in range(M - 1, -1, -1):
+        y[t] = B * w[t + 3] + a1 * y[t + 1] + a2 * y[t + 2] + a3 * y[t + 3]
+    return np.moveaxis(y[:N], 0, axis)
+
+
+def young2d(x, sigma_s: float) -> np.ndarray:
+    """The separable 2-D recursive Gaussian: columns (axis 0), then rows (axis 1)."""
+    return young1d(young1d(x, sigma_s, axis=0), sigma_s, axis=1)
+
+
+def filter_iir(f, p, sigma_s: float, sigma_r: float, mu, tau: float = 0.5):
+    """Algorithm 1 with the recursive Gaussian for the convolutions of loop for3
+    (P:332-333), in the paper's order: b_k and c = A^+ b (loops for1/for2), then per k
+    v += c_k (omega * (b_k f)), r += c_k (omega * b_k), g = v / r.  Rule R9 as in `filter`: eta_hat
+    below tau omega(0) phi(0) = tau (omega(0) = 1 by the gain of R12) -> the brute-force (num)/(den)
+    with the truncated FIR Gaussian, R = ceil(3 sigma_s).  Returns (g, eta_hat, flagged, n_flagged)."""
+    f, p = _fp(f, p)
+    H, W, n = f.shape
+    b, c = coefficients(p, mu, sigma_r)
+    K = b.shape[1]
+    v = np.zeros((H, W, n))
+    r = np.zeros((H, W))
+    for k in range(K):
+        bk = b[:, k].reshape(H, W)
+        ck = c[:, k].reshape(H, W)
+        for ch in range(n):
+            v[:, :, ch] += ck * young2d(bk * f[:, :, ch], sigma_s)
+        r += ck * young2d(bk, sigma_s)
+    g = v / r[..., None]
+    floor = tau * phi(np.zeros(1), sigma_r)
+    fl = (tau > 0.0) & (r < floor)
+    if fl.any():
+        pix = np.flatnonzero(fl)
+        gb, _ = bruteforce(f, p, "gaussian", sigma_s, sigma_r, -1, pix=pix)
+        g.reshape(-1, n)[pix] = gb
+    return g, r, fl, int(fl.sum())

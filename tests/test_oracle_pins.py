@@ -448,3 +448,60 @@ def test_pca_guide_matches_svd_and_is_orthonormal():
 def test_pca_guide_constant_image_is_zero():
     g, B, mu, ev = oracle.pca_guide(np.full((5, 6, 3), 42.0), 3, 4)
     assert np.all(g == 0.0) and np.allclose(mu, 42.0)
+
+
+# ---------------------------------------- NEXT #1: Young's recursive Gaussian -----
+# The recursion is pinned by what its design fixes: unit DC gain per pass (B = 1 - sum a), a
+# zero-phase (symmetric) impulse response from the causal + anti-causal pair, a Gaussian shape of
+# the requested sigma within the approximation's known error, and separability; the filter built on
+# it by the paper's invariants (a constant image maps to itself; close to the FIR filter).
+@pytest.mark.parametrize("s", [0.5, 1.0, 2.0, 2.5, 5.0, 8.0])
+def test_iir_dc_gain_and_symmetry(s):
+    G = math.sqrt(2.0 * math.pi) * s
+    c = oracle.young1d(np.ones(60 * int(math.ceil(s)) + 200), s)
+    mid = c.size // 2
+    assert abs(c[mid] / G - 1.0) < 1e-10              # unit DC gain per pass, times the R12 gain G
+    x = np.zeros(c.size)
+    x[mid] = 1.0
+    h = oracle.young1d(x, s)
+    t = np.arange(1, int(8 * s) + 2)
+    assert np.max(np.abs(h[mid + t] - h[mid - t])) < 1e-12 * h[mid]   # zero phase
+    assert abs(h.sum() / G - 1.0) < 1e-9               # the impulse response integrates to G
+
+
+@pytest.mark.parametrize("s,tol", [(0.5, 0.1), (1.0, 0.1), (2.0, 0.07), (2.5, 0.06), (5.0, 0.04), (8.0, 0.03)])
+def test_iir_impulse_response_is_gaussian(s, tol):
+    n = int(20 * s) + 41
+    x = np.zeros(n)
+    x[n // 2] = 1.0
+    h = oracle.young1d(x, s)
+    t = np.arange(n) - n // 2
+    assert np.max(np.abs(h - np.exp(-t * t / (2.0 * s * s)))) < tol     # peak ~1 (omega(0) = 1, R12)
+    if s >= 2.0:   # the width: h(sigma) / h(0) = exp(-1/2) of a Gaussian of that sigma
+        hs = np.interp(s, t, h)
+        assert abs(hs / h[n // 2] - math.exp(-0.5)) < (0.08 if s < 3.0 else 0.03)   # wider at small sigma
+
+
+def test_iir_separable_and_zero_outside():
+    rng = np.random.default_rng(5)
+    a, b = rng.random(37), rng.random(23)
+    y = oracle.young2d(np.outer(a, b), 2.0)
+    assert np.allclose(y, np.outer(oracle.young1d(a, 2.0), oracle.young1d(b, 2.0)), rtol=1e-12, atol=1e-14)
+    # zero outside Omega at both ends (R12): the result is the convolution of the zero-extended signal
+    # with the symmetric impulse response, so reversing the input reverses the output
+    for s in (0.7, 2.0, 6.0):
+        assert np.allclose(oracle.young1d(a[::-1], s), oracle.young1d(a, s)[::-1], rtol=0, atol=1e-12)
+        # and zeros added outside change nothing on the support
+        z = np.concatenate([np.zeros(50), a, np.zeros(7)])
+        assert np.allclose(oracle.young1d(z, s)[50:50 + a.size], oracle.young1d(a, s), rtol=0, atol=1e-12)
+
+
+def test_iir_filter_constant_image_and_close_to_fir():
+    cfg, f, p = synth.make("c1", 40, 44)
+    mu = oracle.cluster(p, 6)[0]
+    g, eta, fl, nf = oracle.filter_iir(np.full_like(f, 77.0), np.full_like(p, 77.0), 3.0, 30.0, np.full((1, 3), 77.0))
+    assert np.allclose(g, 77.0, rtol=0, atol=1e-9)
+    gi, _, _, _ = oracle.filter_iir(f, p, cfg.sigma_s, cfg.sigma_r, mu)
+    gf, _, _, _ = oracle.filter(f, p, "gaussian", cfg.sigma_s, cfg.sigma_r, mu)
+    d = np.abs(gi - gf) * 255.0 / cfg.R_range
+    assert d.mean() < 1.0 and d.max() < 12.0    # the recursion approximates the truncated Gaussian
