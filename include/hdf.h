@@ -45,7 +45,12 @@ typedef enum {
 
 typedef enum {
     HDF_SPATIAL_GAUSSIAN = 0, /* omega(i) = exp(-||i||^2 / 2 sigma_s^2) on [-S,S]^2 */
-    HDF_SPATIAL_BOX = 1       /* omega = 1 on [-S,S]^2 (nonlocal means)                 */
+    HDF_SPATIAL_BOX = 1,      /* omega = 1 on [-S,S]^2 (nonlocal means)                 */
+    HDF_SPATIAL_GAUSSIAN_IIR = 2 /* Young's O(1) recursive Gaussian, the paper's implementation of
+                                    the Gaussian convolutions; sigma_s >= 0.5; zero
+                                    outside the image, gain sqrt(2 pi) sigma_s per axis so that
+                                    omega(0) ~ 1 (DESIGN R12); `radius` (or ceil(3 sigma_s)) only
+                                    sizes the R9 fallback's direct window sum (exact FIR Gaussian) */
 } hdf_spatial_kind;
 
 /* Limits of this build. */

@@ -20,8 +20,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhdf.so")
 
 OK, ERR_ARG, ERR_K, ERR_WORKSPACE, ERR_CUDA, WARN_ILLCOND = 0, 1, 2, 3, 4, 5
-GAUSSIAN, BOX = 0, 1
-KIND = {"gaussian": GAUSSIAN, "box": BOX}
+GAUSSIAN, BOX, GAUSSIAN_IIR = 0, 1, 2
+KIND = {"gaussian": GAUSSIAN, "box": BOX, "gaussian_iir": GAUSSIAN_IIR}
 MAX_K, MAX_RHO, MAX_N, MAX_RADIUS = 128, 64, 64, 32
 
 # every symbol include/hdf.h declares (checked by the CPU tests)

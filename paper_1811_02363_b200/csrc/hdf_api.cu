@@ -16,6 +16,7 @@
 #include "k_bisect.cuh"
 #include "k_coeffs.cuh"
 #include "k_guide.cuh"
+#include "k_iir.cuh"
 
 namespace {
 
@@ -332,6 +333,8 @@ int padded_radius(int R, bool box) {
 struct FilterPlan {
     int R, Rp, Wp, NP, P;
     bool box;
+    bool iir;   // HDF_SPATIAL_GAUSSIAN_IIR: identity taps in the passes, the recursion in between
+    int Rfb;    // the R9 fallback's window radius (= R for the FIR kinds)
     // F1
     hdf::VLaunch vl;
     int Pg, TY;
@@ -343,7 +346,16 @@ struct FilterPlan {
 int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, FilterPlan* fp, int nsm) {
     FilterPlan& F = *fp;
     F.box = (kind == HDF_SPATIAL_BOX);
-    if (kind != HDF_SPATIAL_GAUSSIAN && kind != HDF_SPATIAL_BOX) return fail(HDF_ERR_ARG, "unknown spatial kind %d", kind);
+    F.iir = (kind == HDF_SPATIAL_GAUSSIAN_IIR);
+    if (kind != HDF_SPATIAL_GAUSSIAN && kind != HDF_SPATIAL_BOX && !F.iir)
+        return fail(HDF_ERR_ARG, "unknown spatial kind %d", kind);
+    F.Rfb = -1;
+    if (F.iir) {   // the recursion replaces the FIR; radius only sizes the R9 fallback's window
+        if (!(sigma_s >= 0.5f)) return fail(HDF_ERR_ARG, "the recursive Gaussian needs sigma_s >= 0.5");
+        F.Rfb = radius >= 0 ? radius : (int)std::ceil(3.0 * (double)sigma_s);
+        if (F.Rfb > HDF_MAX_RADIUS) return fail(HDF_ERR_ARG, "radius %d exceeds HDF_MAX_RADIUS=%d", F.Rfb, HDF_MAX_RADIUS);
+        radius = 0;
+    }
     if (radius < 0) {
         if (F.box) return fail(HDF_ERR_ARG, "the box kernel needs an explicit radius");
         if (!(sigma_s > 0.f)) return fail(HDF_ERR_ARG, "sigma_s must be > 0");
@@ -352,6 +364,7 @@ int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, F
     if (!F.box && !(sigma_s > 0.f)) return fail(HDF_ERR_ARG, "sigma_s must be > 0");
     if (radius > HDF_MAX_RADIUS) return fail(HDF_ERR_ARG, "radius %d exceeds HDF_MAX_RADIUS=%d", radius, HDF_MAX_RADIUS);
     F.R = radius;
+    if (!F.iir) F.Rfb = radius;
     // Running-sum box kernels need a compiled radius equal to S; any other box radius (and S = 0)
     // runs through the FIR kernels with unit taps on [-S, S] and zero taps beyond (exact).
     if (F.box && (radius == 0 || padded_radius(radius, true) < 0)) F.box = false;
@@ -546,6 +559,38 @@ void fill_taps(float* taps, int kind, float sigma_s, int R, int Rp) {
     }
 }
 
+// Young's recursive Gaussian coefficients in fp64 and the anti-causal start matrix of the
+// zero extension (k_iir.cuh, R12): M[:, j] = (y[N], y[N+1], y[N+2]) when (w[N-1], w[N-2], w[N-3]) = e_j
+// and the input is zero from N on (a long zero-input run of both passes, at rest far past the end).
+hdf::IIRParams iir_params(double s) {
+    const double q = s >= 2.5 ? 0.98711 * s - 0.96330 : 3.97156 - 4.14554 * std::sqrt(1.0 - 0.26891 * s);
+    const double b0 = 1.57825 + 2.44413 * q + 1.4281 * q * q + 0.422205 * q * q * q;
+    const double b1 = 2.44413 * q + 2.85619 * q * q + 1.26661 * q * q * q;
+    const double b2 = -(1.4281 * q * q + 1.26661 * q * q * q);
+    const double b3 = 0.422205 * q * q * q;
+    const double a1 = b1 / b0, a2 = b2 / b0, a3 = b3 / b0, B = 1.0 - (b1 + b2 + b3) / b0;
+    const double G = std::sqrt(2.0 * 3.14159265358979323846) * s;
+    hdf::IIRParams P;
+    memset(&P, 0, sizeof(P));
+    P.gB = (float)(G * B);
+    P.B = (float)B;
+    P.a1 = (float)a1;
+    P.a2 = (float)a2;
+    P.a3 = (float)a3;
+    const int L = (int)(60.0 * s) + 100;
+    std::vector<double> w(L + 3), y(L + 3);
+    for (int j = 0; j < 3; j++) {
+        w[0] = (j == 2) ? 1.0 : 0.0;   // w[0..2] = w[N-3], w[N-2], w[N-1]; w[3 + t] = w[N + t]
+        w[1] = (j == 1) ? 1.0 : 0.0;
+        w[2] = (j == 0) ? 1.0 : 0.0;
+        for (int t = 0; t < L; t++) w[3 + t] = a1 * w[2 + t] + a2 * w[1 + t] + a3 * w[t];
+        std::fill(y.begin(), y.end(), 0.0);   // y[t] = y[N + t], at rest from L on
+        for (int t = L - 1; t >= 0; t--) y[t] = B * w[3 + t] + a1 * y[t + 1] + a2 * y[t + 2] + a3 * y[t + 3];
+        for (int r = 0; r < 3; r++) P.M[3 * r + j] = (float)y[r];
+    }
+    return P;
+}
+
 // hard: the hard-assignment variant: c = one-hot(label), no A^+, no fallback (tau = 0).
 // hard_labels: the caller's labels (with its centres), or NULL to cluster here (labels in the workspace).
 int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int kind, float sigma_s, int radius,
@@ -643,6 +688,20 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         vl.smem = vsmem;
         ProfScope prof(HDF_STAGE_VPASS, st);
         HDF_CUDA(hdf::launch_vpass(F.Rp, F.box, vl, st, vp));
+        if (F.iir) {   // NEXT #1: the recursion over the unfiltered planes, columns then rows
+            hdf::IIRParams ip = iir_params((double)sigma_s);
+            ip.planes = w.planes;
+            ip.pstride = (long long)H * F.Wp;
+            ip.P = F.P;
+            ip.H = H;
+            ip.W = W;
+            ip.Wp = F.Wp;
+            hdf::k_iir_cols<<<dim3((unsigned)((W + hdf::kIirColThreads - 1) / hdf::kIirColThreads), (unsigned)F.P),
+                              hdf::kIirColThreads, 0, st>>>(ip);
+            HDF_CUDA(cudaGetLastError());
+            hdf::k_iir_rows<<<dim3((unsigned)((H + 31) / 32), (unsigned)F.P), 32, 0, st>>>(ip);
+            HDF_CUDA(cudaGetLastError());
+        }
     }
     HDF_CUDA(cudaStreamWaitEvent(st, ss.join, 0));   // A^+ is ready
     // loop for2: c(i) = A^+ b(i) -> K coefficient planes
@@ -740,12 +799,12 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         fb.rho = rho;
         fb.H = H;
         fb.W = W;
-        fb.R = F.R;
+        fb.R = F.Rfb;
         fb.neg_inv2sr2 = neg_inv2sr2;
         fb.mu = hard ? centres : nullptr;
         fb.labels = hard ? hard_labels : nullptr;
         float t2[hdf::kMaxTaps];
-        fill_taps(t2, kind, sigma_s, F.R, F.R);
+        fill_taps(t2, F.iir ? (int)HDF_SPATIAL_GAUSSIAN : kind, sigma_s, F.Rfb, F.Rfb);
         memcpy(fb.taps, t2, sizeof(t2));
         ProfScope prof(HDF_STAGE_FALLBACK, st);
         hdf::k_fallback<<<2 * nsm, 256, 0, st>>>(fb);

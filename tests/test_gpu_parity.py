@@ -365,3 +365,37 @@ def test_cluster_k128_rho64_matches_oracle(hdf):
     cen_g, lab_g, info = hdf.cluster(_dev(p), 128, labels=True)
     assert abs(info.e_k - ek_o) <= 1e-9 * ek_o
     assert np.array_equal(lab_g.cpu().numpy().reshape(-1), lab_o)
+
+
+# ---- NEXT #1: the recursive Gaussian against oracle.filter_iir --------------------
+@pytest.mark.parametrize("name,H,W,K,sig", [
+    ("c1", None, None, None, None),   # the config's own size (64x64, sigma 3)
+    ("c1", 61, 77, 5, None),          # ragged, several 32-row / 128-column blocks
+    ("c2a", 96, 130, 8, None),        # sigma 5, colour
+    ("c1", 40, 33, 4, 0.6),           # small sigma (the q formula's lower range)
+    ("c1", 70, 50, 6, 8.0),           # sigma wider than the image's half-height
+    ("c1", 1, 90, 3, 2.0),            # a single row
+    ("c4", 48, 64, 6, 2.0),           # rho = 6 guide, f != p
+])
+def test_parity_gaussian_iir(hdf, name, H, W, K, sig):
+    cfg, f, p = synth.make(name, H, W)
+    K = K or cfg.K
+    s = sig or cfg.sigma_s
+    cen, _, _, _ = oracle.cluster(p, K)
+    mu32 = cen.astype(np.float32)
+    g_o, eta, fl, nf = oracle.filter_iir(f, p, s, cfg.sigma_r, mu32, tau=0.5)
+    fd = _dev(f)
+    pd = fd if p is f else _dev(p)
+    res = hdf.filter(fd, pd, kind="gaussian_iir", sigma_s=s, radius=-1, sigma_r=cfg.sigma_r, centres=_dev(mu32),
+                     tau=0.5, count_flagged=True)
+    torch.cuda.synchronize()
+    g_g = res.g.cpu().numpy().astype(np.float64)
+    _compare(g_g, g_o, eta, fl, 0.5, 255.0 / cfg.R_range, res.n_flagged)
+
+
+def test_gaussian_iir_constant_image_and_argument_errors(hdf):
+    f = torch.full((37, 41, 3), 91.0, device="cuda")
+    res = hdf.filter(f, f, kind="gaussian_iir", sigma_s=3.0, sigma_r=20.0, centres=torch.full((1, 3), 91.0, device="cuda"))
+    assert torch.allclose(res.g, f, rtol=0, atol=1e-3)
+    with pytest.raises(Exception, match="sigma_s >= 0.5"):
+        hdf.filter(f, f, kind="gaussian_iir", sigma_s=0.4, sigma_r=20.0, K=2)
