@@ -101,7 +101,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- algorithmic work ----
-def stage_work(cfg, K: int, H: int, W: int):
+def stage_work(cfg, K: int, H: int, W: int, iir: bool = False):
     """Algorithmic bytes and FP32 FMA-pipe ops per launch of each filter kernel.
     bytes: what the minimal version of the kernel must move (planes written once, read once; the
     coefficient planes c are a design choice of this build and are not counted)."""
@@ -110,6 +110,14 @@ def stage_work(cfg, K: int, H: int, W: int):
     n_in = n if cfg.bilateral else n + rho
     planes = K * (n + 1)
     taps = 2 * R + 1
+    if iir:   # NEXT #1: identity passes; the "vpass" stage adds the column and row recursions, each
+        #       reading and writing every plane twice (causal, then anti-causal), 4 FMAs per sample
+        return {
+            "vpass": {"bytes": 4 * npx * (n_in + 9 * planes), "fma": npx * (planes * 16 + K * (rho + 1 + n))},
+            "hpass": {"bytes": 4 * npx * (planes + n), "fma": npx * (2 * planes + n)},
+            "coeffs": {"bytes": 4 * npx * rho, "fma": npx * (K * K + K * (rho + 1)), "mma_flop": 2 * npx * K * K},
+            "filter": {"bytes": 4 * npx * (n_in + 10 * planes + n)},
+        }
     return {
         "vpass": {"bytes": 4 * npx * (n_in + planes), "fma": npx * (planes * taps + K * (rho + 1 + n))},
         "hpass": {"bytes": 4 * npx * (planes + n),
@@ -142,7 +150,10 @@ def run_ours(args, rank: int, world: int, dist):
     pd = fd if cfg.bilateral else torch.from_numpy(p).to(dev)
     ws = hdf.Workspace()
     g = torch.empty_like(fd)
-    kw = dict(kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r, K=K, tau=0.5,
+    kind = "gaussian_iir" if args.variant == "iir" else cfg.kind
+    if args.variant == "iir" and cfg.kind != "gaussian":
+        raise SystemExit("--variant iir needs a Gaussian config")
+    kw = dict(kind=kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r, K=K, tau=0.5,
               out=g, ws=ws)
 
     if args.strips and world > 1:   # one image over the ranks in row strips (NEXT #4; strong scaling)
@@ -206,14 +217,14 @@ def run_ours(args, rank: int, world: int, dist):
     gh = torch.empty_like(fh).pin_memory()
     ws2 = hdf.Workspace()
     for _ in range(max(1, args.warmup)):
-        hdf.filter_host(fh, ph, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+        hdf.filter_host(fh, ph, kind=kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
                         K=K, out=gh, ws=ws2)
     e2e_ms = []
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        hdf.filter_host(fh, ph, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+        hdf.filter_host(fh, ph, kind=kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
                         K=K, out=gh, ws=ws2)
         b.record(stream)
         b.synchronize()
@@ -229,7 +240,7 @@ def run_ours(args, rank: int, world: int, dist):
 
     # ---- roofline of the dominant kernel (live event timings above) ----
     peaks = _peaks()
-    work = stage_work(cfg, K, H, W)
+    work = stage_work(cfg, K, H, W, iir=(args.variant == "iir"))
     kern = {k: v for k, v in prof.items() if k in ("cluster", "pinv", "coeffs", "vpass", "hpass", "fallback")}
     per_launch = {k: (ms / n if n else 0.0) for k, (ms, n) in kern.items()}
     sm_mhz = clk.get("sm_mhz") or peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1965.0)
@@ -315,7 +326,10 @@ def run_ours(args, rank: int, world: int, dist):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, SURVEY 8(d) generators)",
         "config": dict(workload_config(args.config, world),
                        **({"variant": "hard (one-hot coefficients, P:341-357); e2e is the soft path's"}
-                          if args.variant == "hard" else {})),
+                          if args.variant == "hard" else {}),
+                       **({"variant": "iir (Young's recursive Gaussian, P:332-333, NEXT #1); the vpass stage "
+                                      "includes the column and row recursions"}
+                          if args.variant == "iir" else {})),
         "stages_ms_per_step": {k: round(ms / args.steps, 4) for k, (ms, n) in prof.items() if n},
         "filter": filt, "roofline": roof, "filter_roofline": filter_roof, "gpu_launches": launches, "clocks": clk,
         "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -409,7 +423,7 @@ def main():
     ap.add_argument("--all", action="store_true", help="one line per config (exploration)")
     ap.add_argument("--strips", action="store_true",
                     help="N > 1: one image in row strips over the ranks (strong scaling, exploration)")
-    ap.add_argument("--variant", default="soft", choices=["soft", "hard"],
+    ap.add_argument("--variant", default="soft", choices=["soft", "hard", "iir"],
                     help="hard: the hard-assignment variant (exploration; not the headline)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

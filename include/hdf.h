@@ -49,7 +49,7 @@ typedef enum {
     HDF_SPATIAL_GAUSSIAN_IIR = 2 /* Young's O(1) recursive Gaussian, the paper's implementation of
                                     the Gaussian convolutions; sigma_s >= 0.5; zero
                                     outside the image, gain sqrt(2 pi) sigma_s per axis so that
-                                    omega(0) ~ 1 (DESIGN R12); `radius` (or ceil(3 sigma_s)) only
+                                    omega(0) ~ 1 (DESIGN R17); `radius` (or ceil(3 sigma_s)) only
                                     sizes the R9 fallback's direct window sum (exact FIR Gaussian) */
 } hdf_spatial_kind;
 

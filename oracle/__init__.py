@@ -15,7 +15,7 @@ Functions follow PAPER.md (see the C file for per-function citations):
   pca_guide      PCA-NLM patch guide (reading R11), numpy fp64
   young_coeffs, young1d, young2d, filter_iir
                  Young's O(1) recursive Gaussian (the reference the paper cites) and
-                 Algorithm 1 with it in place of the FIR (NEXT #1; readings R12), numpy fp64
+                 Algorithm 1 with it in place of the FIR (NEXT #1; readings R17), numpy fp64
   conv2          omega * x with the clipped window
   mse, psnr      (rmse), intensities normalised by R
 """
@@ -335,7 +335,7 @@ def young_coeffs(sigma_s: float):
     """Young & van Vliet's recursive Gaussian, the O(1) convolution the paper uses for the Gaussian
     steps: q from sigma (two ranges), the third-order recursion's b0..b3 and the input
     gain B = 1 - (b1 + b2 + b3) / b0 (unit DC gain per pass).  Returns (B, b1/b0, b2/b0, b3/b0).
-    Reading R12: sigma_s >= 0.5 (the range the q formula is given for)."""
+    Reading R17: sigma_s >= 0.5 (the range the q formula is given for)."""
     s = float(sigma_s)
     if s < 0.5:
         raise ValueError("the recursive Gaussian needs sigma_s >= 0.5")
@@ -348,7 +348,7 @@ def young_coeffs(sigma_s: float):
 
 
 def young1d(x, sigma_s: float, axis: int = 0) -> np.ndarray:
-    """One axis of the recursive Gaussian, readings R12: the causal pass
+    """One axis of the recursive Gaussian, readings R17: the causal pass
     w[t] = G B x[t] + a1 w[t-1] + a2 w[t-2] + a3 w[t-3], then the anti-causal pass
     y[t] = B w[t] + a1 y[t+1] + a2 y[t+2] + a3 y[t+3], on the signal extended by zeros outside the image
     (the signal is 0 outside Omega, as under the FIR's clipped window; written out as zero padding past
@@ -380,7 +380,7 @@ def filter_iir(f, p, sigma_s: float, sigma_r: float, mu, tau: float = 0.5):
     """Algorithm 1 with the recursive Gaussian for the convolutions of loop for3
     (P:332-333), in the paper's order: b_k and c = A^+ b (loops for1/for2), then per k
     v += c_k (omega * (b_k f)), r += c_k (omega * b_k), g = v / r.  Rule R9 as in `filter`: eta_hat
-    below tau omega(0) phi(0) = tau (omega(0) = 1 by the gain of R12) -> the brute-force (num)/(den)
+    below tau omega(0) phi(0) = tau (omega(0) = 1 by the gain of R17) -> the brute-force (num)/(den)
     with the truncated FIR Gaussian, R = ceil(3 sigma_s).  Returns (g, eta_hat, flagged, n_flagged)."""
     f, p = _fp(f, p)
     H, W, n = f.shape

@@ -560,7 +560,7 @@ void fill_taps(float* taps, int kind, float sigma_s, int R, int Rp) {
 }
 
 // Young's recursive Gaussian coefficients in fp64 and the anti-causal start matrix of the
-// zero extension (k_iir.cuh, R12): M[:, j] = (y[N], y[N+1], y[N+2]) when (w[N-1], w[N-2], w[N-3]) = e_j
+// zero extension (k_iir.cuh, R17): M[:, j] = (y[N], y[N+1], y[N+2]) when (w[N-1], w[N-2], w[N-3]) = e_j
 // and the input is zero from N on (a long zero-input run of both passes, at rest far past the end).
 hdf::IIRParams iir_params(double s) {
     const double q = s >= 2.5 ? 0.98711 * s - 0.96330 : 3.97156 - 4.14554 * std::sqrt(1.0 - 0.26891 * s);

@@ -1,5 +1,5 @@
 // Young's recursive Gaussian for the plane convolutions (NEXT #1, the paper's own O(1)
-// implementation of the Gaussian steps conv1/conv2).  Readings R12:
+// implementation of the Gaussian steps conv1/conv2).  Readings R17:
 //   causal      w[t] = gB x[t] + a1 w[t-1] + a2 w[t-2] + a3 w[t-3], from rest before the first sample;
 //   anti-causal y[t] = B w[t] + a1 y[t+1] + a2 y[t+2] + a3 y[t+3], started from the state the
 //               zero-input continuation of the causal pass past the last sample gives it:

@@ -460,7 +460,7 @@ def test_iir_dc_gain_and_symmetry(s):
     G = math.sqrt(2.0 * math.pi) * s
     c = oracle.young1d(np.ones(60 * int(math.ceil(s)) + 200), s)
     mid = c.size // 2
-    assert abs(c[mid] / G - 1.0) < 1e-10              # unit DC gain per pass, times the R12 gain G
+    assert abs(c[mid] / G - 1.0) < 1e-10              # unit DC gain per pass, times the R17 gain G
     x = np.zeros(c.size)
     x[mid] = 1.0
     h = oracle.young1d(x, s)
@@ -476,7 +476,7 @@ def test_iir_impulse_response_is_gaussian(s, tol):
     x[n // 2] = 1.0
     h = oracle.young1d(x, s)
     t = np.arange(n) - n // 2
-    assert np.max(np.abs(h - np.exp(-t * t / (2.0 * s * s)))) < tol     # peak ~1 (omega(0) = 1, R12)
+    assert np.max(np.abs(h - np.exp(-t * t / (2.0 * s * s)))) < tol     # peak ~1 (omega(0) = 1, R17)
     if s >= 2.0:   # the width: h(sigma) / h(0) = exp(-1/2) of a Gaussian of that sigma
         hs = np.interp(s, t, h)
         assert abs(hs / h[n // 2] - math.exp(-0.5)) < (0.08 if s < 3.0 else 0.03)   # wider at small sigma
@@ -487,7 +487,7 @@ def test_iir_separable_and_zero_outside():
     a, b = rng.random(37), rng.random(23)
     y = oracle.young2d(np.outer(a, b), 2.0)
     assert np.allclose(y, np.outer(oracle.young1d(a, 2.0), oracle.young1d(b, 2.0)), rtol=1e-12, atol=1e-14)
-    # zero outside Omega at both ends (R12): the result is the convolution of the zero-extended signal
+    # zero outside Omega at both ends (R17): the result is the convolution of the zero-extended signal
     # with the symmetric impulse response, so reversing the input reverses the output
     for s in (0.7, 2.0, 6.0):
         assert np.allclose(oracle.young1d(a[::-1], s), oracle.young1d(a, s)[::-1], rtol=0, atol=1e-12)
