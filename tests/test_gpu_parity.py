@@ -399,3 +399,24 @@ def test_gaussian_iir_constant_image_and_argument_errors(hdf):
     assert torch.allclose(res.g, f, rtol=0, atol=1e-3)
     with pytest.raises(Exception, match="sigma_s >= 0.5"):
         hdf.filter(f, f, kind="gaussian_iir", sigma_s=0.4, sigma_r=20.0, K=2)
+
+
+# ---- the end-to-end host entry point (bench.py's e2e leg): same kernels, same bits -----------
+@pytest.mark.parametrize("name,H,W,kind", [("c2b", None, None, "gaussian"), ("c1", 61, 77, "gaussian"),
+                                           ("c1", 50, 70, "gaussian_iir"), ("c4", 64, 48, "box")])
+def test_filter_host_equals_device_path(hdf, name, H, W, kind):
+    cfg, f, p = synth.make(name, H, W)
+    kd = cfg.kind if kind == "box" else kind
+    fh = torch.from_numpy(np.ascontiguousarray(f, dtype=np.float32)).pin_memory()
+    ph = fh if p is f else torch.from_numpy(np.ascontiguousarray(p, dtype=np.float32)).pin_memory()
+    g_h, cen_h, nfl_h, info = hdf.filter_host(fh, ph, kind=kd, sigma_s=cfg.sigma_s, radius=cfg.radius,
+                                               sigma_r=cfg.sigma_r, K=cfg.K)
+    fd = fh.cuda()
+    pd = fd if p is f else ph.cuda()
+    res = hdf.filter(fd, pd, kind=kd, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r, K=cfg.K,
+                     count_flagged=True)
+    cen_d = hdf.cluster(pd, cfg.K)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(cen_h, cen_d.cpu())
+    assert torch.equal(g_h, res.g.cpu())
+    assert nfl_h == res.n_flagged
