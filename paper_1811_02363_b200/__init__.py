@@ -184,7 +184,9 @@ def filter(f: torch.Tensor, p: torch.Tensor | None = None, *, kind: str = "gauss
     """Steps 2-6 (Algorithm 1): the fast filter g = (HDapprox)/(approxDen).
 
     f [H,W,n] and guide p [H,W,rho] (p=None -> bilateral, p = f).  centres [K,rho] (None -> the
-    library clusters p first).  tau: rule R9 threshold.  count_flagged synchronises and returns
+    library clusters p first).  kind: "gaussian" (exact FIR, radius -1 -> ceil(3 sigma_s)), "box"
+    (radius required) or "gaussian_iir" (Young's recursive Gaussian; radius only sizes
+    the R9 fallback's window).  tau: rule R9 threshold.  count_flagged synchronises and returns
     the number of pixels that took the direct (num)/(den) fallback."""
     f = _dev_f32(f, "f")
     if p is None:
