@@ -176,6 +176,7 @@ int hdf_pca_guide(const float *f, int H, int W, int n, int m, int dim, float *p,
  *   centres, labels  [K][rho] float32 and [H][W] int32 (values in [0, K)), device: both given (e.g.
  *                    from hdf_cluster) or both NULL (clustering runs inside the call, labels kept in
  *                    the workspace); HDF_ERR_ARG otherwise
+ *   kind             HDF_SPATIAL_GAUSSIAN or HDF_SPATIAL_BOX (HDF_ERR_ARG for the recursive Gaussian)
  *   other arguments, workspace (hdf_filter_workspace_bytes) and errors as hdf_filter; asynchronous.
  */
 int hdf_filter_hard(const float *f, int n, const float *p, int rho, int H, int W, int kind, float sigma_s,

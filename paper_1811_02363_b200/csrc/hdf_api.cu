@@ -609,6 +609,8 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     if (misaligned(f) || misaligned(p) || misaligned(g) || misaligned(ws) || (centres && misaligned(centres)))
         return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
     if (g == f || g == p) return fail(HDF_ERR_ARG, "g must not alias f or p");
+    if (hard && kind == HDF_SPATIAL_GAUSSIAN_IIR)   // no oracle for that pairing: not offered
+        return fail(HDF_ERR_ARG, "the hard-assignment variant takes the FIR kinds (gaussian, box)");
     FilterPlan F;
     const int nsm = nsm_of_device();
     rc = make_plan(H, W, n, K, kind, sigma_s, radius, &F, nsm);

@@ -420,3 +420,9 @@ def test_filter_host_equals_device_path(hdf, name, H, W, kind):
     assert torch.equal(cen_h, cen_d.cpu())
     assert torch.equal(g_h, res.g.cpu())
     assert nfl_h == res.n_flagged
+
+
+def test_hard_variant_rejects_recursive_gaussian(hdf):
+    f = torch.rand((16, 16, 3), device="cuda") * 255.0
+    with pytest.raises(Exception, match="FIR kinds"):
+        hdf.filter_hard(f, f, kind="gaussian_iir", sigma_s=2.0, sigma_r=30.0, K=2)
