@@ -50,7 +50,8 @@ typedef enum {
                                     the Gaussian convolutions; sigma_s >= 0.5; zero
                                     outside the image, gain sqrt(2 pi) sigma_s per axis so that
                                     omega(0) ~ 1 (DESIGN R17); `radius` (or ceil(3 sigma_s)) only
-                                    sizes the R9 fallback's direct window sum (exact FIR Gaussian) */
+                                    sizes the R9 fallback's direct window sum (exact FIR Gaussian,
+                                    radius <= 512) */
 } hdf_spatial_kind;
 
 /* Limits of this build. */

@@ -347,6 +347,9 @@ struct FilterPlan {
     int RR, NJW, NWC, NS, Lbox, stage_bytes, planes_bytes;
 };
 
+// the recursive Gaussian's R9 fallback window (a direct sum per flagged pixel, weights computed in place)
+constexpr int kMaxFallbackRadius = 512;
+
 int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, FilterPlan* fp, int nsm) {
     FilterPlan& F = *fp;
     F.box = (kind == HDF_SPATIAL_BOX);
@@ -357,7 +360,8 @@ int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, F
     if (F.iir) {   // the recursion replaces the FIR; radius only sizes the R9 fallback's window
         if (!(sigma_s >= 0.5f)) return fail(HDF_ERR_ARG, "the recursive Gaussian needs sigma_s >= 0.5");
         F.Rfb = radius >= 0 ? radius : (int)std::ceil(3.0 * (double)sigma_s);
-        if (F.Rfb > HDF_MAX_RADIUS) return fail(HDF_ERR_ARG, "radius %d exceeds HDF_MAX_RADIUS=%d", F.Rfb, HDF_MAX_RADIUS);
+        if (F.Rfb > kMaxFallbackRadius)
+            return fail(HDF_ERR_ARG, "fallback radius %d exceeds %d", F.Rfb, kMaxFallbackRadius);
         radius = 0;
     }
     if (radius < 0) {
@@ -576,11 +580,11 @@ hdf::IIRParams iir_params(double s) {
     const double G = std::sqrt(2.0 * 3.14159265358979323846) * s;
     hdf::IIRParams P;
     memset(&P, 0, sizeof(P));
-    P.gB = (float)(G * B);
-    P.B = (float)B;
-    P.a1 = (float)a1;
-    P.a2 = (float)a2;
-    P.a3 = (float)a3;
+    P.gB = G * B;
+    P.B = B;
+    P.a1 = a1;
+    P.a2 = a2;
+    P.a3 = a3;
     const int L = (int)(60.0 * s) + 100;
     std::vector<double> w(L + 3), y(L + 3);
     for (int j = 0; j < 3; j++) {
@@ -590,7 +594,7 @@ hdf::IIRParams iir_params(double s) {
         for (int t = 0; t < L; t++) w[3 + t] = a1 * w[2 + t] + a2 * w[1 + t] + a3 * w[t];
         std::fill(y.begin(), y.end(), 0.0);   // y[t] = y[N + t], at rest from L on
         for (int t = L - 1; t >= 0; t--) y[t] = B * w[3 + t] + a1 * y[t + 1] + a2 * y[t + 2] + a3 * y[t + 3];
-        for (int r = 0; r < 3; r++) P.M[3 * r + j] = (float)y[r];
+        for (int r = 0; r < 3; r++) P.M[3 * r + j] = y[r];
     }
     return P;
 }
@@ -810,7 +814,13 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         fb.mu = hard ? centres : nullptr;
         fb.labels = hard ? hard_labels : nullptr;
         float t2[hdf::kMaxTaps];
-        fill_taps(t2, F.iir ? (int)HDF_SPATIAL_GAUSSIAN : kind, sigma_s, F.Rfb, F.Rfb);
+        fb.neg_inv2ss2 = 0.f;
+        if (F.Rfb <= HDF_MAX_RADIUS) {
+            fill_taps(t2, F.iir ? (int)HDF_SPATIAL_GAUSSIAN : kind, sigma_s, F.Rfb, F.Rfb);
+        } else {   // the recursive Gaussian with a window beyond the table: weights in the kernel
+            memset(t2, 0, sizeof(t2));
+            fb.neg_inv2ss2 = (float)(-1.0 / (2.0 * (double)sigma_s * (double)sigma_s));
+        }
         memcpy(fb.taps, t2, sizeof(t2));
         ProfScope prof(HDF_STAGE_FALLBACK, st);
         hdf::k_fallback<<<2 * nsm, 256, 0, st>>>(fb);

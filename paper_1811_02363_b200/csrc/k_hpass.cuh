@@ -214,6 +214,8 @@ struct FBParams {
     int n, rho, H, W, R;
     float neg_inv2sr2;
     float taps[kMaxTaps];
+    float neg_inv2ss2;         // != 0: Gaussian spatial weights exp(t^2 neg_inv2ss2) computed in place of
+                               // the table (the recursive Gaussian's fallback window beyond kMaxTaps)
     const float* mu;           // hard variant: centres [K][rho] and labels [H*W]: the range kernel is
     const int32_t* labels;     // phi(p(j) - mu_{label(i)}); NULL: phi(p(j) - p(i))
 };
@@ -263,7 +265,9 @@ static __global__ void __launch_bounds__(256) k_fallback(const __grid_constant__
                     float dd = pj[d] - pi[d];
                     d2 = fmaf(dd, dd, d2);
                 }
-                const float wt = P.taps[ty + P.R] * P.taps[tx + P.R] * expf((d2 - dmin) * P.neg_inv2sr2);
+                const float sy = P.neg_inv2ss2 != 0.f ? expf((float)(ty * ty) * P.neg_inv2ss2) : P.taps[ty + P.R];
+                const float sx = P.neg_inv2ss2 != 0.f ? expf((float)(tx * tx) * P.neg_inv2ss2) : P.taps[tx + P.R];
+                const float wt = sy * sx * expf((d2 - dmin) * P.neg_inv2sr2);
                 den += wt;
 #pragma unroll
                 for (int u = 0; u < 8; u++)

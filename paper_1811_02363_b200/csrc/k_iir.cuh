@@ -8,8 +8,8 @@
 // G = sqrt(2 pi) sigma so that omega(0) ~ 1 like the FIR's unnormalised taps (rule R9's floor).
 // Both kernels work in place on the column pass's plane buffer [P][H][Wp] (the range-weighted planes,
 // written unfiltered by k_range_vpass with identity taps), columns first, then rows; the row pass +
-// combine kernel then runs with identity taps.  fp32 arithmetic (stable: poles inside the unit
-// circle), memory-bound: each pass reads and writes every plane twice.
+// combine kernel then runs with identity taps.  The recursion runs in fp64 (planes stored fp32):
+// memory-bound either way, and an fp32 state loses ~sigma^3 x 1e-7 with the poles near 1.
 #pragma once
 #include "hdf_common.cuh"
 
@@ -19,8 +19,9 @@ struct IIRParams {
     float* planes;
     long long pstride;   // H * Wp
     int P, H, W, Wp;
-    float gB, B, a1, a2, a3;
-    float M[9];          // row-major: y[N + r] = sum_c M[3 r + c] w[N - 1 - c]
+    double gB, B, a1, a2, a3;   // fp64 recursion (the planes stay fp32): with poles near 1 at large
+    double M[9];                // sigma an fp32 state loses ~sigma^3 x 1e-7 (measured)
+                                // M row-major: y[N + r] = sum_c M[3 r + c] w[N - 1 - c]
 };
 
 constexpr int kIirColThreads = 128;
@@ -33,7 +34,7 @@ static __global__ void __launch_bounds__(kIirColThreads) k_iir_cols(const __grid
     if (x >= P.W || q >= P.P) return;
     float* col = P.planes + (long long)q * P.pstride + x;
     const long long s = P.Wp;
-    float w1 = 0.f, w2 = 0.f, w3 = 0.f;
+    double w1 = 0.0, w2 = 0.0, w3 = 0.0;
     int y = 0;
     for (; y + kIirBatch <= P.H; y += kIirBatch) {
         float v[kIirBatch];
@@ -41,21 +42,21 @@ static __global__ void __launch_bounds__(kIirColThreads) k_iir_cols(const __grid
         for (int i = 0; i < kIirBatch; i++) v[i] = col[(y + i) * s];
 #pragma unroll
         for (int i = 0; i < kIirBatch; i++) {
-            const float w = fmaf(P.gB, v[i], fmaf(P.a1, w1, fmaf(P.a2, w2, P.a3 * w3)));
+            const double w = fma(P.gB, (double)v[i], fma(P.a1, w1, fma(P.a2, w2, P.a3 * w3)));
             w3 = w2; w2 = w1; w1 = w;
-            v[i] = w;
+            v[i] = (float)w;
         }
 #pragma unroll
         for (int i = 0; i < kIirBatch; i++) col[(y + i) * s] = v[i];
     }
     for (; y < P.H; y++) {
-        const float w = fmaf(P.gB, col[y * s], fmaf(P.a1, w1, fmaf(P.a2, w2, P.a3 * w3)));
+        const double w = fma(P.gB, (double)col[y * s], fma(P.a1, w1, fma(P.a2, w2, P.a3 * w3)));
         w3 = w2; w2 = w1; w1 = w;
-        col[y * s] = w;
+        col[y * s] = (float)w;
     }
-    float y1 = P.M[0] * w1 + P.M[1] * w2 + P.M[2] * w3;   // y[N]
-    float y2 = P.M[3] * w1 + P.M[4] * w2 + P.M[5] * w3;   // y[N+1]
-    float y3 = P.M[6] * w1 + P.M[7] * w2 + P.M[8] * w3;   // y[N+2]
+    double y1 = P.M[0] * w1 + P.M[1] * w2 + P.M[2] * w3;   // y[N]
+    double y2 = P.M[3] * w1 + P.M[4] * w2 + P.M[5] * w3;   // y[N+1]
+    double y3 = P.M[6] * w1 + P.M[7] * w2 + P.M[8] * w3;   // y[N+2]
     y = P.H - 1;
     for (; y + 1 - kIirBatch >= 0; y -= kIirBatch) {
         float v[kIirBatch];
@@ -63,17 +64,17 @@ static __global__ void __launch_bounds__(kIirColThreads) k_iir_cols(const __grid
         for (int i = 0; i < kIirBatch; i++) v[i] = col[(y - i) * s];
 #pragma unroll
         for (int i = 0; i < kIirBatch; i++) {
-            const float o = fmaf(P.B, v[i], fmaf(P.a1, y1, fmaf(P.a2, y2, P.a3 * y3)));
+            const double o = fma(P.B, (double)v[i], fma(P.a1, y1, fma(P.a2, y2, P.a3 * y3)));
             y3 = y2; y2 = y1; y1 = o;
-            v[i] = o;
+            v[i] = (float)o;
         }
 #pragma unroll
         for (int i = 0; i < kIirBatch; i++) col[(y - i) * s] = v[i];
     }
     for (; y >= 0; y--) {
-        const float o = fmaf(P.B, col[y * s], fmaf(P.a1, y1, fmaf(P.a2, y2, P.a3 * y3)));
+        const double o = fma(P.B, (double)col[y * s], fma(P.a1, y1, fma(P.a2, y2, P.a3 * y3)));
         y3 = y2; y2 = y1; y1 = o;
-        col[y * s] = o;
+        col[y * s] = (float)o;
     }
 }
 
@@ -95,27 +96,27 @@ static __global__ void __launch_bounds__(32) k_iir_rows(const __grid_constant__ 
             if (lane < nc) base[(long long)(r0 + r) * P.Wp + c0 + lane] = t[r][lane];
         __syncwarp();
     };
-    float w1 = 0.f, w2 = 0.f, w3 = 0.f;
+    double w1 = 0.0, w2 = 0.0, w3 = 0.0;
     for (int c0 = 0; c0 < P.W; c0 += 32) {
         const int nc = min(32, P.W - c0);
         load(c0, nc);
         for (int c = 0; c < nc; c++) {
-            const float w = fmaf(P.gB, t[lane][c], fmaf(P.a1, w1, fmaf(P.a2, w2, P.a3 * w3)));
+            const double w = fma(P.gB, (double)t[lane][c], fma(P.a1, w1, fma(P.a2, w2, P.a3 * w3)));
             w3 = w2; w2 = w1; w1 = w;
-            t[lane][c] = w;
+            t[lane][c] = (float)w;
         }
         store(c0, nc);
     }
-    float y1 = P.M[0] * w1 + P.M[1] * w2 + P.M[2] * w3;
-    float y2 = P.M[3] * w1 + P.M[4] * w2 + P.M[5] * w3;
-    float y3 = P.M[6] * w1 + P.M[7] * w2 + P.M[8] * w3;
+    double y1 = P.M[0] * w1 + P.M[1] * w2 + P.M[2] * w3;
+    double y2 = P.M[3] * w1 + P.M[4] * w2 + P.M[5] * w3;
+    double y3 = P.M[6] * w1 + P.M[7] * w2 + P.M[8] * w3;
     for (int c0 = ((P.W - 1) / 32) * 32; c0 >= 0; c0 -= 32) {
         const int nc = min(32, P.W - c0);
         load(c0, nc);
         for (int c = nc - 1; c >= 0; c--) {
-            const float o = fmaf(P.B, t[lane][c], fmaf(P.a1, y1, fmaf(P.a2, y2, P.a3 * y3)));
+            const double o = fma(P.B, (double)t[lane][c], fma(P.a1, y1, fma(P.a2, y2, P.a3 * y3)));
             y3 = y2; y2 = y1; y1 = o;
-            t[lane][c] = o;
+            t[lane][c] = (float)o;
         }
         store(c0, nc);
     }

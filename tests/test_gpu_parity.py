@@ -375,6 +375,9 @@ def test_cluster_k128_rho64_matches_oracle(hdf):
     ("c1", 40, 33, 4, 0.6),           # small sigma (the q formula's lower range)
     ("c1", 70, 50, 6, 8.0),           # sigma wider than the image's half-height
     ("c1", 1, 90, 3, 2.0),            # a single row
+    ("c1", 90, 1, 3, 2.0),            # a single column
+    ("c1", 33, 47, 1, 3.0),           # K = 1: the normalised blur (P9's form)
+    ("c1", 130, 260, 8, 24.0),        # sigma beyond the configs' radii, image wider than 2 x 128 columns
     ("c4", 48, 64, 6, 2.0),           # rho = 6 guide, f != p
 ])
 def test_parity_gaussian_iir(hdf, name, H, W, K, sig):
