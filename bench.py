@@ -1,13 +1,14 @@
 #!/usr/bin/env python
 """Benchmark of the hot path (cluster + pinv + K(n+1) convolutions + combine) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2b] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
 One step = one pass of the whole hot path (S1 cluster, S2 pinv, S3-S6
 filter) over one synthetic image resident in HBM, through the C ABI (hdf_filter with centres=NULL
-clusters inside the call).  Default workload = BASELINE.json configs[1] with K=32 ("c2b":
-512x512x3 colour bilateral, sigma_s=5 (R=15), sigma_r=40).  L2 is flushed (a 512 MiB write)
-between timed steps, outside the timed events.
+clusters inside the call).  Default workload = BASELINE.json configs[4] ("c5": 4096x4096x3 colour
+bilateral, sigma_s=8 (R=24), sigma_r=40, K=64), the largest single-GPU configuration (BASELINE's
+metric names no config).  L2 is flushed (a 512 MiB write) between timed steps, outside the timed
+events; value = pixels / the MEDIAN step time.
 
 Multi-GPU (torchrun, one process per GPU): the path partitions into independent images; every
 rank filters its own seeded image with no collective on the data path ("scaling": "weak"); the
@@ -203,12 +204,13 @@ def run_ours(args, rank: int, world: int, dist):
         dist.barrier()
     clk = clocks.stop()
     prof = hdf.profile_collect()
-    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_ms = statistics.median(step_ms)
     if dist is not None:
         t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
-    ms_step = t_ms / args.steps
+    ms_step = t_ms                              # median step (max over ranks)
     value = (1 if (args.strips and world > 1) else world) * H * W / (ms_step * 1e-3) / 1e6
 
     # ---- end to end through the public host API: H2D + cluster + filter + D2H each step ----
@@ -229,12 +231,12 @@ def run_ours(args, rank: int, world: int, dist):
         b.record(stream)
         b.synchronize()
         e2e_ms.append(a.elapsed_time(b))
-    e2e_t = sum(e2e_ms)
+    e2e_t = statistics.median(e2e_ms)
     if dist is not None:
         t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_t = float(t.item())
-    e2e_val = world * H * W / (e2e_t / args.steps * 1e-3) / 1e6
+    e2e_val = world * H * W / (e2e_t * 1e-3) / 1e6
     h2d = fh.numel() * 4 + (0 if cfg.bilateral else ph.numel() * 4)
     d2h = gh.numel() * 4 + K * cfg.rho * 4 + 8
 
@@ -321,7 +323,10 @@ def run_ours(args, rank: int, world: int, dist):
     launches = sum(n for k, (ms, n) in kern.items())
     return {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "ms_per_step_stats": {"median": round(statistics.median(step_ms), 4), "mean": round(statistics.mean(step_ms), 4),
+                              "min": round(min(step_ms), 4), "max": round(max(step_ms), 4)},
+        "higher_is_better": True,
         "scaling": "strong" if (args.strips and world > 1) else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, SURVEY 8(d) generators)",
         "config": dict(workload_config(args.config, world),
@@ -392,6 +397,18 @@ def cores():
     return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
 
+def cpu_model() -> str:
+    """The host CPU (lscpu 'Model name'), for the cpu_baseline record."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
     os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
     vals, secs = [], []
@@ -402,13 +419,13 @@ def run_reference(args):
         if i >= args.warmup:
             vals.append(v)
             secs.append(dt / reps)
-    value = statistics.mean(vals)
+    value = statistics.median(vals)
     return {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.mean(secs), 3), "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(secs), 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8(d) generators)",
             "impl": "reference", "config": workload_config(args.config, 1),
-            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores(), "kind": "oracle",
-                             "sample": "each step: " + sample},
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores(), "cpu_model": cpu_model(),
+                             "kind": "oracle", "sample": "each step: " + sample},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -417,7 +434,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2b")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--all", action="store_true", help="one line per config (exploration)")
@@ -447,8 +464,8 @@ def main():
         if rank == 0 and not args.no_cpu_baseline and not args.all:
             os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
             v, dt, reps, sample = oracle_sample(c, 30.0, min_s=10.0)
-            out["cpu_baseline"] = {"value": round(v, 4), "unit": UNIT, "cores": cores(), "kind": "oracle",
-                                   "sample": sample, "seconds": round(dt, 2)}
+            out["cpu_baseline"] = {"value": round(v, 4), "unit": UNIT, "cores": cores(), "cpu_model": cpu_model(),
+                                   "kind": "oracle", "sample": sample, "seconds": round(dt, 2)}
         if rank == 0:
             print(json.dumps(out), flush=True)
     if dist is not None:

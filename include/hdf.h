@@ -47,7 +47,7 @@ typedef enum {
     HDF_SPATIAL_GAUSSIAN = 0, /* omega(i) = exp(-||i||^2 / 2 sigma_s^2) on [-S,S]^2 */
     HDF_SPATIAL_BOX = 1,      /* omega = 1 on [-S,S]^2 (nonlocal means)                 */
     HDF_SPATIAL_GAUSSIAN_IIR = 2 /* Young's O(1) recursive Gaussian, the paper's implementation of
-                                    the Gaussian convolutions; sigma_s >= 0.5; zero
+                                    the Gaussian convolutions; 0.5 <= sigma_s <= 4096; zero
                                     outside the image, gain sqrt(2 pi) sigma_s per axis so that
                                     omega(0) ~ 1 (DESIGN R17); `radius` (or ceil(3 sigma_s)) only
                                     sizes the R9 fallback's direct window sum (exact FIR Gaussian,
@@ -142,10 +142,18 @@ size_t hdf_filter_workspace_bytes(int H, int W, int n, int rho, int K, int kind,
  *   tau      degenerate-normaliser threshold (R9); 0 disables the rule; callers pass 0.5
  *   g        [H][W][n] float32, device, out
  *   n_flagged_host  int32*, host, out: number of pixels that took the R9 fallback; may be NULL.
- *            Non-NULL synchronises `stream`; the call then also returns HDF_WARN_ILLCOND when A was
- *            numerically singular (its pseudo-inverse truncated eigenvalues below tol, R6).
+ *            Non-NULL synchronises `stream` once, at the end of the call, and the call then reports
+ *            what happened on the device: HDF_ERR_K (centres == NULL and K exceeds the number of
+ *            distinct guide vectors, R5: g holds the result with the padded centres of hdf_cluster),
+ *            HDF_ERR_CUDA (the clustering kernel failed), else HDF_WARN_ILLCOND when A was
+ *            numerically singular (its pseudo-inverse truncated eigenvalues below tol, R6), else
+ *            HDF_OK.  With NULL the call is fully asynchronous and reports argument errors only.
  *   ws, ws_bytes  device workspace of at least hdf_filter_workspace_bytes(...)
  *   stream   cudaStream_t as void*
+ * Threads: calls from several host threads are safe (errors are per thread).  The pseudo-inverse
+ * kernel runs on a library-owned side stream per device, forked from and joined back to `stream` by
+ * events under a per-device lock; calls on different streams therefore serialise their (small)
+ * pseudo-inverse kernels on that side stream.
  */
 int hdf_filter(const float *f, int n, const float *p, int rho, int H, int W, int kind, float sigma_s,
                int radius, float sigma_r, int K, const float *centres, float tau, float *g,
@@ -186,17 +194,32 @@ int hdf_filter_hard(const float *f, int n, const float *p, int rho, int H, int W
 
 /*
  * hdf_filter_host -- the whole hot path end to end from HOST buffers: copies f and p to the device
- * workspace, clusters, filters, and copies g back, all on `stream`, then synchronises it.
+ * workspace, clusters, filters, and copies g back, all on `stream`, then synchronises it once.
  *   f_host [H][W][n], p_host [H][W][rho] (may be the same pointer), g_host [H][W][n]: host float32
  *   (pinned memory gives full-rate copies; pageable memory works but is slower).
- *   centres_host [K][rho] out, may be NULL.  info_host may be NULL.
+ *   centres_host [K][rho] out, may be NULL.  n_flagged_host, info_host: out, may be NULL.
  *   ws: device workspace of at least hdf_filter_host_workspace_bytes(...).
+ * Every argument is checked before the first copy is enqueued (HDF_ERR_ARG / HDF_ERR_WORKSPACE,
+ * nothing enqueued).  A failure after that synchronises `stream` before returning.  Returns HDF_OK,
+ * HDF_ERR_K (K exceeds the number of distinct guide vectors, R5; g_host then holds the result with
+ * the padded centres), HDF_ERR_CUDA, or HDF_WARN_ILLCOND (A^+ truncated, R6; g_host is valid).
+ * The status words are read back through a few bytes of pinned host memory per calling thread
+ * (allocated by the library on first use), so the call does not block mid-way.
  */
 size_t hdf_filter_host_workspace_bytes(int H, int W, int n, int rho, int K, int kind, float sigma_s, int radius);
 int hdf_filter_host(const float *f_host, int n, const float *p_host, int rho, int H, int W, int kind,
                     float sigma_s, int radius, float sigma_r, int K, float tau, float *g_host,
                     float *centres_host, int32_t *n_flagged_host, hdf_cluster_info *info_host,
                     void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * hdf_filter_flagged -- diagnostics and parity tests: the pixels (index y*W + x) that took the R9
+ * fallback in the last hdf_filter / hdf_filter_hard call that used workspace `ws` with the same
+ * H, W, n, rho, K.  Synchronous (device -> host copies).  Copies at most `cap` indices into idx_host
+ * (host, may be NULL when cap is 0), in the order the row pass flagged them (not sorted); returns the
+ * number of flagged pixels, or -1 on a CUDA error or a NULL workspace.
+ */
+int hdf_filter_flagged(const void *ws, int H, int W, int n, int rho, int K, int32_t *idx_host, int cap);
 
 /* ---------------------------------------------------------------------------------------------
  * Per-stage device timing (benchmarking / tracing).  When enabled, every

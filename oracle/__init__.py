@@ -6,6 +6,7 @@ package.  It shares no code with paper_1811_02363_b200 (the CUDA path) and never
 
 Functions follow PAPER.md (see the C file for per-function citations):
   cluster        bisecting K-means (readings R1-R5)
+  farthest_pair  its seed step on its own (R3), for the pins
   gram, pinv     A_kl = phi(mu_k - mu_l) and MATLAB-style pinv (R6)
   filter         Algorithm 1 with the R9 degenerate-normaliser rule
   filter_pixels  the same filter evaluated at selected pixels from (temp1)/(temp2)
@@ -73,9 +74,10 @@ def _L():
             lib.orc_nystrom_pixels.argtypes = [D, i, D, i, i, i, i, d, i, d, i, D, LP, l, D, D]
             lib.orc_coefficients.argtypes = [D, l, i, D, i, d, D, D]
             lib.orc_filter_hard.argtypes = [D, i, D, i, i, i, i, d, i, d, i, D, I32, D]
+            lib.orc_farthest_pair.argtypes = [D, i, LP, l, i, LP, LP]
             for fn in ("orc_spatial_taps", "orc_cluster", "orc_gram", "orc_pinv_sym", "orc_conv2",
                        "orc_bruteforce_pixels", "orc_filter", "orc_filter_pixels",
-                       "orc_nystrom_pixels", "orc_filter_hard", "orc_coefficients"):
+                       "orc_nystrom_pixels", "orc_filter_hard", "orc_coefficients", "orc_farthest_pair"):
                 getattr(lib, fn).restype = C.c_int
             _lib = lib
     return _lib
@@ -134,6 +136,20 @@ def cluster(p, K: int, cap: int = 1024, max_iter: int = 50):
         raise OracleKError(ach.value)
     _check(st, "cluster")
     return cen, lab, sse, ek.value
+
+
+def farthest_pair(p, members, cap: int = 1024):
+    """The seed step of one split (R3): the farthest pair of the stride sample
+    members[0::ceil(m/cap)] of the given members (ascending pixel indices).  Returns the two pixel
+    indices (a, b) of the lexicographically smallest pair in sample order among the maximisers."""
+    p = _d(p)
+    rho = p.shape[-1]
+    P = p.reshape(-1, rho)
+    mem = np.ascontiguousarray(np.asarray(members, dtype=np.int64).reshape(-1))
+    a, b = C.c_long(0), C.c_long(0)
+    _check(_L().orc_farthest_pair(_pd(P), rho, mem.ctypes.data_as(C.POINTER(C.c_long)), mem.size, int(cap),
+                                  C.byref(a), C.byref(b)), "farthest_pair")
+    return a.value, b.value
 
 
 def gram(mu, sigma_r: float) -> np.ndarray:

@@ -133,6 +133,20 @@ static void farthest_pair(const double *p, int rho, const Leaf *L, int cap, long
     *pb = L->idx[bb * stride];
 }
 
+/* The seed step of one split on its own, for the pins (tests/test_oracle_pins.py): the farthest pair
+ * of the stride sample of the members idx[0..m) (ascending pixel index, R3).  Writes the two
+ * pixel indices; no arithmetic beyond farthest_pair above. */
+int orc_farthest_pair(const double *p, int rho, const long *idx, long m, int cap, long *pa, long *pb) {
+    if (!p || rho < 1 || !idx || m < 1 || cap < 2 || !pa || !pb) return ORC_ERR_ARG;
+    Leaf L;
+    L.idx = (long *)idx;
+    L.m = m;
+    L.mean = NULL;
+    L.sse = 0.0;
+    farthest_pair(p, rho, &L, cap, pa, pb);
+    return ORC_OK;
+}
+
 /* Nearest of two centres, ties -> first (R4). */
 static int nearer(const double *x, const double *c0, const double *c1, int rho) {
     return dist2(x, c0, rho) <= dist2(x, c1, rho) ? 0 : 1;

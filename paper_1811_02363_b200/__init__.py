@@ -28,7 +28,7 @@ MAX_K, MAX_RHO, MAX_N, MAX_RADIUS = 128, 64, 64, 32
 EXPORTS = ("hdf_version", "hdf_last_error", "hdf_cluster_workspace_bytes", "hdf_cluster",
            "hdf_filter_workspace_bytes", "hdf_filter", "hdf_filter_hard", "hdf_filter_host_workspace_bytes",
            "hdf_filter_host", "hdf_pca_guide_workspace_bytes", "hdf_pca_guide",
-           "hdf_profile_enable", "hdf_profile_collect", "hdf_cluster_trace")
+           "hdf_profile_enable", "hdf_profile_collect", "hdf_cluster_trace", "hdf_filter_flagged")
 STAGES = ("cluster", "pinv", "coeffs", "vpass", "hpass", "fallback", "h2d", "d2h")
 
 
@@ -90,6 +90,8 @@ def lib():
         L.hdf_profile_collect.restype = i
         L.hdf_cluster_trace.argtypes = [vp, i, i, i, i, vp, C.POINTER(C.c_longlong), i]
         L.hdf_cluster_trace.restype = i
+        L.hdf_filter_flagged.argtypes = [vp, i, i, i, i, i, C.POINTER(C.c_int32), i]
+        L.hdf_filter_flagged.restype = i
         _lib = L
     return _lib
 
@@ -114,6 +116,22 @@ def _dev_f32(t: torch.Tensor, name: str) -> torch.Tensor:
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
     return t
+
+
+def _out(out, shape, device, name="out") -> torch.Tensor:
+    """The caller's output tensor: float32, contiguous, of exactly `shape`, on `device` (the kernels
+    write shape-many floats through its pointer)."""
+    t = _dev_f32(out, name)
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)} (got {tuple(t.shape)})")
+    if t.device != device:
+        raise ValueError(f"{name} must be on {device} (got {t.device})")
+    return t
+
+
+def _same_device(t: torch.Tensor, device, name: str):
+    if t.device != device:
+        raise ValueError(f"{name} must be on {device} (got {t.device})")
 
 
 def _hwc(t: torch.Tensor, name: str):
@@ -196,13 +214,15 @@ def filter(f: torch.Tensor, p: torch.Tensor | None = None, *, kind: str = "gauss
     Hp, Wp, rho = _hwc(p, "p")
     if (Hp, Wp) != (H, W):
         raise ValueError("f and p must have the same H, W")
+    _same_device(p, f.device, "p")
     if centres is not None:
         centres = _dev_f32(centres, "centres")
         if centres.dim() != 2 or centres.shape[1] != rho:
             raise ValueError("centres must be [K, rho]")
+        _same_device(centres, f.device, "centres")
         K = centres.shape[0]
-    g = out if out is not None else torch.empty((H, W, n), dtype=torch.float32, device=f.device)
-    g = _dev_f32(g, "out")
+    g = _out(out, (H, W, n), f.device) if out is not None else \
+        torch.empty((H, W, n), dtype=torch.float32, device=f.device)
     need = filter_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius)
     wsb = (ws or _default_ws).get(need, f.device)
     nfl = C.c_int32(-1)
@@ -210,6 +230,8 @@ def filter(f: torch.Tensor, p: torch.Tensor | None = None, *, kind: str = "gauss
                           float(sigma_r), int(K), centres.data_ptr() if centres is not None else None, float(tau),
                           g.data_ptr(), C.byref(nfl) if count_flagged else None, wsb.data_ptr(), wsb.numel(),
                           _stream_ptr(stream))
+    if st == ERR_K:
+        raise HdfKError(st, lib().hdf_last_error().decode(), -1)
     if st not in (OK, WARN_ILLCOND):
         _raise(st)
     return FilterResult(g, nfl.value if count_flagged else None, st)
@@ -233,6 +255,7 @@ def filter_hard(f: torch.Tensor, p: torch.Tensor | None = None, *, kind: str = "
         raise ValueError("f and p must have the same H, W")
     if (centres is None) != (labels is None):
         raise ValueError("pass both centres and labels, or neither")
+    _same_device(p, f.device, "p")
     if centres is not None:
         centres = _dev_f32(centres, "centres")
         if centres.dim() != 2 or centres.shape[1] != rho:
@@ -241,8 +264,10 @@ def filter_hard(f: torch.Tensor, p: torch.Tensor | None = None, *, kind: str = "
         if not (labels.is_cuda and labels.dtype == torch.int32 and labels.is_contiguous()
                 and labels.numel() == H * W):
             raise TypeError("labels must be a contiguous int32 CUDA tensor of H*W elements")
-    g = out if out is not None else torch.empty((H, W, n), dtype=torch.float32, device=f.device)
-    g = _dev_f32(g, "out")
+        _same_device(centres, f.device, "centres")
+        _same_device(labels, f.device, "labels")
+    g = _out(out, (H, W, n), f.device) if out is not None else \
+        torch.empty((H, W, n), dtype=torch.float32, device=f.device)
     need = filter_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius)
     wsb = (ws or _default_ws).get(need, f.device)
     st = lib().hdf_filter_hard(f.data_ptr(), n, p.data_ptr(), rho, H, W, KIND[kind], float(sigma_s), int(radius),
@@ -283,9 +308,16 @@ def filter_host(f_host: torch.Tensor, p_host: torch.Tensor | None = None, *, kin
         if t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
             raise TypeError(f"{nm} must be a contiguous float32 host tensor")
     H, W, n = _hwc(f_host, "f")
-    _, _, rho = _hwc(p_host, "p")
+    Hp, Wp, rho = _hwc(p_host, "p")
+    if (Hp, Wp) != (H, W):
+        raise ValueError("f and p must have the same H, W")
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    g = out if out is not None else torch.empty((H, W, n), dtype=torch.float32, pin_memory=True)
+    if out is not None:
+        if out.is_cuda or out.dtype != torch.float32 or not out.is_contiguous() or out.numel() != H * W * n:
+            raise ValueError(f"out must be a contiguous float32 host tensor of {H * W * n} elements")
+        g = out
+    else:
+        g = torch.empty((H, W, n), dtype=torch.float32, pin_memory=True)
     cen = torch.empty((K, rho), dtype=torch.float32)
     need = int(lib().hdf_filter_host_workspace_bytes(H, W, n, rho, K, KIND[kind], float(sigma_s), int(radius)))
     wsb = (ws or _default_ws).get(need, dev)
@@ -294,9 +326,22 @@ def filter_host(f_host: torch.Tensor, p_host: torch.Tensor | None = None, *, kin
     st = lib().hdf_filter_host(f_host.data_ptr(), n, p_host.data_ptr(), rho, H, W, KIND[kind], float(sigma_s),
                                int(radius), float(sigma_r), int(K), float(tau), g.data_ptr(), cen.data_ptr(),
                                C.byref(nfl), C.byref(inf), wsb.data_ptr(), wsb.numel(), _stream_ptr(stream))
+    if st == ERR_K:
+        raise HdfKError(st, lib().hdf_last_error().decode(), inf.achievable_k)
     if st not in (OK, WARN_ILLCOND):
         _raise(st)
     return g, cen, nfl.value, inf
+
+
+def flagged_pixels(ws: Workspace, H: int, W: int, n: int, rho: int, K: int):
+    """The pixel indices (y*W + x, sorted) that took the R9 fallback in the last filter() call on
+    workspace ws with these sizes (include/hdf.h, hdf_filter_flagged).  Synchronous."""
+    import numpy as np
+    buf = (C.c_int32 * max(H * W, 1))()
+    cnt = lib().hdf_filter_flagged(ws.buf.data_ptr(), H, W, n, rho, K, buf, H * W)
+    if cnt < 0:
+        _raise(ERR_CUDA)
+    return np.sort(np.frombuffer(buf, dtype=np.int32, count=cnt).copy())
 
 
 def profile_enable(on: bool = True) -> None:

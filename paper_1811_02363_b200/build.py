@@ -24,6 +24,30 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-I" + os.path.join(ROOT, "include")] + os.environ.get("HDF_EXTRA_FLAGS", "").split()
 
 
+def _deps(path: str, seen=None) -> list:
+    """The file and every local header it includes, transitively (#include "...")."""
+    import re
+    seen = set() if seen is None else seen
+    path = os.path.normpath(path)
+    if path in seen or not os.path.exists(path):
+        return []
+    seen.add(path)
+    out = [path]
+    with open(path) as fh:
+        for inc in re.findall(r'^\s*#include\s+"([^"]+)"', fh.read(), re.M):
+            out += _deps(os.path.join(os.path.dirname(path), inc), seen)
+    return out
+
+
+def _digest(src: str, defs=()) -> str:
+    h = hashlib.sha256()
+    for p in sorted(_deps(src)):
+        with open(p, "rb") as fh:
+            h.update(os.path.basename(p).encode() + fh.read())
+    h.update(" ".join(FLAGS + list(defs)).encode())
+    return h.hexdigest()
+
+
 def _sources_digest() -> str:
     h = hashlib.sha256()
     for d in (CSRC, os.path.join(ROOT, "include")):
@@ -53,12 +77,36 @@ def build(force: bool = False, verbose: bool = False) -> str:
     jobs = [(os.path.join(CSRC, "hdf_api.cu"), os.path.join(OBJ, "hdf_api.o"), ())]
     for r in RADII:
         jobs.append((os.path.join(CSRC, "inst_r.cu"), os.path.join(OBJ, f"inst_r{r}.o"), (f"-DHDF_R={r}",)))
+    for r in range(8):     # k_bisect<RHO>, RHO = 0 (runtime) .. 7
+        jobs.append((os.path.join(CSRC, "inst_bisect.cu"), os.path.join(OBJ, f"inst_bisect{r}.o"), (f"-DHDF_BRHO={r}",)))
+    for nt in range(1, 9):  # k_coeffs_mma<NT, *>, K <= 8 NT
+        jobs.append((os.path.join(CSRC, "inst_coeffs.cu"), os.path.join(OBJ, f"inst_coeffs{nt}.o"), (f"-DHDF_CNT={nt}",)))
+    # per object: recompile only when its source, a header it includes or the flags changed
+    todo = []
+    for src, obj, defs in jobs:
+        dg = _digest(src, defs)
+        st = obj + ".digest"
+        if force or not os.path.exists(obj) or not os.path.exists(st) or open(st).read() != dg:
+            todo.append((src, obj, defs, dg))
     logs = []
-    with cf.ThreadPoolExecutor(max_workers=min(len(jobs), max(2, os.cpu_count() or 2))) as ex:
-        for (src, obj, defs), log in zip(jobs, ex.map(lambda j: _compile(*j), jobs)):
+
+    def run(j):
+        src, obj, defs, dg = j
+        log = _compile(src, obj, defs)
+        with open(obj + ".digest", "w") as fh:
+            fh.write(dg)
+        with open(obj + ".ptxas.log", "w") as fh:
+            fh.write(log)
+        return log
+
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(len(todo), max(2, os.cpu_count() or 2)))) as ex:
+        for (src, obj, defs, _), log in zip(todo, ex.map(run, todo)):
             logs.append(f"== {os.path.basename(src)} {' '.join(defs)}\n{log}")
     with open(os.path.join(OBJ, "ptxas.log"), "w") as fh:
-        fh.write("\n".join(logs))
+        for src, obj, defs in jobs:
+            lp = obj + ".ptxas.log"
+            fh.write(f"== {os.path.basename(src)} {' '.join(defs)}\n" + (open(lp).read() if os.path.exists(lp) else "")
+                     + "\n")
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", "-o", tmp,
            *[j[1] for j in jobs], "-lcudart"]

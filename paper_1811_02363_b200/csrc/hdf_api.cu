@@ -55,6 +55,26 @@ struct Carver {
 
 int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
+// No C++ exception crosses the C ABI: every entry point runs its body through guarded().
+template <class Fn>
+int guarded(Fn&& fn) {
+    try {
+        return fn();
+    } catch (const std::exception& e) {
+        return fail(HDF_ERR_CUDA, "internal exception: %s", e.what());
+    } catch (...) {
+        return fail(HDF_ERR_CUDA, "internal exception");
+    }
+}
+template <class Fn>
+size_t guarded_size(Fn&& fn) {
+    try {
+        return fn();
+    } catch (...) {
+        return 0;
+    }
+}
+
 // ------------------------------------------------------------------ per-stage event profiling ----
 // When enabled (hdf_profile_enable), every stage records a start/end CUDA event pair on the call's
 // stream; hdf_profile_collect() waits for them and returns the summed device time per stage.
@@ -154,17 +174,17 @@ size_t bisect_dyn_smem(int rho, int cap) {
     return x + w + smp;
 }
 
-using BisectKernel = void (*)(const hdf::BisectArgs);
+using BisectKernel = hdf::BisectFn;
 BisectKernel bisect_kernel(int rho) {
     switch (rho) {
-        case 1: return hdf::k_bisect<1>;
-        case 2: return hdf::k_bisect<2>;
-        case 3: return hdf::k_bisect<3>;
-        case 4: return hdf::k_bisect<4>;
-        case 5: return hdf::k_bisect<5>;
-        case 6: return hdf::k_bisect<6>;
-        case 7: return hdf::k_bisect<7>;
-        default: return hdf::k_bisect<0>;
+        case 1: return hdf::bisect_kernel_rho1();
+        case 2: return hdf::bisect_kernel_rho2();
+        case 3: return hdf::bisect_kernel_rho3();
+        case 4: return hdf::bisect_kernel_rho4();
+        case 5: return hdf::bisect_kernel_rho5();
+        case 6: return hdf::bisect_kernel_rho6();
+        case 7: return hdf::bisect_kernel_rho7();
+        default: return hdf::bisect_kernel_rho0();
     }
 }
 
@@ -185,19 +205,85 @@ int env_cluster_dim() {
     return e ? atoi(e) : 0;
 }
 
+// The clustering launch shape (cached per rho): one 512-thread CTA per SM with the largest tile that
+// fits, in a cooperative grid of thread-block clusters.
+struct ClusterShape {
+    int cdim, nclusters, cap;
+    size_t smem;
+};
+
+// Per-thread pinned host words that the calls with *_host outputs read back into: the clustering's
+// control words and E_K, the filter's status and flag count.  Pinned, so that the read-backs are
+// enqueued asynchronously and read after the call's one final synchronisation (a read into pageable
+// memory would block the host mid-call).  Allocated on first use (a few hundred bytes of pinned host
+// memory per calling thread, never freed); the library allocates no device memory.
+struct HostStage {
+    int ctrl[hdf::B_NUM];
+    double ek;
+    int hv[2];   // filter: A^+ status, number of flagged pixels
+};
+HostStage* host_stage() {
+    static thread_local HostStage* hs = nullptr;
+    if (!hs) {
+        void* p = nullptr;
+        if (cudaMallocHost(&p, sizeof(HostStage)) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        hs = static_cast<HostStage*>(p);
+    }
+    return hs;
+}
+
+// The clustering kernel's control words and E_K in the calling thread's pinned stage, read back
+// with the caller's final synchronisation.
+struct ClusterReadback {
+    HostStage* hs = nullptr;
+    ClusterShape sh;
+};
+
+// Status of a finished clustering from its control words; fills info (may be NULL).
+int cluster_status(const ClusterReadback& rb, int K, hdf_cluster_info* info) {
+    const int* ctrl = rb.hs->ctrl;
+    if (info) {
+        memset(info, 0, sizeof(*info));
+        info->launch_ctas = (int)(rb.sh.cdim * rb.sh.nclusters);
+        info->cluster_ctas = rb.sh.cdim;
+        info->status = ctrl[hdf::B_STATUS];
+        info->achievable_k = ctrl[hdf::B_ACH];
+        info->splits_computed = ctrl[hdf::B_SPLITS];
+        info->lloyd_iters = ctrl[hdf::B_ITERS];
+        info->grid_splits = ctrl[hdf::B_GRIDSPLITS];
+        unsigned long long pp, pm;
+        memcpy(&pp, &ctrl[hdf::B_PTPASS], 8);
+        memcpy(&pm, &ctrl[hdf::B_PTSPLIT], 8);
+        info->point_passes = (int64_t)pp;
+        info->points_split = (int64_t)pm;
+        info->tile_points = rb.sh.cap;
+        info->e_k = rb.hs->ek;
+    }
+    if (ctrl[hdf::B_STATUS] == HDF_ERR_CUDA)
+        return fail(HDF_ERR_CUDA,
+                    "clustering kernel: internal error (abort %d, nodes %d, splits %d, not done %d, diag %d %d %d %d "
+                    "%d %d)",
+                    ctrl[hdf::B_ABORT], ctrl[hdf::B_NALLOC], ctrl[hdf::B_SPLITS], ctrl[hdf::B_NOTDONE],
+                    ctrl[hdf::B_DIAG0], ctrl[hdf::B_DIAG1], ctrl[hdf::B_DIAG2], ctrl[hdf::B_DIAG3], ctrl[hdf::B_DIAG4],
+                    ctrl[hdf::B_DIAG5]);
+    if (ctrl[hdf::B_STATUS] == HDF_ERR_K)
+        return fail(HDF_ERR_K, "K=%d exceeds the number of distinct guide vectors (%d)", K, ctrl[hdf::B_ACH]);
+    return HDF_OK;
+}
+
+// Launch the clustering.  info != NULL: read the result back now (synchronises `st`).  rb != NULL:
+// enqueue the read-back into *rb (which must stay alive until the caller synchronises `st`).
 int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres, int32_t* labels,
-                   hdf_cluster_info* info, void* ws, cudaStream_t st) {
+                   hdf_cluster_info* info, void* ws, cudaStream_t st, ClusterReadback* rb = nullptr) {
     Carver cv(ws);
     hdf::BisectArgs A = carve_cluster(cv, p, H, W, rho, K);
     A.centres = centres;
     A.labels = labels;
     BisectKernel kern = bisect_kernel(rho);
-    // Launch shape (cached per rho): one 512-thread CTA per SM with the largest tile that fits, in a
-    // cooperative grid of thread-block clusters.
-    struct Shape {
-        int cdim, nclusters, cap;
-        size_t smem;
-    };
+    using Shape = ClusterShape;
     static std::mutex mu;
     static Shape cache[17][HDF_MAX_RHO + 1];   // by requested cluster size (0 = default) and rho
     Shape sh;
@@ -289,38 +375,18 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
         ProfScope prof(HDF_STAGE_CLUSTER, st);
         HDF_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
     }
-    if (info) {
-        int ctrl[hdf::B_NUM];
-        double ek = 0.0;
-        HDF_CUDA(cudaMemcpyAsync(ctrl, A.ctl, sizeof(ctrl), cudaMemcpyDeviceToHost, st));
-        HDF_CUDA(cudaMemcpyAsync(&ek, A.ek, sizeof(double), cudaMemcpyDeviceToHost, st));
+    ClusterReadback local;
+    ClusterReadback* r = rb ? rb : (info ? &local : nullptr);
+    if (r) {
+        r->sh = sh;
+        r->hs = host_stage();
+        if (!r->hs) return fail(HDF_ERR_CUDA, "pinned host stage: cudaMallocHost failed");
+        HDF_CUDA(cudaMemcpyAsync(r->hs->ctrl, A.ctl, sizeof(r->hs->ctrl), cudaMemcpyDeviceToHost, st));
+        HDF_CUDA(cudaMemcpyAsync(&r->hs->ek, A.ek, sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    if (info && !rb) {
         HDF_CUDA(cudaStreamSynchronize(st));
-        memset(info, 0, sizeof(*info));
-        info->launch_ctas = (int)(sh.cdim * sh.nclusters);
-        info->cluster_ctas = sh.cdim;
-        info->status = ctrl[hdf::B_STATUS];
-        info->achievable_k = ctrl[hdf::B_ACH];
-        info->splits_computed = ctrl[hdf::B_SPLITS];
-        info->lloyd_iters = ctrl[hdf::B_ITERS];
-        info->grid_splits = ctrl[hdf::B_GRIDSPLITS];
-        {
-            unsigned long long pp, pm;
-            memcpy(&pp, &ctrl[hdf::B_PTPASS], 8);
-            memcpy(&pm, &ctrl[hdf::B_PTSPLIT], 8);
-            info->point_passes = (int64_t)pp;
-            info->points_split = (int64_t)pm;
-        }
-        info->tile_points = sh.cap;
-        info->e_k = ek;
-        if (info->status == HDF_ERR_CUDA)
-            return fail(HDF_ERR_CUDA,
-                        "clustering kernel: internal error (abort %d, nodes %d, splits %d, not done %d, diag %d %d %d %d "
-                        "%d %d)",
-                        ctrl[hdf::B_ABORT], ctrl[hdf::B_NALLOC], ctrl[hdf::B_SPLITS], ctrl[hdf::B_NOTDONE],
-                        ctrl[hdf::B_DIAG0], ctrl[hdf::B_DIAG1], ctrl[hdf::B_DIAG2], ctrl[hdf::B_DIAG3],
-                        ctrl[hdf::B_DIAG4], ctrl[hdf::B_DIAG5]);
-        if (info->status == HDF_ERR_K)
-            return fail(HDF_ERR_K, "K=%d exceeds the number of distinct guide vectors (%d)", K, info->achievable_k);
+        return cluster_status(local, K, info);
     }
     return HDF_OK;
 }
@@ -349,6 +415,9 @@ struct FilterPlan {
 
 // the recursive Gaussian's R9 fallback window (a direct sum per flagged pixel, weights computed in place)
 constexpr int kMaxFallbackRadius = 512;
+// the recursive Gaussian's largest sigma_s (its anti-causal start matrix is simulated on the host over
+// 60 sigma_s + 100 samples, iir_params)
+constexpr float kMaxIirSigma = 4096.f;
 
 int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, FilterPlan* fp, int nsm) {
     FilterPlan& F = *fp;
@@ -359,6 +428,8 @@ int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, F
     F.Rfb = -1;
     if (F.iir) {   // the recursion replaces the FIR; radius only sizes the R9 fallback's window
         if (!(sigma_s >= 0.5f)) return fail(HDF_ERR_ARG, "the recursive Gaussian needs sigma_s >= 0.5");
+        if (!(sigma_s <= kMaxIirSigma))
+            return fail(HDF_ERR_ARG, "the recursive Gaussian needs sigma_s <= %g", (double)kMaxIirSigma);
         F.Rfb = radius >= 0 ? radius : (int)std::ceil(3.0 * (double)sigma_s);
         if (F.Rfb > kMaxFallbackRadius)
             return fail(HDF_ERR_ARG, "fallback radius %d exceeds %d", F.Rfb, kMaxFallbackRadius);
@@ -507,12 +578,19 @@ int encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2, 
 // Library-owned side stream and fork/join events (per device): k_gram_pinv runs on it, concurrently
 // with the column pass (which leaves one SM free for it), and the main stream waits for it before the
 // coefficient kernel.  Created once, never destroyed (process lifetime).
+// The fork/join events are shared by every call on the device, so a call holds the device's `mu`
+// from recording `fork` until its main stream has waited on `join` (host-side only, a few launches):
+// another thread can then neither re-record `fork` before this call's side stream waited on it, nor
+// `join` before this call's main stream did.  Calls on different caller streams share the side
+// stream, so their k_gram_pinv launches are serialised on it (correct, not concurrent).
 struct SideStream {
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
+    std::mutex* mu = nullptr;
 };
 int side_stream(SideStream* out) {
     static std::mutex mu;
+    static std::mutex dev_mu[64];
     static SideStream cache[64];
     int dev = 0;
     HDF_CUDA(cudaGetDevice(&dev));
@@ -523,28 +601,23 @@ int side_stream(SideStream* out) {
         HDF_CUDA(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
         HDF_CUDA(cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming));
         HDF_CUDA(cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming));
+        c.mu = &dev_mu[dev];
     }
     *out = c;
     return HDF_OK;
 }
 
-using CoefKernel = void (*)(const hdf::CoefParams);
-template <int NT>
-CoefKernel coeffs_mma_rho(int rho) {
-    if (rho == 3) return hdf::k_coeffs_mma<NT, 3>;
-    if (rho == 6) return hdf::k_coeffs_mma<NT, 6>;
-    return hdf::k_coeffs_mma<NT, 0>;
-}
+using CoefKernel = hdf::CoefFn;
 CoefKernel coeffs_mma_kernel(int nt, int rho) {
     switch (nt) {
-        case 1: return coeffs_mma_rho<1>(rho);
-        case 2: return coeffs_mma_rho<2>(rho);
-        case 3: return coeffs_mma_rho<3>(rho);
-        case 4: return coeffs_mma_rho<4>(rho);
-        case 5: return coeffs_mma_rho<5>(rho);
-        case 6: return coeffs_mma_rho<6>(rho);
-        case 7: return coeffs_mma_rho<7>(rho);
-        case 8: return coeffs_mma_rho<8>(rho);
+        case 1: return hdf::coeffs_mma_kernel_nt1(rho);
+        case 2: return hdf::coeffs_mma_kernel_nt2(rho);
+        case 3: return hdf::coeffs_mma_kernel_nt3(rho);
+        case 4: return hdf::coeffs_mma_kernel_nt4(rho);
+        case 5: return hdf::coeffs_mma_kernel_nt5(rho);
+        case 6: return hdf::coeffs_mma_kernel_nt6(rho);
+        case 7: return hdf::coeffs_mma_kernel_nt7(rho);
+        case 8: return hdf::coeffs_mma_kernel_nt8(rho);
         default: return nullptr;
     }
 }
@@ -601,48 +674,73 @@ hdf::IIRParams iir_params(double s) {
 
 // hard: the hard-assignment variant: c = one-hot(label), no A^+, no fallback (tau = 0).
 // hard_labels: the caller's labels (with its centres), or NULL to cluster here (labels in the workspace).
-int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int kind, float sigma_s, int radius,
-               float sigma_r, int K, const float* centres, float tau, float* g, int32_t* n_flagged_host, void* ws,
-               size_t ws_bytes, cudaStream_t st, bool hard = false, const int32_t* hard_labels = nullptr) {
+// Every argument check of a filter call that needs no pointer (shared by the device and host entry
+// points, so that both reject bad arguments before anything is enqueued).
+// (1) the scalar arguments (no CUDA call)
+int validate_scalars(int n, int rho, int H, int W, int kind, float sigma_r, int K, float tau, bool hard) {
     int rc = check_common(H, W, rho, K);
     if (rc) return rc;
-    if (!f || !p || !g || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
     if (n < 1 || n > HDF_MAX_N) return fail(HDF_ERR_ARG, "n must be in [1, %d] (got %d)", HDF_MAX_N, n);
     if (!(sigma_r > 0.f)) return fail(HDF_ERR_ARG, "sigma_r must be > 0");
     if (!(tau >= 0.f)) return fail(HDF_ERR_ARG, "tau must be >= 0");
+    if (hard && kind == HDF_SPATIAL_GAUSSIAN_IIR)   // no oracle for that pairing: not offered
+        return fail(HDF_ERR_ARG, "the hard-assignment variant takes the FIR kinds (gaussian, box)");
+    return HDF_OK;
+}
+
+// (2) the plan and the device limits
+int validate_filter(int n, int rho, int H, int W, int kind, float sigma_s, int radius, float sigma_r, int K,
+                    float tau, bool f_is_p, bool hard, FilterPlan* F, size_t* vsmem) {
+    int rc = validate_scalars(n, rho, H, W, kind, sigma_r, K, tau, hard);
+    if (rc) return rc;
+    rc = make_plan(H, W, n, K, kind, sigma_s, radius, F, nsm_of_device());
+    if (rc) return rc;
+    // the column pass keeps J raw rows (rho or rho + n floats per pixel, double buffered) and J range-
+    // weight rows of its plane group in shared memory: checked before anything is enqueued
+    *vsmem = vpass_smem(*F, rho, n, f_is_p);
+    int dev = 0, optin = 0;
+    HDF_CUDA(cudaGetDevice(&dev));
+    HDF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (*vsmem > (size_t)optin)
+        return fail(HDF_ERR_ARG,
+                    "the column pass needs %zu bytes of shared memory (rho %d, n %d, radius %d) > %d: reduce "
+                    "rho + n or the radius",
+                    *vsmem, rho, n, F->Rp, optin);
+    return HDF_OK;
+}
+
+// hard: the hard-assignment variant: c = one-hot(label), no A^+, no fallback (tau = 0).
+// hard_labels: the caller's labels (with its centres), or NULL to cluster here (labels in the workspace).
+// n_flagged_host != NULL: read the flag count, the pinv status and (when the clustering ran inside
+// the call) the clustering status back with one synchronisation at the end.
+int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int kind, float sigma_s, int radius,
+               float sigma_r, int K, const float* centres, float tau, float* g, int32_t* n_flagged_host, void* ws,
+               size_t ws_bytes, cudaStream_t st, bool hard = false, const int32_t* hard_labels = nullptr) {
+    FilterPlan F;
+    size_t vsmem = 0;
+    int rc = validate_scalars(n, rho, H, W, kind, sigma_r, K, tau, hard);
+    if (rc) return rc;
+    if (!f || !p || !g || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
     if (misaligned(f) || misaligned(p) || misaligned(g) || misaligned(ws) || (centres && misaligned(centres)))
         return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
     if (g == f || g == p) return fail(HDF_ERR_ARG, "g must not alias f or p");
-    if (hard && kind == HDF_SPATIAL_GAUSSIAN_IIR)   // no oracle for that pairing: not offered
-        return fail(HDF_ERR_ARG, "the hard-assignment variant takes the FIR kinds (gaussian, box)");
-    FilterPlan F;
-    const int nsm = nsm_of_device();
-    rc = make_plan(H, W, n, K, kind, sigma_s, radius, &F, nsm);
+    rc = validate_filter(n, rho, H, W, kind, sigma_s, radius, sigma_r, K, tau, f == p, hard, &F, &vsmem);
     if (rc) return rc;
+    const int nsm = nsm_of_device();
     const size_t need = hdf_filter_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
     if (ws_bytes < need) return fail(HDF_ERR_WORKSPACE, "workspace %zu < required %zu bytes", ws_bytes, need);
-    // the column pass keeps J raw rows (rho or rho + n floats per pixel, double buffered) and J range-
-    // weight rows of its plane group in shared memory: checked before anything is enqueued
-    const size_t vsmem = vpass_smem(F, rho, n, f == p);
-    {
-        int dev = 0, optin = 0;
-        HDF_CUDA(cudaGetDevice(&dev));
-        HDF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        if (vsmem > (size_t)optin)
-            return fail(HDF_ERR_ARG,
-                        "the column pass needs %zu bytes of shared memory (rho %d, n %d, radius %d) > %d: reduce "
-                        "rho + n or the radius",
-                        vsmem, rho, n, F.Rp, optin);
-    }
     Carver cv(ws);
     FilterWS w = carve_filter(cv, H, W, n, rho, K, F.Wp, true);
     const float neg_inv2sr2 = (float)(-1.0 / (2.0 * (double)sigma_r * (double)sigma_r));
 
     if (hard) tau = 0.5f;   // small r_s(i): the direct window sum with mu_s (k_fallback, hard mode)
     // step 1 (optional): cluster the guide inside this call
+    ClusterReadback crb;
+    const bool cluster_here = !centres;
     if (!centres) {
         int32_t* lab = hard ? w.labels : nullptr;
-        rc = launch_cluster(p, H, W, rho, K, w.centres, lab, nullptr, w.cluster_ws, st);
+        rc = launch_cluster(p, H, W, rho, K, w.centres, lab, nullptr, w.cluster_ws, st,
+                            n_flagged_host ? &crb : nullptr);
         if (rc) return rc;
         centres = w.centres;
         if (hard) hard_labels = lab;
@@ -651,6 +749,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     SideStream ss;
     rc = side_stream(&ss);
     if (rc) return rc;
+    std::unique_lock<std::mutex> side_lock(*ss.mu);   // until st has waited on ss.join
     HDF_CUDA(cudaEventRecord(ss.fork, st));
     HDF_CUDA(cudaStreamWaitEvent(ss.s, ss.fork, 0));
     if (!hard) {
@@ -714,6 +813,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         }
     }
     HDF_CUDA(cudaStreamWaitEvent(st, ss.join, 0));   // A^+ is ready
+    side_lock.unlock();
     // loop for2: c(i) = A^+ b(i) -> K coefficient planes
     {
         hdf::CoefParams cp;
@@ -827,11 +927,17 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         HDF_CUDA(cudaGetLastError());
     }
     if (n_flagged_host) {
-        int hv[2] = {0, 0};
-        HDF_CUDA(cudaMemcpyAsync(hv, w.status, sizeof(hv), cudaMemcpyDeviceToHost, st));
+        HostStage* hs = cluster_here ? crb.hs : host_stage();
+        if (!hs) return fail(HDF_ERR_CUDA, "pinned host stage: cudaMallocHost failed");
+        HDF_CUDA(cudaMemcpyAsync(hs->hv, w.status, sizeof(hs->hv), cudaMemcpyDeviceToHost, st));
         HDF_CUDA(cudaStreamSynchronize(st));
-        *n_flagged_host = hv[1];
-        if (hv[0] == HDF_WARN_ILLCOND) return fail(HDF_WARN_ILLCOND, "A is numerically singular; A^+ truncated (R6)");
+        *n_flagged_host = hs->hv[1];
+        if (cluster_here) {   // HDF_ERR_K: the output was filtered with the padded centres (hdf.h)
+            rc = cluster_status(crb, K, nullptr);
+            if (rc) return rc;
+        }
+        if (hs->hv[0] == HDF_WARN_ILLCOND)
+            return fail(HDF_WARN_ILLCOND, "A is numerically singular; A^+ truncated (R6)");
     }
     return HDF_OK;
 }
@@ -897,8 +1003,12 @@ int hdf_profile_enable(int on) {
     return HDF_OK;
 }
 
+static int profile_collect_impl(double* ms_total, int32_t* launches);
 int hdf_profile_collect(double* ms_total, int32_t* launches) {
     g_err.clear();
+    return guarded([&]() -> int { return profile_collect_impl(ms_total, launches); });
+}
+static int profile_collect_impl(double* ms_total, int32_t* launches) {
     std::vector<ProfRec> recs;
     {
         std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -937,14 +1047,16 @@ size_t hdf_cluster_workspace_bytes(int H, int W, int rho, int K) {
 int hdf_cluster(const float* p, int H, int W, int rho, int K, float* centres, int32_t* labels,
                 hdf_cluster_info* info_host, void* ws, size_t ws_bytes, void* stream) {
     g_err.clear();
-    int rc = check_common(H, W, rho, K);
-    if (rc) return rc;
-    if (!p || !centres || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
-    if (misaligned(p) || misaligned(centres) || misaligned(ws) || (labels && misaligned(labels)))
-        return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
-    const size_t need = hdf_cluster_workspace_bytes(H, W, rho, K);
-    if (ws_bytes < need) return fail(HDF_ERR_WORKSPACE, "workspace %zu < required %zu bytes", ws_bytes, need);
-    return launch_cluster(p, H, W, rho, K, centres, labels, info_host, ws, static_cast<cudaStream_t>(stream));
+    return guarded([&]() -> int {
+        int rc = check_common(H, W, rho, K);
+        if (rc) return rc;
+        if (!p || !centres || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
+        if (misaligned(p) || misaligned(centres) || misaligned(ws) || (labels && misaligned(labels)))
+            return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
+        const size_t need = hdf_cluster_workspace_bytes(H, W, rho, K);
+        if (ws_bytes < need) return fail(HDF_ERR_WORKSPACE, "workspace %zu < required %zu bytes", ws_bytes, need);
+        return launch_cluster(p, H, W, rho, K, centres, labels, info_host, ws, static_cast<cudaStream_t>(stream));
+    });
 }
 
 size_t hdf_filter_workspace_bytes(int H, int W, int n, int rho, int K, int kind, float sigma_s, int radius) {
@@ -961,19 +1073,23 @@ int hdf_filter(const float* f, int n, const float* p, int rho, int H, int W, int
                float sigma_r, int K, const float* centres, float tau, float* g, int32_t* n_flagged_host, void* ws,
                size_t ws_bytes, void* stream) {
     g_err.clear();
-    return run_filter(f, n, p, rho, H, W, kind, sigma_s, radius, sigma_r, K, centres, tau, g, n_flagged_host, ws,
-                      ws_bytes, static_cast<cudaStream_t>(stream));
+    return guarded([&]() -> int {
+        return run_filter(f, n, p, rho, H, W, kind, sigma_s, radius, sigma_r, K, centres, tau, g, n_flagged_host, ws,
+                          ws_bytes, static_cast<cudaStream_t>(stream));
+    });
 }
 
 int hdf_filter_hard(const float* f, int n, const float* p, int rho, int H, int W, int kind, float sigma_s, int radius,
                     float sigma_r, int K, const float* centres, const int32_t* labels, float* g, void* ws,
                     size_t ws_bytes, void* stream) {
     g_err.clear();
-    if ((centres == nullptr) != (labels == nullptr))
-        return fail(HDF_ERR_ARG, "hdf_filter_hard: pass both centres and labels, or neither");
-    if (labels && misaligned(labels)) return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
-    return run_filter(f, n, p, rho, H, W, kind, sigma_s, radius, sigma_r, K, centres, 0.f, g, nullptr, ws, ws_bytes,
-                      static_cast<cudaStream_t>(stream), true, labels);
+    return guarded([&]() -> int {
+        if ((centres == nullptr) != (labels == nullptr))
+            return fail(HDF_ERR_ARG, "hdf_filter_hard: pass both centres and labels, or neither");
+        if (labels && misaligned(labels)) return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
+        return run_filter(f, n, p, rho, H, W, kind, sigma_s, radius, sigma_r, K, centres, 0.f, g, nullptr, ws,
+                          ws_bytes, static_cast<cudaStream_t>(stream), true, labels);
+    });
 }
 
 // ------------------------------------------------------------------ PCA-NLM guide (NEXT #3) ----
@@ -989,9 +1105,15 @@ size_t hdf_pca_guide_workspace_bytes(int H, int W, int n, int m, int dim) {
     return cv.off + 256;
 }
 
+static int pca_guide_impl(const float* f, int H, int W, int n, int m, int dim, float* p, float* basis_out, void* ws,
+                          size_t ws_bytes, void* stream);
 int hdf_pca_guide(const float* f, int H, int W, int n, int m, int dim, float* p, float* basis_out, void* ws,
                   size_t ws_bytes, void* stream) {
     g_err.clear();
+    return guarded([&]() -> int { return pca_guide_impl(f, H, W, n, m, dim, p, basis_out, ws, ws_bytes, stream); });
+}
+static int pca_guide_impl(const float* f, int H, int W, int n, int m, int dim, float* p, float* basis_out, void* ws,
+                          size_t ws_bytes, void* stream) {
     if (!f || !p || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
     if (H < 1 || W < 1 || n < 1) return fail(HDF_ERR_ARG, "H, W, n must be >= 1");
     if (m < 1 || m % 2 == 0) return fail(HDF_ERR_ARG, "patch side m must be odd and >= 1 (got %d)", m);
@@ -1042,47 +1164,92 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
                     int radius, float sigma_r, int K, float tau, float* g_host, float* centres_host,
                     int32_t* n_flagged_host, hdf_cluster_info* info_host, void* ws, size_t ws_bytes, void* stream) {
     g_err.clear();
-    int rc = check_common(H, W, rho, K);
-    if (rc) return rc;
-    if (!f_host || !p_host || !g_host || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
-    if (n < 1 || n > HDF_MAX_N) return fail(HDF_ERR_ARG, "n must be in [1, %d]", HDF_MAX_N);
-    const size_t need = hdf_filter_host_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
-    if (ws_bytes < need) return fail(HDF_ERR_WORKSPACE, "workspace %zu < required %zu bytes", ws_bytes, need);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    Carver cv(ws);
-    const size_t fbytes = hdf_filter_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
-    void* fws = cv.take<char>(fbytes);
-    float* fd = cv.take<float>((size_t)H * W * n);
-    float* pd = cv.take<float>((size_t)H * W * rho);
-    float* gd = cv.take<float>((size_t)H * W * n);
-    float* cd = cv.take<float>((size_t)K * rho);
-    const float* pdev = fd;
-    {
-        ProfScope prof(HDF_STAGE_H2D, st);
-        HDF_CUDA(cudaMemcpyAsync(fd, f_host, sizeof(float) * (size_t)H * W * n, cudaMemcpyHostToDevice, st));
-        if (p_host != f_host || rho != n) {
-            HDF_CUDA(cudaMemcpyAsync(pd, p_host, sizeof(float) * (size_t)H * W * rho, cudaMemcpyHostToDevice, st));
-            pdev = pd;
+    return guarded([&]() -> int {
+        // every argument is checked before the first copy is enqueued
+        const bool f_is_p = (p_host == f_host && rho == n);
+        FilterPlan F;
+        size_t vsmem = 0;
+        int rc = validate_scalars(n, rho, H, W, kind, sigma_r, K, tau, false);
+        if (rc) return rc;
+        if (!f_host || !p_host || !g_host || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
+        if (misaligned(ws)) return fail(HDF_ERR_ARG, "the workspace must be 16-byte aligned");
+        rc = validate_filter(n, rho, H, W, kind, sigma_s, radius, sigma_r, K, tau, f_is_p, false, &F, &vsmem);
+        if (rc) return rc;
+        const size_t need = hdf_filter_host_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
+        if (ws_bytes < need) return fail(HDF_ERR_WORKSPACE, "workspace %zu < required %zu bytes", ws_bytes, need);
+        HostStage* hs = host_stage();
+        if (!hs) return fail(HDF_ERR_CUDA, "pinned host stage: cudaMallocHost failed");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        Carver cv(ws);
+        const size_t fbytes = hdf_filter_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
+        void* fws = cv.take<char>(fbytes);
+        float* fd = cv.take<float>((size_t)H * W * n);
+        float* pd = cv.take<float>((size_t)H * W * rho);
+        float* gd = cv.take<float>((size_t)H * W * n);
+        float* cd = cv.take<float>((size_t)K * rho);
+        const float* pdev = fd;
+        // from here on, a failure synchronises the stream before returning (copies from the caller's
+        // buffers may be in flight)
+        auto bail = [&](int code) {
+            cudaStreamSynchronize(st);
+            return code;
+        };
+        {
+            ProfScope prof(HDF_STAGE_H2D, st);
+            if (cudaMemcpyAsync(fd, f_host, sizeof(float) * (size_t)H * W * n, cudaMemcpyHostToDevice, st) !=
+                cudaSuccess)
+                return bail(fail(HDF_ERR_CUDA, "input copy: %s", cudaGetErrorString(cudaGetLastError())));
+            if (!f_is_p) {
+                if (cudaMemcpyAsync(pd, p_host, sizeof(float) * (size_t)H * W * rho, cudaMemcpyHostToDevice, st) !=
+                    cudaSuccess)
+                    return bail(fail(HDF_ERR_CUDA, "guide copy: %s", cudaGetErrorString(cudaGetLastError())));
+                pdev = pd;
+            }
         }
-    }
-    // cluster (in the filter workspace's cluster region) then filter
-    Carver c2(fws);
-    FilterWS w = carve_filter(c2, H, W, n, rho, K, round_up(W, 4), true);
-    rc = launch_cluster(pdev, H, W, rho, K, cd, nullptr, info_host, w.cluster_ws, st);
-    if (rc) return rc;
-    rc = run_filter(fd, n, pdev, rho, H, W, kind, sigma_s, radius, sigma_r, K, cd, tau, gd, nullptr, fws, fbytes, st);
-    if (rc) return rc;
-    int hv[2] = {0, 0};
-    {
-        ProfScope prof(HDF_STAGE_D2H, st);
-        HDF_CUDA(cudaMemcpyAsync(g_host, gd, sizeof(float) * (size_t)H * W * n, cudaMemcpyDeviceToHost, st));
-        if (centres_host)
-            HDF_CUDA(cudaMemcpyAsync(centres_host, cd, sizeof(float) * (size_t)K * rho, cudaMemcpyDeviceToHost, st));
-        HDF_CUDA(cudaMemcpyAsync(hv, w.status, sizeof(hv), cudaMemcpyDeviceToHost, st));
-    }
-    HDF_CUDA(cudaStreamSynchronize(st));
-    if (n_flagged_host) *n_flagged_host = hv[1];
-    return HDF_OK;
+        // cluster (in the filter workspace's cluster region; status read back at the end) then filter
+        Carver c2(fws);
+        FilterWS w = carve_filter(c2, H, W, n, rho, K, round_up(W, 4), true);
+        ClusterReadback crb;
+        rc = launch_cluster(pdev, H, W, rho, K, cd, nullptr, nullptr, w.cluster_ws, st, &crb);
+        if (rc) return bail(rc);
+        rc = run_filter(fd, n, pdev, rho, H, W, kind, sigma_s, radius, sigma_r, K, cd, tau, gd, nullptr, fws, fbytes,
+                        st);
+        if (rc) return bail(rc);
+        {
+            ProfScope prof(HDF_STAGE_D2H, st);
+            cudaError_t e = cudaMemcpyAsync(g_host, gd, sizeof(float) * (size_t)H * W * n, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess && centres_host)
+                e = cudaMemcpyAsync(centres_host, cd, sizeof(float) * (size_t)K * rho, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(hs->hv, w.status, sizeof(hs->hv), cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) return bail(fail(HDF_ERR_CUDA, "output copy: %s", cudaGetErrorString(e)));
+        }
+        HDF_CUDA(cudaStreamSynchronize(st));
+        if (n_flagged_host) *n_flagged_host = hs->hv[1];
+        rc = cluster_status(crb, K, info_host);   // HDF_ERR_K: g_host holds the padded-centre result
+        if (rc) return rc;
+        if (hs->hv[0] == HDF_WARN_ILLCOND)
+            return fail(HDF_WARN_ILLCOND, "A is numerically singular; A^+ truncated (R6)");
+        return HDF_OK;
+    });
+}
+
+// Diagnostics / parity tests: the pixels that took the R9 fallback in the last hdf_filter call on
+// workspace `ws` with the same sizes (synchronous).  Returns their number (at most cap copied, in the
+// order the row pass flagged them), or -1 on a CUDA error.
+int hdf_filter_flagged(const void* ws, int H, int W, int n, int rho, int K, int32_t* idx_host, int cap) {
+    g_err.clear();
+    return guarded([&]() -> int {
+        if (!ws || H < 1 || W < 1 || n < 1 || rho < 1 || K < 1) return -1;
+        Carver cv(const_cast<void*>(ws));
+        FilterWS w = carve_filter(cv, H, W, n, rho, K, round_up(W, 4), true);
+        int cnt = 0;
+        if (cudaMemcpy(&cnt, w.flag_count, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+        const int m = std::min(cnt, std::max(cap, 0));
+        if (m > 0 && idx_host &&
+            cudaMemcpy(idx_host, w.flag_list, sizeof(int32_t) * (size_t)m, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return -1;
+        return cnt;
+    });
 }
 
 }  // extern "C"

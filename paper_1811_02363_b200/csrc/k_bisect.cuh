@@ -2011,6 +2011,18 @@ HDF_DEV void finalise(const BisectArgs& A, unsigned char* dyn) {
 }
 
 // --------------------------------------------------------------------------------- kernel -----
+// Instantiated per RHO in inst_bisect.cu (one translation unit each); the host code gets the
+// launchable pointers from these accessors.
+using BisectFn = void (*)(const BisectArgs);
+BisectFn bisect_kernel_rho0();
+BisectFn bisect_kernel_rho1();
+BisectFn bisect_kernel_rho2();
+BisectFn bisect_kernel_rho3();
+BisectFn bisect_kernel_rho4();
+BisectFn bisect_kernel_rho5();
+BisectFn bisect_kernel_rho6();
+BisectFn bisect_kernel_rho7();
+
 template <int RHO>
 __global__ void __launch_bounds__(kBT, 1) k_bisect(const __grid_constant__ BisectArgs A) {
     cg::grid_group grid = cg::this_grid();

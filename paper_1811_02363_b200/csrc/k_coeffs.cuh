@@ -23,6 +23,7 @@ struct PinvOut {
 constexpr int kPinvThreads = 1024;
 constexpr int kPinvMaxE = (HDF_MAX_K * HDF_MAX_K + kPinvThreads - 1) / kPinvThreads;   // elements per thread
 
+#ifndef HDF_COEFFS_MMA_ONLY   // inst_coeffs.cu compiles only k_coeffs_mma
 __global__ void __launch_bounds__(kPinvThreads) k_gram_pinv(const float* __restrict__ centres, int K, int rho,
                                                              double neg_inv2sr2, PinvOut out) {
     extern __shared__ double sm_pinv[];
@@ -181,6 +182,9 @@ inline size_t pinv_smem_bytes(int K) { return sizeof(double) * (size_t)(K * K + 
 // c(i) = A^+ b(i).  One thread per pixel; b staged in shared memory [K][kCoefPix]; A^+ (fp32) in
 // shared memory, read as broadcast float4.  Output planes cpl[k][y][x] with row pitch Wp.
 // ---------------------------------------------------------------------------------------------
+
+#endif  // HDF_COEFFS_MMA_ONLY
+
 constexpr int kCoefPix = 256;
 
 struct CoefParams {
@@ -193,6 +197,7 @@ struct CoefParams {
     float neg_inv2sr2;
 };
 
+#ifndef HDF_COEFFS_MMA_ONLY   // inst_coeffs.cu compiles only k_coeffs_mma
 __global__ void __launch_bounds__(kCoefPix) k_coeffs(const CoefParams P) {
     extern __shared__ float sm_coef[];
     const int K = P.K, rho = P.rho;
@@ -240,6 +245,8 @@ __global__ void __launch_bounds__(kCoefPix) k_coeffs(const CoefParams P) {
 // Compile-time K (8, 16, 32, 64): b(i) in registers, A^+ (symmetric) rows as broadcast float4 from
 // shared memory, accumulators in chunks of up to 32 coefficients.  b = 2^(d2 log2(e) (-1/2 sr^2))
 // (ex2.approx, relative error < 2^-21).
+#endif  // HDF_COEFFS_MMA_ONLY
+
 template <int KC>
 __global__ void __launch_bounds__(kCoefPix) k_coeffs_t(const CoefParams P) {
     extern __shared__ __align__(16) float sm_ct[];
@@ -332,6 +339,17 @@ HDF_DEV void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// Instantiated per NT in inst_coeffs.cu; the host code gets the kernels from these accessors.
+using CoefFn = void (*)(const CoefParams);
+CoefFn coeffs_mma_kernel_nt1(int rho);
+CoefFn coeffs_mma_kernel_nt2(int rho);
+CoefFn coeffs_mma_kernel_nt3(int rho);
+CoefFn coeffs_mma_kernel_nt4(int rho);
+CoefFn coeffs_mma_kernel_nt5(int rho);
+CoefFn coeffs_mma_kernel_nt6(int rho);
+CoefFn coeffs_mma_kernel_nt7(int rho);
+CoefFn coeffs_mma_kernel_nt8(int rho);
+
 template <int NT, int RHO>   // RHO > 0: compile-time guide dimension, 0: runtime
 __global__ void __launch_bounds__(kCoefMmaThreads) k_coeffs_mma(const CoefParams P) {
     extern __shared__ __align__(16) float smq[];
@@ -450,6 +468,7 @@ __global__ void __launch_bounds__(kCoefMmaThreads) k_coeffs_mma(const CoefParams
     }
 }
 
+#ifndef HDF_COEFFS_MMA_ONLY   // inst_coeffs.cu compiles only k_coeffs_mma
 // Hard-assignment variant (coeffICIP)/(HDapprox2): c(i) = one-hot(label(i)), so the row
 // pass's combine gives g(i) = v_s(i) / r_s(i), s = label(i).  Plane k, row y, column x.
 __global__ void __launch_bounds__(256) k_coeffs_onehot(const int32_t* labels, float* cpl, long long cstride, int H,
@@ -462,5 +481,7 @@ __global__ void __launch_bounds__(256) k_coeffs_onehot(const int32_t* labels, fl
         for (int k = 0; k < K; k++) o[(long long)k * cstride] = (k == s) ? 1.f : 0.f;
     }
 }
+
+#endif  // HDF_COEFFS_MMA_ONLY
 
 }  // namespace hdf

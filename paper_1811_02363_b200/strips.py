@@ -47,6 +47,10 @@ def filter_strips(f, p=None, *, kind: str = "gaussian", sigma_s: float = 1.0, ra
 
     if p is None:
         p = f
+    if kind == "gaussian_iir":
+        # Young's recursion has infinite support: a strip filtered with zero extension at its own
+        # edges differs from the whole image near the strip borders, so strips are not exact
+        raise ValueError("row strips need a finite window (kind 'gaussian' or 'box'), not 'gaussian_iir'")
     rank = dist.get_rank() if dist is not None else 0
     world = dist.get_world_size() if dist is not None else 1
     H = f.shape[0]

@@ -123,3 +123,46 @@ def test_root_split_of_two_values(hdf):
     assert got == [(0.0, 0.0, 0.0), (200.0, 10.0, 3.5)]
     lab = lab.cpu().numpy().reshape(64, 64)
     assert len(np.unique(lab[:, :20])) == 1 and len(np.unique(lab[:, 20:])) == 1 and lab[0, 0] != lab[0, 30]
+
+
+def test_empty_side_reseed_matches_oracle(hdf):
+    """R4's empty-side reseed (pinned in test_oracle_pins): 2048 points whose stride sample holds only
+    copies of v = 0, so the seeds coincide and side 1 starts empty; the GPU reseeds it at the member
+    farthest from c0 exactly as the oracle does (same labels, same E_K)."""
+    P = np.zeros((32, 64, 3), np.float32)
+    flat = P.reshape(-1, 3)
+    odd = np.arange(1, 2048, 2)
+    flat[odd[:400]] = (100.0, 0.0, 0.0)
+    flat[odd[400:]] = (-40.0, 0.0, 0.0)
+    cen_o, lab_o, _, ek_o = oracle.cluster(P, 2)
+    cen_g, lab_g, info = hdf.cluster(_dev(P), 2, labels=True)
+    assert np.array_equal(lab_g.cpu().numpy().reshape(-1), lab_o)
+    assert abs(info.e_k - ek_o) <= 1e-9 * ek_o
+    # deeper: K = 4 on the same guide (one leaf then has a single distinct value)
+    cen_o, lab_o, _, ek_o = oracle.cluster(P, 3)
+    cen_g, lab_g, info = hdf.cluster(_dev(P), 3, labels=True)
+    assert np.array_equal(lab_g.cpu().numpy().reshape(-1), lab_o)
+
+
+@pytest.mark.slow
+def test_c5_clustering_matches_oracle_and_five_percent_rule(hdf):
+    """Config 5 (BASELINE configs[4]: 4096^2 x 3, K = 64) at full size: the GPU's bisecting K-means
+    (its streamed-node and grid-team paths run only here) gives the oracle's labels and E_K, and R15's
+    5% rule holds on a seeded 2^16-pixel sample of brute-force (num)/(den) values."""
+    cfg, f, p = synth.make("c5")
+    cen_o, lab_o, _, ek_o = oracle.cluster(p, cfg.K)
+    pd = _dev(p)
+    cen_g, lab_g, info = hdf.cluster(pd, cfg.K, labels=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(lab_g.cpu().numpy().reshape(-1), lab_o)
+    assert abs(info.e_k - ek_o) <= 1e-9 * ek_o
+    assert info.grid_splits >= 1                                  # the grid path ran
+    rng = np.random.default_rng(5 << 16)
+    pix = np.sort(rng.choice(cfg.H * cfg.W, 1 << 16, replace=False))
+    g_bf, _ = oracle.bruteforce(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, r=cfg.radius, pix=pix)
+    g_o, _, _ = oracle.filter_pixels(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, cen_o, pix, r=cfg.radius)
+    g_g = hdf.filter(pd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                     centres=cen_g).g.cpu().numpy().reshape(-1, 3)[pix]
+    mse_o = oracle.mse(g_o, g_bf, cfg.R_range)
+    mse_g = oracle.mse(g_g, g_bf, cfg.R_range)
+    assert mse_g <= 1.05 * mse_o + 1e-12, f"GPU MSE {mse_g:.4e} vs oracle {mse_o:.4e}"

@@ -32,16 +32,22 @@ def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
 
 
-def _run_gpu(hdf, f, p, cfg, mu32, tau=0.5, H=None, W=None):
+def _run_gpu(hdf, f, p, cfg, mu32, tau=0.5, H=None, W=None, flagged=False):
     fd = _dev(f)
     pd = fd if p is f else _dev(p)
+    ws = hdf.Workspace()
     res = hdf.filter(fd, pd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
-                     centres=_dev(mu32), tau=tau, count_flagged=True)
+                     centres=_dev(mu32), tau=tau, count_flagged=True, ws=ws)
     torch.cuda.synchronize()
-    return res.g.cpu().numpy().astype(np.float64), res.n_flagged
+    g = res.g.cpu().numpy().astype(np.float64)
+    if flagged:   # the pixels that took the R9 fallback on the GPU (hdf_filter_flagged)
+        idx = hdf.flagged_pixels(ws, f.shape[0], f.shape[1], f.shape[2], p.shape[2], mu32.shape[0])
+        assert len(idx) == res.n_flagged
+        return g, res.n_flagged, idx
+    return g, res.n_flagged
 
 
-def _compare(g_gpu, g_orc, eta, flagged_orc, floor, scale, n_flag_gpu=None):
+def _compare(g_gpu, g_orc, eta, flagged_orc, floor, scale, n_flag_gpu=None, flagged_gpu=None):
     d = np.abs(g_gpu - g_orc) * scale
     straddle = np.abs(eta - floor) <= 1e-3 * abs(floor)
     keep = ~straddle
@@ -51,6 +57,13 @@ def _compare(g_gpu, g_orc, eta, flagged_orc, floor, scale, n_flag_gpu=None):
     if n_flag_gpu is not None:
         nf = int(flagged_orc.sum())
         assert abs(n_flag_gpu - nf) <= int(straddle.sum()), f"flag count gpu {n_flag_gpu} vs oracle {nf}"
+    if flagged_gpu is not None:
+        # the flagged SETS are identical, except for straddles (R9's decision in fp32 vs fp64)
+        gpu_set = np.zeros(flagged_orc.size, bool)
+        gpu_set[flagged_gpu] = True
+        ora_set = np.asarray(flagged_orc).reshape(-1).astype(bool)
+        differ = np.nonzero(gpu_set != ora_set)[0]
+        assert np.all(straddle.reshape(-1)[differ]), f"flagged sets differ at {differ[:10]} (not straddles)"
     assert mx <= MAX_TOL, f"max |dg| = {mx:.3e} (scale {scale})"
     assert mean <= MEAN_TOL, f"mean |dg| = {mean:.3e}"
     return mx, mean
@@ -62,10 +75,10 @@ def _parity_case(hdf, name, H=None, W=None, K=None, tau=0.5):
     cen, _, _, _ = oracle.cluster(p, K)
     mu32 = cen.astype(np.float32)                       # R14: both sides use fp32-rounded centres
     g_o, eta, fl, nf = oracle.filter(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, mu32, r=cfg.radius, tau=tau)
-    g_g, nfg = _run_gpu(hdf, f, p, cfg, mu32, tau)
+    g_g, nfg, idx = _run_gpu(hdf, f, p, cfg, mu32, tau, flagged=True)
     floor = tau * 1.0
     scale = 255.0 / cfg.R_range
-    return _compare(g_g, g_o, eta, fl, floor, scale, nfg)
+    return _compare(g_g, g_o, eta, fl, floor, scale, nfg, idx)
 
 
 # ---- parity at the configs' own sizes and at ragged sizes spanning several tiles -------------
@@ -293,22 +306,24 @@ def test_pca_guide_feeds_the_nlm_filter(hdf):
     cen, _, _, _ = oracle.cluster(p, cfg.K)
     mu32 = cen.astype(np.float32)
     g_o, eta, fl, nf = oracle.filter(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, mu32, r=cfg.radius, tau=0.5)
-    g_g, nfg = _run_gpu(hdf, f, p, cfg, mu32, 0.5)
-    _compare(g_g, g_o, eta, fl, 0.5, 255.0 / cfg.R_range, nfg)
+    g_g, nfg, idx = _run_gpu(hdf, f, p, cfg, mu32, 0.5, flagged=True)
+    _compare(g_g, g_o, eta, fl, 0.5, 255.0 / cfg.R_range, nfg, idx)
 
 
 # ------------------------------------------------------- row strips (NEXT #4) on one GPU ----------
 @pytest.mark.parametrize("name,H,W,world", [("c2a", 200, 160, 3), ("c4", 150, 120, 4), ("c1", None, None, 2)])
-def test_row_strips_match_the_whole_image(hdf, name, H, W, world):
-    """Each strip (with its R-row halo) filtered by the CUDA path with the whole image's centres and
-    stitched: the same as filtering the whole image (strip borders are never image borders)."""
+def test_row_strips_match_the_oracle(hdf, name, H, W, world):
+    """Each strip (with its R-row halo) filtered by the CUDA path with the oracle's centres of the
+    whole image (R14) and stitched: equal to oracle.filter on the whole image (strip borders are never
+    image borders), flagged sets included."""
     from paper_1811_02363_b200 import strips
     cfg, f, p = synth.make(name, H, W)
     fd = _dev(f)
     pd = fd if cfg.bilateral else _dev(p)
-    cen, _, _ = hdf.cluster(pd, cfg.K)
-    full = hdf.filter(fd, pd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
-                      centres=cen, tau=0.5).g
+    cen_o, _, _, _ = oracle.cluster(p, cfg.K)
+    mu32 = cen_o.astype(np.float32)
+    cen = _dev(mu32)
+    g_o, eta, fl, nf = oracle.filter(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, mu32, r=cfg.radius, tau=0.5)
     R = strips.radius_of(cfg.kind, cfg.sigma_s, cfg.radius)
     parts = []
     for y0, y1, h0, h1 in strips.strip_bounds(f.shape[0], world, R):
@@ -317,8 +332,83 @@ def test_row_strips_match_the_whole_image(hdf, name, H, W, world):
         g = hdf.filter(fs, ps, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=R, sigma_r=cfg.sigma_r, centres=cen,
                        tau=0.5).g
         parts.append(g[y0 - h0:y1 - h0])
-    got = torch.cat(parts, 0)
-    assert torch.allclose(got, full, rtol=0, atol=1e-5 * cfg.R_range)
+    got = torch.cat(parts, 0).cpu().numpy().astype(np.float64)
+    _compare(got, g_o, eta, fl, 0.5, 255.0 / cfg.R_range)
+    # and through strips.filter_strips itself (one rank: the whole image as a single strip)
+    one = strips.filter_strips(fd, None if cfg.bilateral else pd, kind=cfg.kind, sigma_s=cfg.sigma_s,
+                               radius=cfg.radius, sigma_r=cfg.sigma_r, K=cfg.K, centres=cen)
+    _compare(one.cpu().numpy().astype(np.float64), g_o, eta, fl, 0.5, 255.0 / cfg.R_range)
+
+
+def test_row_strips_reject_the_recursive_gaussian(hdf):
+    from paper_1811_02363_b200 import strips
+    f = torch.rand((16, 16, 3), device="cuda")
+    with pytest.raises(ValueError, match="finite window"):
+        strips.filter_strips(f, kind="gaussian_iir", sigma_s=2.0, sigma_r=30.0, K=2)
+
+
+# ------------------------------------------------------- the pseudo-inverse's truncation path (R6) ----
+@pytest.mark.parametrize("name,K,dups", [("c1", 6, (0, 3)), ("c2a", 10, (9, 9, 2)), ("c4", 12, (5,))])
+def test_pinv_truncation_with_duplicate_centres(hdf, name, K, dups):
+    """Duplicate centres make A singular: MATLAB's pinv (R6) truncates the zero
+    eigenvalues.  The GPU takes its Jacobi path, returns HDF_WARN_ILLCOND, and matches oracle.filter
+    (whose pinv is the same truncated eigen-decomposition in fp64) on the same centres."""
+    cfg, f, p = synth.make(name, 96, 120)
+    cen, _, _, _ = oracle.cluster(p, K)
+    mu = np.concatenate([cen, cen[list(dups)]], 0).astype(np.float32)
+    g_o, eta, fl, nf = oracle.filter(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, mu, r=cfg.radius, tau=0.5)
+    _, lam, rank, _ = oracle.pinv(oracle.gram(mu.astype(np.float64), cfg.sigma_r))
+    assert rank == K                              # the oracle truncated exactly the duplicates
+    fd = _dev(f)
+    pd = fd if cfg.bilateral else _dev(p)
+    ws = hdf.Workspace()
+    res = hdf.filter(fd, pd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                     centres=_dev(mu), tau=0.5, count_flagged=True, ws=ws)
+    assert res.status == hdf.WARN_ILLCOND
+    idx = hdf.flagged_pixels(ws, f.shape[0], f.shape[1], f.shape[2], p.shape[2], mu.shape[0])
+    _compare(res.g.cpu().numpy().astype(np.float64), g_o, eta, fl, 0.5, 255.0 / cfg.R_range, res.n_flagged, idx)
+
+
+def test_k_too_large_inside_filter_pads_centres(hdf):
+    """R5 through hdf_filter(centres=NULL): a guide with 5 distinct values and K = 7.  Asynchronous
+    call: the clustering pads centres 5, 6 with copies of centre 0 (include/hdf.h), A is singular, the
+    truncated pinv (R6) handles it, and g equals oracle.filter on those padded centres.  With
+    count_flagged (one synchronisation) the call reports HDF_ERR_K."""
+    lab, pal, p = synth.gen_kdistinct(60, 80, 5, 3, seed=7, spread=255.0, min_sep=50.0)
+    rng = np.random.default_rng(8)
+    f = rng.uniform(0, 255, (60, 80, 3)).astype(np.float32)
+    cen5, _, _, _ = oracle.cluster(p, 5)
+    mu = np.concatenate([cen5, cen5[[0, 0]]], 0).astype(np.float32)
+    g_o, eta, fl, nf = oracle.filter(f, p, "gaussian", 2.0, 40.0, mu, r=6, tau=0.5)
+    fd, pd = _dev(f), _dev(p)
+    g = hdf.filter(fd, pd, kind="gaussian", sigma_s=2.0, radius=6, sigma_r=40.0, K=7, tau=0.5).g
+    _compare(g.cpu().numpy().astype(np.float64), g_o, eta, fl, 0.5, 1.0)
+    out = torch.empty_like(fd)
+    with pytest.raises(hdf.HdfKError):
+        hdf.filter(fd, pd, kind="gaussian", sigma_s=2.0, radius=6, sigma_r=40.0, K=7, tau=0.5, out=out,
+                   count_flagged=True)
+    torch.cuda.synchronize()
+    _compare(out.cpu().numpy().astype(np.float64), g_o, eta, fl, 0.5, 1.0)
+    fh = torch.from_numpy(f).pin_memory()
+    ph = torch.from_numpy(p).pin_memory()
+    with pytest.raises(hdf.HdfKError) as e:
+        hdf.filter_host(fh, ph, kind="gaussian", sigma_s=2.0, radius=6, sigma_r=40.0, K=7, tau=0.5)
+    assert e.value.achievable == 5
+
+
+def test_filter_host_validates_before_copying_and_reports_illcond(hdf):
+    fh = torch.rand((20, 30, 3)).pin_memory() * 255.0
+    with pytest.raises(hdf.HdfError) as e:          # sigma_r <= 0: rejected before any copy
+        hdf.filter_host(fh, kind="gaussian", sigma_s=1.0, sigma_r=-2.0, K=2)
+    assert e.value.status == hdf.ERR_ARG
+    with pytest.raises(hdf.HdfError) as e:          # radius beyond the limit
+        hdf.filter_host(fh, kind="gaussian", sigma_s=30.0, sigma_r=20.0, K=2)
+    assert e.value.status == hdf.ERR_ARG
+    with pytest.raises(ValueError):                 # out of the wrong size
+        hdf.filter_host(fh, kind="gaussian", sigma_s=1.0, sigma_r=20.0, K=2, out=torch.empty(5))
+    with pytest.raises(ValueError):                 # device out of the wrong shape
+        hdf.filter(fh.cuda(), kind="gaussian", sigma_s=1.0, sigma_r=20.0, K=2,
+                   out=torch.empty((20, 30, 2), device="cuda"))
 
 
 # ------------------------------------------------------- the ABI's maximum sizes ------------------

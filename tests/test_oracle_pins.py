@@ -142,6 +142,76 @@ def test_p2_farthest_pair_seed_on_line():
     assert np.allclose(sorted(cen[:, 0]), [25.0, 75.5])
 
 
+def _bruteforce_farthest_pair(P, members, cap):
+    """R3 written out by brute force: every pair (a < b) of the stride sample members[0::ceil(m/cap)],
+    squared distance summed over dimensions in index order, the lexicographically smallest (a, b)
+    among the maximisers."""
+    m = len(members)
+    stride = -(-m // cap)
+    smp = np.asarray(members)[0::stride]
+    X = P[smp]
+    best, arg = -1.0, (0, 0)
+    for a in range(len(smp) - 1):
+        diff = X[a + 1:] - X[a]
+        d = np.zeros(len(diff))
+        for k in range(P.shape[1]):            # (d0^2 + d1^2) + d2^2 ..., the definition's order
+            d = d + diff[:, k] * diff[:, k]
+        j = int(np.argmax(d))                  # first maximiser in the row
+        if d[j] > best:
+            best, arg = float(d[j]), (a, a + 1 + j)
+    if len(smp) < 2:
+        return int(smp[0]), int(smp[0])
+    return int(smp[arg[0]]), int(smp[arg[1]])
+
+
+@pytest.mark.parametrize("m,cap,integer,seed", [(1024, 1024, False, 1), (1025, 1024, False, 2),
+                                                (5000, 1024, False, 3), (100000, 1024, False, 4),
+                                                (3000, 1024, True, 5), (6001, 1024, True, 6),
+                                                (700, 64, True, 7), (1, 1024, False, 8)])
+def test_p2_farthest_pair_stride_sample_against_bruteforce(m, cap, integer, seed):
+    """R3 (P:329): the seeds are the farthest pair of the stride sample members[0::ceil(m/1024)] in
+    member order (ascending pixel index), ties -> lexicographically smallest pair.  The members are a
+    sparse ascending subset of the pixels; the farthest pair of ALL members is planted off the
+    sample (so a search over every member, or another stride, gives a different pair), and integer
+    coordinates in a small range make many pairs tie."""
+    rng = np.random.default_rng(seed)
+    N = 3 * m + 10
+    P = (rng.integers(0, 12, (N, 3)).astype(np.float64) if integer else rng.normal(0, 10, (N, 3)))
+    members = np.sort(rng.choice(N, m, replace=False))
+    stride = -(-m // cap)
+    if stride > 1 and not integer:
+        P[members[1]] = (1e3, 1e3, 1e3)        # off the sample: index 1 is not a multiple of the stride
+        P[members[-2 if (m - 2) % stride else -3]] = (-1e3, -1e3, -1e3)
+    a, b = oracle.farthest_pair(P, members, cap)
+    assert (a, b) == _bruteforce_farthest_pair(P, members, cap)
+    if stride > 1 and not integer:
+        assert 1e3 not in (P[a][0], P[b][0])   # the planted pair is not seen
+
+
+def test_p2_empty_side_is_reseeded_at_the_farthest_member():
+    """R4: when one side of a 2-means step is empty it is reseeded at the member farthest from the
+    other centre.  Construction: 2048 points, so the stride sample (stride 2) holds only the even
+    pixels, which are all v = 0; the farthest pair of the sample is two copies of v, every point
+    ties to the first centre, side 1 is empty.  The odd pixels are 400 copies of a = (100, 0, 0)
+    followed by 624 copies of c = (-40, 0, 0).  The member farthest from v is the first a (ties ->
+    first), so c1 = a, and Lloyd converges to {v, c} | {a}: centres (-40 * 624 / 1648, 0, 0) and a,
+    E_K = the two leaves' SSE written out in closed form."""
+    N = 2048
+    P = np.zeros((N, 3))
+    odd = np.arange(1, N, 2)
+    P[odd[:400]] = (100.0, 0.0, 0.0)
+    P[odd[400:]] = (-40.0, 0.0, 0.0)
+    cen, lab, sse, ek = oracle.cluster(P, 2)
+    want = np.zeros(N, dtype=np.int32)
+    want[odd[:400]] = 1
+    assert np.array_equal(lab, want)
+    m0 = 1024 + 624
+    x0 = -40.0 * 624 / m0
+    assert np.allclose(cen[0], (x0, 0, 0), rtol=0, atol=1e-12) and np.array_equal(cen[1], (100.0, 0, 0))
+    sse0 = 1024 * x0 ** 2 + 624 * (-40.0 - x0) ** 2
+    assert abs(ek - sse0) <= 1e-9 * sse0 and sse[1] == 0.0
+
+
 # ---------------------------------------------------------------- P4: A and A^+ ----------------
 def test_p4_gram_closed_form():
     g = GOLD["gram_K2"]

@@ -1,14 +1,32 @@
-# one gpurun call: smoke, all GPU tests, bench (default + all configs), ncu launch list + full capture
+# One gpurun call of a measurement round (run from the repo root on the GPU box):
+#   TAG=r02a STEPS="smoke tests bench all launches full" CONFIGS="c5 c3 c4" bash tools/gpu_round.sh
+# smoke: __graft_entry__ smoke(); tests: pytest -m gpu; bench: the default bench line (c5) with the
+# cpu_baseline; all: one bench line per config; launches: ncu launch list of the default bench;
+# full: one ncu --set full capture per config in CONFIGS (each only after the same command exited 0).
 mkdir -p gpurun_out
-TAG=${TAG:-r01}
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
-nproc > gpurun_out/nproc.txt; lscpu | head -20 >> gpurun_out/nproc.txt
-timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
-timeout 1500 python -m pytest tests -m gpu -q -x --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
-tail -3 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
-timeout 900 python bench.py --all --steps 10 --no-cpu-baseline > gpurun_out/bench_all.json 2> gpurun_out/bench_all.err; echo all rc=$?
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
-$CMD > gpurun_out/ncu_plain_$TAG.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo launches rc=$?
-ncu --set full --clock-control none --import-source on -k regex:"k_range_vpass|k_hpass_combine|k_coeffs_mma|k_bisect" -s 4 -c 4 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo full rc=$?
+TAG=${TAG:-r02}
+STEPS=${STEPS:-"smoke tests bench all launches full"}
+CONFIGS=${CONFIGS:-"c5"}
+has() { case " $STEPS " in *" $1 "*) return 0;; esac; return 1; }
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi_$TAG.txt
+(nproc; lscpu | grep "Model name") > gpurun_out/host_$TAG.txt
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1; echo build rc=$?
+if has smoke; then timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo smoke rc=$?; fi
+if has tests; then
+  timeout 1800 python -m pytest tests -m gpu -q -x --timeout 600 -p no:cacheprovider ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo pytest rc=$?
+  tail -3 gpurun_out/pytest_gpu_$TAG.log
+fi
+if has bench; then timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo bench rc=$?; fi
+if has all; then timeout 1200 python bench.py --all --steps 10 --no-cpu-baseline > gpurun_out/bench_all_$TAG.jsonl 2> gpurun_out/bench_all_$TAG.err; echo all rc=$?; fi
+if has launches; then
+  CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
+  $CMD > gpurun_out/ncu_plain_$TAG.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_c5.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo launches rc=$?
+fi
+if has full; then
+  for c in $CONFIGS; do
+    CMD="python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline"
+    $CMD > gpurun_out/ncu_plain_${TAG}_$c.log 2>&1 && \
+    ncu --set full --clock-control none --import-source on -k regex:"${NCU_K:-k_range_vpass|k_hpass_combine|k_coeffs_mma|k_bisect|k_fallback}" -s ${NCU_S:-15} -c ${NCU_C:-5} -o gpurun_out/prof_${TAG}_$c $CMD > gpurun_out/ncu_full_${TAG}_$c.log 2>&1; echo full $c rc=$?
+  done
+fi
