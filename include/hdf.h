@@ -178,6 +178,23 @@ int hdf_pca_guide(const float *f, int H, int W, int n, int m, int dim, float *p,
                   size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * hdf_scale_guide -- anisotropic and augmented guides.
+ * The diagonal range kernel phi(x) = exp(-sum_d x_d^2 / 2 sigma_d^2) is the isotropic kernel with
+ * sigma_r = 1 on the guide scaled per channel by 1 / sigma_d; an extra guide channel (the paper's
+ * infrared band) is appended with its own scale.  Pass the result to hdf_cluster /
+ * hdf_filter with sigma_r = 1.
+ *   out(i) = (p(i)_d * scale[d])_{d < rho} ++ (extra(i)_j * extra_scale[j])_{j < e}
+ *   p      [H][W][rho] float32, device (read only)
+ *   scale_host        [rho] float32, host (NULL: all 1)
+ *   extra  [H][W][e] float32, device, or NULL when e = 0
+ *   extra_scale_host  [e] float32, host (NULL: all 1)
+ *   out    [H][W][rho + e] float32, device, out; rho + e <= HDF_MAX_RHO; must not alias p or extra
+ * Errors: HDF_ERR_ARG (sizes, NULL, alignment, aliasing, a non-finite scale); asynchronous on `stream`.
+ */
+int hdf_scale_guide(const float *p, int H, int W, int rho, const float *scale_host, const float *extra, int e,
+                    const float *extra_scale_host, float *out, void *stream);
+
+/* ---------------------------------------------------------------------------------------------
  * hdf_filter_hard -- the hard-assignment variant (coeffICIP)/(HDapprox2): every pixel keeps
  * only its own cluster's term, g(i) = v_s(i) / r_s(i) with s = label(i) (no pseudo-inverse, no
  * fallback: r_s(i) >= omega(0) phi(p(i) - mu_s) > 0).  Theorem 1 bounds its error

@@ -14,6 +14,9 @@ Functions follow PAPER.md (see the C file for per-function citations):
   nystrom        Appendix A identity written as a direct window sum
   filter_hard    hard-assignment variant (coeffICIP)/(HDapprox2)
   pca_guide      PCA-NLM patch guide (reading R11), numpy fp64
+  phi_aniso, bruteforce_aniso, filter_aniso
+                 the diagonal (anisotropic) range kernel (NEXT #3) and Algorithm 1
+                 with it, numpy fp64 (small images)
   young_coeffs, young1d, young2d, filter_iir
                  Young's O(1) recursive Gaussian (the reference the paper cites) and
                  Algorithm 1 with it in place of the FIR (NEXT #1; readings R17), numpy fp64
@@ -344,6 +347,73 @@ def pca_guide(img, m: int = 3, dim: int = 6):
         if B[k, j] < 0:
             B[:, j] = -B[:, j]
     return (Pc @ B).reshape(H, W, dim), B, mean, evals[order]
+
+
+# ------------------------------------------------ anisotropic range kernel (NEXT #3) --
+def phi_aniso(x, sigmas) -> np.ndarray:
+    """The diagonal Gaussian range kernel phi(x) = exp(-sum_d x_d^2 / (2 sigma_d^2)) (per-
+    dimension range widths; sigma_r = 50 on the PCA dimensions, 10 on the infrared band),
+    evaluated on the last axis of x, summed over d in index order.  fp64."""
+    x = _d(x)
+    s = _d(sigmas).reshape(-1)
+    q = np.zeros(x.shape[:-1])
+    for d in range(x.shape[-1]):
+        q = q + (x[..., d] * x[..., d]) / (s[d] * s[d])
+    return np.exp(-q / 2.0)
+
+
+def bruteforce_aniso(f, p, kind: str, sigma_s: float, sigmas, r: int = -1, pix=None):
+    """(num)/(den) of P:43-51 with the diagonal range kernel, window clipped to Omega (R8), written out
+    pixel by pixel (small images).  Returns (g [npix, n], eta [npix]) for the pixels pix (flat indices;
+    None: all)."""
+    f, p = _fp(f, p)
+    H, W, n = f.shape
+    R = radius(kind, sigma_s, r)
+    w = spatial_taps(kind, sigma_s, R)
+    idx = np.arange(H * W) if pix is None else np.asarray(pix, dtype=np.int64).reshape(-1)
+    g = np.zeros((idx.size, n))
+    eta = np.zeros(idx.size)
+    for t, i in enumerate(idx):
+        y, x = divmod(int(i), W)
+        y0, y1, x0, x1 = max(0, y - R), min(H, y + R + 1), max(0, x - R), min(W, x + R + 1)
+        om = w[y0 - y + R:y1 - y + R, None] * w[None, x0 - x + R:x1 - x + R]
+        wt = om * phi_aniso(p[y0:y1, x0:x1] - p[y, x], sigmas)
+        eta[t] = wt.sum()
+        g[t] = (wt[..., None] * f[y0:y1, x0:x1]).sum((0, 1)) / eta[t]
+    return g, eta
+
+
+def filter_aniso(f, p, kind: str, sigma_s: float, sigmas, mu, r: int = -1, tau: float = 0.5):
+    """Algorithm 1 with the diagonal range kernel phi_aniso, step by step in the paper's
+    order (small images, numpy fp64): A_kl = phi(mu_k - mu_l) and A^+ (the oracle's MATLAB-style pinv,
+    R6); loop for1: b_k(i) = phi(mu_k - p(i)); loop for2: c(i) = A^+ b(i); loop for3: v += c_k (omega *
+    (b_k f)), r += c_k (omega * b_k) with the oracle's clipped-window convolution (R8); g = v / r; rule R9
+    with the direct (num)/(den) of bruteforce_aniso at flagged pixels.  Returns (g, eta_hat, flagged,
+    n_flagged) like filter()."""
+    f, p = _fp(f, p)
+    H, W, n = f.shape
+    mu = _d(mu)
+    K = mu.shape[0]
+    R = radius(kind, sigma_s, r)
+    A = phi_aniso(mu[:, None, :] - mu[None, :, :], sigmas)
+    Ap, _, _, _ = pinv(A)
+    b = np.stack([phi_aniso(mu[k] - p, sigmas) for k in range(K)])            # [K, H, W]
+    c = np.einsum("kl,lhw->khw", Ap, b)
+    v = np.zeros((n, H, W))
+    rr = np.zeros((H, W))
+    for k in range(K):
+        for ch in range(n):
+            v[ch] = v[ch] + c[k] * conv2(b[k] * f[..., ch], kind, sigma_s, R)
+        rr = rr + c[k] * conv2(b[k], kind, sigma_s, R)
+    g = np.ascontiguousarray(np.moveaxis(v / rr, 0, -1))
+    w = spatial_taps(kind, sigma_s, R)
+    floor = tau * w[R] * w[R] * 1.0
+    fl = (rr < floor) if tau > 0 else np.zeros((H, W), bool)
+    if fl.any():
+        pix = np.nonzero(fl.reshape(-1))[0]
+        gb, _ = bruteforce_aniso(f, p, kind, sigma_s, sigmas, R, pix)
+        g.reshape(-1, n)[pix] = gb
+    return g, rr, fl, int(fl.sum())
 
 
 # ---------------------------------------------------------------- recursive Gaussian (NEXT #1) --

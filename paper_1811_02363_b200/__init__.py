@@ -28,7 +28,7 @@ MAX_K, MAX_RHO, MAX_N, MAX_RADIUS = 128, 64, 64, 32
 EXPORTS = ("hdf_version", "hdf_last_error", "hdf_cluster_workspace_bytes", "hdf_cluster",
            "hdf_filter_workspace_bytes", "hdf_filter", "hdf_filter_hard", "hdf_filter_host_workspace_bytes",
            "hdf_filter_host", "hdf_pca_guide_workspace_bytes", "hdf_pca_guide",
-           "hdf_profile_enable", "hdf_profile_collect", "hdf_cluster_trace", "hdf_filter_flagged")
+           "hdf_profile_enable", "hdf_profile_collect", "hdf_cluster_trace", "hdf_filter_flagged", "hdf_scale_guide")
 STAGES = ("cluster", "pinv", "coeffs", "vpass", "hpass", "fallback", "h2d", "d2h")
 
 
@@ -92,6 +92,8 @@ def lib():
         L.hdf_cluster_trace.restype = i
         L.hdf_filter_flagged.argtypes = [vp, i, i, i, i, i, C.POINTER(C.c_int32), i]
         L.hdf_filter_flagged.restype = i
+        L.hdf_scale_guide.argtypes = [vp, i, i, i, vp, vp, i, vp, vp, vp]
+        L.hdf_scale_guide.restype = i
         _lib = L
     return _lib
 
@@ -295,6 +297,42 @@ def pca_guide(f: torch.Tensor, m: int = 3, dim: int = 6, *, basis: bool = False,
     if st != OK:
         _raise(st)
     return (p, B) if basis else p
+
+
+def scale_guide(p: torch.Tensor, scale=None, extra: torch.Tensor | None = None, extra_scale=None,
+                stream=None) -> torch.Tensor:
+    """Anisotropic / augmented guide: [p * scale, extra * extra_scale] per channel
+    (include/hdf.h, hdf_scale_guide).  With scale = 1 / sigma_d the isotropic filter at sigma_r = 1 on
+    the result is the filter with the diagonal range kernel exp(-sum_d x_d^2 / 2 sigma_d^2)."""
+    p = _dev_f32(p, "p")
+    H, W, rho = _hwc(p, "p")
+    e = 0
+    if extra is not None:
+        extra = _dev_f32(extra, "extra")
+        He, We, e = _hwc(extra, "extra")
+        if (He, We) != (H, W):
+            raise ValueError("extra must have the guide's H, W")
+        _same_device(extra, p.device, "extra")
+    sc = (C.c_float * rho)(*[float(v) for v in scale]) if scale is not None else None
+    es = (C.c_float * e)(*[float(v) for v in extra_scale]) if (extra_scale is not None and e) else None
+    if scale is not None and len(scale) != rho:
+        raise ValueError(f"scale must have {rho} entries")
+    if extra_scale is not None and len(extra_scale) != e:
+        raise ValueError(f"extra_scale must have {e} entries")
+    out = torch.empty((H, W, rho + e), dtype=torch.float32, device=p.device)
+    st = lib().hdf_scale_guide(p.data_ptr(), H, W, rho, sc, extra.data_ptr() if extra is not None else None, e,
+                               es, out.data_ptr(), _stream_ptr(stream))
+    if st != OK:
+        _raise(st)
+    return out
+
+
+def anisotropic_guide(p: torch.Tensor, sigmas, extra: torch.Tensor | None = None, extra_sigmas=None,
+                      stream=None) -> torch.Tensor:
+    """The guide for per-channel range sigmas (e.g. sigma_r = 50 on PCA dimensions and 10 on an
+    appended infrared channel): scale_guide with scale = 1 / sigma; filter it at sigma_r = 1."""
+    return scale_guide(p, [1.0 / float(s) for s in sigmas], extra,
+                       [1.0 / float(s) for s in extra_sigmas] if extra_sigmas is not None else None, stream)
 
 
 def filter_host(f_host: torch.Tensor, p_host: torch.Tensor | None = None, *, kind: str = "gaussian",

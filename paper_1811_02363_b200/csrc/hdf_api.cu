@@ -1149,6 +1149,38 @@ static int pca_guide_impl(const float* f, int H, int W, int n, int m, int dim, f
     return HDF_OK;
 }
 
+int hdf_scale_guide(const float* p, int H, int W, int rho, const float* scale_host, const float* extra, int e,
+                    const float* extra_scale_host, float* out, void* stream) {
+    g_err.clear();
+    return guarded([&]() -> int {
+        if (!p || !out) return fail(HDF_ERR_ARG, "NULL pointer argument");
+        if (H < 1 || W < 1) return fail(HDF_ERR_ARG, "H, W must be >= 1");
+        if (rho < 1 || e < 0 || rho + e > HDF_MAX_RHO)
+            return fail(HDF_ERR_ARG, "rho >= 1, e >= 0 and rho + e <= %d required (got %d, %d)", HDF_MAX_RHO, rho, e);
+        if (e > 0 && !extra) return fail(HDF_ERR_ARG, "extra is NULL with e = %d", e);
+        if (misaligned(p) || misaligned(out) || (extra && misaligned(extra)))
+            return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
+        if (out == p || (extra && out == extra)) return fail(HDF_ERR_ARG, "out must not alias p or extra");
+        hdf::ScaleParams sp;
+        sp.p = p;
+        sp.extra = e > 0 ? extra : nullptr;
+        sp.out = out;
+        sp.N = (long long)H * W;
+        sp.rho = rho;
+        sp.e = e;
+        for (int d = 0; d < HDF_MAX_RHO; d++) sp.s[d] = 0.f;
+        for (int d = 0; d < rho; d++) sp.s[d] = scale_host ? scale_host[d] : 1.f;
+        for (int j = 0; j < e; j++) sp.s[rho + j] = extra_scale_host ? extra_scale_host[j] : 1.f;
+        for (int d = 0; d < rho + e; d++)
+            if (!std::isfinite(sp.s[d])) return fail(HDF_ERR_ARG, "scale %d is not finite", d);
+        const long long tot = sp.N * (rho + e);
+        const unsigned nb = (unsigned)std::min<long long>((tot + 255) / 256, (long long)nsm_of_device() * 16);
+        hdf::k_scale_guide<<<nb, 256, 0, static_cast<cudaStream_t>(stream)>>>(sp);
+        HDF_CUDA(cudaGetLastError());
+        return HDF_OK;
+    });
+}
+
 size_t hdf_filter_host_workspace_bytes(int H, int W, int n, int rho, int K, int kind, float sigma_s, int radius) {
     const size_t base = hdf_filter_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
     if (!base) return 0;

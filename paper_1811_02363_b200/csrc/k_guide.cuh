@@ -287,4 +287,30 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_project(const float* f, int
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Anisotropic / augmented guides: the diagonal range kernel
+// phi(x) = exp(-sum_d x_d^2 / 2 sigma_d^2) equals the isotropic kernel with sigma_r = 1 on the guide
+// scaled per channel by s_d = 1 / sigma_d, and an extra guide channel (e.g. an infrared band, P:672-
+// 679) is appended with its own scale.  out(i) = (p(i)_d s_d)_{d < rho} ++ (extra(i)_j t_j)_{j < e}.
+// One thread per output element, coalesced over the flat [H*W][rho + e] output.
+struct ScaleParams {
+    const float* p;        // [N][rho]
+    const float* extra;    // [N][e] or NULL
+    float* out;            // [N][rho + e]
+    long long N;
+    int rho, e;
+    float s[HDF_MAX_RHO];  // per-channel scales: s_0..s_{rho-1}, then t_0..t_{e-1}
+};
+
+__global__ void __launch_bounds__(256) k_scale_guide(const __grid_constant__ ScaleParams P) {
+    const int D = P.rho + P.e;
+    const long long tot = P.N * D;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+        const long long i = t / D;
+        const int d = (int)(t - i * D);
+        const float v = d < P.rho ? __ldg(P.p + i * P.rho + d) : __ldg(P.extra + i * P.e + (d - P.rho));
+        P.out[t] = v * P.s[d];
+    }
+}
+
 }  // namespace hdf

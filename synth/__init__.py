@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 __all__ = ["Config", "CONFIGS", "make", "gen_rectangles", "gen_voronoi", "gen_hyperspectral",
-           "gen_nlm", "gen_kdistinct", "pca_patch_guide"]
+           "gen_nlm", "gen_kdistinct", "gen_ir", "pca_patch_guide"]
 
 
 @dataclass(frozen=True)
@@ -179,6 +179,22 @@ def gen_nlm(H: int = 512, W: int = 512, seed: int = 4, sigma: float = NLM_SIGMA,
     noisy = noisy.astype(np.float32)
     guide = pca_patch_guide(noisy, 3, 6)
     return noisy, guide, clean
+
+
+def gen_ir(f: np.ndarray, seed: int = 9, noise: float = 5.0) -> np.ndarray:
+    """An infrared-like extra guide channel for the low-light use case (the
+    paper's IR images are not available): a different linear mix of the image's channels (their mean
+    when f has fewer than 3), a smooth random shading, N(0, noise^2), clipped to [0, 255].  [H, W]
+    float32."""
+    rng = np.random.default_rng(seed)
+    x = np.asarray(f, dtype=np.float64)
+    H, W = x.shape[:2]
+    mix = rng.dirichlet(np.ones(3)) if x.shape[2] >= 3 else None
+    base = x[..., :3] @ mix if mix is not None else x.mean(-1)
+    yy, xx = _grid01(H, W)
+    shade = 30.0 * np.sin(np.pi * (rng.uniform(0.5, 2.0) * yy[..., 0] + rng.uniform(0.5, 2.0) * xx[..., 0]))
+    ir = 0.8 * base + shade + rng.normal(0.0, noise, (H, W))
+    return np.clip(ir, 0.0, 255.0).astype(np.float32)
 
 
 def gen_kdistinct(H: int, W: int, K: int, rho: int, seed: int, spread: float = 255.0,

@@ -297,17 +297,25 @@ def test_pca_guide_matches_oracle(hdf, H, W, n, m, dim, seed):
 
 
 def test_pca_guide_feeds_the_nlm_filter(hdf):
-    """C4 with the guide built on the GPU: the filter on that guide matches the oracle filter on the
-    same guide (the parity bar of the main path)."""
+    """C4 end to end with the guide built on each side: the GPU pipeline (hdf_pca_guide -> filter) and
+    the oracle pipeline (oracle.pca_guide -> oracle.filter) on the same noisy image, with the oracle's
+    centres of its own guide on both sides (R14).  No oracle input comes from the GPU.  The two guides
+    differ by the GPU's fp32 projection (~1e-6 of the guide's range), so pixels whose eta_hat lies
+    within 1e-2 (relative) of the R9 threshold are counted as straddles."""
     cfg, f, _ = synth.make("c4", 120, 150)
+    p_o, _, _, _ = oracle.pca_guide(f, 3, 6)
+    cen, _, _, _ = oracle.cluster(p_o, cfg.K)
+    mu32 = cen.astype(np.float32)
+    g_o, eta, fl, nf = oracle.filter(f, p_o, cfg.kind, cfg.sigma_s, cfg.sigma_r, mu32, r=cfg.radius, tau=0.5)
     fd = _dev(f)
     pd = hdf.pca_guide(fd, 3, 6)
-    p = pd.cpu().numpy()
-    cen, _, _, _ = oracle.cluster(p, cfg.K)
-    mu32 = cen.astype(np.float32)
-    g_o, eta, fl, nf = oracle.filter(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, mu32, r=cfg.radius, tau=0.5)
-    g_g, nfg, idx = _run_gpu(hdf, f, p, cfg, mu32, 0.5, flagged=True)
-    _compare(g_g, g_o, eta, fl, 0.5, 255.0 / cfg.R_range, nfg, idx)
+    res = hdf.filter(fd, pd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                     centres=_dev(mu32), tau=0.5, count_flagged=True)
+    g_g = res.g.cpu().numpy().astype(np.float64)
+    straddle = np.abs(eta - 0.5) <= 1e-2 * 0.5
+    d = np.abs(g_g - g_o)[~straddle]
+    assert d.max() <= MAX_TOL and d.mean() <= MEAN_TOL, (d.max(), d.mean())
+    assert abs(res.n_flagged - nf) <= int(straddle.sum())
 
 
 # ------------------------------------------------------- row strips (NEXT #4) on one GPU ----------
@@ -519,3 +527,41 @@ def test_hard_variant_rejects_recursive_gaussian(hdf):
     f = torch.rand((16, 16, 3), device="cuda") * 255.0
     with pytest.raises(Exception, match="FIR kinds"):
         hdf.filter_hard(f, f, kind="gaussian_iir", sigma_s=2.0, sigma_r=30.0, K=2)
+
+
+# ------------------------------------------- anisotropic / IR-augmented guides (NEXT #3) ----
+@pytest.mark.parametrize("H,W,K,seed", [(96, 120, 16, 1), (61, 77, 8, 2)])
+def test_anisotropic_ir_guide_matches_oracle(hdf, H, W, K, seed):
+    """The low-light use case: the PCA-6 NLM guide plus an infrared channel, sigma_r = 50
+    on the PCA dimensions and 10 on the IR band.  GPU: hdf_scale_guide (1/sigma per
+    channel) then the isotropic filter at sigma_r = 1; oracle: Algorithm 1 with the diagonal kernel
+    (oracle.filter_aniso, pinned to the isotropic oracle on the scaled guide).  Same fp32 centres
+    (R14), parity bar and identical flagged sets."""
+    cfg, f, p6 = synth.make("c4", H, W)
+    ir = synth.gen_ir(f, seed)
+    sig, sig_ir = [50.0] * 6, [10.0]
+    sall = np.array(sig + sig_ir)
+    pg = np.concatenate([p6.astype(np.float64), ir[..., None].astype(np.float64)], -1)
+    cen_s, _, _, _ = oracle.cluster(pg / sall, K)
+    mu32 = cen_s.astype(np.float32)
+    g_o, eta, fl, nf = oracle.filter_aniso(f, pg, "box", 0.0, sall, mu32.astype(np.float64) * sall, r=10, tau=0.5)
+    pd = hdf.anisotropic_guide(_dev(p6), sig, _dev(ir[..., None]), sig_ir)
+    assert np.allclose(pd.cpu().numpy(), pg / sall, rtol=1e-6, atol=1e-6)
+    ws = hdf.Workspace()
+    res = hdf.filter(_dev(f), pd, kind="box", radius=10, sigma_r=1.0, centres=_dev(mu32), tau=0.5,
+                     count_flagged=True, ws=ws)
+    idx = hdf.flagged_pixels(ws, H, W, 3, 7, K)
+    _compare(res.g.cpu().numpy().astype(np.float64), g_o, eta, fl, 0.5, 1.0, res.n_flagged, idx)
+
+
+def test_scale_guide_argument_errors(hdf):
+    p = torch.rand((8, 9, 3), device="cuda")
+    with pytest.raises(ValueError):
+        hdf.scale_guide(p, [1.0, 2.0])                       # wrong number of scales
+    with pytest.raises(hdf.HdfError) as e:
+        hdf.scale_guide(p, [1.0, float("inf"), 1.0])
+    assert e.value.status == hdf.ERR_ARG
+    q = hdf.scale_guide(p, [2.0, 0.5, 1.0], torch.ones((8, 9, 2), device="cuda"), [3.0, 4.0])
+    want = torch.cat([p * torch.tensor([2.0, 0.5, 1.0], device="cuda"), torch.tensor([3.0, 4.0], device="cuda")
+                      .expand(8, 9, 2)], -1)
+    assert torch.equal(q, want)

@@ -575,3 +575,66 @@ def test_iir_filter_constant_image_and_close_to_fir():
     gf, _, _, _ = oracle.filter(f, p, "gaussian", cfg.sigma_s, cfg.sigma_r, mu)
     d = np.abs(gi - gf) * 255.0 / cfg.R_range
     assert d.mean() < 1.0 and d.max() < 12.0    # the recursion approximates the truncated Gaussian
+
+
+# ------------------------------------------- anisotropic range kernel (NEXT #3) ------
+def _aniso_case(seed, H=24, W=30):
+    rng = np.random.default_rng(seed)
+    cfg, f, p = synth.make("c1", H, W)
+    ir = synth.gen_ir(f, seed=seed)                         # an extra guide channel
+    pg = np.concatenate([p.astype(np.float64), ir[..., None]], -1)
+    sig = np.array([30.0, 45.0, 60.0, 12.0])
+    return f, pg, sig, rng
+
+
+def test_aniso_phi_closed_form():
+    """phi(x) = exp(-sum_d x_d^2 / 2 sigma_d^2): one standard deviation along each axis gives e^-1/2."""
+    sig = np.array([3.0, 50.0, 10.0])
+    for d in range(3):
+        x = np.zeros(3)
+        x[d] = sig[d]
+        assert abs(oracle.phi_aniso(x, sig) - math.exp(-0.5)) <= 1e-15
+    assert oracle.phi_aniso(np.array([3.0, 50.0, 10.0]), sig) == pytest.approx(math.exp(-1.5), rel=1e-15)
+
+
+def test_aniso_equal_sigmas_is_the_isotropic_oracle():
+    """Special case: every sigma_d = sigma_r reduces filter_aniso / bruteforce_aniso to the (pinned)
+    isotropic C oracle."""
+    cfg, f, p = synth.make("c1", 26, 31)
+    cen, _, _, _ = oracle.cluster(p, 6)
+    g1, e1, fl1, _ = oracle.filter(f, p, "gaussian", 2.0, 30.0, cen, r=6)
+    g2, e2, fl2, _ = oracle.filter_aniso(f, p, "gaussian", 2.0, [30.0] * 3, cen, r=6)
+    assert np.allclose(g1, g2, rtol=0, atol=1e-9) and np.allclose(e1, e2, rtol=1e-12, atol=1e-12)
+    pix = np.arange(0, 26 * 31, 7)
+    b1, _ = oracle.bruteforce(f, p, "gaussian", 2.0, 30.0, r=6, pix=pix)
+    b2, _ = oracle.bruteforce_aniso(f, p, "gaussian", 2.0, [30.0] * 3, r=6, pix=pix)
+    assert np.allclose(b1, b2, rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_aniso_equals_isotropic_on_the_scaled_guide(seed):
+    """The identity behind the GPU path: per-channel scaling of the guide by 1/sigma_d
+    with sigma_r = 1 equals the anisotropic kernel, for the filter (the centres scaled alike) and for
+    brute force; here against the isotropic C oracle on the scaled guide."""
+    f, pg, sig, rng = _aniso_case(seed)
+    ps = pg / sig
+    cen_s, _, _, _ = oracle.cluster(ps, 5)
+    g_iso, e_iso, _, nf = oracle.filter(f, ps, "gaussian", 2.0, 1.0, cen_s, r=6)
+    g_an, e_an, _, nf2 = oracle.filter_aniso(f, pg, "gaussian", 2.0, sig, cen_s * sig, r=6)
+    assert nf == nf2
+    assert np.allclose(g_iso, g_an, rtol=0, atol=1e-8) and np.allclose(e_iso, e_an, rtol=1e-10, atol=1e-10)
+    b_iso, _ = oracle.bruteforce(f, ps, "box", 0.0, 1.0, r=3, pix=np.arange(0, 24 * 30, 5))
+    b_an, _ = oracle.bruteforce_aniso(f, pg, "box", 0.0, sig, r=3, pix=np.arange(0, 24 * 30, 5))
+    assert np.allclose(b_iso, b_an, rtol=0, atol=1e-9)
+
+
+def test_aniso_k_distinct_exactness_against_bruteforce():
+    """P3 with the diagonal kernel: a guide with exactly K well-separated values and the centres equal
+    to them gives b(i) = A e_s, c(i) = e_s, so the fast filter equals brute force (num)/(den)."""
+    lab, pal, p = synth.gen_kdistinct(20, 22, 5, 4, seed=3, spread=255.0, min_sep=80.0)
+    rng = np.random.default_rng(4)
+    f = rng.uniform(0, 255, (20, 22, 3))
+    sig = np.array([40.0, 60.0, 25.0, 90.0])
+    g, _, _, _ = oracle.filter_aniso(f, p, "gaussian", 1.5, sig, pal, r=5, tau=0.0)
+    gb, _ = oracle.bruteforce_aniso(f, p, "gaussian", 1.5, sig, r=5)
+    assert np.allclose(g.reshape(-1, 3), gb, rtol=0, atol=1e-8)
