@@ -89,6 +89,27 @@ typedef struct {
     int64_t points_split;    /* sum over the K-1 splits of the procedure: members                   */
 } hdf_cluster_info;
 
+/* ---------------------------------------------------------------------------------------------
+ * Sampled clustering mode.  The paper notes that "any efficient clustering method" can provide the
+ * centres.  hdf_cluster_sampled runs the same bisecting K-means (R2-R4) on the stride sample
+ * {p(i) : i = 0, s, 2s, ...} of the pixels (flat index order) instead of all of them: mu_k are the
+ * leaf means of the sample.  stride = 1 is hdf_cluster exactly.  Its quality is checked by the R15
+ * rule (error against brute force within 5% of the exact oracle pipeline's, tests/test_gpu_cluster.py);
+ * on the sample itself the result equals the oracle's bisecting K-means of the same sample.
+ *   stride   s >= 1; the sample has M = ceil(H W / s) points
+ *   info_host  as hdf_cluster (E_K, labels are those of the SAMPLE)
+ *   ws         at least hdf_cluster_sampled_workspace_bytes(H, W, rho, K, stride)
+ * Errors as hdf_cluster.
+ * hdf_sample_guide: the gather on its own (the multi-GPU split gathers each rank's share of the
+ * global sample, strips.py): out[j] = p[i0 + j stride], j < M, rho floats each; device pointers;
+ * HDF_ERR_ARG if the sample runs past N; asynchronous.
+ * ------------------------------------------------------------------------------------------- */
+size_t hdf_cluster_sampled_workspace_bytes(int H, int W, int rho, int K, int stride);
+int hdf_cluster_sampled(const float *p, int H, int W, int rho, int K, int stride, float *centres,
+                        hdf_cluster_info *info_host, void *ws, size_t ws_bytes, void *stream);
+int hdf_sample_guide(const float *p, long long N, int rho, long long i0, long long stride, float *out, long long M,
+                     void *stream);
+
 /* Device workspace (bytes) for hdf_cluster on an H x W guide of dimension rho. */
 size_t hdf_cluster_workspace_bytes(int H, int W, int rho, int K);
 
@@ -214,6 +235,8 @@ int hdf_filter_hard(const float *f, int n, const float *p, int rho, int H, int W
  * workspace, clusters, filters, and copies g back, all on `stream`, then synchronises it once.
  *   f_host [H][W][n], p_host [H][W][rho] (may be the same pointer), g_host [H][W][n]: host float32
  *   (pinned memory gives full-rate copies; pageable memory works but is slower).
+ *   cluster_stride  1: the exact clustering of every pixel (hdf_cluster); s > 1: the sampled mode
+ *            (hdf_cluster_sampled with stride s)
  *   centres_host [K][rho] out, may be NULL.  n_flagged_host, info_host: out, may be NULL.
  *   ws: device workspace of at least hdf_filter_host_workspace_bytes(...).
  * Every argument is checked before the first copy is enqueued (HDF_ERR_ARG / HDF_ERR_WORKSPACE,
@@ -225,7 +248,7 @@ int hdf_filter_hard(const float *f, int n, const float *p, int rho, int H, int W
  */
 size_t hdf_filter_host_workspace_bytes(int H, int W, int n, int rho, int K, int kind, float sigma_s, int radius);
 int hdf_filter_host(const float *f_host, int n, const float *p_host, int rho, int H, int W, int kind,
-                    float sigma_s, int radius, float sigma_r, int K, float tau, float *g_host,
+                    float sigma_s, int radius, float sigma_r, int K, float tau, int cluster_stride, float *g_host,
                     float *centres_host, int32_t *n_flagged_host, hdf_cluster_info *info_host,
                     void *ws, size_t ws_bytes, void *stream);
 

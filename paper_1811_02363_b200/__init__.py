@@ -28,7 +28,8 @@ MAX_K, MAX_RHO, MAX_N, MAX_RADIUS = 128, 64, 64, 32
 EXPORTS = ("hdf_version", "hdf_last_error", "hdf_cluster_workspace_bytes", "hdf_cluster",
            "hdf_filter_workspace_bytes", "hdf_filter", "hdf_filter_hard", "hdf_filter_host_workspace_bytes",
            "hdf_filter_host", "hdf_pca_guide_workspace_bytes", "hdf_pca_guide",
-           "hdf_profile_enable", "hdf_profile_collect", "hdf_cluster_trace", "hdf_filter_flagged", "hdf_scale_guide")
+           "hdf_profile_enable", "hdf_profile_collect", "hdf_cluster_trace", "hdf_filter_flagged", "hdf_scale_guide",
+           "hdf_cluster_sampled_workspace_bytes", "hdf_cluster_sampled", "hdf_sample_guide")
 STAGES = ("cluster", "pinv", "coeffs", "vpass", "hpass", "fallback", "h2d", "d2h")
 
 
@@ -81,8 +82,15 @@ def lib():
         L.hdf_filter_hard.restype = i
         L.hdf_filter_host_workspace_bytes.argtypes = [i, i, i, i, i, i, f, i]
         L.hdf_filter_host_workspace_bytes.restype = sz
-        L.hdf_filter_host.argtypes = [vp, i, vp, i, i, i, i, f, i, f, i, f, vp, vp, C.POINTER(C.c_int32),
+        L.hdf_filter_host.argtypes = [vp, i, vp, i, i, i, i, f, i, f, i, f, i, vp, vp, C.POINTER(C.c_int32),
                                       C.POINTER(ClusterInfo), vp, sz, vp]
+        L.hdf_cluster_sampled_workspace_bytes.argtypes = [i, i, i, i, i]
+        L.hdf_cluster_sampled_workspace_bytes.restype = sz
+        L.hdf_cluster_sampled.argtypes = [vp, i, i, i, i, i, vp, C.POINTER(ClusterInfo), vp, sz, vp]
+        L.hdf_cluster_sampled.restype = i
+        ll = C.c_longlong
+        L.hdf_sample_guide.argtypes = [vp, ll, i, ll, ll, vp, ll, vp]
+        L.hdf_sample_guide.restype = i
         L.hdf_filter_host.restype = i
         L.hdf_profile_enable.argtypes = [i]
         L.hdf_profile_enable.restype = i
@@ -188,6 +196,40 @@ def cluster(p: torch.Tensor, K: int, labels: bool = False, info: bool = True, ws
     if st != OK:
         _raise(st)
     return cen, lab, inf
+
+
+def cluster_sampled(p: torch.Tensor, K: int, stride: int, info: bool = True, ws: Workspace | None = None,
+                    stream=None):
+    """The sampled clustering mode ("any efficient clustering method"): bisecting K-means of the
+    stride sample p.flat[0::stride] (include/hdf.h, hdf_cluster_sampled).  stride = 1 is cluster().
+    Returns (centres [K,rho] fp32, ClusterInfo of the sample or None)."""
+    p = _dev_f32(p, "p")
+    H, W, rho = _hwc(p, "p")
+    cen = torch.empty((K, rho), dtype=torch.float32, device=p.device)
+    need = int(lib().hdf_cluster_sampled_workspace_bytes(H, W, rho, K, int(stride)))
+    wsb = (ws or _default_ws).get(max(need, 256), p.device)
+    inf = ClusterInfo() if info else None
+    st = lib().hdf_cluster_sampled(p.data_ptr(), H, W, rho, K, int(stride), cen.data_ptr(),
+                                   C.byref(inf) if inf is not None else None, wsb.data_ptr(), wsb.numel(),
+                                   _stream_ptr(stream))
+    if st == ERR_K:
+        raise HdfKError(st, lib().hdf_last_error().decode(), inf.achievable_k)
+    if st != OK:
+        _raise(st)
+    return cen, inf
+
+
+def sample_guide(p: torch.Tensor, i0: int, stride: int, M: int, stream=None) -> torch.Tensor:
+    """Gather p.flat[i0 + j stride], j < M ([M, rho]; include/hdf.h, hdf_sample_guide)."""
+    p = _dev_f32(p, "p")
+    rho = p.shape[-1] if p.dim() == 3 else 1
+    N = p.numel() // rho
+    out = torch.empty((max(M, 0), rho), dtype=torch.float32, device=p.device)
+    st = lib().hdf_sample_guide(p.data_ptr(), N, rho, int(i0), int(stride), out.data_ptr(), int(M),
+                                _stream_ptr(stream))
+    if st != OK:
+        _raise(st)
+    return out
 
 
 @dataclass
@@ -337,9 +379,11 @@ def anisotropic_guide(p: torch.Tensor, sigmas, extra: torch.Tensor | None = None
 
 def filter_host(f_host: torch.Tensor, p_host: torch.Tensor | None = None, *, kind: str = "gaussian",
                 sigma_s: float = 1.0, radius: int = -1, sigma_r: float = 1.0, K: int = 16, tau: float = 0.5,
-                out: torch.Tensor | None = None, ws: Workspace | None = None, device=None, stream=None):
-    """End-to-end from HOST buffers (pinned preferred): H2D copy, cluster, filter, D2H copy, all
-    inside the library on one stream.  Returns (g_host, centres_host, n_flagged, ClusterInfo)."""
+                cluster_stride: int = 1, out: torch.Tensor | None = None, ws: Workspace | None = None, device=None,
+                stream=None):
+    """End-to-end from HOST buffers (pinned preferred): H2D copy, cluster (exact, or the sampled mode
+    with cluster_stride > 1), filter, D2H copy, all inside the library on one stream.  Returns
+    (g_host, centres_host, n_flagged, ClusterInfo)."""
     if p_host is None:
         p_host = f_host
     for t, nm in ((f_host, "f"), (p_host, "p")):
@@ -362,7 +406,8 @@ def filter_host(f_host: torch.Tensor, p_host: torch.Tensor | None = None, *, kin
     nfl = C.c_int32(0)
     inf = ClusterInfo()
     st = lib().hdf_filter_host(f_host.data_ptr(), n, p_host.data_ptr(), rho, H, W, KIND[kind], float(sigma_s),
-                               int(radius), float(sigma_r), int(K), float(tau), g.data_ptr(), cen.data_ptr(),
+                               int(radius), float(sigma_r), int(K), float(tau), int(cluster_stride), g.data_ptr(),
+                               cen.data_ptr(),
                                C.byref(nfl), C.byref(inf), wsb.data_ptr(), wsb.numel(), _stream_ptr(stream))
     if st == ERR_K:
         raise HdfKError(st, lib().hdf_last_error().decode(), inf.achievable_k)

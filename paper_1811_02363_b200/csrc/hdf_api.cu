@@ -1149,6 +1149,61 @@ static int pca_guide_impl(const float* f, int H, int W, int n, int m, int dim, f
     return HDF_OK;
 }
 
+int hdf_sample_guide(const float* p, long long N, int rho, long long i0, long long stride, float* out, long long M,
+                     void* stream) {
+    g_err.clear();
+    return guarded([&]() -> int {
+        if (!p || !out) return fail(HDF_ERR_ARG, "NULL pointer argument");
+        if (rho < 1 || rho > HDF_MAX_RHO) return fail(HDF_ERR_ARG, "rho must be in [1, %d]", HDF_MAX_RHO);
+        if (N < 1 || stride < 1 || i0 < 0 || M < 0) return fail(HDF_ERR_ARG, "need N >= 1, stride >= 1, i0, M >= 0");
+        if (M > 0 && i0 + (M - 1) * stride >= N) return fail(HDF_ERR_ARG, "the sample runs past the guide");
+        if (M == 0) return HDF_OK;
+        const unsigned nb =
+            (unsigned)std::min<long long>((M * rho + 255) / 256, (long long)nsm_of_device() * 16);
+        hdf::k_sample_guide<<<nb, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, rho, i0, stride, out, M);
+        HDF_CUDA(cudaGetLastError());
+        return HDF_OK;
+    });
+}
+
+size_t hdf_cluster_sampled_workspace_bytes(int H, int W, int rho, int K, int stride) {
+    if (H < 1 || W < 1 || rho < 1 || K < 1 || stride < 1) return 0;
+    const long long N = (long long)H * W, M = (N + stride - 1) / stride;
+    if (M > (1LL << 30)) return 0;
+    Carver cv(nullptr);
+    cv.take<float>((size_t)M * rho + 4);
+    return cv.off + 256 + hdf_cluster_workspace_bytes(1, (int)M, rho, K);
+}
+
+int hdf_cluster_sampled(const float* p, int H, int W, int rho, int K, int stride, float* centres,
+                        hdf_cluster_info* info_host, void* ws, size_t ws_bytes, void* stream) {
+    g_err.clear();
+    return guarded([&]() -> int {
+        int rc = check_common(H, W, rho, K);
+        if (rc) return rc;
+        if (stride < 1) return fail(HDF_ERR_ARG, "stride must be >= 1 (got %d)", stride);
+        if (!p || !centres || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
+        if (misaligned(p) || misaligned(centres) || misaligned(ws))
+            return fail(HDF_ERR_ARG, "device pointers must be 16-byte aligned");
+        const size_t need = hdf_cluster_sampled_workspace_bytes(H, W, rho, K, stride);
+        if (ws_bytes < need) return fail(HDF_ERR_WORKSPACE, "workspace %zu < required %zu bytes", ws_bytes, need);
+        const long long N = (long long)H * W, M = (N + stride - 1) / stride;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        Carver cv(ws);
+        float* smp = cv.take<float>((size_t)M * rho + 4);
+        cv.off = (cv.off + 255) & ~size_t(255);
+        void* cws = cv.base + cv.off;
+        if (stride == 1) {
+            smp = const_cast<float*>(p);   // the exact procedure on the whole guide
+        } else {
+            const unsigned nb = (unsigned)std::min<long long>((M * rho + 255) / 256, (long long)nsm_of_device() * 16);
+            hdf::k_sample_guide<<<nb, 256, 0, st>>>(p, rho, 0, stride, smp, M);
+            HDF_CUDA(cudaGetLastError());
+        }
+        return launch_cluster(smp, 1, (int)M, rho, K, centres, nullptr, info_host, cws, st);
+    });
+}
+
 int hdf_scale_guide(const float* p, int H, int W, int rho, const float* scale_host, const float* extra, int e,
                     const float* extra_scale_host, float* out, void* stream) {
     g_err.clear();
@@ -1189,11 +1244,12 @@ size_t hdf_filter_host_workspace_bytes(int H, int W, int n, int rho, int K, int 
     cv.take<float>((size_t)H * W * rho);
     cv.take<float>((size_t)H * W * n);
     cv.take<float>((size_t)K * rho);
+    cv.take<float>((size_t)H * W * rho);   // the stride sample (cluster_stride > 1)
     return base + cv.off + 256;
 }
 
 int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, int H, int W, int kind, float sigma_s,
-                    int radius, float sigma_r, int K, float tau, float* g_host, float* centres_host,
+                    int radius, float sigma_r, int K, float tau, int cluster_stride, float* g_host, float* centres_host,
                     int32_t* n_flagged_host, hdf_cluster_info* info_host, void* ws, size_t ws_bytes, void* stream) {
     g_err.clear();
     return guarded([&]() -> int {
@@ -1205,6 +1261,7 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
         if (rc) return rc;
         if (!f_host || !p_host || !g_host || !ws) return fail(HDF_ERR_ARG, "NULL pointer argument");
         if (misaligned(ws)) return fail(HDF_ERR_ARG, "the workspace must be 16-byte aligned");
+        if (cluster_stride < 1) return fail(HDF_ERR_ARG, "cluster_stride must be >= 1 (got %d)", cluster_stride);
         rc = validate_filter(n, rho, H, W, kind, sigma_s, radius, sigma_r, K, tau, f_is_p, false, &F, &vsmem);
         if (rc) return rc;
         const size_t need = hdf_filter_host_workspace_bytes(H, W, n, rho, K, kind, sigma_s, radius);
@@ -1219,6 +1276,7 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
         float* pd = cv.take<float>((size_t)H * W * rho);
         float* gd = cv.take<float>((size_t)H * W * n);
         float* cd = cv.take<float>((size_t)K * rho);
+        float* smp = cv.take<float>((size_t)H * W * rho);
         const float* pdev = fd;
         // from here on, a failure synchronises the stream before returning (copies from the caller's
         // buffers may be in flight)
@@ -1242,7 +1300,15 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
         Carver c2(fws);
         FilterWS w = carve_filter(c2, H, W, n, rho, K, round_up(W, 4), true);
         ClusterReadback crb;
-        rc = launch_cluster(pdev, H, W, rho, K, cd, nullptr, nullptr, w.cluster_ws, st, &crb);
+        if (cluster_stride == 1) {
+            rc = launch_cluster(pdev, H, W, rho, K, cd, nullptr, nullptr, w.cluster_ws, st, &crb);
+        } else {   // the sampled mode (hdf_cluster_sampled): the stride sample, then the same procedure
+            const long long N = (long long)H * W, M = (N + cluster_stride - 1) / cluster_stride;
+            const unsigned nb = (unsigned)std::min<long long>((M * rho + 255) / 256, (long long)nsm_of_device() * 16);
+            hdf::k_sample_guide<<<nb, 256, 0, st>>>(pdev, rho, 0, cluster_stride, smp, M);
+            if (cudaGetLastError() != cudaSuccess) return bail(fail(HDF_ERR_CUDA, "sample launch failed"));
+            rc = launch_cluster(smp, 1, (int)M, rho, K, cd, nullptr, nullptr, w.cluster_ws, st, &crb);
+        }
         if (rc) return bail(rc);
         rc = run_filter(fd, n, pdev, rho, H, W, kind, sigma_s, radius, sigma_r, K, cd, tau, gd, nullptr, fws, fbytes,
                         st);

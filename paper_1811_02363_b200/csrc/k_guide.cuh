@@ -313,4 +313,17 @@ __global__ void __launch_bounds__(256) k_scale_guide(const __grid_constant__ Sca
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Stride sample of the guide for the sampled clustering mode ("any efficient clustering
+// method" may replace the exact procedure): out[j] = p[i0 + j * stride], j < M (rho floats each).
+__global__ void __launch_bounds__(256) k_sample_guide(const float* __restrict__ p, int rho, long long i0,
+                                                      long long stride, float* __restrict__ out, long long M) {
+    const long long tot = M * rho;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+        const long long j = t / rho;
+        const int d = (int)(t - j * rho);
+        out[t] = __ldg(p + (i0 + j * stride) * rho + d);
+    }
+}
+
 }  // namespace hdf

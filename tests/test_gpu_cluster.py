@@ -166,3 +166,36 @@ def test_c5_clustering_matches_oracle_and_five_percent_rule(hdf):
     mse_o = oracle.mse(g_o, g_bf, cfg.R_range)
     mse_g = oracle.mse(g_g, g_bf, cfg.R_range)
     assert mse_g <= 1.05 * mse_o + 1e-12, f"GPU MSE {mse_g:.4e} vs oracle {mse_o:.4e}"
+
+
+@pytest.mark.parametrize("name,stride", [("c1", 3), ("c2b", 4), ("c4", 5), ("c3", 2)])
+def test_sampled_mode_equals_the_oracle_on_the_sample(hdf, name, stride):
+    """hdf_cluster_sampled (any efficient clustering) = the bisecting K-means (R2-R4) of the
+    stride sample p.flat[0::stride]: the oracle's centres and E_K of the same sample."""
+    cfg, f, p = synth.make(name)
+    smp = p.reshape(-1, p.shape[-1])[0::stride]
+    cen_o, _, _, ek_o = oracle.cluster(smp, cfg.K)
+    cen_g, info = hdf.cluster_sampled(_dev(p), cfg.K, stride)
+    assert np.allclose(cen_g.cpu().numpy().astype(np.float64), cen_o, rtol=1e-6, atol=1e-5 * cfg.R_range)
+    assert abs(info.e_k - ek_o) <= 1e-9 * ek_o
+    # the gather on its own, with an offset (the multi-GPU split's per-rank share)
+    g = hdf.sample_guide(_dev(p), 7, stride, 100).cpu().numpy()
+    assert np.array_equal(g, p.reshape(-1, p.shape[-1])[7::stride][:100])
+
+
+@pytest.mark.parametrize("name,stride", [("c2b", 4), ("c3", 4), ("c4", 4)])
+def test_sampled_mode_five_percent_rule(hdf, name, stride):
+    """R15 for the sampled mode: MSE([hdf_cluster_sampled -> hdf_filter] vs brute force) <= 1.05 x
+    MSE([oracle.cluster (all pixels) -> oracle.filter] vs brute force)."""
+    cfg, f, p = synth.make(name)
+    g_bf, _ = oracle.bruteforce(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, r=cfg.radius)
+    cen_o, _, _, _ = oracle.cluster(p, cfg.K)
+    g_o, _, _, _ = oracle.filter(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, cen_o, r=cfg.radius)
+    pd = _dev(p)
+    fd = pd if cfg.bilateral else _dev(f)
+    cen_g, _ = hdf.cluster_sampled(pd, cfg.K, stride)
+    g_g = hdf.filter(fd, pd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                     centres=cen_g).g.cpu().numpy()
+    mse_o = oracle.mse(g_o, g_bf, cfg.R_range)
+    mse_g = oracle.mse(g_g, g_bf, cfg.R_range)
+    assert mse_g <= 1.05 * mse_o + 1e-12, f"{name}/{stride}: GPU MSE {mse_g:.4e} vs oracle {mse_o:.4e}"

@@ -2,8 +2,10 @@
 import csv, io, subprocess, sys
 rep = sys.argv[1]
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+if len(sys.argv) > 3:   # one kernel (regex on its name)
+    cmd += ["-k", "regex:" + sys.argv[3]]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 fname, res, hdr, tot = None, [], None, 0
 for r in rows:

@@ -68,6 +68,9 @@ def full(path):
 
 
 if __name__ == "__main__":
-    launches(sys.argv[1])
-    if len(sys.argv) > 2:
+    if sys.argv[1] == "--full-only":
         full(sys.argv[2])
+    else:
+        launches(sys.argv[1])
+        if len(sys.argv) > 2:
+            full(sys.argv[2])
