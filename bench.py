@@ -171,6 +171,14 @@ def run_ours(args, rank: int, world: int, dist):
 
         def step():
             hdf.filter_hard(fd, None if cfg.bilateral else pd, **kwh)
+    elif args.cluster_stride > 1:    # the sampled clustering mode, then the filter
+        cws = hdf.Workspace()
+        kwc = dict(kw)
+        kwc.pop("K")
+
+        def step():
+            cen, _ = hdf.cluster_sampled(pd, K, args.cluster_stride, info=False, ws=cws)
+            hdf.filter(fd, pd, centres=cen, **kwc)
     else:
         def step():
             hdf.filter(fd, pd, **kw)        # centres=None: clustering runs inside the call
@@ -220,14 +228,14 @@ def run_ours(args, rank: int, world: int, dist):
     ws2 = hdf.Workspace()
     for _ in range(max(1, args.warmup)):
         hdf.filter_host(fh, ph, kind=kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
-                        K=K, out=gh, ws=ws2)
+                        K=K, out=gh, ws=ws2, cluster_stride=args.cluster_stride)
     e2e_ms = []
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         hdf.filter_host(fh, ph, kind=kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
-                        K=K, out=gh, ws=ws2)
+                        K=K, out=gh, ws=ws2, cluster_stride=args.cluster_stride)
         b.record(stream)
         b.synchronize()
         e2e_ms.append(a.elapsed_time(b))
@@ -303,7 +311,10 @@ def run_ours(args, rank: int, world: int, dist):
         # procedure, each reading the node's members once per Lloyd pass, then once more and writing
         # them (coordinates + index) for the partition.  It is bound by the latency
         # of its dependent chain of passes and exchanges, not by bandwidth, hence the low fraction.
-        _, _, info = hdf.cluster(pd, K)
+        if args.cluster_stride > 1:
+            _, info = hdf.cluster_sampled(pd, K, args.cluster_stride)
+        else:
+            _, _, info = hdf.cluster(pd, K)
         cb = 4 * cfg.rho * (info.point_passes + info.points_split) + 4 * (cfg.rho + 1) * info.points_split
         t = per_launch[dom] * 1e-3
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(cb / t / 1e9, 1), "peak": hbm_peak,
@@ -334,7 +345,10 @@ def run_ours(args, rank: int, world: int, dist):
                           if args.variant == "hard" else {}),
                        **({"variant": "iir (Young's recursive Gaussian, P:332-333, NEXT #1); the vpass stage "
                                       "includes the column and row recursions"}
-                          if args.variant == "iir" else {})),
+                          if args.variant == "iir" else {}),
+                       cluster=("exact bisecting K-means of every pixel (P:328-329, R1-R4)" if args.cluster_stride == 1
+                                else f"sampled mode: bisecting K-means of the stride-{args.cluster_stride} sample "
+                                     f"(P:329 'any efficient clustering'; R15 5% rule checked in tests)")),
         "stages_ms_per_step": {k: round(ms / args.steps, 4) for k, (ms, n) in prof.items() if n},
         "filter": filt, "roofline": roof, "filter_roofline": filter_roof, "gpu_launches": launches, "clocks": clk,
         "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -440,6 +454,8 @@ def main():
     ap.add_argument("--all", action="store_true", help="one line per config (exploration)")
     ap.add_argument("--strips", action="store_true",
                     help="N > 1: one image in row strips over the ranks (strong scaling, exploration)")
+    ap.add_argument("--cluster-stride", type=int, default=1,
+                    help="1: exact clustering of every pixel; s > 1: the sampled mode (hdf_cluster_sampled)")
     ap.add_argument("--variant", default="soft", choices=["soft", "hard", "iir"],
                     help="hard: the hard-assignment variant (exploration; not the headline)")
     args = ap.parse_args()
