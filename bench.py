@@ -165,7 +165,8 @@ def run_ours(args, rank: int, world: int, dist):
 
         def step():
             _strips.filter_strips(fd, None if cfg.bilateral else pd, kind=cfg.kind, sigma_s=cfg.sigma_s,
-                                  radius=cfg.radius, sigma_r=cfg.sigma_r, K=K, tau=0.5, gather=False, dist=dist)
+                                  radius=cfg.radius, sigma_r=cfg.sigma_r, K=K, tau=0.5, gather=False, dist=dist,
+                                  cluster_stride=args.cluster_stride if args.cluster_stride > 1 else None)
     elif args.variant == "hard":     # hard-assignment variant: one-hot coefficients, no A^+
         kwh = {k: v for k, v in kw.items() if k != "tau"}
 

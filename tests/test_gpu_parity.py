@@ -565,3 +565,17 @@ def test_scale_guide_argument_errors(hdf):
     want = torch.cat([p * torch.tensor([2.0, 0.5, 1.0], device="cuda"), torch.tensor([3.0, 4.0], device="cuda")
                       .expand(8, 9, 2)], -1)
     assert torch.equal(q, want)
+
+
+def test_row_strips_sharded_sampled_clustering_on_one_gpu(hdf):
+    """The sharded sampled clustering (strips.py) through the CUDA path on one rank:
+    centres equal the single-GPU sampled mode's, hence the same output bits."""
+    from paper_1811_02363_b200 import strips
+    cfg, f, p = synth.make("c2a", 200, 160)
+    fd = _dev(f)
+    got = strips.filter_strips(fd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                               K=cfg.K, cluster_stride=5)
+    cen, _ = hdf.cluster_sampled(fd, cfg.K, 5)
+    want = hdf.filter(fd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                      centres=cen, tau=0.5).g
+    assert torch.equal(got, want)
