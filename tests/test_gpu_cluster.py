@@ -183,10 +183,12 @@ def test_sampled_mode_equals_the_oracle_on_the_sample(hdf, name, stride):
     assert np.array_equal(g, p.reshape(-1, p.shape[-1])[7::stride][:100])
 
 
-@pytest.mark.parametrize("name,stride", [("c2b", 4), ("c3", 4), ("c4", 4)])
+@pytest.mark.parametrize("name,stride", [("c2b", 4), ("c3", 4)])
 def test_sampled_mode_five_percent_rule(hdf, name, stride):
     """R15 for the sampled mode: MSE([hdf_cluster_sampled -> hdf_filter] vs brute force) <= 1.05 x
-    MSE([oracle.cluster (all pixels) -> oracle.filter] vs brute force)."""
+    MSE([oracle.cluster (all pixels) -> oracle.filter] vs brute force).  (The NLM config c4 fails it at
+    strides 4, 16 and 64 -- 1.22, 1.41, 1.15 in profiles/r02b_sampled_sweep.jsonl -- so the bench
+    clusters every pixel there.)"""
     cfg, f, p = synth.make(name)
     g_bf, _ = oracle.bruteforce(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, r=cfg.radius)
     cen_o, _, _, _ = oracle.cluster(p, cfg.K)
@@ -199,3 +201,23 @@ def test_sampled_mode_five_percent_rule(hdf, name, stride):
     mse_o = oracle.mse(g_o, g_bf, cfg.R_range)
     mse_g = oracle.mse(g_g, g_bf, cfg.R_range)
     assert mse_g <= 1.05 * mse_o + 1e-12, f"{name}/{stride}: GPU MSE {mse_g:.4e} vs oracle {mse_o:.4e}"
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("stride", [64, 16])
+def test_sampled_mode_five_percent_rule_c5(hdf, stride):
+    """R15 at config 5 for the sampled mode the bench uses (stride 64) and a denser one, on a seeded
+    2^16-pixel sample of brute-force values."""
+    cfg, f, p = synth.make("c5")
+    rng = np.random.default_rng(5 << 16)
+    pix = np.sort(rng.choice(cfg.H * cfg.W, 1 << 16, replace=False))
+    g_bf, _ = oracle.bruteforce(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, r=cfg.radius, pix=pix)
+    cen_o, _, _, _ = oracle.cluster(p, cfg.K)
+    g_o, _, _ = oracle.filter_pixels(f, p, cfg.kind, cfg.sigma_s, cfg.sigma_r, cen_o, pix, r=cfg.radius)
+    pd = _dev(p)
+    cen_g, _ = hdf.cluster_sampled(pd, cfg.K, stride)
+    g_g = hdf.filter(pd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                     centres=cen_g).g.cpu().numpy().reshape(-1, 3)[pix]
+    mse_o = oracle.mse(g_o, g_bf, cfg.R_range)
+    mse_g = oracle.mse(g_g, g_bf, cfg.R_range)
+    assert mse_g <= 1.05 * mse_o + 1e-12, f"stride {stride}: GPU MSE {mse_g:.4e} vs oracle {mse_o:.4e}"
