@@ -15,6 +15,7 @@
 #include "hdf_dispatch.h"
 #include "k_bisect.cuh"
 #include "k_coeffs.cuh"
+#include "k_coeffs_tc.cuh"
 #include "k_guide.cuh"
 #include "k_iir.cuh"
 
@@ -832,9 +833,17 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         const unsigned nblk = (unsigned)((npix + hdf::kCoefPix - 1) / hdf::kCoefPix);
         void (*kt)(const hdf::CoefParams) = nullptr;
         void (*km)(const hdf::CoefParams) = nullptr;
-        km = coeffs_mma_kernel((K + 7) / 8, rho);   // tensor cores (3xTF32), K <= 64 padded to 8 NT
+        // tcgen05 (5th-generation tensor cores, TMEM accumulator, 3xTF32) for K <= 64; the legacy
+        // mma.sync kernel (HDF_COEFFS_MMA=1) and the CUDA-core kernels (HDF_COEFFS_FMA=1) are kept for
+        // comparison and for K > 64
+        void (*ktc)(const hdf::CoefParams) = nullptr;
+        if (K <= hdf::kTcMaxK) ktc = rho == 3 ? hdf::k_coeffs_tc<3> : rho == 6 ? hdf::k_coeffs_tc<6> : hdf::k_coeffs_tc<0>;
+        km = coeffs_mma_kernel((K + 7) / 8, rho);   // mma.sync (3xTF32), K <= 64 padded to 8 NT
+        if (const char* e = getenv("HDF_COEFFS_MMA")) {
+            if (atoi(e)) ktc = nullptr;
+        }
         if (const char* e = getenv("HDF_COEFFS_FMA")) {   // diagnostics: the CUDA-core kernel instead
-            if (atoi(e)) km = nullptr;
+            if (atoi(e)) km = ktc = nullptr;
         }
         if (K == 8) kt = hdf::k_coeffs_t<8>;
         else if (K == 16) kt = hdf::k_coeffs_t<16>;
@@ -845,6 +854,14 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             const long long ntot = npix;
             const unsigned nb = (unsigned)std::min<long long>((ntot + 255) / 256, (long long)nsm * 16);
             hdf::k_coeffs_onehot<<<nb, 256, 0, st>>>(hard_labels, w.cpl, (long long)H * F.Wp, H, W, F.Wp, K);
+        } else if (ktc) {
+            const size_t smem = hdf::coeffs_tc_smem(K, rho);
+            HDF_CUDA(cudaFuncSetAttribute(ktc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int per_sm = 1;
+            HDF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ktc, hdf::kTcThreads, smem));
+            const long long ntile = (npix + hdf::kTcM - 1) / hdf::kTcM;
+            const unsigned nb = (unsigned)std::min<long long>(ntile, (long long)nsm * std::max(1, std::min(per_sm, 2)));
+            ktc<<<nb, hdf::kTcThreads, smem, st>>>(cp);
         } else if (km) {
             const int nt = (K + 7) / 8;
             const size_t smem = sizeof(float) * ((size_t)2 * nt * nt * 2 * 32 + (size_t)8 * nt * rho);
