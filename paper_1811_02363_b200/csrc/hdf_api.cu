@@ -456,13 +456,13 @@ int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, F
     // F1: planes per CTA; a persistent grid (one 512-thread CTA per SM) with equal shares of the
     // (strip, plane group) x rows space
     {
-        const int npl = hdf::vfir_npl(hdf::vpass_pack(F.Rp));
+        const int npl = hdf::vfir_npl(hdf::vpass_pack(F.Rp), hdf::vpass_nt(F.Rp));
         F.Pg = npl;
         const long long gx = (W + hdf::kVTX - 1) / hdf::kVTX, gz = (F.P + npl - 1) / npl;
         F.TY = (int)gx;   // reused: number of strips
         const long long cols = gx * gz;
         F.vl.grid = dim3((unsigned)std::max(1LL, std::min<long long>(std::max(1, nsm - 1), cols * H)));
-        F.vl.threads = hdf::kVNT;
+        F.vl.threads = hdf::vpass_nt(F.Rp);
         F.vl.smem = 0;   // depends on rho and on f aliasing p: set at launch
     }
     // F2

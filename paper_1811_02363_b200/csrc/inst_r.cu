@@ -12,8 +12,9 @@ template <int R, int RHO, int NPC>
 static cudaError_t vp(bool box, const VLaunch& L, cudaStream_t st, const VParams& P) {
     constexpr int J = vpass_j(R);
     constexpr bool PK = vpass_pack(R);
+    constexpr int NT = vpass_nt(R);
     void (*kern)(const VParams) =
-        box ? k_range_vpass<R, J, true, PK, RHO, NPC> : k_range_vpass<R, J, false, PK, RHO, NPC>;
+        box ? k_range_vpass<R, J, true, PK, RHO, NPC, NT> : k_range_vpass<R, J, false, PK, RHO, NPC, NT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
     if (e != cudaSuccess) return e;
     kern<<<L.grid, L.threads, L.smem, st>>>(P);

@@ -8,22 +8,23 @@
 // the tensor core reads its top 19 bits, so hi + lo carries x to ~2^-21 relative), and
 //   C = b_lo A_hi^T + b_hi A_lo^T + b_hi A_hi^T   (fp32 accumulation in TMEM, small terms first).
 //
-// One CTA = one warpgroup (128 threads), persistent over tiles of 128 consecutive pixels:
-//   1. thread m evaluates b(i) for pixel i = 128 t + m (K exp2's) and writes b_hi, b_lo into row m of
-//      the A operands (canonical K-major no-swizzle layout: 8 x 16-byte core matrices);
+// One CTA = two warpgroups (256 threads), persistent over tiles of 128 consecutive pixels; thread
+// (h, m) = (tid / 128, tid % 128) serves pixel row m and half h of the K coefficients:
+//   1. it evaluates b_l(i), l in its half, for pixel i = 128 t + m (exp2) and writes b_hi, b_lo into row
+//      m of the A operands (canonical K-major no-swizzle layout: 8 x 16-byte core matrices);
 //   2. one thread issues 3 (K/8) MMAs of M = 128, N = round_up(K, 16), K-step 8 and commits them to an
 //      mbarrier;
-//   3. thread m (TMEM lane m of its warp's 32-lane quarter) loads its row of the accumulator with
-//      tcgen05.ld (16 columns at a time) and stores c_k(i) to the coefficient planes (coalesced over m).
-// A^+ (hi, lo) is staged once per CTA as the B operands.  Two CTAs per SM overlap one tile's exp2 /
-// stores with the other's.
+//   3. warp w reads TMEM lanes 32 (w % 4) .. + 31 (its quarter), columns of its half, with tcgen05.ld
+//      (16 at a time) and stores c_k(i) to the coefficient planes (coalesced over m).
+// A^+ (hi, lo) is staged once per CTA as the B operands.  Two CTAs per SM (16 warps) hide the exp2 /
+// shared-memory latency of step 1 and the stores of step 3.
 #pragma once
 #include "hdf_common.cuh"
 #include "k_coeffs.cuh"
 
 namespace hdf {
 
-constexpr int kTcThreads = 128;   // one warpgroup: thread m <-> accumulator row / TMEM lane m
+constexpr int kTcThreads = 256;   // two warpgroups: thread (h, m) <-> accumulator row / TMEM lane m, half h
 constexpr int kTcM = 128;         // pixels per MMA tile (UMMA M)
 constexpr int kTcMaxK = 64;       // N = round_up(K, 16) <= 64 (larger K: the CUDA-core kernels)
 
@@ -128,15 +129,19 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_coeffs_tc(const __grid_consta
     const long long ntile = (npix + kTcM - 1) / kTcM;
     uint32_t phase = 0;
     for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
-        // 1. b(i) for this thread's pixel, split into the A operands' row `tid`
-        const long long i = tile * kTcM + tid;
+        // 1. b(i) for this thread's pixel and half, split into the A operands' row m
+        const int m = tid & (kTcM - 1), half = tid >> 7;
+        const long long i = tile * kTcM + m;
         const bool valid = i < npix;
         float x[RR];
         if (RHO > 0) {
 #pragma unroll
             for (int d = 0; d < RR; d++) x[d] = valid ? __ldg(P.p + i * RR + d) : 0.f;
         }
-        for (int l0 = 0; l0 < Kr; l0 += 4) {
+        const int lh = ((Kr / 4 + 1) / 2) * 4;   // the first half's columns (a multiple of 4)
+        const int la = half ? lh : 0, lb = half ? Kr : lh;
+#pragma unroll 2
+        for (int l0 = la; l0 < lb; l0 += 4) {
             uint32_t h[4], q[4];
 #pragma unroll
             for (int u = 0; u < 4; u++) {
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_coeffs_tc(const __grid_consta
                 h[u] = tf32_hi(b);
                 q[u] = tf32_lo(b, h[u]);
             }
-            const uint32_t off = tc_off(tid, l0, Kr);
+            const uint32_t off = tc_off(m, l0, Kr);
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aH + off), "r"(h[0]), "r"(h[1]), "r"(h[2]),
                          "r"(h[3])
                          : "memory");
@@ -188,14 +193,15 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_coeffs_tc(const __grid_consta
         mbar_wait(&mma_done, phase);
         phase ^= 1u;
         tc_fence_after();
-        const uint32_t trow = tbase + ((uint32_t)(32 * warp) << 16);
+        const uint32_t trow = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
         long long y = 0, xx = 0;
         if (valid) {
             y = i / P.W;
             xx = i - y * P.W;
         }
         float* o = P.cpl + y * P.Wp + xx;
-        for (int n0 = 0; n0 < N; n0 += 16) {
+        const int nh = ((N / 16 + 1) / 2) * 16;   // the first half's columns (a multiple of 16)
+        for (int n0 = half ? nh : 0; n0 < (half ? N : nh); n0 += 16) {
             float v[16];
             tmem_ld16(trow + (uint32_t)n0, v);
             if (valid) {

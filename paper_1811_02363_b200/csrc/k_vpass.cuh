@@ -27,8 +27,9 @@
 namespace hdf {
 
 constexpr int kVTX = 32;   // columns per CTA
-constexpr int kVNT = 512;  // threads per CTA
-__host__ __device__ constexpr int vfir_npl(bool pack) { return pack ? 32 : 16; }   // planes per CTA
+constexpr int kVNT = 512;  // threads per CTA (256 for the packed large-radius kernels, vpass_nt)
+// planes per CTA: 16 column pairs (packed) or 32 columns per plane
+__host__ __device__ constexpr int vfir_npl(bool pack, int nt = kVNT) { return pack ? nt / 16 : nt / 32; }
 
 struct VParams {
     const float* f;        // [H][W][n]
@@ -82,14 +83,14 @@ inline __host__ __device__ int vfir_nkmax(int NP, int npl) { return (npl + NP - 
 // raw rows of step `step` (input rows ystart + step*J + r) -> raw buffer [J][32][RW].
 // When f aliases p the 32 pixels of a row are one contiguous run of 32*rho floats (16-byte copies when
 // aligned); otherwise p and f are interleaved per pixel with 4-byte copies.
-template <int J, int RHO>
+template <int J, int RHO, int NT>
 HDF_DEV void vfir_issue_raw(const VParams& P, float* raw, int ystart, int step, int x0, int nx, int RW, bool vec) {
     const int rho = RHO > 0 ? RHO : P.rho;
     if (P.f_is_p) {
         const int per_row = nx * rho;
         if (vec) {   // nx == 32, W * rho % 4 == 0: rows of 8 rho 16-byte chunks
             const int cpr = 8 * rho;
-            for (int e = threadIdx.x; e < J * cpr; e += kVNT) {
+            for (int e = threadIdx.x; e < J * cpr; e += NT) {
                 const int r = e / cpr, w = e - r * cpr;
                 const int y = ystart + step * J + r;
                 if (y < 0 || y >= P.H) continue;
@@ -99,7 +100,7 @@ HDF_DEV void vfir_issue_raw(const VParams& P, float* raw, int ystart, int step, 
                              : "memory");
             }
         } else {
-            for (int e = threadIdx.x; e < J * per_row; e += kVNT) {
+            for (int e = threadIdx.x; e < J * per_row; e += NT) {
                 const int r = e / per_row, w = e - r * per_row;
                 const int y = ystart + step * J + r;
                 if (y < 0 || y >= P.H) continue;
@@ -108,7 +109,7 @@ HDF_DEV void vfir_issue_raw(const VParams& P, float* raw, int ystart, int step, 
         }
     } else {
         const int per_row = nx * RW;
-        for (int e = threadIdx.x; e < J * per_row; e += kVNT) {
+        for (int e = threadIdx.x; e < J * per_row; e += NT) {
             const int r = e / per_row, w = e - r * per_row;
             const int y = ystart + step * J + r;
             if (y < 0 || y >= P.H) continue;
@@ -133,12 +134,12 @@ HDF_DEV float ex2_approx(float x) {
 // Raw rows for the specialised path: [J][32][RHO] (pixel-major, as in memory).  A full strip whose rows
 // are 16-byte aligned is copied in 16-byte chunks; rows / columns off the image are zero-filled (their
 // b is 0, but 0 * garbage could be NaN).
-template <int J, int RHO>
+template <int J, int RHO, int NT>
 HDF_DEV void vfir_issue_raw_aos(const VParams& P, float* raw, int ystart, int step, int x0, int nx, bool vec) {
     constexpr int PR = kVTX * RHO;   // floats per row
     if (vec) {
         constexpr int CR = PR / 4;   // 16-byte chunks per row (RHO * 8)
-        for (int e = threadIdx.x; e < J * CR; e += kVNT) {
+        for (int e = threadIdx.x; e < J * CR; e += NT) {
             const int r = e / CR, c = e - r * CR;
             const int y = ystart + step * J + r;
             float* dst = raw + r * PR + 4 * c;
@@ -151,7 +152,7 @@ HDF_DEV void vfir_issue_raw_aos(const VParams& P, float* raw, int ystart, int st
             }
         }
     } else {
-        for (int e = threadIdx.x; e < J * PR; e += kVNT) {
+        for (int e = threadIdx.x; e < J * PR; e += NT) {
             const int r = e / PR, w = e - r * PR;
             const int y = ystart + step * J + r;
             float* dst = raw + r * PR + w;
@@ -163,15 +164,16 @@ HDF_DEV void vfir_issue_raw_aos(const VParams& P, float* raw, int ystart, int st
 }
 
 // Specialised stage A: RHO, NPC compile-time and plane groups aligned to clusters (NPL % NPC == 0).
-template <int J, int NPL, int RHO, int NPC>
+template <int J, int NPL, int RHO, int NPC, int NT>
 HDF_DEV void vfir_stage_a_fast(const VParams& P, const float* raw, float* zs, const float* mus, int ystart, int step,
                                int x0, int nk) {
     // thread -> (column pair xp, cluster kl, row phase h); packed f32x2 arithmetic on the column pair
     constexpr int NK = NPL / NPC;                 // clusters per group
-    constexpr int HS = (32 / NK) > 0 ? (32 / NK) : 1;   // 512 threads = 16 pairs x NK x HS
+    constexpr int NW = NT / 16;                   // NT threads = 16 pairs x NK x HS
+    constexpr int HS = (NW / NK) > 0 ? (NW / NK) : 1;
     constexpr int RPT = (J + HS - 1) / HS;
     const int xp = threadIdx.x & 15;
-    const int w = threadIdx.x >> 4;               // 0..31
+    const int w = threadIdx.x >> 4;               // 0..NW-1
     const int kl = w / HS, h = w - kl * HS;
     if (kl >= nk) return;
     const int xa = x0 + 2 * xp;
@@ -222,15 +224,15 @@ HDF_DEV void vfir_stage_a_fast(const VParams& P, const float* raw, float* zs, co
     }
 }
 
-template <int J, int NPL, int RHO, int NPC>
+template <int J, int NPL, int RHO, int NPC, int NT>
 HDF_DEV void vfir_stage_a(const VParams& P, const float* raw, float* zs, const float* mus, int ystart, int step,
                           int x0, int q0, int kA, int nk, int RW) {
     const int rho = RHO > 0 ? RHO : P.rho;
     const int NP = NPC > 0 ? NPC : P.NP;
     const int n = NP - 1;
     const int x = threadIdx.x & (kVTX - 1);
-    const int w = threadIdx.x >> 5;                 // 0..15
-    const int HS = max(1, 16 / nk);                 // row phases per (column, cluster)
+    const int w = threadIdx.x >> 5;                 // 0..NT/32-1
+    const int HS = max(1, (NT / 32) / nk);          // row phases per (column, cluster)
     const int kl = w / HS, h = w - kl * HS;
     if (kl >= nk) return;
     const int k = kA + kl;
@@ -293,11 +295,11 @@ HDF_DEV void wload(float& v, const float* p) { v = lds_f32(p); }
 HDF_DEV void wstore(float* p, unsigned long long v) { *reinterpret_cast<unsigned long long*>(p) = v; }
 HDF_DEV void wstore(float* p, float v) { *p = v; }
 
-template <int R, int J, bool BOX, bool PACK, int RHO, int NPC>
+template <int R, int J, bool BOX, bool PACK, int RHO, int NPC, int NT>
 HDF_DEV void vfir_segment(const VParams& P, float* sm_v, int strip, int group, int y0, int y1) {
     using WT = typename std::conditional<PACK, unsigned long long, float>::type;
-    constexpr int NPL = vfir_npl(PACK);
-    constexpr int NCW = kVNT / NPL;          // column workers per plane (16 pairs or 32 columns)
+    constexpr int NPL = vfir_npl(PACK, NT);
+    constexpr int NCW = NT / NPL;            // column workers per plane (16 pairs or 32 columns)
     constexpr int CPW = kVTX / NCW;          // columns per worker (2 or 1)
     constexpr int S = 2 * R + J;
     constexpr int NSTEP = S / J;
@@ -315,7 +317,7 @@ HDF_DEV void vfir_segment(const VParams& P, float* sm_v, int strip, int group, i
     float* zs0 = raw0 + 2 * raw_len;
     constexpr int zs_len = J * NPL * kVTX;
     __syncthreads();   // the previous segment is done with the shared buffers
-    for (int e = threadIdx.x; e < nk * rho; e += kVNT) mus[e] = P.centres[kA * rho + e];
+    for (int e = threadIdx.x; e < nk * rho; e += NT) mus[e] = P.centres[kA * rho + e];
 
     const int tid = threadIdx.x;
     const int cw = tid % NCW, pq = tid / NCW;
@@ -337,15 +339,15 @@ HDF_DEV void vfir_segment(const VParams& P, float* sm_v, int strip, int group, i
     constexpr bool FAST = (RHO > 0) && (NPC > 0) && (NPL % (NPC > 0 ? NPC : 1) == 0) && (RHO == NPC - 1);
     const bool fast = FAST && P.f_is_p;
     auto issue = [&](float* dst, int step) {
-        if (fast) vfir_issue_raw_aos<J, (RHO > 0 ? RHO : 1)>(P, dst, ystart, step, x0, nx, vec);
-        else vfir_issue_raw<J, RHO>(P, dst, ystart, step, x0, nx, RW, vec);
+        if (fast) vfir_issue_raw_aos<J, (RHO > 0 ? RHO : 1), NT>(P, dst, ystart, step, x0, nx, vec);
+        else vfir_issue_raw<J, RHO, NT>(P, dst, ystart, step, x0, nx, RW, vec);
     };
     issue(raw0, 0);
     if (nsteps > 1) issue(raw0 + raw_len, 1);
     cp_async_wait_all();
     __syncthreads();
-    if (fast) vfir_stage_a_fast<J, NPL, (RHO > 0 ? RHO : 1), (NPC > 0 ? NPC : 1)>(P, raw0, zs0, mus, ystart, 0, x0, nk);
-    else vfir_stage_a<J, NPL, RHO, NPC>(P, raw0, zs0, mus, ystart, 0, x0, q0, kA, nk, RW);
+    if (fast) vfir_stage_a_fast<J, NPL, (RHO > 0 ? RHO : 1), (NPC > 0 ? NPC : 1), NT>(P, raw0, zs0, mus, ystart, 0, x0, nk);
+    else vfir_stage_a<J, NPL, RHO, NPC, NT>(P, raw0, zs0, mus, ystart, 0, x0, q0, kA, nk, RW);
     __syncthreads();
     int g = 0;
     while (true) {
@@ -354,11 +356,11 @@ HDF_DEV void vfir_segment(const VParams& P, float* sm_v, int strip, int group, i
             if (g + 2 < nsteps) issue(raw0 + (g & 1) * raw_len, g + 2);
             if (g + 1 < nsteps) {
                 if (fast)
-                    vfir_stage_a_fast<J, NPL, (RHO > 0 ? RHO : 1), (NPC > 0 ? NPC : 1)>(
+                    vfir_stage_a_fast<J, NPL, (RHO > 0 ? RHO : 1), (NPC > 0 ? NPC : 1), NT>(
                         P, raw0 + ((g + 1) & 1) * raw_len, zs0 + ((g + 1) & 1) * zs_len, mus, ystart, g + 1, x0, nk);
                 else
-                    vfir_stage_a<J, NPL, RHO, NPC>(P, raw0 + ((g + 1) & 1) * raw_len, zs0 + ((g + 1) & 1) * zs_len, mus,
-                                                   ystart, g + 1, x0, q0, kA, nk, RW);
+                    vfir_stage_a<J, NPL, RHO, NPC, NT>(P, raw0 + ((g + 1) & 1) * raw_len, zs0 + ((g + 1) & 1) * zs_len,
+                                                       mus, ystart, g + 1, x0, q0, kA, nk, RW);
             }
             const float* st = zs0 + (g & 1) * zs_len + pq * kVTX + CPW * cw;
 #pragma unroll
@@ -418,8 +420,8 @@ HDF_DEV void vfir_segment(const VParams& P, float* sm_v, int strip, int group, i
 // CTA b takes the contiguous share [T b / G, T (b + 1) / G) (T = columns * H): every CTA gets the same
 // number of output rows (no wave quantisation) and a window is primed at most once per column
 // touched.
-template <int R, int J, bool BOX, bool PACK, int RHO, int NPC>
-__global__ void __launch_bounds__(kVNT, 1) k_range_vpass(const __grid_constant__ VParams P) {
+template <int R, int J, bool BOX, bool PACK, int RHO, int NPC, int NT>
+__global__ void __launch_bounds__(NT, 1) k_range_vpass(const __grid_constant__ VParams P) {
     extern __shared__ __align__(16) float sm_v[];
     const long long T = (long long)P.ncol * P.H;
     const long long u0 = T * blockIdx.x / gridDim.x, u1 = T * (blockIdx.x + 1) / gridDim.x;
@@ -428,7 +430,7 @@ __global__ void __launch_bounds__(kVNT, 1) k_range_vpass(const __grid_constant__
         const int col = (int)(u / P.H);
         const int ya = (int)(u - (long long)col * P.H);
         const int yb = (int)((u1 - u < (long long)(P.H - ya)) ? ya + (u1 - u) : P.H);
-        vfir_segment<R, J, BOX, PACK, RHO, NPC>(P, sm_v, col % P.nstrip, col / P.nstrip, ya, yb);
+        vfir_segment<R, J, BOX, PACK, RHO, NPC, NT>(P, sm_v, col % P.nstrip, col / P.nstrip, ya, yb);
         u += yb - ya;
     }
 }
