@@ -940,7 +940,10 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         }
         memcpy(fb.taps, t2, sizeof(t2));
         ProfScope prof(HDF_STAGE_FALLBACK, st);
-        hdf::k_fallback<<<2 * nsm, 256, 0, st>>>(fb);
+        // one CTA per flagged pixel (grid-stride): the count is on the device, so the grid is sized for
+        // the worst case the SMs can hold at once (16 CTAs of 128 threads per SM)
+        const long long npix = (long long)H * W;
+        hdf::k_fallback<<<(unsigned)std::min<long long>(npix, 16LL * nsm), hdf::kFbThreads, 0, st>>>(fb);
         HDF_CUDA(cudaGetLastError());
     }
     if (n_flagged_host) {
