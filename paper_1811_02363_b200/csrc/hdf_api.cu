@@ -857,6 +857,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         } else if (ktc) {
             const size_t smem = hdf::coeffs_tc_smem(K, rho);
             HDF_CUDA(cudaFuncSetAttribute(ktc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            HDF_CUDA(cudaFuncSetAttribute(ktc, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
             int per_sm = 1;
             HDF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ktc, hdf::kTcThreads, smem));
             const long long ntile = (npix + hdf::kTcM - 1) / hdf::kTcM;
@@ -940,10 +941,13 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         }
         memcpy(fb.taps, t2, sizeof(t2));
         ProfScope prof(HDF_STAGE_FALLBACK, st);
-        // one CTA per flagged pixel (grid-stride): the count is on the device, so the grid is sized for
-        // the worst case the SMs can hold at once (16 CTAs of 128 threads per SM)
+        // one warp per flagged pixel (grid-stride): the count is on the device, so the grid is sized for
+        // the worst case the SMs can hold at once (8 CTAs of 8 warps per SM), capped by the pixel count
         const long long npix = (long long)H * W;
-        hdf::k_fallback<<<(unsigned)std::min<long long>(npix, 16LL * nsm), hdf::kFbThreads, 0, st>>>(fb);
+        const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((npix + 7) / 8, 8LL * nsm));
+        void (*kfb)(const hdf::FBParams) =
+            n <= 4 ? hdf::k_fallback<4> : n <= 16 ? hdf::k_fallback<16> : hdf::k_fallback<64>;
+        kfb<<<nb, hdf::kFbThreads, 0, st>>>(fb);
         HDF_CUDA(cudaGetLastError());
     }
     if (n_flagged_host) {

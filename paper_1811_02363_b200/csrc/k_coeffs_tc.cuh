@@ -128,15 +128,23 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_coeffs_tc(const __grid_consta
     const long long npix = (long long)P.H * P.W;
     const long long ntile = (npix + kTcM - 1) / kTcM;
     uint32_t phase = 0;
+    const int m = tid & (kTcM - 1), half = tid >> 7;
+    // compile-time rho: the guide values of the CTA's next tile are loaded while this tile's MMAs run
+    float xn[RR];
+    auto load_x = [&](long long tile) {
+        const long long ii = tile * kTcM + m;
+#pragma unroll
+        for (int d = 0; d < RR; d++) xn[d] = (ii < npix) ? __ldg(P.p + ii * RR + d) : 0.f;
+    };
+    if (RHO > 0) load_x(blockIdx.x);
     for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
         // 1. b(i) for this thread's pixel and half, split into the A operands' row m
-        const int m = tid & (kTcM - 1), half = tid >> 7;
         const long long i = tile * kTcM + m;
         const bool valid = i < npix;
         float x[RR];
         if (RHO > 0) {
 #pragma unroll
-            for (int d = 0; d < RR; d++) x[d] = valid ? __ldg(P.p + i * RR + d) : 0.f;
+            for (int d = 0; d < RR; d++) x[d] = xn[d];
         }
         const int lh = ((Kr / 4 + 1) / 2) * 4;   // the first half's columns (a multiple of 4)
         const int la = half ? lh : 0, lb = half ? Kr : lh;
@@ -189,6 +197,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_coeffs_tc(const __grid_consta
             }
             umma_commit(&mma_done);
         }
+        if (RHO > 0 && tile + gridDim.x < ntile) load_x(tile + gridDim.x);
         // 3. the accumulator row of this thread's pixel -> coefficient planes
         mbar_wait(&mma_done, phase);
         phase ^= 1u;

@@ -202,12 +202,12 @@ __global__ void __launch_bounds__(1024, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
-// F3: direct (num)/(den) for the pixels flagged by rule R9.  One CTA (kFbThreads threads)
-// per flagged pixel (grid-stride over the list): every thread takes window taps j, evaluates the
-// weight omega(j) phi(p(i - j) - p(i)) once and accumulates it times all n channels of f(i - j) in
-// registers; warp shuffles and one shared-memory pass reduce den and num; fp32 throughout.
+// F3: direct (num)/(den) for the pixels flagged by rule R9.  One warp per flagged pixel
+// (grid-stride over the list, a grid of many warps so that each takes about one pixel): every lane
+// takes window taps j, evaluates the weight omega(j) phi(p(i - j) - p(i)) once and accumulates it times
+// all n <= NC channels of f(i - j) in registers; warp shuffles reduce den and num; fp32 throughout.
 // ---------------------------------------------------------------------------------------------
-constexpr int kFbThreads = 128;
+constexpr int kFbThreads = 256;
 
 struct FBParams {
     const float* f;
@@ -224,53 +224,41 @@ struct FBParams {
     const int32_t* labels;     // phi(p(j) - mu_{label(i)}); NULL: phi(p(j) - p(i))
 };
 
-static __global__ void __launch_bounds__(kFbThreads) k_fallback(const __grid_constant__ FBParams P) {
-    __shared__ float red[kFbThreads / 32][HDF_MAX_N + 1];
-    __shared__ float pi_s[HDF_MAX_RHO];
-    __shared__ float dmin_s;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+template <int NC>   // channels held in registers (n <= NC)
+__global__ void __launch_bounds__(kFbThreads) k_fallback(const __grid_constant__ FBParams P) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
     const int cnt = *P.flag_count;
     const int side = 2 * P.R + 1, win = side * side;
-    for (int t = blockIdx.x; t < cnt; t += gridDim.x) {
+    for (int t = gw; t < cnt; t += nw) {
         const int i = P.flag_list[t];
         const int y = i / P.W, x = i % P.W;
         const float* pi = P.labels ? P.mu + (long long)__ldg(P.labels + i) * P.rho : P.p + (long long)i * P.rho;
-        __syncthreads();   // the previous pixel is done with the shared buffers
-        for (int d = tid; d < P.rho; d += kFbThreads) pi_s[d] = pi[d];
-        __syncthreads();
         // hard variant: the window's weights are scaled by exp(-d2min / (2 sr^2)) (the ratio is
         // unchanged) so that a window far from its centre does not underflow
         float dmin = 0.f;
         if (P.labels) {
-            float m = INFINITY;
-            for (int e = tid; e < win; e += kFbThreads) {
+            dmin = INFINITY;
+            for (int e = lane; e < win; e += 32) {
                 const int ty = e / side - P.R, tx = e % side - P.R;
                 const int yy = y - ty, xx = x - tx;
                 if (yy < 0 || yy >= P.H || xx < 0 || xx >= P.W) continue;
                 const float* pj = P.p + ((long long)yy * P.W + xx) * P.rho;
                 float d2 = 0.f;
                 for (int d = 0; d < P.rho; d++) {
-                    const float dd = __ldg(pj + d) - pi_s[d];
+                    const float dd = __ldg(pj + d) - __ldg(pi + d);
                     d2 = fmaf(dd, dd, d2);
                 }
-                m = fminf(m, d2);
+                dmin = fminf(dmin, d2);
             }
-            for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-            if (lane == 0) red[warp][0] = m;
-            __syncthreads();
-            if (tid == 0) {
-                float mm = red[0][0];
-                for (int w = 1; w < kFbThreads / 32; w++) mm = fminf(mm, red[w][0]);
-                dmin_s = mm;
-            }
-            __syncthreads();
-            dmin = dmin_s;
+            for (int o = 16; o > 0; o >>= 1) dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
         }
-        float num[HDF_MAX_N];
+        float num[NC];
 #pragma unroll
-        for (int c = 0; c < HDF_MAX_N; c++) num[c] = 0.f;
+        for (int c = 0; c < NC; c++) num[c] = 0.f;
         float den = 0.f;
-        for (int e = tid; e < win; e += kFbThreads) {
+        for (int e = lane; e < win; e += 32) {
             const int ty = e / side - P.R, tx = e % side - P.R;
             const int yy = y - ty, xx = x - tx;
             if (yy < 0 || yy >= P.H || xx < 0 || xx >= P.W) continue;
@@ -278,7 +266,7 @@ static __global__ void __launch_bounds__(kFbThreads) k_fallback(const __grid_con
             const float* pj = P.p + jj * P.rho;
             float d2 = 0.f;
             for (int d = 0; d < P.rho; d++) {
-                const float dd = __ldg(pj + d) - pi_s[d];
+                const float dd = __ldg(pj + d) - __ldg(pi + d);
                 d2 = fmaf(dd, dd, d2);
             }
             const float sy = P.neg_inv2ss2 != 0.f ? expf((float)(ty * ty) * P.neg_inv2ss2) : P.taps[ty + P.R];
@@ -287,27 +275,16 @@ static __global__ void __launch_bounds__(kFbThreads) k_fallback(const __grid_con
             den += wt;
             const float* fj = P.f + jj * P.n;
 #pragma unroll
-            for (int c = 0; c < HDF_MAX_N; c++)
+            for (int c = 0; c < NC; c++)
                 if (c < P.n) num[c] = fmaf(wt, __ldg(fj + c), num[c]);
         }
-        // reduce: warps by shuffles, then across warps through shared memory
         den = warp_sum(den);
-        if (lane == 0) red[warp][HDF_MAX_N] = den;
 #pragma unroll
-        for (int c = 0; c < HDF_MAX_N; c++) {
+        for (int c = 0; c < NC; c++) {
             if (c < P.n) {
                 const float v = warp_sum(num[c]);
-                if (lane == 0) red[warp][c] = v;
+                if (lane == 0) P.g[(long long)i * P.n + c] = v / den;
             }
-        }
-        __syncthreads();
-        if (tid < P.n) {
-            float a = 0.f, b = 0.f;
-            for (int w = 0; w < kFbThreads / 32; w++) {
-                a += red[w][tid];
-                b += red[w][HDF_MAX_N];
-            }
-            P.g[(long long)i * P.n + tid] = a / b;
         }
     }
 }

@@ -80,7 +80,33 @@ HDF_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory
 // Shared-memory layout (floats): mus [nkmax * rho, rounded to 4] | raw [2][J][32][RW] | zs [2][J][NPL][32]
 inline __host__ __device__ int vfir_nkmax(int NP, int npl) { return (npl + NP - 1) / NP + 1; }
 
-// raw rows of step `step` (input rows ystart + step*J + r) -> raw buffer [J][32][RW].
+// J rows (from row y0) of a 32-pixel segment [x0, x0 + nx) of an [H][W][c] image -> dst [J][32][c]:
+// 16-byte cp.async chunks when the segment is whole and rows are 16-byte aligned, else 4-byte ones.
+template <int J, int NT>
+HDF_DEV void vfir_copy_rows(float* dst, const float* src, int c, int W, int H, int y0, int x0, int nx) {
+    if (nx == kVTX && (W * c) % 4 == 0) {
+        const int cpr = 8 * c;   // 16-byte chunks per row (32 c floats)
+        for (int e = threadIdx.x; e < J * cpr; e += NT) {
+            const int r = e / cpr, w = e - r * cpr;
+            const int y = y0 + r;
+            if (y < 0 || y >= H) continue;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + r * kVTX * c + 4 * w)),
+                         "l"(src + ((long long)y * W + x0) * c + 4 * w)
+                         : "memory");
+        }
+    } else {
+        const int per_row = nx * c;
+        for (int e = threadIdx.x; e < J * per_row; e += NT) {
+            const int r = e / per_row, w = e - r * per_row;
+            const int y = y0 + r;
+            if (y < 0 || y >= H) continue;
+            cp_async4(dst + r * kVTX * c + w, src + ((long long)y * W + x0) * c + w);
+        }
+    }
+}
+
+// raw rows of step `step` (input rows ystart + step*J + r) -> raw buffer: [J][32][rho] when f is p,
+// else [J][32][rho] guide rows followed by [J][32][n] image rows.
 // When f aliases p the 32 pixels of a row are one contiguous run of 32*rho floats (16-byte copies when
 // aligned); otherwise p and f are interleaved per pixel with 4-byte copies.
 template <int J, int RHO, int NT>
@@ -108,16 +134,12 @@ HDF_DEV void vfir_issue_raw(const VParams& P, float* raw, int ystart, int step, 
             }
         }
     } else {
-        const int per_row = nx * RW;
-        for (int e = threadIdx.x; e < J * per_row; e += NT) {
-            const int r = e / per_row, w = e - r * per_row;
-            const int y = ystart + step * J + r;
-            if (y < 0 || y >= P.H) continue;
-            const int x = w / RW, d = w - x * RW;
-            const long long pix = (long long)y * P.W + x0 + x;
-            const float* src = (d < rho) ? P.p + pix * rho + d : P.f + pix * P.n + (d - rho);
-            cp_async4(raw + (r * kVTX + x) * RW + d, src);
-        }
+        // f is not p: the guide rows [J][32][rho] and the image rows [J][32][n] in two arrays, each row
+        // segment one contiguous run (16-byte copies when aligned)
+        (void)RW;
+        float* rawf = raw + J * kVTX * rho;
+        vfir_copy_rows<J, NT>(raw, P.p, rho, P.W, P.H, ystart + step * J, x0, nx);
+        vfir_copy_rows<J, NT>(rawf, P.f, P.n, P.W, P.H, ystart + step * J, x0, nx);
     }
     cp_async_commit();
 }
@@ -249,7 +271,7 @@ HDF_DEV void vfir_stage_a(const VParams& P, const float* raw, float* zs, const f
     for (int r = h; r < J; r += HS) {
         const int y = ystart + step * J + r;
         const bool valid = xok && (y >= 0) && (y < P.H);
-        const float* pp = raw + (r * kVTX + x) * RW;
+        const float* pp = raw + (r * kVTX + x) * rho;
         float d2 = 0.f;
         if (RHO > 0) {
 #pragma unroll
@@ -257,14 +279,25 @@ HDF_DEV void vfir_stage_a(const VParams& P, const float* raw, float* zs, const f
                 const float t = lds_f32(pp + d) - mu[d];
                 d2 = fmaf(t, t, d2);
             }
-        } else {
-            for (int d = 0; d < rho; d++) {
-                const float t = lds_f32(pp + d) - lds_f32(mus + kl * rho + d);
-                d2 = fmaf(t, t, d2);
+        } else {   // runtime rho (large: 31 at config 3): four independent partial sums
+            float s4[4] = {0.f, 0.f, 0.f, 0.f};
+            const float* mk = mus + kl * rho;
+            int d = 0;
+            for (; d + 4 <= rho; d += 4) {
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const float t = lds_f32(pp + d + u) - lds_f32(mk + d + u);
+                    s4[u] = fmaf(t, t, s4[u]);
+                }
             }
+            for (; d < rho; d++) {
+                const float t = lds_f32(pp + d) - lds_f32(mk + d);
+                s4[0] = fmaf(t, t, s4[0]);
+            }
+            d2 = (s4[0] + s4[1]) + (s4[2] + s4[3]);
         }
         const float b = valid ? ex2_approx(d2 * c2) : 0.f;
-        const float* fp = P.f_is_p ? pp : pp + rho;
+        const float* fp = P.f_is_p ? pp : raw + J * kVTX * rho + (r * kVTX + x) * n;
         float* zo = zs + (r * NPL - q0) * kVTX + x;
         if (whole) {
 #pragma unroll
