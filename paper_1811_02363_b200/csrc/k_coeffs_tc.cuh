@@ -8,23 +8,25 @@
 // the tensor core reads its top 19 bits, so hi + lo carries x to ~2^-21 relative), and
 //   C = b_lo A_hi^T + b_hi A_lo^T + b_hi A_hi^T   (fp32 accumulation in TMEM, small terms first).
 //
-// One CTA = two warpgroups (256 threads), persistent over tiles of 128 consecutive pixels; thread
-// (h, m) = (tid / 128, tid % 128) serves pixel row m and half h of the K coefficients:
-//   1. it evaluates b_l(i), l in its half, for pixel i = 128 t + m (exp2) and writes b_hi, b_lo into row
-//      m of the A operands (canonical K-major no-swizzle layout: 8 x 16-byte core matrices);
-//   2. one thread issues 3 (K/8) MMAs of M = 128, N = round_up(K, 16), K-step 8 and commits them to an
-//      mbarrier;
-//   3. warp w reads TMEM lanes 32 (w % 4) .. + 31 (its quarter), columns of its half, with tcgen05.ld
-//      (16 at a time) and stores c_k(i) to the coefficient planes (coalesced over m).
-// A^+ (hi, lo) is staged once per CTA as the B operands.  Two CTAs per SM (16 warps) hide the exp2 /
-// shared-memory latency of step 1 and the stores of step 3.
+// Warp-specialised, double-buffered pipeline, one CTA of three warpgroups per SM (persistent over tiles
+// of 128 consecutive pixels; tile t uses stage s = t % 2 of the A operands and of the TMEM accumulator):
+//   * producers (warpgroups 0 and 1): thread (h, m) evaluates b_l(i) for pixel i = 128 t + m and the
+//     half h of l (exp2), splits it and writes row m of A_hi[s], A_lo[s] (canonical K-major no-swizzle
+//     layout: 8 x 16-byte core matrices); after a named barrier one thread issues the 3 (K/8) MMAs of
+//     M = 128, N = round_up(K, 16), K-step 8 into D[s] and commits them to two mbarriers (A[s] free,
+//     D[s] full);
+//   * consumer (warpgroup 2): warp w reads TMEM lanes 32 (w % 4) .. + 31 of D[s] (its pixels' rows)
+//     with tcgen05.ld, releases D[s] (mbarrier) and stores c_k(i) to the coefficient planes
+//     (coalesced over m) while the producers already compute tile t + 1.
+// A^+ (hi, lo) is staged once per CTA as the B operands.
 #pragma once
 #include "hdf_common.cuh"
 #include "k_coeffs.cuh"
 
 namespace hdf {
 
-constexpr int kTcThreads = 256;   // two warpgroups: thread (h, m) <-> accumulator row / TMEM lane m, half h
+constexpr int kTcProd = 256;      // producer threads: (half h, pixel row m)
+constexpr int kTcThreads = 384;   // + one consumer warpgroup
 constexpr int kTcM = 128;         // pixels per MMA tile (UMMA M)
 constexpr int kTcMaxK = 64;       // N = round_up(K, 16) <= 64 (larger K: the CUDA-core kernels)
 
@@ -74,27 +76,27 @@ HDF_DEV uint32_t tc_off(int row, int k, int Kr) {
     return (uint32_t)((row >> 3) * (Kr * 32) + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
 }
 
-// Dynamic shared memory: B_hi, B_lo [N][Kr], A_hi, A_lo [128][Kr], centres [N][rho].
+// Dynamic shared memory: B_hi, B_lo [N][Kr], 2 stages of A_hi, A_lo [128][Kr], centres [N][rho].
 inline __host__ __device__ size_t coeffs_tc_smem(int K, int rho) {
     const int Kr = (K + 7) & ~7, N = (K + 15) & ~15;
-    return (size_t)(2 * N + 2 * kTcM) * Kr * 4 + (size_t)N * rho * 4 + 64;
+    return (size_t)(2 * N + 4 * kTcM) * Kr * 4 + (size_t)N * rho * 4 + 64;
 }
 
 template <int RHO>   // RHO > 0: compile-time guide dimension, 0: runtime
-__global__ void __launch_bounds__(kTcThreads, 2) k_coeffs_tc(const __grid_constant__ CoefParams P) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_constant__ CoefParams P) {
     extern __shared__ __align__(128) unsigned char sm_tc[];
-    __shared__ uint64_t mma_done;
+    __shared__ uint64_t a_free[2], d_full[2], d_free[2];
     __shared__ uint32_t tmem_base_sh;
     constexpr int RR = RHO > 0 ? RHO : 1;
     const int K = P.K, rho = RHO > 0 ? RHO : P.rho;
     const int Kr = (K + 7) & ~7, N = (K + 15) & ~15;
     const int tid = threadIdx.x, warp = tid >> 5;
+    const size_t abytes = (size_t)kTcM * Kr * 4;
     unsigned char* Bh = sm_tc;
     unsigned char* Bl = Bh + (size_t)N * Kr * 4;
-    unsigned char* Ah = Bl + (size_t)N * Kr * 4;
-    unsigned char* Al = Ah + (size_t)kTcM * Kr * 4;
-    float* mus = reinterpret_cast<float*>(Al + (size_t)kTcM * Kr * 4);
-    const uint32_t ncols = N <= 32 ? 32u : 64u;
+    unsigned char* A0 = Bl + (size_t)N * Kr * 4;   // stage s: A_hi at A0 + 2 s abytes, A_lo after it
+    float* mus = reinterpret_cast<float*>(A0 + 4 * abytes);
+    const uint32_t ncols = N <= 32 ? 64u : 128u;   // two accumulator stages of N (<= 64) columns
 
     // A^+ (hi, lo) as the B operands: row n = output coefficient n, K index l; zero-padded
     for (int e = tid; e < N * Kr; e += kTcThreads) {
@@ -106,7 +108,11 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_coeffs_tc(const __grid_consta
     }
     for (int e = tid; e < N * rho; e += kTcThreads) mus[e] = (e < K * rho) ? P.centres[e] : 0.f;
     if (tid == 0) {
-        mbar_init(&mma_done, 1);
+        for (int s = 0; s < 2; s++) {
+            mbar_init(&a_free[s], 1);
+            mbar_init(&d_full[s], 1);
+            mbar_init(&d_free[s], kTcM);
+        }
         fence_barrier_init();
     }
     if (warp == 0) {
@@ -120,109 +126,129 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_coeffs_tc(const __grid_consta
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = tmem_base_sh;
-    const uint32_t idesc = umma_idesc_tf32(kTcM, N);
-    const uint32_t sbo = (uint32_t)Kr * 32u, lbo = 128u;
-    const uint32_t aH = smem_u32(Ah), aL = smem_u32(Al), bH = smem_u32(Bh), bL = smem_u32(Bl);
-
-    const float c2 = P.neg_inv2sr2 * 1.4426950408889634f;
     const long long npix = (long long)P.H * P.W;
     const long long ntile = (npix + kTcM - 1) / kTcM;
-    uint32_t phase = 0;
-    const int m = tid & (kTcM - 1), half = tid >> 7;
-    // compile-time rho: the guide values of the CTA's next tile are loaded while this tile's MMAs run
-    float xn[RR];
-    auto load_x = [&](long long tile) {
-        const long long ii = tile * kTcM + m;
-#pragma unroll
-        for (int d = 0; d < RR; d++) xn[d] = (ii < npix) ? __ldg(P.p + ii * RR + d) : 0.f;
-    };
-    if (RHO > 0) load_x(blockIdx.x);
-    for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
-        // 1. b(i) for this thread's pixel and half, split into the A operands' row m
-        const long long i = tile * kTcM + m;
-        const bool valid = i < npix;
-        float x[RR];
-        if (RHO > 0) {
-#pragma unroll
-            for (int d = 0; d < RR; d++) x[d] = xn[d];
-        }
+    const uint32_t dcols = ncols / 2;
+
+    if (tid < kTcProd) {   // ------------------------------------------------ producers --------
+        const uint32_t idesc = umma_idesc_tf32(kTcM, N);
+        const uint32_t sbo = (uint32_t)Kr * 32u, lbo = 128u;
+        const uint32_t bH = smem_u32(Bh), bL = smem_u32(Bl);
+        const float c2 = P.neg_inv2sr2 * 1.4426950408889634f;
+        const int m = tid & (kTcM - 1), half = tid >> 7;
         const int lh = ((Kr / 4 + 1) / 2) * 4;   // the first half's columns (a multiple of 4)
         const int la = half ? lh : 0, lb = half ? Kr : lh;
+        // compile-time rho: the guide values of the next tile are loaded one tile ahead
+        float xn[RR];
+        auto load_x = [&](long long tile) {
+            const long long ii = tile * kTcM + m;
+#pragma unroll
+            for (int d = 0; d < RR; d++) xn[d] = (ii < npix) ? __ldg(P.p + ii * RR + d) : 0.f;
+        };
+        if (RHO > 0) load_x(blockIdx.x);
+        int it = 0;
+        for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x, it++) {
+            const int s = it & 1;
+            const uint32_t ph = (uint32_t)(it >> 1) & 1u;
+            const long long i = tile * kTcM + m;
+            const bool valid = i < npix;
+            float x[RR];
+            if (RHO > 0) {
+#pragma unroll
+                for (int d = 0; d < RR; d++) x[d] = xn[d];
+                if (tile + gridDim.x < ntile) load_x(tile + gridDim.x);
+            }
+            mbar_wait(&a_free[s], ph ^ 1u);   // the MMAs of tile it - 2 have read A[s]
+            const uint32_t aH = smem_u32(A0 + 2 * s * abytes), aL = aH + (uint32_t)abytes;
 #pragma unroll 2
-        for (int l0 = la; l0 < lb; l0 += 4) {
-            uint32_t h[4], q[4];
+            for (int l0 = la; l0 < lb; l0 += 4) {
+                uint32_t h[4], q[4];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int l = l0 + u;
-                float b = 0.f;
-                if (valid && l < K) {
-                    const float* mu = mus + l * rho;
-                    float d2 = 0.f;
-                    if (RHO > 0) {
+                for (int u = 0; u < 4; u++) {
+                    const int l = l0 + u;
+                    float b = 0.f;
+                    if (valid && l < K) {
+                        const float* mu = mus + l * rho;
+                        float d2 = 0.f;
+                        if (RHO > 0) {
 #pragma unroll
-                        for (int d = 0; d < RR; d++) {
-                            const float t = x[d] - mu[d];
-                            d2 = fmaf(t, t, d2);
+                            for (int d = 0; d < RR; d++) {
+                                const float t = x[d] - mu[d];
+                                d2 = fmaf(t, t, d2);
+                            }
+                        } else {
+                            for (int d = 0; d < rho; d++) {
+                                const float t = __ldg(P.p + i * rho + d) - mu[d];
+                                d2 = fmaf(t, t, d2);
+                            }
                         }
-                    } else {
-                        for (int d = 0; d < rho; d++) {
-                            const float t = __ldg(P.p + i * rho + d) - mu[d];
-                            d2 = fmaf(t, t, d2);
-                        }
+                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
                     }
-                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
+                    h[u] = tf32_hi(b);
+                    q[u] = tf32_lo(b, h[u]);
                 }
-                h[u] = tf32_hi(b);
-                q[u] = tf32_lo(b, h[u]);
+                const uint32_t off = tc_off(m, l0, Kr);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aH + off), "r"(h[0]), "r"(h[1]),
+                             "r"(h[2]), "r"(h[3])
+                             : "memory");
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aL + off), "r"(q[0]), "r"(q[1]),
+                             "r"(q[2]), "r"(q[3])
+                             : "memory");
             }
-            const uint32_t off = tc_off(m, l0, Kr);
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aH + off), "r"(h[0]), "r"(h[1]), "r"(h[2]),
-                         "r"(h[3])
-                         : "memory");
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aL + off), "r"(q[0]), "r"(q[1]), "r"(q[2]),
-                         "r"(q[3])
-                         : "memory");
+            fence_proxy_async();   // generic-proxy writes of A[s] -> visible to the tensor core
+            named_sync(1, kTcProd);
+            if (tid == 0) {        // D = b_lo A_hi^T + b_hi A_lo^T + b_hi A_hi^T into D[s]
+                mbar_wait(&d_free[s], ph ^ 1u);   // the consumer has read D[s] of tile it - 2
+                tc_fence_after();
+                const uint32_t td = tbase + (uint32_t)s * dcols;
+                for (int k8 = 0; k8 < Kr / 8; k8++) {
+                    const uint32_t ko = (uint32_t)k8 * 256u;   // two 16-byte core matrices per K step of 8
+                    umma_tf32(td, umma_desc(aL + ko, lbo, sbo), umma_desc(bH + ko, lbo, sbo), idesc, k8 > 0 ? 1u : 0u);
+                    umma_tf32(td, umma_desc(aH + ko, lbo, sbo), umma_desc(bL + ko, lbo, sbo), idesc, 1u);
+                    umma_tf32(td, umma_desc(aH + ko, lbo, sbo), umma_desc(bH + ko, lbo, sbo), idesc, 1u);
+                }
+                umma_commit(&a_free[s]);
+                umma_commit(&d_full[s]);
+            }
         }
-        fence_proxy_async();   // generic-proxy writes of A -> visible to the tensor core
-        tc_fence_before();     // (the previous tile's tcgen05.ld are complete: wait::ld in tmem_ld16)
-        __syncthreads();
-        // 2. one thread issues the MMAs: D = b_lo A_hi^T + b_hi A_lo^T + b_hi A_hi^T
-        if (tid == 0) {
+    } else {               // ------------------------------------------------ consumer ---------
+        const int m = tid - kTcProd;
+        const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+        int it = 0;
+        for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x, it++) {
+            const int s = it & 1;
+            const uint32_t ph = (uint32_t)(it >> 1) & 1u;
+            const long long i = tile * kTcM + m;
+            const bool valid = i < npix;
+            long long y = 0, xx = 0;
+            if (valid) {
+                y = i / P.W;
+                xx = i - y * P.W;
+            }
+            float* o = P.cpl + y * P.Wp + xx;
+            mbar_wait(&d_full[s], ph);
             tc_fence_after();
-            for (int s = 0; s < Kr / 8; s++) {
-                const uint32_t ko = (uint32_t)s * 256u;   // two 16-byte core matrices per K step of 8
-                umma_tf32(tbase, umma_desc(aL + ko, lbo, sbo), umma_desc(bH + ko, lbo, sbo), idesc, s > 0 ? 1u : 0u);
-                umma_tf32(tbase, umma_desc(aH + ko, lbo, sbo), umma_desc(bL + ko, lbo, sbo), idesc, 1u);
-                umma_tf32(tbase, umma_desc(aH + ko, lbo, sbo), umma_desc(bH + ko, lbo, sbo), idesc, 1u);
+            float v[kTcMaxK];
+#pragma unroll
+            for (int n0 = 0; n0 < kTcMaxK; n0 += 16) {
+                if (n0 < N) {
+                    float t16[16];
+                    tmem_ld16(tbase + lane_base + (uint32_t)s * dcols + (uint32_t)n0, t16);
+#pragma unroll
+                    for (int j = 0; j < 16; j++) v[n0 + j] = t16[j];
+                }
             }
-            umma_commit(&mma_done);
-        }
-        if (RHO > 0 && tile + gridDim.x < ntile) load_x(tile + gridDim.x);
-        // 3. the accumulator row of this thread's pixel -> coefficient planes
-        mbar_wait(&mma_done, phase);
-        phase ^= 1u;
-        tc_fence_after();
-        const uint32_t trow = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
-        long long y = 0, xx = 0;
-        if (valid) {
-            y = i / P.W;
-            xx = i - y * P.W;
-        }
-        float* o = P.cpl + y * P.Wp + xx;
-        const int nh = ((N / 16 + 1) / 2) * 16;   // the first half's columns (a multiple of 16)
-        for (int n0 = half ? nh : 0; n0 < (half ? N : nh); n0 += 16) {
-            float v[16];
-            tmem_ld16(trow + (uint32_t)n0, v);
+            tc_fence_before();
+            mbar_arrive(&d_free[s]);
             if (valid) {
 #pragma unroll
-                for (int j = 0; j < 16; j++)
-                    if (n0 + j < K) o[(long long)(n0 + j) * P.cstride] = v[j];
+                for (int n = 0; n < kTcMaxK; n++)
+                    if (n < K) o[(long long)n * P.cstride] = v[n];
             }
         }
-        tc_fence_before();
-        __syncthreads();   // every lane's tcgen05.ld is done before the next tile's MMAs overwrite D,
-                           // and the A operands are no longer read
     }
+    tc_fence_before();
+    __syncthreads();
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols) : "memory");

@@ -289,4 +289,95 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(const __grid_constant__
     }
 }
 
+// Wide images (n > 16 channels, e.g. the 31-band config): one CTA of kFbCtaThreads per flagged pixel
+// instead of one warp, the taps spread over the CTA, warp shuffles then one shared-memory pass.
+constexpr int kFbCtaThreads = 128;
+static __global__ void __launch_bounds__(kFbCtaThreads) k_fallback_cta(const __grid_constant__ FBParams P) {
+    __shared__ float red[kFbCtaThreads / 32][HDF_MAX_N + 1];
+    __shared__ float pi_s[HDF_MAX_RHO];
+    __shared__ float dmin_s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int cnt = *P.flag_count;
+    const int side = 2 * P.R + 1, win = side * side;
+    for (int t = blockIdx.x; t < cnt; t += gridDim.x) {
+        const int i = P.flag_list[t];
+        const int y = i / P.W, x = i % P.W;
+        const float* pi = P.labels ? P.mu + (long long)__ldg(P.labels + i) * P.rho : P.p + (long long)i * P.rho;
+        __syncthreads();   // the previous pixel is done with the shared buffers
+        for (int d = tid; d < P.rho; d += kFbCtaThreads) pi_s[d] = pi[d];
+        __syncthreads();
+        // hard variant: the window's weights are scaled by exp(-d2min / (2 sr^2)) (the ratio is
+        // unchanged) so that a window far from its centre does not underflow
+        float dmin = 0.f;
+        if (P.labels) {
+            float m = INFINITY;
+            for (int e = tid; e < win; e += kFbCtaThreads) {
+                const int ty = e / side - P.R, tx = e % side - P.R;
+                const int yy = y - ty, xx = x - tx;
+                if (yy < 0 || yy >= P.H || xx < 0 || xx >= P.W) continue;
+                const float* pj = P.p + ((long long)yy * P.W + xx) * P.rho;
+                float d2 = 0.f;
+                for (int d = 0; d < P.rho; d++) {
+                    const float dd = __ldg(pj + d) - pi_s[d];
+                    d2 = fmaf(dd, dd, d2);
+                }
+                m = fminf(m, d2);
+            }
+            for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) red[warp][0] = m;
+            __syncthreads();
+            if (tid == 0) {
+                float mm = red[0][0];
+                for (int w = 1; w < kFbCtaThreads / 32; w++) mm = fminf(mm, red[w][0]);
+                dmin_s = mm;
+            }
+            __syncthreads();
+            dmin = dmin_s;
+        }
+        float num[HDF_MAX_N];
+#pragma unroll
+        for (int c = 0; c < HDF_MAX_N; c++) num[c] = 0.f;
+        float den = 0.f;
+        for (int e = tid; e < win; e += kFbCtaThreads) {
+            const int ty = e / side - P.R, tx = e % side - P.R;
+            const int yy = y - ty, xx = x - tx;
+            if (yy < 0 || yy >= P.H || xx < 0 || xx >= P.W) continue;
+            const long long jj = (long long)yy * P.W + xx;
+            const float* pj = P.p + jj * P.rho;
+            float d2 = 0.f;
+            for (int d = 0; d < P.rho; d++) {
+                const float dd = __ldg(pj + d) - pi_s[d];
+                d2 = fmaf(dd, dd, d2);
+            }
+            const float sy = P.neg_inv2ss2 != 0.f ? expf((float)(ty * ty) * P.neg_inv2ss2) : P.taps[ty + P.R];
+            const float sx = P.neg_inv2ss2 != 0.f ? expf((float)(tx * tx) * P.neg_inv2ss2) : P.taps[tx + P.R];
+            const float wt = sy * sx * expf((d2 - dmin) * P.neg_inv2sr2);
+            den += wt;
+            const float* fj = P.f + jj * P.n;
+#pragma unroll
+            for (int c = 0; c < HDF_MAX_N; c++)
+                if (c < P.n) num[c] = fmaf(wt, __ldg(fj + c), num[c]);
+        }
+        // reduce: warps by shuffles, then across warps through shared memory
+        den = warp_sum(den);
+        if (lane == 0) red[warp][HDF_MAX_N] = den;
+#pragma unroll
+        for (int c = 0; c < HDF_MAX_N; c++) {
+            if (c < P.n) {
+                const float v = warp_sum(num[c]);
+                if (lane == 0) red[warp][c] = v;
+            }
+        }
+        __syncthreads();
+        if (tid < P.n) {
+            float a = 0.f, b = 0.f;
+            for (int w = 0; w < kFbCtaThreads / 32; w++) {
+                a += red[w][tid];
+                b += red[w][HDF_MAX_N];
+            }
+            P.g[(long long)i * P.n + tid] = a / b;
+        }
+    }
+}
+
 }  // namespace hdf
