@@ -11,8 +11,10 @@
 // Warp-specialised, double-buffered pipeline, one CTA of three warpgroups per SM (persistent over tiles
 // of 128 consecutive pixels; tile t uses stage s = t % 2 of the A operands and of the TMEM accumulator):
 //   * producers (warpgroups 0 and 1): thread (h, m) evaluates b_l(i) for pixel i = 128 t + m and the
-//     half h of l (exp2), splits it and writes row m of A_hi[s], A_lo[s] (canonical K-major no-swizzle
-//     layout: 8 x 16-byte core matrices); after a named barrier one thread issues the 3 (K/8) MMAs of
+//     half h of l (exp2; for rho = 3 its 32 centres live in registers and the 32 evaluations are
+//     independent), splits it, writes row m of A_hi[s], A_lo[s] (canonical K-major no-swizzle layout:
+//     8 x 16-byte core matrices) and arrives on the mbarrier A[s] full;
+//   * the MMA warp (one elected thread): waits for A[s] full and D[s] free, issues the 3 (K/8) MMAs of
 //     M = 128, N = round_up(K, 16), K-step 8 into D[s] and commits them to two mbarriers (A[s] free,
 //     D[s] full);
 //   * consumer (warpgroup 2): warp w reads TMEM lanes 32 (w % 4) .. + 31 of D[s] (its pixels' rows)
@@ -26,7 +28,7 @@
 namespace hdf {
 
 constexpr int kTcProd = 256;      // producer threads: (half h, pixel row m)
-constexpr int kTcThreads = 384;   // + one consumer warpgroup
+constexpr int kTcThreads = 416;   // + one consumer warpgroup + one MMA-issuing warp
 constexpr int kTcM = 128;         // pixels per MMA tile (UMMA M)
 constexpr int kTcMaxK = 64;       // N = round_up(K, 16) <= 64 (larger K: the CUDA-core kernels)
 
@@ -85,7 +87,7 @@ inline __host__ __device__ size_t coeffs_tc_smem(int K, int rho) {
 template <int RHO>   // RHO > 0: compile-time guide dimension, 0: runtime
 __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_constant__ CoefParams P) {
     extern __shared__ __align__(128) unsigned char sm_tc[];
-    __shared__ uint64_t a_free[2], d_full[2], d_free[2];
+    __shared__ uint64_t a_full[2], a_free[2], d_full[2], d_free[2];
     __shared__ uint32_t tmem_base_sh;
     constexpr int RR = RHO > 0 ? RHO : 1;
     const int K = P.K, rho = RHO > 0 ? RHO : P.rho;
@@ -109,6 +111,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
     for (int e = tid; e < N * rho; e += kTcThreads) mus[e] = (e < K * rho) ? P.centres[e] : 0.f;
     if (tid == 0) {
         for (int s = 0; s < 2; s++) {
+            mbar_init(&a_full[s], kTcProd);
             mbar_init(&a_free[s], 1);
             mbar_init(&d_full[s], 1);
             mbar_init(&d_free[s], kTcM);
@@ -131,13 +134,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
     const uint32_t dcols = ncols / 2;
 
     if (tid < kTcProd) {   // ------------------------------------------------ producers --------
-        const uint32_t idesc = umma_idesc_tf32(kTcM, N);
-        const uint32_t sbo = (uint32_t)Kr * 32u, lbo = 128u;
-        const uint32_t bH = smem_u32(Bh), bL = smem_u32(Bl);
         const float c2 = P.neg_inv2sr2 * 1.4426950408889634f;
         const int m = tid & (kTcM - 1), half = tid >> 7;
-        const int lh = ((Kr / 4 + 1) / 2) * 4;   // the first half's columns (a multiple of 4)
+        const int lh = ((Kr / 4 + 1) / 2) * 4;   // the first half's columns (a multiple of 4, <= 32)
         const int la = half ? lh : 0, lb = half ? Kr : lh;
+        // rho = 3: the half's 32 evaluations fully unrolled (independent; centre loads at fixed offsets)
+        constexpr bool MUREG = (RHO == 3);
+        const float* mh = mus + la * RR;
         // compile-time rho: the guide values of the next tile are loaded one tile ahead
         float xn[RR];
         auto load_x = [&](long long tile) {
@@ -160,46 +163,88 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
             }
             mbar_wait(&a_free[s], ph ^ 1u);   // the MMAs of tile it - 2 have read A[s]
             const uint32_t aH = smem_u32(A0 + 2 * s * abytes), aL = aH + (uint32_t)abytes;
-#pragma unroll 2
-            for (int l0 = la; l0 < lb; l0 += 4) {
-                uint32_t h[4], q[4];
+            if (MUREG) {
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int l = l0 + u;
-                    float b = 0.f;
-                    if (valid && l < K) {
-                        const float* mu = mus + l * rho;
-                        float d2 = 0.f;
-                        if (RHO > 0) {
+                for (int j0 = 0; j0 < 32; j0 += 4) {
+                    if (la + j0 < lb) {
+                        uint32_t h[4], q[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const int j = j0 + u;
+                            float d2 = 0.f;
 #pragma unroll
                             for (int d = 0; d < RR; d++) {
-                                const float t = x[d] - mu[d];
+                                const float t = x[d] - mh[j * RR + d];
                                 d2 = fmaf(t, t, d2);
                             }
-                        } else {
-                            for (int d = 0; d < rho; d++) {
-                                const float t = __ldg(P.p + i * rho + d) - mu[d];
-                                d2 = fmaf(t, t, d2);
-                            }
+                            float b;
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
+                            b = (valid && la + j < K) ? b : 0.f;
+                            h[u] = tf32_hi(b);
+                            q[u] = tf32_lo(b, h[u]);
                         }
-                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
+                        const uint32_t off = tc_off(m, la + j0, Kr);
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aH + off), "r"(h[0]), "r"(h[1]),
+                                     "r"(h[2]), "r"(h[3])
+                                     : "memory");
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aL + off), "r"(q[0]), "r"(q[1]),
+                                     "r"(q[2]), "r"(q[3])
+                                     : "memory");
                     }
-                    h[u] = tf32_hi(b);
-                    q[u] = tf32_lo(b, h[u]);
                 }
-                const uint32_t off = tc_off(m, l0, Kr);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aH + off), "r"(h[0]), "r"(h[1]),
-                             "r"(h[2]), "r"(h[3])
-                             : "memory");
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aL + off), "r"(q[0]), "r"(q[1]),
-                             "r"(q[2]), "r"(q[3])
-                             : "memory");
+            } else {
+#pragma unroll 2
+                for (int l0 = la; l0 < lb; l0 += 4) {
+                    uint32_t h[4], q[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int l = l0 + u;
+                        float b = 0.f;
+                        if (valid && l < K) {
+                            const float* mu = mus + l * rho;
+                            float d2 = 0.f;
+                            if (RHO > 0) {
+#pragma unroll
+                                for (int d = 0; d < RR; d++) {
+                                    const float t = x[d] - mu[d];
+                                    d2 = fmaf(t, t, d2);
+                                }
+                            } else {
+                                for (int d = 0; d < rho; d++) {
+                                    const float t = __ldg(P.p + i * rho + d) - mu[d];
+                                    d2 = fmaf(t, t, d2);
+                                }
+                            }
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
+                        }
+                        h[u] = tf32_hi(b);
+                        q[u] = tf32_lo(b, h[u]);
+                    }
+                    const uint32_t off = tc_off(m, l0, Kr);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aH + off), "r"(h[0]), "r"(h[1]),
+                                 "r"(h[2]), "r"(h[3])
+                                 : "memory");
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aL + off), "r"(q[0]), "r"(q[1]),
+                                 "r"(q[2]), "r"(q[3])
+                                 : "memory");
+                }
             }
             fence_proxy_async();   // generic-proxy writes of A[s] -> visible to the tensor core
-            named_sync(1, kTcProd);
-            if (tid == 0) {        // D = b_lo A_hi^T + b_hi A_lo^T + b_hi A_hi^T into D[s]
-                mbar_wait(&d_free[s], ph ^ 1u);   // the consumer has read D[s] of tile it - 2
+            mbar_arrive(&a_full[s]);
+        }
+    } else if (warp == (kTcProd + kTcM) / 32) {   // ---------------------------- MMA warp ----------
+        if ((tid & 31) == 0) {    // D = b_lo A_hi^T + b_hi A_lo^T + b_hi A_hi^T into D[s]
+            const uint32_t idesc = umma_idesc_tf32(kTcM, N);
+            const uint32_t sbo = (uint32_t)Kr * 32u, lbo = 128u;
+            const uint32_t bH = smem_u32(Bh), bL = smem_u32(Bl);
+            int it = 0;
+            for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x, it++) {
+                const int s = it & 1;
+                const uint32_t ph = (uint32_t)(it >> 1) & 1u;
+                mbar_wait(&a_full[s], ph);          // the producers wrote A[s]
+                mbar_wait(&d_free[s], ph ^ 1u);     // the consumer has read D[s] of tile it - 2
                 tc_fence_after();
+                const uint32_t aH = smem_u32(A0 + 2 * s * abytes), aL = aH + (uint32_t)abytes;
                 const uint32_t td = tbase + (uint32_t)s * dcols;
                 for (int k8 = 0; k8 < Kr / 8; k8++) {
                     const uint32_t ko = (uint32_t)k8 * 256u;   // two 16-byte core matrices per K step of 8
@@ -212,7 +257,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
             }
         }
     } else {               // ------------------------------------------------ consumer ---------
-        const int m = tid - kTcProd;
+        const int m = tid - kTcProd;   // warps 8..11: TMEM lane quarters 0..3
         const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
         int it = 0;
         for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x, it++) {
