@@ -413,26 +413,28 @@ HDF_DEV void vfir_segment(const VParams& P, float* sm_v, int strip, int group, i
                     }
                 } else {
                     const bool full = yb + J <= y1;
-                    // taps outer, outputs inner: J independent accumulation chains in flight
+                    // Every output accumulates its taps in four independent partial sums (taps t mod 4),
+                    // added at the end: the scheduler tends to run one output's taps back to back (to
+                    // save registers), so the ILP has to be inside one output's chain (measured: with a
+                    // single chain per output the FP32 pipe waited on the FMA latency, ~55% busy).
                     WT acc[J];
 #pragma unroll
                     for (int j = 0; j < J; j++) {
                         const int c = oldest + j + R;
-                        if constexpr (PACK) acc[j] = wmul0((WT)P.tw[0], win[c % S]);
-                        else acc[j] = wmul0((WT)P.tws[R], win[c % S]);
-                    }
+                        WT a4[4];
+                        if constexpr (PACK) a4[0] = wmul0((WT)P.tw[0], win[c % S]);
+                        else a4[0] = wmul0((WT)P.tws[R], win[c % S]);
+                        a4[1] = a4[2] = a4[3] = WT(0);
 #pragma unroll
-                    for (int t = 1; t <= R; t++) {
-#pragma unroll
-                        for (int j = 0; j < J; j++) {
-                            const int c = oldest + j + R;
+                        for (int t = 1; t <= R; t++) {
                             if constexpr (PACK) {
-                                acc[j] = wfma((WT)P.tw[t], wadd(win[(c - t) % S], win[(c + t) % S]), acc[j]);
+                                a4[t & 3] = wfma((WT)P.tw[t], wadd(win[(c - t) % S], win[(c + t) % S]), a4[t & 3]);
                             } else {
-                                acc[j] = wfma((WT)P.tws[R - t], win[(c + t) % S], acc[j]);
-                                acc[j] = wfma((WT)P.tws[R + t], win[(c - t) % S], acc[j]);
+                                a4[t & 3] = wfma((WT)P.tws[R - t], win[(c + t) % S], a4[t & 3]);
+                                a4[t & 3] = wfma((WT)P.tws[R + t], win[(c - t) % S], a4[t & 3]);
                             }
                         }
+                        acc[j] = wadd(wadd(a4[0], a4[1]), wadd(a4[2], a4[3]));
                     }
 #pragma unroll
                     for (int j = 0; j < J; j++) {
