@@ -421,20 +421,26 @@ HDF_DEV void vfir_segment(const VParams& P, float* sm_v, int strip, int group, i
 #pragma unroll
                     for (int j = 0; j < J; j++) {
                         const int c = oldest + j + R;
-                        WT a4[4];
+                        constexpr int NC = 4;   // partial sums per output (8 measured slower at R = 24: 11.7 vs 10.1 ms)
+                        WT a4[NC];
                         if constexpr (PACK) a4[0] = wmul0((WT)P.tw[0], win[c % S]);
                         else a4[0] = wmul0((WT)P.tws[R], win[c % S]);
-                        a4[1] = a4[2] = a4[3] = WT(0);
+#pragma unroll
+                        for (int u = 1; u < NC; u++) a4[u] = WT(0);
 #pragma unroll
                         for (int t = 1; t <= R; t++) {
                             if constexpr (PACK) {
-                                a4[t & 3] = wfma((WT)P.tw[t], wadd(win[(c - t) % S], win[(c + t) % S]), a4[t & 3]);
+                                a4[t % NC] = wfma((WT)P.tw[t], wadd(win[(c - t) % S], win[(c + t) % S]), a4[t % NC]);
                             } else {
-                                a4[t & 3] = wfma((WT)P.tws[R - t], win[(c + t) % S], a4[t & 3]);
-                                a4[t & 3] = wfma((WT)P.tws[R + t], win[(c - t) % S], a4[t & 3]);
+                                a4[t % NC] = wfma((WT)P.tws[R - t], win[(c + t) % S], a4[t % NC]);
+                                a4[t % NC] = wfma((WT)P.tws[R + t], win[(c - t) % S], a4[t % NC]);
                             }
                         }
-                        acc[j] = wadd(wadd(a4[0], a4[1]), wadd(a4[2], a4[3]));
+#pragma unroll
+                        for (int h = NC / 2; h >= 1; h /= 2)
+#pragma unroll
+                            for (int u = 0; u < h; u++) a4[u] = wadd(a4[u], a4[u + h]);
+                        acc[j] = a4[0];
                     }
 #pragma unroll
                     for (int j = 0; j < J; j++) {
