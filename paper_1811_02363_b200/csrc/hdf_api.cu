@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -589,6 +590,18 @@ struct SideStream {
     cudaEvent_t fork = nullptr, join = nullptr;
     std::mutex* mu = nullptr;
 };
+// The host path's copy-out stream: one per (calling thread, device), created on first use.
+cudaStream_t copy_stream() {
+    static thread_local cudaStream_t cs[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (!cs[dev] && cudaStreamCreateWithFlags(&cs[dev], cudaStreamNonBlocking) != cudaSuccess) {
+        cs[dev] = nullptr;
+        return nullptr;
+    }
+    return cs[dev];
+}
+
 int side_stream(SideStream* out) {
     static std::mutex mu;
     static std::mutex dev_mu[64];
@@ -714,9 +727,13 @@ int validate_filter(int n, int rho, int H, int W, int kind, float sigma_s, int r
 // hard_labels: the caller's labels (with its centres), or NULL to cluster here (labels in the workspace).
 // n_flagged_host != NULL: read the flag count, the pinv status and (when the clustering ran inside
 // the call) the clustering status back with one synchronisation at the end.
+// nchunks / after_chunk (the host path): the row pass runs in nchunks row chunks and after_chunk(y0, y1)
+// is called once the rows [y0, y1) of g are final (enqueued on st), e.g. to start their copy-out.
+using ChunkFn = std::function<int(int, int)>;
 int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int kind, float sigma_s, int radius,
                float sigma_r, int K, const float* centres, float tau, float* g, int32_t* n_flagged_host, void* ws,
-               size_t ws_bytes, cudaStream_t st, bool hard = false, const int32_t* hard_labels = nullptr) {
+               size_t ws_bytes, cudaStream_t st, bool hard = false, const int32_t* hard_labels = nullptr,
+               int nchunks = 1, const ChunkFn& after_chunk = ChunkFn()) {
     FilterPlan F;
     size_t vsmem = 0;
     int rc = validate_scalars(n, rho, H, W, kind, sigma_r, K, tau, hard);
@@ -885,52 +902,50 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         }
         HDF_CUDA(cudaGetLastError());
     }
-    // F2: row pass + combine + normalise (TMA-fed)
+    // F2 + F3 in row chunks (one chunk unless the host path asks for more, to overlap the copy-out of
+    // finished rows with the rest of the row pass): row pass + combine + normalise (TMA-fed), then the
+    // direct (num)/(den) for the pixels this chunk flagged (R9)
+    CUtensorMap tp, tc;
+    rc = encode3d(&tp, w.planes, (uint64_t)W, (uint64_t)H, (uint64_t)F.P, (uint64_t)F.Wp * 4, (uint64_t)H * F.Wp * 4,
+                  (uint32_t)F.Lbox, (uint32_t)F.RR, (uint32_t)F.NP);
+    if (rc) return rc;
+    rc = encode3d(&tc, w.cpl, (uint64_t)W, (uint64_t)H, (uint64_t)K, (uint64_t)F.Wp * 4, (uint64_t)H * F.Wp * 4,
+                  (uint32_t)hdf::kCoefBox, (uint32_t)F.RR, 1u);
+    if (rc) return rc;
+    hdf::HParams hp;
+    hp.g = g;
+    hp.flag_count = w.flag_count;
+    hp.flag_list = w.flag_list;
+    hp.n = n;
+    hp.NP = F.NP;
+    hp.H = H;
+    hp.W = W;
+    hp.K = K;
+    hp.RR = F.RR;
+    hp.NJW = F.NJW;
+    hp.NWC = F.NWC;
+    hp.NS = F.NS;
+    hp.Lbox = F.Lbox;
+    hp.stage_bytes = F.stage_bytes;
+    hp.planes_bytes = F.planes_bytes;
+    hp.tau_floor = tau * taps[F.Rp] * taps[F.Rp] * 1.0f;   // tau * omega(0) * phi(0)
+    memcpy(hp.taps, taps, sizeof(taps));
+    hdf::FBParams fb;
+    fb.f = f;
+    fb.p = p;
+    fb.g = g;
+    fb.flag_count = w.flag_count;
+    fb.flag_list = w.flag_list;
+    fb.flag_start = nullptr;
+    fb.n = n;
+    fb.rho = rho;
+    fb.H = H;
+    fb.W = W;
+    fb.R = F.Rfb;
+    fb.neg_inv2sr2 = neg_inv2sr2;
+    fb.mu = hard ? centres : nullptr;
+    fb.labels = hard ? hard_labels : nullptr;
     {
-        CUtensorMap tp, tc;
-        rc = encode3d(&tp, w.planes, (uint64_t)W, (uint64_t)H, (uint64_t)F.P, (uint64_t)F.Wp * 4,
-                      (uint64_t)H * F.Wp * 4, (uint32_t)F.Lbox, (uint32_t)F.RR, (uint32_t)F.NP);
-        if (rc) return rc;
-        rc = encode3d(&tc, w.cpl, (uint64_t)W, (uint64_t)H, (uint64_t)K, (uint64_t)F.Wp * 4, (uint64_t)H * F.Wp * 4,
-                      (uint32_t)hdf::kCoefBox, (uint32_t)F.RR, 1u);
-        if (rc) return rc;
-        hdf::HParams hp;
-        hp.g = g;
-        hp.flag_count = w.flag_count;
-        hp.flag_list = w.flag_list;
-        hp.n = n;
-        hp.NP = F.NP;
-        hp.H = H;
-        hp.W = W;
-        hp.K = K;
-        hp.RR = F.RR;
-        hp.NJW = F.NJW;
-        hp.NWC = F.NWC;
-        hp.NS = F.NS;
-        hp.Lbox = F.Lbox;
-        hp.stage_bytes = F.stage_bytes;
-        hp.planes_bytes = F.planes_bytes;
-        hp.tau_floor = tau * taps[F.Rp] * taps[F.Rp] * 1.0f;   // tau * omega(0) * phi(0)
-        memcpy(hp.taps, taps, sizeof(taps));
-        ProfScope prof(HDF_STAGE_HPASS, st);
-        HDF_CUDA(hdf::launch_hpass(F.Rp, F.box, F.hl, st, tp, tc, hp));
-    }
-    // F3: direct (num)/(den) for the flagged pixels (R9)
-    if (tau > 0.f) {
-        hdf::FBParams fb;
-        fb.f = f;
-        fb.p = p;
-        fb.g = g;
-        fb.flag_count = w.flag_count;
-        fb.flag_list = w.flag_list;
-        fb.n = n;
-        fb.rho = rho;
-        fb.H = H;
-        fb.W = W;
-        fb.R = F.Rfb;
-        fb.neg_inv2sr2 = neg_inv2sr2;
-        fb.mu = hard ? centres : nullptr;
-        fb.labels = hard ? hard_labels : nullptr;
         float t2[hdf::kMaxTaps];
         fb.neg_inv2ss2 = 0.f;
         if (F.Rfb <= HDF_MAX_RADIUS) {
@@ -940,18 +955,42 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             fb.neg_inv2ss2 = (float)(-1.0 / (2.0 * (double)sigma_s * (double)sigma_s));
         }
         memcpy(fb.taps, t2, sizeof(t2));
-        ProfScope prof(HDF_STAGE_FALLBACK, st);
-        // one warp per flagged pixel (grid-stride): the count is on the device, so the grid is sized for
-        // the worst case the SMs can hold at once (8 CTAs of 8 warps per SM), capped by the pixel count
-        const long long npix = (long long)H * W;
-        const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((npix + 7) / 8, 8LL * nsm));
-        if (n <= 16) {
-            void (*kfb)(const hdf::FBParams) = n <= 4 ? hdf::k_fallback<4> : hdf::k_fallback<16>;
-            kfb<<<nb, hdf::kFbThreads, 0, st>>>(fb);
-        } else {   // many channels: one CTA per pixel (measured at config 3: 20 us vs 51 us for a warp)
-            hdf::k_fallback_cta<<<(unsigned)std::min<long long>(npix, 16LL * nsm), hdf::kFbCtaThreads, 0, st>>>(fb);
+    }
+    const int row_tiles = (int)F.hl.grid.y;
+    const int nch = std::max(1, std::min(nchunks, row_tiles));
+    int* flag_start = w.status + 2;   // list entries before this chunk (device)
+    for (int ch = 0; ch < nch; ch++) {
+        const int ty0 = (int)((long long)row_tiles * ch / nch), ty1 = (int)((long long)row_tiles * (ch + 1) / nch);
+        hp.ytile0 = ty0;
+        hdf::HLaunch hl = F.hl;
+        hl.grid.y = (unsigned)(ty1 - ty0);
+        if (nch > 1) {
+            HDF_CUDA(cudaMemcpyAsync(flag_start, w.flag_count, sizeof(int), cudaMemcpyDeviceToDevice, st));
+            fb.flag_start = flag_start;
         }
-        HDF_CUDA(cudaGetLastError());
+        {
+            ProfScope prof(HDF_STAGE_HPASS, st);
+            HDF_CUDA(hdf::launch_hpass(F.Rp, F.box, hl, st, tp, tc, hp));
+        }
+        if (tau > 0.f) {
+            ProfScope prof(HDF_STAGE_FALLBACK, st);
+            // one warp per flagged pixel (grid-stride): the count is on the device, so the grid is sized for
+            // the worst case the SMs can hold at once (8 CTAs of 8 warps per SM), capped by the pixel count
+            const long long npix = (long long)H * W;
+            const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((npix + 7) / 8, 8LL * nsm));
+            if (n <= 16) {
+                void (*kfb)(const hdf::FBParams) = n <= 4 ? hdf::k_fallback<4> : hdf::k_fallback<16>;
+                kfb<<<nb, hdf::kFbThreads, 0, st>>>(fb);
+            } else {   // many channels: one CTA per pixel (measured at config 3: 20 us vs 51 us for a warp)
+                hdf::k_fallback_cta<<<(unsigned)std::min<long long>(npix, 16LL * nsm), hdf::kFbCtaThreads, 0, st>>>(
+                    fb);
+            }
+            HDF_CUDA(cudaGetLastError());
+        }
+        if (after_chunk) {
+            rc = after_chunk(std::min(H, ty0 * F.RR), std::min(H, ty1 * F.RR));
+            if (rc) return rc;
+        }
     }
     if (n_flagged_host) {
         HostStage* hs = cluster_here ? crb.hs : host_stage();
@@ -1337,18 +1376,59 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
             rc = launch_cluster(smp, 1, (int)M, rho, K, cd, nullptr, nullptr, w.cluster_ws, st, &crb);
         }
         if (rc) return bail(rc);
+        // the output rows are copied out chunk by chunk on a copy stream while the row pass continues
+        cudaStream_t cs = copy_stream();
+        if (!cs) return bail(fail(HDF_ERR_CUDA, "copy stream creation failed"));
+        constexpr int kChunks = 8;
+        cudaEvent_t evs[kChunks];
+        int nev = 0;
+        auto release = [&]() {
+            for (int e = 0; e < nev; e++) cudaEventDestroy(evs[e]);
+            nev = 0;
+        };
+        const size_t rowf = (size_t)W * n;
+        const bool chunked = (long long)H * W >= (1LL << 20);   // small images: one copy after the filter
+        auto after = [&](int y0, int y1) -> int {
+            if (nev >= kChunks) return fail(HDF_ERR_CUDA, "too many output chunks");
+            cudaEvent_t ev;
+            HDF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            evs[nev++] = ev;
+            HDF_CUDA(cudaEventRecord(ev, st));
+            HDF_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+            ProfScope prof(HDF_STAGE_D2H, cs);
+            HDF_CUDA(cudaMemcpyAsync(g_host + (size_t)y0 * rowf, gd + (size_t)y0 * rowf, sizeof(float) * (size_t)(y1 - y0) * rowf,
+                                     cudaMemcpyDeviceToHost, cs));
+            return HDF_OK;
+        };
         rc = run_filter(fd, n, pdev, rho, H, W, kind, sigma_s, radius, sigma_r, K, cd, tau, gd, nullptr, fws, fbytes,
-                        st);
-        if (rc) return bail(rc);
+                        st, false, nullptr, chunked ? kChunks : 1, after);
+        if (rc) {
+            cudaStreamSynchronize(cs);
+            release();
+            return bail(rc);
+        }
         {
-            ProfScope prof(HDF_STAGE_D2H, st);
-            cudaError_t e = cudaMemcpyAsync(g_host, gd, sizeof(float) * (size_t)H * W * n, cudaMemcpyDeviceToHost, st);
-            if (e == cudaSuccess && centres_host)
+            cudaError_t e = cudaSuccess;
+            if (centres_host)
                 e = cudaMemcpyAsync(centres_host, cd, sizeof(float) * (size_t)K * rho, cudaMemcpyDeviceToHost, st);
             if (e == cudaSuccess) e = cudaMemcpyAsync(hs->hv, w.status, sizeof(hs->hv), cudaMemcpyDeviceToHost, st);
-            if (e != cudaSuccess) return bail(fail(HDF_ERR_CUDA, "output copy: %s", cudaGetErrorString(e)));
+            if (e != cudaSuccess) {
+                cudaStreamSynchronize(cs);
+                release();
+                return bail(fail(HDF_ERR_CUDA, "output copy: %s", cudaGetErrorString(e)));
+            }
         }
-        HDF_CUDA(cudaStreamSynchronize(st));
+        // the caller's stream ends after the last copy (its events / a later sync see the whole call)
+        cudaEvent_t done;
+        if (cudaEventCreateWithFlags(&done, cudaEventDisableTiming) == cudaSuccess) {
+            cudaEventRecord(done, cs);
+            cudaStreamWaitEvent(st, done, 0);
+            cudaEventDestroy(done);
+        }
+        const cudaError_t se = cudaStreamSynchronize(st);
+        cudaStreamSynchronize(cs);
+        release();
+        if (se != cudaSuccess) return fail(HDF_ERR_CUDA, "stream: %s", cudaGetErrorString(se));
         if (n_flagged_host) *n_flagged_host = hs->hv[1];
         rc = cluster_status(crb, K, info_host);   // HDF_ERR_K: g_host holds the padded-centre result
         if (rc) return rc;

@@ -36,6 +36,7 @@ struct HParams {
     int stage_bytes;       // bytes per stage (planes + coef, 128-aligned parts)
     int planes_bytes;      // bytes of the plane part of a stage
     float tau_floor;       // tau * omega(0) * phi(0); <= 0 disables flagging
+    int ytile0;            // first row tile of this launch (the host path launches row chunks)
     float taps[kMaxTaps];
 };
 
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(1024, 1)
     float* den_s = reinterpret_cast<float*>(sm_h + 128);          // [RR][128]
     unsigned char* stages = sm_h + 128 + ((P.RR * kHTW * 4 + 127) & ~127);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int x0 = blockIdx.x * kHTW, y0 = blockIdx.y * P.RR;
+    const int x0 = blockIdx.x * kHTW, y0 = (blockIdx.y + P.ytile0) * P.RR;
 
     if (threadIdx.x == 0) {
         prefetch_tmap(&tm_planes);
@@ -215,6 +216,7 @@ struct FBParams {
     float* g;
     const int* flag_count;
     const int* flag_list;
+    const int* flag_start;     // first list entry to evaluate (device; NULL: 0) -- row chunks of the host path
     int n, rho, H, W, R;
     float neg_inv2sr2;
     float taps[kMaxTaps];
@@ -230,8 +232,9 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(const __grid_constant__
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const int cnt = *P.flag_count;
+    const int t0 = P.flag_start ? *P.flag_start : 0;
     const int side = 2 * P.R + 1, win = side * side;
-    for (int t = gw; t < cnt; t += nw) {
+    for (int t = t0 + gw; t < cnt; t += nw) {
         const int i = P.flag_list[t];
         const int y = i / P.W, x = i % P.W;
         const float* pi = P.labels ? P.mu + (long long)__ldg(P.labels + i) * P.rho : P.p + (long long)i * P.rho;
@@ -298,8 +301,9 @@ static __global__ void __launch_bounds__(kFbCtaThreads) k_fallback_cta(const __g
     __shared__ float dmin_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int cnt = *P.flag_count;
+    const int t0 = P.flag_start ? *P.flag_start : 0;
     const int side = 2 * P.R + 1, win = side * side;
-    for (int t = blockIdx.x; t < cnt; t += gridDim.x) {
+    for (int t = t0 + blockIdx.x; t < cnt; t += gridDim.x) {
         const int i = P.flag_list[t];
         const int y = i / P.W, x = i % P.W;
         const float* pi = P.labels ? P.mu + (long long)__ldg(P.labels + i) * P.rho : P.p + (long long)i * P.rho;

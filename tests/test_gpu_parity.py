@@ -504,7 +504,10 @@ def test_gaussian_iir_constant_image_and_argument_errors(hdf):
 
 # ---- the end-to-end host entry point (bench.py's e2e leg): same kernels, same bits -----------
 @pytest.mark.parametrize("name,H,W,kind", [("c2b", None, None, "gaussian"), ("c1", 61, 77, "gaussian"),
-                                           ("c1", 50, 70, "gaussian_iir"), ("c4", 64, 48, "box")])
+                                           ("c1", 50, 70, "gaussian_iir"), ("c4", 64, 48, "box"),
+                                           # >= 2^20 pixels: the row pass runs in 8 chunks whose rows are
+                                           # copied out while the next chunk computes (flags per chunk)
+                                           ("c2a", 1030, 1100, "gaussian"), ("c4", 1024, 1030, "box")])
 def test_filter_host_equals_device_path(hdf, name, H, W, kind):
     cfg, f, p = synth.make(name, H, W)
     kd = cfg.kind if kind == "box" else kind
