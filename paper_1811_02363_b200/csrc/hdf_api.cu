@@ -17,6 +17,7 @@
 #include "k_bisect.cuh"
 #include "k_coeffs.cuh"
 #include "k_coeffs_tc.cuh"
+#include "k_vpass_tc.cuh"
 #include "k_guide.cuh"
 #include "k_iir.cuh"
 
@@ -814,7 +815,47 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         hdf::VLaunch vl = F.vl;
         vl.smem = vsmem;
         ProfScope prof(HDF_STAGE_VPASS, st);
-        HDF_CUDA(hdf::launch_vpass(F.Rp, F.box, vl, st, vp));
+        // the column FIR on the tensor cores (k_vpass_tc.cuh) for colour images with the Gaussian FIR;
+        // HDF_VPASS_FMA=1 keeps the CUDA-core kernel
+        bool use_tc = !F.box && !F.iir && F.NP == 4 && rho == 3 && F.R >= 4;
+        if (const char* e = getenv("HDF_VPASS_FMA")) {
+            if (atoi(e)) use_tc = false;
+        }
+        if (use_tc) {
+            int* amax = w.status + 3;
+            HDF_CUDA(cudaMemsetAsync(amax, 0, sizeof(int), st));
+            const long long nf = (long long)H * W * n;
+            hdf::k_absmax<<<(unsigned)std::min<long long>((nf + 255) / 256, (long long)nsm * 8), 256, 0, st>>>(f, nf, amax);
+            HDF_CUDA(cudaGetLastError());
+            hdf::VtcParams tp;
+            tp.f = f;
+            tp.p = p;
+            tp.centres = centres;
+            tp.planes = w.planes;
+            tp.absmax = amax;
+            tp.pstride = (long long)H * F.Wp;
+            tp.H = H;
+            tp.W = W;
+            tp.Wp = F.Wp;
+            tp.K = K;
+            tp.R = F.R;
+            tp.nstrip = (W + 31) / 32;
+            const int grid = std::max(1, nsm - 1);
+            const long long ncol = (long long)tp.nstrip * K;
+            const int maxseg = (H + hdf::kVtcRows - 1) / hdf::kVtcRows;
+            tp.nseg = (int)std::max<long long>(1, std::min<long long>(maxseg, (4LL * grid + ncol - 1) / ncol));
+            tp.seglen = ((H + tp.nseg - 1) / tp.nseg + hdf::kVtcRows - 1) / hdf::kVtcRows * hdf::kVtcRows;
+            tp.nseg = (H + tp.seglen - 1) / tp.seglen;
+            tp.neg_inv2sr2 = neg_inv2sr2;
+            for (int t = 0; t < hdf::kMaxTaps; t++) tp.taps[t] = 0.f;
+            for (int t = 0; t <= 2 * F.R; t++) tp.taps[t] = taps[F.Rp - F.R + t];
+            const size_t smem = hdf::vpass_tc_smem(F.R);
+            HDF_CUDA(cudaFuncSetAttribute(hdf::k_range_vpass_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            hdf::k_range_vpass_tc<3><<<(unsigned)std::min<long long>(grid, ncol * tp.nseg), hdf::kVtcThreads, smem, st>>>(tp);
+            HDF_CUDA(cudaGetLastError());
+        } else {
+            HDF_CUDA(hdf::launch_vpass(F.Rp, F.box, vl, st, vp));
+        }
         if (F.iir) {   // NEXT #1: the recursion over the unfiltered planes, columns then rows
             hdf::IIRParams ip = iir_params((double)sigma_s);
             ip.planes = w.planes;
