@@ -817,7 +817,8 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         ProfScope prof(HDF_STAGE_VPASS, st);
         // the column FIR on the tensor cores (k_vpass_tc.cuh) for colour images with the Gaussian FIR;
         // HDF_VPASS_FMA=1 keeps the CUDA-core kernel
-        bool use_tc = !F.box && !F.iir && F.NP == 4 && rho == 3 && F.R >= 4;
+        bool use_tc = !F.box && !F.iir && F.NP == 4 && rho == 3 && f == p && F.R >= 4 && F.R <= hdf::kVtcMaxR &&
+                      (W % 4) == 0;
         if (const char* e = getenv("HDF_VPASS_FMA")) {
             if (atoi(e)) use_tc = false;
         }
@@ -828,8 +829,6 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             hdf::k_absmax<<<(unsigned)std::min<long long>((nf + 255) / 256, (long long)nsm * 8), 256, 0, st>>>(f, nf, amax);
             HDF_CUDA(cudaGetLastError());
             hdf::VtcParams tp;
-            tp.f = f;
-            tp.p = p;
             tp.centres = centres;
             tp.planes = w.planes;
             tp.absmax = amax;
@@ -849,9 +848,14 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             tp.neg_inv2sr2 = neg_inv2sr2;
             for (int t = 0; t < hdf::kMaxTaps; t++) tp.taps[t] = 0.f;
             for (int t = 0; t <= 2 * F.R; t++) tp.taps[t] = taps[F.Rp - F.R + t];
+            CUtensorMap tmp;
+            rc = encode3d(&tmp, const_cast<float*>(p), (uint64_t)W * 3, (uint64_t)H, 1, (uint64_t)W * 3 * 4,
+                          (uint64_t)H * W * 3 * 4, 96u, 64u, 1u);
+            if (rc) return rc;
             const size_t smem = hdf::vpass_tc_smem(F.R);
-            HDF_CUDA(cudaFuncSetAttribute(hdf::k_range_vpass_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            hdf::k_range_vpass_tc<3><<<(unsigned)std::min<long long>(grid, ncol * tp.nseg), hdf::kVtcThreads, smem, st>>>(tp);
+            HDF_CUDA(cudaFuncSetAttribute(hdf::k_range_vpass_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            hdf::k_range_vpass_tc<<<(unsigned)std::min<long long>(grid, ncol * tp.nseg), hdf::kVtcThreads, smem, st>>>(
+                tmp, tp);
             HDF_CUDA(cudaGetLastError());
         } else {
             HDF_CUDA(hdf::launch_vpass(F.Rp, F.box, vl, st, vp));

@@ -15,15 +15,19 @@
 // reduction, k_absmax, so any finite image works).
 //
 // One CTA per SM (persistent over (32-column strip, cluster) columns x row segments, in tiles of 64
-// output rows), warp-specialised and double-buffered:
-//   * producers (warpgroup 0): per tile, z for the Kp input rows of the strip's 32 columns and the
-//     cluster's 4 planes (b_k = exp2(-|p - mu_k|^2 log2(e) / 2 sigma_r^2), u_k = b_k f), split, stored
-//     into the A stage in the canonical K-major no-swizzle layout (8 x 16-byte core matrices; one
-//     16-byte store = 8 consecutive rows of one (plane, column)); arrive on "A full";
-//   * MMA warp (one thread): waits "A full" and "D free", issues 3 Kp/16 MMAs (M = 128, N = 64, K = 16),
-//     commits to "A free" and "D full";
-//   * consumers (warpgroup 1, TMEM lane quarter = plane): load the 64 output rows of their (plane,
-//     column) from TMEM, release the stage, scale back and store (coalesced over the 32 columns).
+// output rows; every unit has the same number of tiles), warp-specialised:
+//   * the MMA warp's lane 0 also streams the raw guide rows of the strip, [64 rows x 32 pixels x 3] per
+//     TMA box (rows outside the image zero-filled), into a ring of 3 slots: a tile reads 2 consecutive
+//     slots (Kp <= 128 rows), the next slot loads while it computes, and each slot is released by the
+//     last tile that reads it;
+//   * producers (8 warps): z for the Kp input rows of the strip's 32 columns and the cluster's 4 planes
+//     (b_k = exp2(-|p - mu_k|^2 log2(e) / 2 sigma_r^2), u_k = b_k f, f = p) from the raw stage, split,
+//     stored into the Z operand in the canonical K-major no-swizzle layout (8 x 16-byte core matrices;
+//     one 16-byte store = 8 consecutive rows of one (plane, column)); arrive on "Z full";
+//   * MMA warp: waits "Z full" and "D free", issues 3 Kp/16 MMAs (M = 128, N = 64, K = 16) and commits
+//     them to "Z free" and "D full" (Z double-buffered in shared memory, D in TMEM);
+//   * consumers (4 warps, TMEM lane quarter = plane): load the 64 output rows of their (plane, column),
+//     release the stage, scale back and store (coalesced over the 32 columns).
 // The Toeplitz operand T (hi, lo) is staged once per CTA.
 #pragma once
 #include <cuda_fp16.h>
@@ -36,24 +40,25 @@ namespace hdf {
 
 constexpr int kVtcRows = 64;       // output rows per tile (UMMA N)
 constexpr int kVtcM = 128;         // (plane, column) pairs per tile (UMMA M): 4 planes x 32 columns
-constexpr int kVtcThreads = 288;   // producers 128 + consumers 128 + MMA warp 32
+constexpr int kVtcProd = 256;      // producer threads (8 warps)
+constexpr int kVtcThreads = kVtcProd + 128 + 64;   // + consumers + MMA warp + TMA warp
 
 inline __host__ __device__ int vtc_kp(int R) { return ((kVtcRows + 2 * R) + 15) & ~15; }
-// Dynamic shared memory: T_hi, T_lo [64][Kp] and two stages of Z_hi, Z_lo [128][Kp] (fp16)
+constexpr int kVtcMaxR = 24;       // Kp <= 112: the shared-memory budget below
+// Dynamic shared memory: T_hi, T_lo [64][Kp], two stages of Z_hi, Z_lo [128][Kp] (fp16), the raw ring
+// [3][64][96] fp32
 inline __host__ __device__ size_t vpass_tc_smem(int R) {
     const int Kp = vtc_kp(R);
-    return (size_t)2 * kVtcRows * Kp * 2 + (size_t)4 * kVtcM * Kp * 2 + 64;
+    return (size_t)2 * kVtcRows * Kp * 2 + (size_t)4 * kVtcM * Kp * 2 + (size_t)3 * 64 * 96 * 4 + 128;
 }
 
 struct VtcParams {
-    const float* f;        // [H][W][3]
-    const float* p;        // [H][W][RHO]
-    const float* centres;  // [K][RHO]
+    const float* centres;  // [K][3]
     float* planes;         // [4K][H][Wp]
     const int* absmax;     // max |f| as float bits (k_absmax)
     long long pstride;     // H * Wp
     int H, W, Wp, K, R;
-    int nstrip, nseg, seglen;   // 32-column strips, row segments per column and their length
+    int nstrip, nseg, seglen;   // 32-column strips, row segments per column and their length (multiple of 64)
     float neg_inv2sr2;     // -1 / (2 sigma_r^2)
     float taps[kMaxTaps];  // w_{-R..R}
 };
@@ -91,17 +96,21 @@ HDF_DEV uint32_t vtc_off(int r, int k, int nrow) {
     return (uint32_t)((k >> 3) * (nrow * 16) + (r >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
 }
 
-template <int RHO>
-__global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_constant__ VtcParams P) {
-    extern __shared__ __align__(128) unsigned char sm_vt[];
-    __shared__ uint64_t a_full[2], a_free[2], d_full[2], d_free[2];
+// f = p, rho = n = 3 (the colour bilateral filter); tm_p: p as [H][3W] fp32, box [96][64]
+__global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_constant__ CUtensorMap tm_p,
+                                                                   const __grid_constant__ VtcParams P) {
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    unsigned char* sm_vt = sm_raw + ((128u - (smem_u32(sm_raw) & 127u)) & 127u);
+    __shared__ uint64_t c_full[3], c_free[3], z_full[2], z_free[2], d_full[2], d_free[2];
     __shared__ uint32_t tmem_base_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int R = P.R, Kp = vtc_kp(R);
     const size_t tbytes = (size_t)kVtcRows * Kp * 2, zbytes = (size_t)kVtcM * Kp * 2;
+    constexpr uint32_t kSlotBytes = 64 * 96 * 4;
     unsigned char* Th = sm_vt;
     unsigned char* Tl = Th + tbytes;
-    unsigned char* Z0 = Tl + tbytes;   // stage s: Z_hi at Z0 + 2 s zbytes, Z_lo after it
+    unsigned char* Z0 = Tl + tbytes;                                 // stage s: Z_hi at Z0 + 2 s zbytes, Z_lo after
+    float* ring = reinterpret_cast<float*>(Z0 + 4 * zbytes);       // [3 slots][64 rows][96]
 
     // the Toeplitz operand: row j (output row), column i (input row): w_{i - j - R}
     for (int e = tid; e < kVtcRows * Kp; e += kVtcThreads) {
@@ -114,9 +123,14 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
         *reinterpret_cast<unsigned short*>(Tl + vtc_off(j, i, kVtcRows)) = l;
     }
     if (tid == 0) {
+        prefetch_tmap(&tm_p);
+        for (int s = 0; s < 3; s++) {
+            mbar_init(&c_full[s], 1);
+            mbar_init(&c_free[s], kVtcProd);
+        }
         for (int s = 0; s < 2; s++) {
-            mbar_init(&a_full[s], 128);
-            mbar_init(&a_free[s], 1);
+            mbar_init(&z_full[s], kVtcProd);
+            mbar_init(&z_free[s], 1);
             mbar_init(&d_full[s], 1);
             mbar_init(&d_free[s], 128);
         }
@@ -138,142 +152,165 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
     int e2;
     frexpf(fmaxf(__int_as_float(*P.absmax), 1e-30f), &e2);   // max |f| <= 2^e2
     const float su = ldexpf(1.f, 14 - e2), sr = 16384.f;
-    const long long ncol = (long long)P.nstrip * P.K;
-    const long long nunit = ncol * P.nseg;
-    // the tile sequence (identical in every role): units u = blockIdx.x + i gridDim.x, each the row segment
-    // [ys, ye) of column (strip, cluster), in tiles of 64 output rows
-    auto unit_rows = [&](long long u, int& strip, int& k, int& ys, int& ye) {
+    // the tile sequence (identical in every role): tile `it` of this CTA is tile j = it % TU of its
+    // unit number ui = it / TU, unit u = blockIdx.x + ui gridDim.x = the row segment of column (strip,
+    // cluster).  The raw rows of a unit are its chunks c = 0 .. TU (64 rows each, from ys - R); the
+    // CTA's chunk sequence number is g = ui (TU + 1) + c, ring slot g % 3, and tile j reads chunks j, j+1.
+    const long long nunit = (long long)P.nstrip * P.K * P.nseg;
+    const int TU = P.seglen / kVtcRows;
+    const long long nui = nunit > blockIdx.x ? (nunit - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long long nit = nui * TU;
+    auto unit_of = [&](long long ui, int& strip, int& k, int& ys) {
+        const long long u = blockIdx.x + ui * (long long)gridDim.x;
         const long long col = u / P.nseg;
         const int seg = (int)(u - col * P.nseg);
         strip = (int)(col % P.nstrip);
         k = (int)(col / P.nstrip);
         ys = seg * P.seglen;
-        ye = min(P.H, ys + P.seglen);
     };
 
-    if (warp < 4) {   // ---------------------------------------------------------- producers ----------
+    if (warp < kVtcProd / 32) {   // ------------------------------------------------ producers -------
         const int col = tid & 31, cg = tid >> 5;   // this thread's column and first 8-row chunk
         const float c2 = P.neg_inv2sr2 * 1.4426950408889634f;
-        int it = 0;
-        for (long long u = blockIdx.x; u < nunit; u += gridDim.x) {
-            int strip, k, ys, ye;
-            unit_rows(u, strip, k, ys, ye);
-            const int x = strip * 32 + col;
-            const bool xok = x < P.W;
-            float mu[RHO];
+        for (long long it = 0; it < nit; it++) {
+            const long long ui = it / TU;
+            const int j = (int)(it - ui * TU);
+            int strip, k, ys;
+            unit_of(ui, strip, k, ys);
+            const int yt = ys + j * kVtcRows;
+            const int s = (int)(it & 1);
+            const bool xok = strip * 32 + col < P.W;
+            const float m0 = __ldg(P.centres + k * 3), m1 = __ldg(P.centres + k * 3 + 1),
+                        m2 = __ldg(P.centres + k * 3 + 2);
+            const long long ga = ui * (TU + 1) + j, gb = ga + 1;
+            mbar_wait(&c_full[ga % 3], (uint32_t)(ga / 3) & 1u);
+            mbar_wait(&c_full[gb % 3], (uint32_t)(gb / 3) & 1u);
+            mbar_wait(&z_free[s], ((uint32_t)(it >> 1) & 1u) ^ 1u);   // the MMAs of tile it - 2 have read Z[s]
+            const float* slot_a = ring + (size_t)(ga % 3) * (64 * 96) + col * 3;
+            const float* slot_b = ring + (size_t)(gb % 3) * (64 * 96) + col * 3;
+            unsigned char* Zh = Z0 + 2 * s * zbytes;
+            unsigned char* Zl = Zh + zbytes;
+            for (int ch = cg; ch < Kp / 8; ch += kVtcProd / 32) {
+                unsigned short hv[4][8], lv[4][8];
+                const float* sl = (ch < 8) ? slot_a : slot_b;
 #pragma unroll
-            for (int d = 0; d < RHO; d++) mu[d] = __ldg(P.centres + k * RHO + d);
-            for (int yt = ys; yt < ye; yt += kVtcRows, it++) {
-                const int s = it & 1;
-                const uint32_t ph = (uint32_t)(it >> 1) & 1u;
-                mbar_wait(&a_free[s], ph ^ 1u);   // the MMAs of tile it - 2 have read Z[s]
-                unsigned char* Zh = Z0 + 2 * s * zbytes;
-                unsigned char* Zl = Zh + zbytes;
-                for (int ch = cg; ch < Kp / 8; ch += 4) {
-                    unsigned short hv[4][8], lv[4][8];
-#pragma unroll
-                    for (int r = 0; r < 8; r++) {
-                        const int i = ch * 8 + r;             // input row index within the tile
-                        const int yy = yt - R + i;
-                        const bool ok = xok && i < kVtcRows + 2 * R && yy >= 0 && yy < P.H;
-                        float pv[RHO], fv[3];
-                        const long long pix = ok ? (long long)yy * P.W + x : 0;
-#pragma unroll
-                        for (int d = 0; d < RHO; d++) pv[d] = ok ? __ldg(P.p + pix * RHO + d) : 0.f;
-#pragma unroll
-                        for (int c = 0; c < 3; c++) fv[c] = (RHO == 3 && P.f == P.p) ? pv[c] : (ok ? __ldg(P.f + pix * 3 + c) : 0.f);
-                        float d2 = 0.f;
-#pragma unroll
-                        for (int d = 0; d < RHO; d++) {
-                            const float t = pv[d] - mu[d];
-                            d2 = fmaf(t, t, d2);
-                        }
-                        float b;
-                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
-                        b = ok ? b : 0.f;
-                        const float bu = b * su;
-#pragma unroll
-                        for (int c = 0; c < 3; c++) split_f16(bu * fv[c], hv[c][r], lv[c][r]);
-                        split_f16(b * sr, hv[3][r], lv[3][r]);
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        const uint32_t off = vtc_off(q * 32 + col, ch * 8, kVtcM);
-                        uint4 h4, l4;
-                        h4.x = hv[q][0] | ((uint32_t)hv[q][1] << 16);
-                        h4.y = hv[q][2] | ((uint32_t)hv[q][3] << 16);
-                        h4.z = hv[q][4] | ((uint32_t)hv[q][5] << 16);
-                        h4.w = hv[q][6] | ((uint32_t)hv[q][7] << 16);
-                        l4.x = lv[q][0] | ((uint32_t)lv[q][1] << 16);
-                        l4.y = lv[q][2] | ((uint32_t)lv[q][3] << 16);
-                        l4.z = lv[q][4] | ((uint32_t)lv[q][5] << 16);
-                        l4.w = lv[q][6] | ((uint32_t)lv[q][7] << 16);
-                        *reinterpret_cast<uint4*>(Zh + off) = h4;
-                        *reinterpret_cast<uint4*>(Zl + off) = l4;
-                    }
+                for (int r = 0; r < 8; r++) {
+                    const int i = ch * 8 + r;   // input row within the tile (zero-filled outside the image)
+                    const float* px = sl + (i & 63) * 96;
+                    const float p0 = px[0], p1 = px[1], p2 = px[2];
+                    const float t0 = p0 - m0, t1 = p1 - m1, t2 = p2 - m2;
+                    const float d2 = fmaf(t2, t2, fmaf(t1, t1, t0 * t0));
+                    float b;
+                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
+                    const int yy = yt - R + i;
+                    b = (xok && i < kVtcRows + 2 * R && yy >= 0 && yy < P.H) ? b : 0.f;
+                    const float bu = b * su;
+                    split_f16(bu * p0, hv[0][r], lv[0][r]);
+                    split_f16(bu * p1, hv[1][r], lv[1][r]);
+                    split_f16(bu * p2, hv[2][r], lv[2][r]);
+                    split_f16(b * sr, hv[3][r], lv[3][r]);
                 }
-                fence_proxy_async();   // generic-proxy writes of Z[s] -> visible to the tensor core
-                mbar_arrive(&a_full[s]);
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const uint32_t off = vtc_off(q * 32 + col, ch * 8, kVtcM);
+                    uint4 h4, l4;
+                    h4.x = hv[q][0] | ((uint32_t)hv[q][1] << 16);
+                    h4.y = hv[q][2] | ((uint32_t)hv[q][3] << 16);
+                    h4.z = hv[q][4] | ((uint32_t)hv[q][5] << 16);
+                    h4.w = hv[q][6] | ((uint32_t)hv[q][7] << 16);
+                    l4.x = lv[q][0] | ((uint32_t)lv[q][1] << 16);
+                    l4.y = lv[q][2] | ((uint32_t)lv[q][3] << 16);
+                    l4.z = lv[q][4] | ((uint32_t)lv[q][5] << 16);
+                    l4.w = lv[q][6] | ((uint32_t)lv[q][7] << 16);
+                    *reinterpret_cast<uint4*>(Zh + off) = h4;
+                    *reinterpret_cast<uint4*>(Zl + off) = l4;
+                }
             }
+            // chunk j has no later reader in this unit (tile j + 1 reads j + 1, j + 2); the last tile also
+            // releases chunk j + 1
+            mbar_arrive(&c_free[ga % 3]);
+            if (j == TU - 1) mbar_arrive(&c_free[gb % 3]);
+            fence_proxy_async();   // generic-proxy writes of Z[s] -> visible to the tensor core
+            mbar_arrive(&z_full[s]);
         }
-    } else if (warp < 8) {   // ---------------------------------------------------- consumers ------
+    } else if (warp < kVtcProd / 32 + 4) {   // -------------------------------------- consumers -------
         const int q = warp & 3, col = lane;   // TMEM lane quarter q = plane q, lane = column
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         const float inv = (q < 3) ? 1.f / su : 1.f / sr;   // exact (powers of two)
-        int it = 0;
-        for (long long u = blockIdx.x; u < nunit; u += gridDim.x) {
-            int strip, k, ys, ye;
-            unit_rows(u, strip, k, ys, ye);
+        for (long long it = 0; it < nit; it++) {
+            const long long ui = it / TU;
+            const int j = (int)(it - ui * TU);
+            int strip, k, ys;
+            unit_of(ui, strip, k, ys);
+            const int yt = ys + j * kVtcRows;
+            const int s = (int)(it & 1);
             const int x = strip * 32 + col;
-            float* out = P.planes + (long long)(4 * k + q) * P.pstride + x;
-            for (int yt = ys; yt < ye; yt += kVtcRows, it++) {
-                const int s = it & 1;
-                const uint32_t ph = (uint32_t)(it >> 1) & 1u;
-                mbar_wait(&d_full[s], ph);
-                tc_fence_after();
-                float v[kVtcRows];
+            mbar_wait(&d_full[s], (uint32_t)(it >> 1) & 1u);
+            tc_fence_after();
+            float v[kVtcRows];
 #pragma unroll
-                for (int n0 = 0; n0 < kVtcRows; n0 += 16) {
-                    float t16[16];
-                    tmem_ld16(tbase + lane_base + (uint32_t)(s * kVtcRows + n0), t16);
+            for (int n0 = 0; n0 < kVtcRows; n0 += 16) {
+                float t16[16];
+                tmem_ld16(tbase + lane_base + (uint32_t)(s * kVtcRows + n0), t16);
 #pragma unroll
-                    for (int j = 0; j < 16; j++) v[n0 + j] = t16[j];
-                }
-                tc_fence_before();
-                mbar_arrive(&d_free[s]);
-                if (x < P.W) {
-                    const int nr = min(kVtcRows, ye - yt);
+                for (int jj = 0; jj < 16; jj++) v[n0 + jj] = t16[jj];
+            }
+            tc_fence_before();
+            mbar_arrive(&d_free[s]);
+            if (x < P.W && yt < P.H) {
+                const int nr = min(kVtcRows, P.H - yt);
+                float* o = P.planes + (long long)(4 * k + q) * P.pstride + (long long)yt * P.Wp + x;
+                const int step = P.Wp;
+                if (nr == kVtcRows) {   // whole tile: a running pointer, no per-row predicate
 #pragma unroll
-                    for (int j = 0; j < kVtcRows; j++)
-                        if (j < nr) out[(long long)(yt + j) * P.Wp] = v[j] * inv;
+                    for (int jj = 0; jj < kVtcRows; jj++) {
+                        o[0] = v[jj] * inv;
+                        o += step;
+                    }
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < kVtcRows; jj++) {
+                        if (jj < nr) o[0] = v[jj] * inv;
+                        o += step;
+                    }
                 }
             }
         }
-    } else if (lane == 0) {   // -------------------------------------------------- MMA warp ------
-        const uint32_t idesc = umma_idesc_f16(kVtcM, kVtcRows);
-        const uint32_t tH = smem_u32(Th), tL = smem_u32(Tl);
-        const uint32_t lboZ = kVtcM * 16, lboT = kVtcRows * 16, sbo = 128;
-        int it = 0;
-        for (long long u = blockIdx.x; u < nunit; u += gridDim.x) {
-            int strip, k, ys, ye;
-            unit_rows(u, strip, k, ys, ye);
-            for (int yt = ys; yt < ye; yt += kVtcRows, it++) {
-                const int s = it & 1;
-                const uint32_t ph = (uint32_t)(it >> 1) & 1u;
-                mbar_wait(&a_full[s], ph);
-                mbar_wait(&d_free[s], ph ^ 1u);
+    } else if (warp == kVtcProd / 32 + 4) {   // -------------------------------------- MMA warp ---------
+        if (lane == 0) {
+            const uint32_t idesc = umma_idesc_f16(kVtcM, kVtcRows);
+            const uint32_t tH = smem_u32(Th), tL = smem_u32(Tl);
+            const uint32_t lboZ = kVtcM * 16, lboT = kVtcRows * 16, sbo = 128;
+            for (long long it = 0; it < nit; it++) {
+                const int s = (int)(it & 1);
+                mbar_wait(&z_full[s], (uint32_t)(it >> 1) & 1u);
+                mbar_wait(&d_free[s], ((uint32_t)(it >> 1) & 1u) ^ 1u);
                 tc_fence_after();
                 const uint32_t zH = smem_u32(Z0 + 2 * s * zbytes), zL = zH + (uint32_t)zbytes;
                 const uint32_t td = tbase + (uint32_t)(s * kVtcRows);
                 for (int ks = 0; ks < Kp / 16; ks++) {
                     const uint32_t oz = (uint32_t)ks * 2u * lboZ, ot = (uint32_t)ks * 2u * lboT;
-                    umma_f16(td, umma_desc(zL + oz, lboZ, sbo), umma_desc(tH + ot, lboT, sbo), idesc, ks > 0 ? 1u : 0u);
+                    umma_f16(td, umma_desc(zL + oz, lboZ, sbo), umma_desc(tH + ot, lboT, sbo), idesc,
+                             ks > 0 ? 1u : 0u);
                     umma_f16(td, umma_desc(zH + oz, lboZ, sbo), umma_desc(tL + ot, lboT, sbo), idesc, 1u);
                     umma_f16(td, umma_desc(zH + oz, lboZ, sbo), umma_desc(tH + ot, lboT, sbo), idesc, 1u);
                 }
-                umma_commit(&a_free[s]);
+                umma_commit(&z_free[s]);
                 umma_commit(&d_full[s]);
             }
+        }
+    } else if (lane == 0) {   // ------------------------------------------------------- TMA warp -----
+        // the CTA's raw chunks in order; chunk g waits for the release of chunk g - 3 (its ring slot)
+        const long long nchunk = nui * (TU + 1);
+        for (long long g = 0; g < nchunk; g++) {
+            const long long ui = g / (TU + 1);
+            const int c = (int)(g - ui * (TU + 1));
+            int strip, k, ys;
+            unit_of(ui, strip, k, ys);
+            const int sl = (int)(g % 3);
+            if (g >= 3) mbar_wait(&c_free[sl], (uint32_t)((g / 3) - 1) & 1u);
+            mbar_arrive_expect_tx(&c_full[sl], kSlotBytes);
+            tma_load_3d(ring + (size_t)sl * (64 * 96), &tm_p, &c_full[sl], strip * 96, ys - R + 64 * c, 0);
         }
     }
     tc_fence_before();
