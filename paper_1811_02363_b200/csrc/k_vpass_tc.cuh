@@ -90,6 +90,16 @@ HDF_DEV void split_f16(float x, unsigned short& hi, unsigned short& lo) {
     lo = __half_as_ushort(__float2half_rn(x - __half2float(h)));
 }
 
+// packed split of two values (rows r, r + 1 of one operand column): the 32-bit words of hi and lo
+// (one cvt.rn.f16x2.f32 each; the conversions stay off the transcendental pipe)
+HDF_DEV void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
 // Byte offset of (row r, k) in an operand of nrow rows (multiple of 8) and Kp columns, K-major, no
 // swizzle, layout "m-groups adjacent": core matrix (r / 8, k / 8) at (k / 8) * (nrow * 16) + (r / 8) * 128.
 HDF_DEV uint32_t vtc_off(int r, int k, int nrow) {
@@ -172,106 +182,105 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
     if (warp < kVtcProd / 32) {   // ------------------------------------------------ producers -------
         const int col = tid & 31, cg = tid >> 5;   // this thread's column and first 8-row chunk
         const float c2 = P.neg_inv2sr2 * 1.4426950408889634f;
-        for (long long it = 0; it < nit; it++) {
-            const long long ui = it / TU;
-            const int j = (int)(it - ui * TU);
+        long long it = 0;
+        for (long long ui = 0; ui < nui; ui++) {
             int strip, k, ys;
             unit_of(ui, strip, k, ys);
-            const int yt = ys + j * kVtcRows;
-            const int s = (int)(it & 1);
             const bool xok = strip * 32 + col < P.W;
             const float m0 = __ldg(P.centres + k * 3), m1 = __ldg(P.centres + k * 3 + 1),
                         m2 = __ldg(P.centres + k * 3 + 2);
-            const long long ga = ui * (TU + 1) + j, gb = ga + 1;
-            mbar_wait(&c_full[ga % 3], (uint32_t)(ga / 3) & 1u);
-            mbar_wait(&c_full[gb % 3], (uint32_t)(gb / 3) & 1u);
-            mbar_wait(&z_free[s], ((uint32_t)(it >> 1) & 1u) ^ 1u);   // the MMAs of tile it - 2 have read Z[s]
-            const float* slot_a = ring + (size_t)(ga % 3) * (64 * 96) + col * 3;
-            const float* slot_b = ring + (size_t)(gb % 3) * (64 * 96) + col * 3;
-            unsigned char* Zh = Z0 + 2 * s * zbytes;
-            unsigned char* Zl = Zh + zbytes;
-            for (int ch = cg; ch < Kp / 8; ch += kVtcProd / 32) {
-                unsigned short hv[4][8], lv[4][8];
-                const float* sl = (ch < 8) ? slot_a : slot_b;
+            for (int j = 0; j < TU; j++, it++) {
+                const int yt = ys + j * kVtcRows;
+                const int s = (int)(it & 1);
+                const long long ga = ui * (TU + 1) + j, gb = ga + 1;
+                mbar_wait(&c_full[ga % 3], (uint32_t)(ga / 3) & 1u);
+                mbar_wait(&c_full[gb % 3], (uint32_t)(gb / 3) & 1u);
+                mbar_wait(&z_free[s], ((uint32_t)(it >> 1) & 1u) ^ 1u);   // the MMAs of tile it - 2 have read Z[s]
+                const float* slot_a = ring + (size_t)(ga % 3) * (64 * 96) + col * 3;
+                const float* slot_b = ring + (size_t)(gb % 3) * (64 * 96) + col * 3;
+                unsigned char* Zh = Z0 + 2 * s * zbytes;
+                unsigned char* Zl = Zh + zbytes;
+                for (int ch = cg; ch < Kp / 8; ch += kVtcProd / 32) {
+                    float zv[4][8];
+                    const float* sl = (ch < 8) ? slot_a : slot_b;
 #pragma unroll
-                for (int r = 0; r < 8; r++) {
-                    const int i = ch * 8 + r;   // input row within the tile (zero-filled outside the image)
-                    const float* px = sl + (i & 63) * 96;
-                    const float p0 = px[0], p1 = px[1], p2 = px[2];
-                    const float t0 = p0 - m0, t1 = p1 - m1, t2 = p2 - m2;
-                    const float d2 = fmaf(t2, t2, fmaf(t1, t1, t0 * t0));
-                    float b;
-                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
-                    const int yy = yt - R + i;
-                    b = (xok && i < kVtcRows + 2 * R && yy >= 0 && yy < P.H) ? b : 0.f;
-                    const float bu = b * su;
-                    split_f16(bu * p0, hv[0][r], lv[0][r]);
-                    split_f16(bu * p1, hv[1][r], lv[1][r]);
-                    split_f16(bu * p2, hv[2][r], lv[2][r]);
-                    split_f16(b * sr, hv[3][r], lv[3][r]);
-                }
+                    for (int r = 0; r < 8; r++) {
+                        const int i = ch * 8 + r;   // input row within the tile (zero-filled outside the image)
+                        const float* px = sl + (i & 63) * 96;
+                        const float p0 = px[0], p1 = px[1], p2 = px[2];
+                        const float t0 = p0 - m0, t1 = p1 - m1, t2 = p2 - m2;
+                        const float d2 = fmaf(t2, t2, fmaf(t1, t1, t0 * t0));
+                        float b;
+                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
+                        const int yy = yt - R + i;
+                        b = (xok && i < kVtcRows + 2 * R && yy >= 0 && yy < P.H) ? b : 0.f;
+                        const float bu = b * su;
+                        zv[0][r] = bu * p0;
+                        zv[1][r] = bu * p1;
+                        zv[2][r] = bu * p2;
+                        zv[3][r] = b * sr;
+                    }
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const uint32_t off = vtc_off(q * 32 + col, ch * 8, kVtcM);
-                    uint4 h4, l4;
-                    h4.x = hv[q][0] | ((uint32_t)hv[q][1] << 16);
-                    h4.y = hv[q][2] | ((uint32_t)hv[q][3] << 16);
-                    h4.z = hv[q][4] | ((uint32_t)hv[q][5] << 16);
-                    h4.w = hv[q][6] | ((uint32_t)hv[q][7] << 16);
-                    l4.x = lv[q][0] | ((uint32_t)lv[q][1] << 16);
-                    l4.y = lv[q][2] | ((uint32_t)lv[q][3] << 16);
-                    l4.z = lv[q][4] | ((uint32_t)lv[q][5] << 16);
-                    l4.w = lv[q][6] | ((uint32_t)lv[q][7] << 16);
-                    *reinterpret_cast<uint4*>(Zh + off) = h4;
-                    *reinterpret_cast<uint4*>(Zl + off) = l4;
+                    for (int q = 0; q < 4; q++) {
+                        const uint32_t off = vtc_off(q * 32 + col, ch * 8, kVtcM);
+                        uint4 h4, l4;
+                        split_f16x2(zv[q][0], zv[q][1], h4.x, l4.x);
+                        split_f16x2(zv[q][2], zv[q][3], h4.y, l4.y);
+                        split_f16x2(zv[q][4], zv[q][5], h4.z, l4.z);
+                        split_f16x2(zv[q][6], zv[q][7], h4.w, l4.w);
+                        *reinterpret_cast<uint4*>(Zh + off) = h4;
+                        *reinterpret_cast<uint4*>(Zl + off) = l4;
+                    }
                 }
+                // chunk j has no later reader in this unit (tile j + 1 reads j + 1, j + 2); the last tile
+                // also releases chunk j + 1
+                mbar_arrive(&c_free[ga % 3]);
+                if (j == TU - 1) mbar_arrive(&c_free[gb % 3]);
+                fence_proxy_async();   // generic-proxy writes of Z[s] -> visible to the tensor core
+                mbar_arrive(&z_full[s]);
             }
-            // chunk j has no later reader in this unit (tile j + 1 reads j + 1, j + 2); the last tile also
-            // releases chunk j + 1
-            mbar_arrive(&c_free[ga % 3]);
-            if (j == TU - 1) mbar_arrive(&c_free[gb % 3]);
-            fence_proxy_async();   // generic-proxy writes of Z[s] -> visible to the tensor core
-            mbar_arrive(&z_full[s]);
         }
     } else if (warp < kVtcProd / 32 + 4) {   // -------------------------------------- consumers -------
         const int q = warp & 3, col = lane;   // TMEM lane quarter q = plane q, lane = column
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         const float inv = (q < 3) ? 1.f / su : 1.f / sr;   // exact (powers of two)
-        for (long long it = 0; it < nit; it++) {
-            const long long ui = it / TU;
-            const int j = (int)(it - ui * TU);
+        const int step = P.Wp;
+        long long it = 0;
+        for (long long ui = 0; ui < nui; ui++) {
             int strip, k, ys;
             unit_of(ui, strip, k, ys);
-            const int yt = ys + j * kVtcRows;
-            const int s = (int)(it & 1);
             const int x = strip * 32 + col;
-            mbar_wait(&d_full[s], (uint32_t)(it >> 1) & 1u);
-            tc_fence_after();
-            float v[kVtcRows];
+            float* base = P.planes + (long long)(4 * k + q) * P.pstride + x;
+            for (int j = 0; j < TU; j++, it++) {
+                const int yt = ys + j * kVtcRows;
+                const int s = (int)(it & 1);
+                mbar_wait(&d_full[s], (uint32_t)(it >> 1) & 1u);
+                tc_fence_after();
+                float v[kVtcRows];
 #pragma unroll
-            for (int n0 = 0; n0 < kVtcRows; n0 += 16) {
-                float t16[16];
-                tmem_ld16(tbase + lane_base + (uint32_t)(s * kVtcRows + n0), t16);
+                for (int n0 = 0; n0 < kVtcRows; n0 += 16) {
+                    float t16[16];
+                    tmem_ld16(tbase + lane_base + (uint32_t)(s * kVtcRows + n0), t16);
 #pragma unroll
-                for (int jj = 0; jj < 16; jj++) v[n0 + jj] = t16[jj];
-            }
-            tc_fence_before();
-            mbar_arrive(&d_free[s]);
-            if (x < P.W && yt < P.H) {
-                const int nr = min(kVtcRows, P.H - yt);
-                float* o = P.planes + (long long)(4 * k + q) * P.pstride + (long long)yt * P.Wp + x;
-                const int step = P.Wp;
-                if (nr == kVtcRows) {   // whole tile: a running pointer, no per-row predicate
+                    for (int jj = 0; jj < 16; jj++) v[n0 + jj] = t16[jj];
+                }
+                tc_fence_before();
+                mbar_arrive(&d_free[s]);
+                if (x < P.W && yt < P.H) {
+                    const int nr = min(kVtcRows, P.H - yt);
+                    float* o = base + (long long)yt * step;
+                    if (nr == kVtcRows) {   // whole tile: a running pointer, no per-row predicate
 #pragma unroll
-                    for (int jj = 0; jj < kVtcRows; jj++) {
-                        o[0] = v[jj] * inv;
-                        o += step;
-                    }
-                } else {
+                        for (int jj = 0; jj < kVtcRows; jj++) {
+                            o[0] = v[jj] * inv;
+                            o += step;
+                        }
+                    } else {
 #pragma unroll
-                    for (int jj = 0; jj < kVtcRows; jj++) {
-                        if (jj < nr) o[0] = v[jj] * inv;
-                        o += step;
+                        for (int jj = 0; jj < kVtcRows; jj++) {
+                            if (jj < nr) o[0] = v[jj] * inv;
+                            o += step;
+                        }
                     }
                 }
             }
