@@ -45,11 +45,14 @@ constexpr int kVtcThreads = kVtcProd + 128 + 64;   // + consumers + MMA warp + T
 
 inline __host__ __device__ int vtc_kp(int R) { return ((kVtcRows + 2 * R) + 15) & ~15; }
 constexpr int kVtcMaxR = 24;       // Kp <= 112: the shared-memory budget below
-// Dynamic shared memory: T_hi, T_lo [64][Kp], two stages of Z_hi, Z_lo [128][Kp] (fp16), the raw ring
-// [3][64][96] fp32
+constexpr int kVtcZChunks = 22;    // Z ring: 8-row chunks (a tile reads Kp / 8 <= 14, the next tile's 8 new
+                                   // ones are written meanwhile; even, so a 16-row K step never wraps)
+constexpr int kVtcZChunkBytes = kVtcM * 8 * 2;
+// Dynamic shared memory: T_hi, T_lo [64][Kp], the Z ring hi and lo [22 chunks][128][8] (fp16), the raw
+// ring [3][64][96] fp32
 inline __host__ __device__ size_t vpass_tc_smem(int R) {
     const int Kp = vtc_kp(R);
-    return (size_t)2 * kVtcRows * Kp * 2 + (size_t)4 * kVtcM * Kp * 2 + (size_t)3 * 64 * 96 * 4 + 128;
+    return (size_t)2 * kVtcRows * Kp * 2 + (size_t)2 * kVtcZChunks * kVtcZChunkBytes + (size_t)3 * 64 * 96 * 4 + 128;
 }
 
 struct VtcParams {
@@ -119,8 +122,10 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
     constexpr uint32_t kSlotBytes = 64 * 96 * 4;
     unsigned char* Th = sm_vt;
     unsigned char* Tl = Th + tbytes;
-    unsigned char* Z0 = Tl + tbytes;                                 // stage s: Z_hi at Z0 + 2 s zbytes, Z_lo after
-    float* ring = reinterpret_cast<float*>(Z0 + 4 * zbytes);       // [3 slots][64 rows][96]
+    unsigned char* ZH = Tl + tbytes;                                          // Z ring, hi
+    unsigned char* ZL = ZH + (size_t)kVtcZChunks * kVtcZChunkBytes;            // Z ring, lo
+    float* ring = reinterpret_cast<float*>(ZL + (size_t)kVtcZChunks * kVtcZChunkBytes);   // [3][64][96]
+    (void)zbytes;
 
     // the Toeplitz operand: row j (output row), column i (input row): w_{i - j - R}
     for (int e = tid; e < kVtcRows * Kp; e += kVtcThreads) {
@@ -191,16 +196,23 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                         m2 = __ldg(P.centres + k * 3 + 2);
             for (int j = 0; j < TU; j++, it++) {
                 const int yt = ys + j * kVtcRows;
-                const int s = (int)(it & 1);
                 const long long ga = ui * (TU + 1) + j, gb = ga + 1;
                 mbar_wait(&c_full[ga % 3], (uint32_t)(ga / 3) & 1u);
                 mbar_wait(&c_full[gb % 3], (uint32_t)(gb / 3) & 1u);
-                mbar_wait(&z_free[s], ((uint32_t)(it >> 1) & 1u) ^ 1u);   // the MMAs of tile it - 2 have read Z[s]
+                // Z chunks of this unit: c = 0 .. 8 TU + 5 (tile j reads 8j .. 8j + Kp/8 - 1).  Tile j writes
+                // the chunks no earlier tile wrote: all Kp/8 for j = 0, else 8j + Kp/8 - 8 .. 8j + Kp/8 - 1.
+                // Their ring slots were last read by tile it - 2 (it - 1 at a unit's first tile).
+                const long long zg0 = ui * (8LL * TU + 6);   // the unit's first chunk (global, even)
+                const int c0 = (j == 0) ? 0 : 8 * j + Kp / 8 - 8, c1 = 8 * j + Kp / 8;
+                if (j == 0) {
+                    if (it >= 1) mbar_wait(&z_free[(it - 1) & 1], (uint32_t)((it - 1) >> 1) & 1u);
+                } else if (it >= 2) {
+                    mbar_wait(&z_free[it & 1], (uint32_t)((it - 2) >> 1) & 1u);
+                }
                 const float* slot_a = ring + (size_t)(ga % 3) * (64 * 96) + col * 3;
                 const float* slot_b = ring + (size_t)(gb % 3) * (64 * 96) + col * 3;
-                unsigned char* Zh = Z0 + 2 * s * zbytes;
-                unsigned char* Zl = Zh + zbytes;
-                for (int ch = cg; ch < Kp / 8; ch += kVtcProd / 32) {
+                for (int cc = c0 + cg; cc < c1; cc += kVtcProd / 32) {
+                    const int ch = cc - 8 * j;   // 8-row chunk within the tile
                     float zv[4][8];
                     const float* sl = (ch < 8) ? slot_a : slot_b;
 #pragma unroll
@@ -213,31 +225,32 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                         float b;
                         asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
                         const int yy = yt - R + i;
-                        b = (xok && i < kVtcRows + 2 * R && yy >= 0 && yy < P.H) ? b : 0.f;
+                        b = (xok && yy >= 0 && yy < P.H) ? b : 0.f;   // (rows past 64 + 2R: T is zero there; a chunk may be shared with the next tile)
                         const float bu = b * su;
                         zv[0][r] = bu * p0;
                         zv[1][r] = bu * p1;
                         zv[2][r] = bu * p2;
                         zv[3][r] = b * sr;
                     }
+                    const size_t zoff = (size_t)((zg0 + cc) % kVtcZChunks) * kVtcZChunkBytes;
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
-                        const uint32_t off = vtc_off(q * 32 + col, ch * 8, kVtcM);
+                        const uint32_t off = (uint32_t)(((q * 32 + col) >> 3) * 128 + (col & 7) * 16);
                         uint4 h4, l4;
                         split_f16x2(zv[q][0], zv[q][1], h4.x, l4.x);
                         split_f16x2(zv[q][2], zv[q][3], h4.y, l4.y);
                         split_f16x2(zv[q][4], zv[q][5], h4.z, l4.z);
                         split_f16x2(zv[q][6], zv[q][7], h4.w, l4.w);
-                        *reinterpret_cast<uint4*>(Zh + off) = h4;
-                        *reinterpret_cast<uint4*>(Zl + off) = l4;
+                        *reinterpret_cast<uint4*>(ZH + zoff + off) = h4;
+                        *reinterpret_cast<uint4*>(ZL + zoff + off) = l4;
                     }
                 }
-                // chunk j has no later reader in this unit (tile j + 1 reads j + 1, j + 2); the last tile
+                // raw chunk j has no later reader in this unit (tile j + 1 reads j + 1, j + 2); the last tile
                 // also releases chunk j + 1
                 mbar_arrive(&c_free[ga % 3]);
                 if (j == TU - 1) mbar_arrive(&c_free[gb % 3]);
-                fence_proxy_async();   // generic-proxy writes of Z[s] -> visible to the tensor core
-                mbar_arrive(&z_full[s]);
+                fence_proxy_async();   // generic-proxy writes of Z -> visible to the tensor core
+                mbar_arrive(&z_full[it & 1]);
             }
         }
     } else if (warp < kVtcProd / 32 + 4) {   // -------------------------------------- consumers -------
@@ -289,16 +302,20 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
         if (lane == 0) {
             const uint32_t idesc = umma_idesc_f16(kVtcM, kVtcRows);
             const uint32_t tH = smem_u32(Th), tL = smem_u32(Tl);
-            const uint32_t lboZ = kVtcM * 16, lboT = kVtcRows * 16, sbo = 128;
+            const uint32_t lboZ = kVtcZChunkBytes, lboT = kVtcRows * 16, sbo = 128;
+            const uint32_t zH = smem_u32(ZH), zL = smem_u32(ZL);
             for (long long it = 0; it < nit; it++) {
                 const int s = (int)(it & 1);
+                const long long ui = it / TU;
+                const int j = (int)(it - ui * TU);
+                const long long zg = ui * (8LL * TU + 6) + 8 * j;   // the tile's first Z chunk (even)
                 mbar_wait(&z_full[s], (uint32_t)(it >> 1) & 1u);
                 mbar_wait(&d_free[s], ((uint32_t)(it >> 1) & 1u) ^ 1u);
                 tc_fence_after();
-                const uint32_t zH = smem_u32(Z0 + 2 * s * zbytes), zL = zH + (uint32_t)zbytes;
                 const uint32_t td = tbase + (uint32_t)(s * kVtcRows);
                 for (int ks = 0; ks < Kp / 16; ks++) {
-                    const uint32_t oz = (uint32_t)ks * 2u * lboZ, ot = (uint32_t)ks * 2u * lboT;
+                    const uint32_t oz = (uint32_t)((zg + 2 * ks) % kVtcZChunks) * (uint32_t)kVtcZChunkBytes;
+                    const uint32_t ot = (uint32_t)ks * 2u * lboT;
                     umma_f16(td, umma_desc(zL + oz, lboZ, sbo), umma_desc(tH + ot, lboT, sbo), idesc,
                              ks > 0 ? 1u : 0u);
                     umma_f16(td, umma_desc(zH + oz, lboZ, sbo), umma_desc(tL + ot, lboT, sbo), idesc, 1u);
