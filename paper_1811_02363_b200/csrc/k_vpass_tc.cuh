@@ -45,8 +45,10 @@ constexpr int kVtcThreads = kVtcProd + 128 + 64;   // + consumers + MMA warp + T
 
 inline __host__ __device__ int vtc_kp(int R) { return ((kVtcRows + 2 * R) + 15) & ~15; }
 constexpr int kVtcMaxR = 24;       // Kp <= 112: the shared-memory budget below
-constexpr int kVtcZChunks = 22;    // Z ring: 8-row chunks (a tile reads Kp / 8 <= 14, the next tile's 8 new
-                                   // ones are written meanwhile; even, so a 16-row K step never wraps)
+constexpr int kVtcStages = 3;      // tiles in flight between the producers, the MMA warp and the consumers
+constexpr int kVtcZChunks = 30;    // Z ring: 8-row chunks (a tile reads Kp / 8 <= 14; the producers write up
+                                   // to two further tiles' 8 new chunks meanwhile; even, so a 16-row K step
+                                   // never wraps)
 constexpr int kVtcZChunkBytes = kVtcM * 8 * 2;
 // Dynamic shared memory: T_hi, T_lo [64][Kp], the Z ring hi and lo [22 chunks][128][8] (fp16), the raw
 // ring [3][64][96] fp32
@@ -114,7 +116,8 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                                                                    const __grid_constant__ VtcParams P) {
     extern __shared__ __align__(128) unsigned char sm_raw[];
     unsigned char* sm_vt = sm_raw + ((128u - (smem_u32(sm_raw) & 127u)) & 127u);
-    __shared__ uint64_t c_full[3], c_free[3], z_full[2], z_free[2], d_full[2], d_free[2];
+    __shared__ uint64_t c_full[3], c_free[3], z_full[kVtcStages], z_free[kVtcStages], d_full[kVtcStages],
+        d_free[kVtcStages];
     __shared__ uint32_t tmem_base_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int R = P.R, Kp = vtc_kp(R);
@@ -143,7 +146,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
             mbar_init(&c_full[s], 1);
             mbar_init(&c_free[s], kVtcProd);
         }
-        for (int s = 0; s < 2; s++) {
+        for (int s = 0; s < kVtcStages; s++) {
             mbar_init(&z_full[s], kVtcProd);
             mbar_init(&z_free[s], 1);
             mbar_init(&d_full[s], 1);
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                     "r"(128)
+                     "r"(256)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -201,13 +204,13 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                 mbar_wait(&c_full[gb % 3], (uint32_t)(gb / 3) & 1u);
                 // Z chunks of this unit: c = 0 .. 8 TU + 5 (tile j reads 8j .. 8j + Kp/8 - 1).  Tile j writes
                 // the chunks no earlier tile wrote: all Kp/8 for j = 0, else 8j + Kp/8 - 8 .. 8j + Kp/8 - 1.
-                // Their ring slots were last read by tile it - 2 (it - 1 at a unit's first tile).
-                const long long zg0 = ui * (8LL * TU + 6);   // the unit's first chunk (global, even)
+                // Their ring slots (30 chunks back) were last read by tile it - 3 (it - 2 at a unit's first
+                // tile); the MMAs complete in order.
+                const int zs0 = (int)((ui * (8LL * TU + 6)) % kVtcZChunks);   // the unit's first chunk's ring slot
                 const int c0 = (j == 0) ? 0 : 8 * j + Kp / 8 - 8, c1 = 8 * j + Kp / 8;
-                if (j == 0) {
-                    if (it >= 1) mbar_wait(&z_free[(it - 1) & 1], (uint32_t)((it - 1) >> 1) & 1u);
-                } else if (it >= 2) {
-                    mbar_wait(&z_free[it & 1], (uint32_t)((it - 2) >> 1) & 1u);
+                {
+                    const long long tw = it - (j == 0 ? 2 : 3);   // the tile whose MMAs must have completed
+                    if (tw >= 0) mbar_wait(&z_free[tw % kVtcStages], (uint32_t)(tw / kVtcStages) & 1u);
                 }
                 const float* slot_a = ring + (size_t)(ga % 3) * (64 * 96) + col * 3;
                 const float* slot_b = ring + (size_t)(gb % 3) * (64 * 96) + col * 3;
@@ -232,7 +235,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                         zv[2][r] = bu * p2;
                         zv[3][r] = b * sr;
                     }
-                    const size_t zoff = (size_t)((zg0 + cc) % kVtcZChunks) * kVtcZChunkBytes;
+                    const size_t zoff = (size_t)((zs0 + cc) % kVtcZChunks) * kVtcZChunkBytes;
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
                         const uint32_t off = (uint32_t)(((q * 32 + col) >> 3) * 128 + (col & 7) * 16);
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                 mbar_arrive(&c_free[ga % 3]);
                 if (j == TU - 1) mbar_arrive(&c_free[gb % 3]);
                 fence_proxy_async();   // generic-proxy writes of Z -> visible to the tensor core
-                mbar_arrive(&z_full[it & 1]);
+                mbar_arrive(&z_full[it % kVtcStages]);
             }
         }
     } else if (warp < kVtcProd / 32 + 4) {   // -------------------------------------- consumers -------
@@ -266,8 +269,8 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
             float* base = P.planes + (long long)(4 * k + q) * P.pstride + x;
             for (int j = 0; j < TU; j++, it++) {
                 const int yt = ys + j * kVtcRows;
-                const int s = (int)(it & 1);
-                mbar_wait(&d_full[s], (uint32_t)(it >> 1) & 1u);
+                const int s = (int)(it % kVtcStages);
+                mbar_wait(&d_full[s], (uint32_t)(it / kVtcStages) & 1u);
                 tc_fence_after();
                 float v[kVtcRows];
 #pragma unroll
@@ -300,29 +303,47 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
         }
     } else if (warp == kVtcProd / 32 + 4) {   // -------------------------------------- MMA warp ---------
         if (lane == 0) {
+            // a single thread issues everything: 32-bit incremental index math only (the ring slot of the
+            // tile's first chunk advances by 8 per tile and by 8 TU + 6 per unit, modulo the ring)
             const uint32_t idesc = umma_idesc_f16(kVtcM, kVtcRows);
-            const uint32_t tH = smem_u32(Th), tL = smem_u32(Tl);
-            const uint32_t lboZ = kVtcZChunkBytes, lboT = kVtcRows * 16, sbo = 128;
-            const uint32_t zH = smem_u32(ZH), zL = smem_u32(ZL);
-            for (long long it = 0; it < nit; it++) {
-                const int s = (int)(it & 1);
-                const long long ui = it / TU;
-                const int j = (int)(it - ui * TU);
-                const long long zg = ui * (8LL * TU + 6) + 8 * j;   // the tile's first Z chunk (even)
-                mbar_wait(&z_full[s], (uint32_t)(it >> 1) & 1u);
-                mbar_wait(&d_free[s], ((uint32_t)(it >> 1) & 1u) ^ 1u);
-                tc_fence_after();
-                const uint32_t td = tbase + (uint32_t)(s * kVtcRows);
-                for (int ks = 0; ks < Kp / 16; ks++) {
-                    const uint32_t oz = (uint32_t)((zg + 2 * ks) % kVtcZChunks) * (uint32_t)kVtcZChunkBytes;
-                    const uint32_t ot = (uint32_t)ks * 2u * lboT;
-                    umma_f16(td, umma_desc(zL + oz, lboZ, sbo), umma_desc(tH + ot, lboT, sbo), idesc,
-                             ks > 0 ? 1u : 0u);
-                    umma_f16(td, umma_desc(zH + oz, lboZ, sbo), umma_desc(tL + ot, lboT, sbo), idesc, 1u);
-                    umma_f16(td, umma_desc(zH + oz, lboZ, sbo), umma_desc(tH + ot, lboT, sbo), idesc, 1u);
+            const uint64_t dz = umma_desc(0, kVtcZChunkBytes, 128), dt = umma_desc(0, kVtcRows * 16, 128);
+            const uint32_t tH = smem_u32(Th), tL = smem_u32(Tl), zH = smem_u32(ZH), zL = smem_u32(ZL);
+            const int per_unit = (8 * TU + 6) % kVtcZChunks;
+            int ubase = (int)((long long)0 % kVtcZChunks);
+            int s = 0, wrap = 0;   // stage = it % kVtcStages, phase parity = (it / kVtcStages) & 1
+            long long it = 0;
+            for (long long ui = 0; ui < nui; ui++) {
+                int base = ubase;
+                for (int j = 0; j < TU; j++, it++) {
+                    mbar_wait(&z_full[s], (uint32_t)wrap);
+                    if (it >= kVtcStages) mbar_wait(&d_free[s], (uint32_t)(wrap ^ 1));
+                    tc_fence_after();
+                    const uint32_t td = tbase + (uint32_t)(s * kVtcRows);
+                    int slot = base;
+                    for (int ks = 0; ks < Kp / 16; ks++) {
+                        const uint32_t oz = (uint32_t)slot * (uint32_t)kVtcZChunkBytes;
+                        const uint32_t ot = (uint32_t)ks * (2u * kVtcRows * 16u);
+                        const uint64_t aL = dz | (uint64_t)(((zL + oz) >> 4) & 0x3FFFu);
+                        const uint64_t aH = dz | (uint64_t)(((zH + oz) >> 4) & 0x3FFFu);
+                        const uint64_t bH = dt | (uint64_t)(((tH + ot) >> 4) & 0x3FFFu);
+                        const uint64_t bL = dt | (uint64_t)(((tL + ot) >> 4) & 0x3FFFu);
+                        umma_f16(td, aL, bH, idesc, ks > 0 ? 1u : 0u);
+                        umma_f16(td, aH, bL, idesc, 1u);
+                        umma_f16(td, aH, bH, idesc, 1u);
+                        slot += 2;
+                        if (slot >= kVtcZChunks) slot -= kVtcZChunks;
+                    }
+                    umma_commit(&z_free[s]);
+                    umma_commit(&d_full[s]);
+                    base += 8;
+                    if (base >= kVtcZChunks) base -= kVtcZChunks;
+                    if (++s == kVtcStages) {
+                        s = 0;
+                        wrap ^= 1;
+                    }
                 }
-                umma_commit(&z_free[s]);
-                umma_commit(&d_full[s]);
+                ubase += per_unit;
+                if (ubase >= kVtcZChunks) ubase -= kVtcZChunks;
             }
         }
     } else if (lane == 0) {   // ------------------------------------------------------- TMA warp -----
@@ -343,7 +364,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(128) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(256) : "memory");
     }
 }
 
