@@ -182,8 +182,11 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
         const long long u = blockIdx.x + ui * (long long)gridDim.x;
         const long long col = u / P.nseg;
         const int seg = (int)(u - col * P.nseg);
-        strip = (int)(col % P.nstrip);
-        k = (int)(col / P.nstrip);
+        // cluster-fastest: the CTAs running at the same time cover all clusters of a few strips, so a
+        // strip's raw rows come from L2 for all but the first of them (strip-fastest re-read the whole
+        // guide from DRAM once per cluster: 10.9 GB at config 5)
+        k = (int)(col % P.K);
+        strip = (int)(col / P.K);
         ys = seg * P.seglen;
     };
 
