@@ -88,6 +88,25 @@ HDF_DEV void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t 
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Whole-warp forms: every lane of the warp executes them (warp-uniform operands, so the descriptors stay
+// in uniform registers) and elect.sync picks the one lane that issues (always the same: the lowest).
+HDF_DEV void umma_f16_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+HDF_DEV void umma_commit_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\t"
+        "elect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
 // fp16 hi/lo split of x: hi = fp16(x), lo = fp16(x - hi)
 HDF_DEV void split_f16(float x, unsigned short& hi, unsigned short& lo) {
     const __half h = __float2half_rn(x);
@@ -305,9 +324,10 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
             }
         }
     } else if (warp == kVtcProd / 32 + 4) {   // -------------------------------------- MMA warp ---------
-        if (lane == 0) {
-            // a single thread issues everything: 32-bit incremental index math only (the ring slot of the
-            // tile's first chunk advances by 8 per tile and by 8 TU + 6 per unit, modulo the ring)
+        {
+            // the whole warp runs the loop (warp-uniform values in uniform registers) and one elected lane
+            // issues: 32-bit incremental index math only (the ring slot of the tile's first chunk advances by
+            // 8 per tile and by 8 TU + 6 per unit, modulo the ring)
             const uint32_t idesc = umma_idesc_f16(kVtcM, kVtcRows);
             const uint64_t dz = umma_desc(0, kVtcZChunkBytes, 128), dt = umma_desc(0, kVtcRows * 16, 128);
             const uint32_t tH = smem_u32(Th), tL = smem_u32(Tl), zH = smem_u32(ZH), zL = smem_u32(ZL);
@@ -330,14 +350,14 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                         const uint64_t aH = dz | (uint64_t)(((zH + oz) >> 4) & 0x3FFFu);
                         const uint64_t bH = dt | (uint64_t)(((tH + ot) >> 4) & 0x3FFFu);
                         const uint64_t bL = dt | (uint64_t)(((tL + ot) >> 4) & 0x3FFFu);
-                        umma_f16(td, aL, bH, idesc, ks > 0 ? 1u : 0u);
-                        umma_f16(td, aH, bL, idesc, 1u);
-                        umma_f16(td, aH, bH, idesc, 1u);
+                        umma_f16_warp(td, aL, bH, idesc, ks > 0 ? 1u : 0u);
+                        umma_f16_warp(td, aH, bL, idesc, 1u);
+                        umma_f16_warp(td, aH, bH, idesc, 1u);
                         slot += 2;
                         if (slot >= kVtcZChunks) slot -= kVtcZChunks;
                     }
-                    umma_commit(&z_free[s]);
-                    umma_commit(&d_full[s]);
+                    umma_commit_warp(&z_free[s]);
+                    umma_commit_warp(&d_full[s]);
                     base += 8;
                     if (base >= kVtcZChunks) base -= kVtcZChunks;
                     if (++s == kVtcStages) {
