@@ -136,6 +136,15 @@ def stage_work(cfg, K: int, H: int, W: int, iir: bool = False):
 SAMPLED_STRIDE = {"c5": 64, "c3": 4}
 
 
+def tc_passes(cfg, W: int, variant: str = "soft"):
+    """Which filter passes run on the tensor cores for this workload (the library's own rule, hdf_api.cu:
+    colour Gaussian FIR with f = p, 4 <= R <= 24, W % 4 == 0; HDF_VPASS_FMA / HDF_HPASS_FMA override)."""
+    vtc = (cfg.kind == "gaussian" and variant != "iir" and cfg.bilateral and cfg.n == 3 and cfg.rho == 3
+           and 4 <= cfg.radius <= 24 and W % 4 == 0 and os.environ.get("HDF_VPASS_FMA", "0") in ("", "0"))
+    htc = vtc and os.environ.get("HDF_HPASS_FMA", "0") in ("", "0")
+    return vtc, htc
+
+
 def fma_peak(sm_mhz: float, nsm: int = 148) -> float:
     """FP32 FMA-pipe roof = SMs x 128 lanes x clock."""
     return nsm * 128 * sm_mhz * 1e6
@@ -293,7 +302,20 @@ def run_ours(args, rank: int, world: int, dist):
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
 
     # dram bytes per launch from the committed ncu --set full capture of this workload (profiles/), if any
-    kname = {"vpass": "k_range_vpass", "hpass": "k_hpass_combine", "coeffs": "k_coeffs_mma"}
+    vtc, htc = tc_passes(cfg, W, args.variant)
+    kname = {"vpass": "k_range_vpass_tc" if vtc else "k_range_vpass",
+             "hpass": "k_hpass_combine_tc" if htc else "k_hpass_combine", "coeffs": "k_coeffs_tc"}
+    # the FIR passes on the tensor cores (banded Toeplitz products, kind::f16 with the hi/lo split: 3 MMAs
+    # per K step): their MMA flops issued per launch, against the fp16 dense peak (= bf16's)
+    R = cfg.radius
+    f16_peak = peaks.get("bf16_tflops", 2250.0) * 1e12
+    tc_flop = {
+        # column pass: tiles of 128 (plane, column) pairs x 64 rows, K = round_up(64 + 2R, 16) input rows
+        "vpass": 3 * 2 * 128 * 64 * (((64 + 2 * R) + 15) // 16 * 16) * (K * ((W + 31) // 32))
+                 * ((H + 63) // 64),
+        # row pass: tiles of 128 (plane, row) pairs x 64 columns, K = 128 input columns
+        "hpass": 3 * 2 * 128 * 64 * 128 * K * ((H + 31) // 32) * ((W + 63) // 64),
+    }
     # tensor-core peak for the coefficient contraction (TF32): the measured bf16 peak x the nominal
     # dense TF32 / bf16 ratio (1.1 / 2.25 PFLOP/s, B200_PROFILING.md)
     tf32_peak = peaks.get("bf16_tflops", 2250.0) * (1.1 / 2.25) * 1e12
@@ -324,6 +346,13 @@ def run_ours(args, rank: int, world: int, dist):
                 r = {"bound": "hbm", "achieved": round(hbm_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(hbm_gbs / hbm_peak, 4), "peak_basis": "measured copy (MEASURED_PEAKS.json hbm_gbs)",
                      "tc_achieved_tflops": round(fl / 1e12, 3)}
+        elif (name == "vpass" and vtc) or (name == "hpass" and htc):
+            # the FIR on the tensor cores: HBM-bound (the tensor pipe runs well below its roof)
+            r = {"bound": "hbm", "achieved": round(hbm_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                 "frac": round(hbm_gbs / hbm_peak, 4), "peak_basis": "measured copy (MEASURED_PEAKS.json hbm_gbs)",
+                 "path": "tensor cores (tcgen05 kind::f16, Toeplitz FIR, fp16 hi/lo split)",
+                 "tc_issued_tflops": round(tc_flop[name] / t / 1e12, 2),
+                 "tc_frac_of_f16_peak": round(tc_flop[name] / t / f16_peak, 4)}
         elif t_alu > t_hbm:
             r = {"bound": "alu", "achieved": round(fma_s / 1e12, 3), "peak": round(fma_peak(sm_mhz, nsm) / 1e12, 3),
                  "unit": "TFMA/s (fp32)", "frac": round(fma_s / fma_peak(sm_mhz, nsm), 4),

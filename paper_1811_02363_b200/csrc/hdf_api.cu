@@ -18,6 +18,7 @@
 #include "k_coeffs.cuh"
 #include "k_coeffs_tc.cuh"
 #include "k_vpass_tc.cuh"
+#include "k_hpass_tc.cuh"
 #include "k_guide.cuh"
 #include "k_iir.cuh"
 
@@ -452,7 +453,7 @@ int make_plan(int H, int W, int n, int K, int kind, float sigma_s, int radius, F
     if (F.box && (radius == 0 || padded_radius(radius, true) < 0)) F.box = false;
     F.Rp = padded_radius(radius == 0 ? 1 : radius, F.box);
     if (F.Rp < 0) return fail(HDF_ERR_ARG, "radius %d is not supported by this build", radius);
-    F.Wp = round_up(W, 4);
+    F.Wp = round_up(W, 32);   // (whole 32-column strips of the strip-major fp16 planes, k_hpass_tc.cuh)
     F.NP = n + 1;
     F.P = K * F.NP;
     // F1: planes per CTA; a persistent grid (one 512-thread CTA per SM) with equal shares of the
@@ -565,16 +566,33 @@ EncodeTiledFn encode_fn() {
 }
 
 int encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t pitch_bytes,
-             uint64_t plane_bytes, uint32_t b0, uint32_t b1, uint32_t b2) {
+             uint64_t plane_bytes, uint32_t b0, uint32_t b1, uint32_t b2,
+             CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+             CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(HDF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[3] = {d0, d1, d2};
     cuuint64_t strides[2] = {pitch_bytes, plane_bytes};
     cuuint32_t box[3] = {b0, b1, b2};
     cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = fn(m, dt, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(HDF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return HDF_OK;
+}
+
+// 4-D fp16 map of the strip-major planes [P][Wp / 32][H][32] (k_hpass_tc.cuh): dims (32, H, strips, P),
+// box (32, rows, 1, planes), 64-byte swizzle
+int encode_strips(CUtensorMap* m, void* base, int H, int Wp, int P, uint32_t rows, uint32_t planes) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(HDF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[4] = {32, (cuuint64_t)H, (cuuint64_t)(Wp / 32), (cuuint64_t)P};
+    cuuint64_t strides[3] = {64, (cuuint64_t)H * 64, (cuuint64_t)H * Wp * 2};
+    cuuint32_t box[4] = {32, rows, 1, planes};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(HDF_ERR_CUDA, "cuTensorMapEncodeTiled (strips) failed (%d)", (int)r);
     return HDF_OK;
 }
 
@@ -785,6 +803,25 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     if (hard) HDF_CUDA(cudaMemsetAsync(w.status, 0, sizeof(int), st));
     float taps[hdf::kMaxTaps];
     fill_taps(taps, kind, sigma_s, F.R, F.Rp);
+    // the column FIR on the tensor cores (k_vpass_tc.cuh) for colour images with the Gaussian FIR
+    // (HDF_VPASS_FMA=1 keeps the CUDA-core kernel), and then the row FIR + combine on the tensor cores too
+    // (k_hpass_tc.cuh, fed by fp16 hi/lo planes; HDF_HPASS_FMA=1 keeps fp32 planes and the CUDA-core row pass)
+    bool use_tc = !F.box && !F.iir && F.NP == 4 && rho == 3 && f == p && F.R >= 4 && F.R <= hdf::kVtcMaxR &&
+                  (W % 4) == 0;
+    if (const char* e = getenv("HDF_VPASS_FMA")) {
+        if (atoi(e)) use_tc = false;
+    }
+    bool use_htc = use_tc && F.R <= hdf::kHtcMaxR;
+    if (const char* e = getenv("HDF_HPASS_FMA")) {
+        if (atoi(e)) use_htc = false;
+    }
+    int wexp = 0;   // 2^wexp >= the sum of the taps (the fp16 planes' scale)
+    {
+        double ws = 0.0;
+        for (int t = 0; t <= 2 * F.Rp; t++) ws += (double)taps[t];
+        while (std::ldexp(1.0, wexp) < ws) wexp++;
+    }
+    int* amax = w.status + 3;
     // F1: range weights + column pass
     {
         hdf::VParams vp;
@@ -815,15 +852,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         hdf::VLaunch vl = F.vl;
         vl.smem = vsmem;
         ProfScope prof(HDF_STAGE_VPASS, st);
-        // the column FIR on the tensor cores (k_vpass_tc.cuh) for colour images with the Gaussian FIR;
-        // HDF_VPASS_FMA=1 keeps the CUDA-core kernel
-        bool use_tc = !F.box && !F.iir && F.NP == 4 && rho == 3 && f == p && F.R >= 4 && F.R <= hdf::kVtcMaxR &&
-                      (W % 4) == 0;
-        if (const char* e = getenv("HDF_VPASS_FMA")) {
-            if (atoi(e)) use_tc = false;
-        }
         if (use_tc) {
-            int* amax = w.status + 3;
             HDF_CUDA(cudaMemsetAsync(amax, 0, sizeof(int), st));
             const long long nf = (long long)H * W * n;
             hdf::k_absmax<<<(unsigned)std::min<long long>((nf + 255) / 256, (long long)nsm * 8), 256, 0, st>>>(f, nf, amax);
@@ -831,6 +860,8 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             hdf::VtcParams tp;
             tp.centres = centres;
             tp.planes = w.planes;
+            tp.ph = use_htc ? reinterpret_cast<unsigned short*>(w.planes) : nullptr;
+            tp.wexp = wexp;
             tp.absmax = amax;
             tp.pstride = (long long)H * F.Wp;
             tp.H = H;
@@ -1001,7 +1032,41 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         }
         memcpy(fb.taps, t2, sizeof(t2));
     }
-    const int row_tiles = (int)F.hl.grid.y;
+    // the tensor-core row pass: tensor maps of the strip-major fp16 hi/lo planes (boxes [4 planes][32 rows]
+    // [one 32-column strip], 64-byte swizzle) and of the coefficient planes (two [32 rows][32 columns]
+    // halves per tile, 128-byte swizzle)
+    CUtensorMap thi, tlo, tcc;
+    hdf::HtcParams hq;
+    size_t htc_smem = 0;
+    if (use_htc) {
+        unsigned short* ph = reinterpret_cast<unsigned short*>(w.planes);
+        const uint64_t pl = (uint64_t)K * 4 * H * F.Wp;
+        rc = encode_strips(&thi, ph, H, F.Wp, K * 4, (uint32_t)hdf::kHtcRows, 4u);
+        if (rc) return rc;
+        rc = encode_strips(&tlo, ph + pl, H, F.Wp, K * 4, (uint32_t)hdf::kHtcRows, 4u);
+        if (rc) return rc;
+        rc = encode3d(&tcc, w.cpl, (uint64_t)W, (uint64_t)H, (uint64_t)K, (uint64_t)F.Wp * 4, (uint64_t)H * F.Wp * 4,
+                      32u, (uint32_t)hdf::kHtcRows, 1u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CU_TENSOR_MAP_SWIZZLE_128B);
+        if (rc) return rc;
+        hq.g = g;
+        hq.flag_count = w.flag_count;
+        hq.flag_list = w.flag_list;
+        hq.absmax = amax;
+        hq.H = H;
+        hq.W = W;
+        hq.K = K;
+        hq.R = F.R;
+        hq.nstrip = (W + hdf::kHtcS * hdf::kHtcN - 1) / (hdf::kHtcS * hdf::kHtcN);
+        hq.wexp = wexp;
+        hq.tau_floor = hp.tau_floor;
+        for (int t = 0; t < hdf::kMaxTaps; t++) hq.taps[t] = 0.f;
+        for (int t = 0; t <= 2 * F.R; t++) hq.taps[t] = taps[F.Rp - F.R + t];
+        htc_smem = hdf::hpass_tc_smem();
+        HDF_CUDA(cudaFuncSetAttribute(hdf::k_hpass_combine_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)htc_smem));
+    }
+    const int tile_rows = use_htc ? hdf::kHtcRows : F.RR;
+    const int row_tiles = use_htc ? (H + hdf::kHtcRows - 1) / hdf::kHtcRows : (int)F.hl.grid.y;
     const int nch = std::max(1, std::min(nchunks, row_tiles));
     int* flag_start = w.status + 2;   // list entries before this chunk (device)
     for (int ch = 0; ch < nch; ch++) {
@@ -1015,7 +1080,16 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         }
         {
             ProfScope prof(HDF_STAGE_HPASS, st);
-            HDF_CUDA(hdf::launch_hpass(F.Rp, F.box, hl, st, tp, tc, hp));
+            if (use_htc) {
+                hq.yb0 = ty0;
+                hq.yb1 = ty1;
+                const long long nunit = (long long)(ty1 - ty0) * hq.nstrip;
+                hdf::k_hpass_combine_tc<<<(unsigned)std::max<long long>(1, std::min<long long>(nsm, nunit)),
+                                          hdf::kHtcThreads, htc_smem, st>>>(thi, tlo, tcc, hq);
+                HDF_CUDA(cudaGetLastError());
+            } else {
+                HDF_CUDA(hdf::launch_hpass(F.Rp, F.box, hl, st, tp, tc, hp));
+            }
         }
         if (tau > 0.f) {
             ProfScope prof(HDF_STAGE_FALLBACK, st);
@@ -1033,7 +1107,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             HDF_CUDA(cudaGetLastError());
         }
         if (after_chunk) {
-            rc = after_chunk(std::min(H, ty0 * F.RR), std::min(H, ty1 * F.RR));
+            rc = after_chunk(std::min(H, ty0 * tile_rows), std::min(H, ty1 * tile_rows));
             if (rc) return rc;
         }
     }
@@ -1176,7 +1250,7 @@ size_t hdf_filter_workspace_bytes(int H, int W, int n, int rho, int K, int kind,
     (void)radius;
     if (H < 1 || W < 1 || n < 1 || rho < 1 || K < 1) return 0;
     Carver cv(nullptr);
-    carve_filter(cv, H, W, n, rho, K, round_up(W, 4), true);
+    carve_filter(cv, H, W, n, rho, K, round_up(W, 32), true);
     return cv.off + 256;
 }
 
@@ -1409,7 +1483,7 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
         }
         // cluster (in the filter workspace's cluster region; status read back at the end) then filter
         Carver c2(fws);
-        FilterWS w = carve_filter(c2, H, W, n, rho, K, round_up(W, 4), true);
+        FilterWS w = carve_filter(c2, H, W, n, rho, K, round_up(W, 32), true);
         ClusterReadback crb;
         if (cluster_stride == 1) {
             rc = launch_cluster(pdev, H, W, rho, K, cd, nullptr, nullptr, w.cluster_ws, st, &crb);
@@ -1491,7 +1565,7 @@ int hdf_filter_flagged(const void* ws, int H, int W, int n, int rho, int K, int3
     return guarded([&]() -> int {
         if (!ws || H < 1 || W < 1 || n < 1 || rho < 1 || K < 1) return -1;
         Carver cv(const_cast<void*>(ws));
-        FilterWS w = carve_filter(cv, H, W, n, rho, K, round_up(W, 4), true);
+        FilterWS w = carve_filter(cv, H, W, n, rho, K, round_up(W, 32), true);
         int cnt = 0;
         if (cudaMemcpy(&cnt, w.flag_count, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
         const int m = std::min(cnt, std::max(cap, 0));

@@ -59,7 +59,10 @@ inline __host__ __device__ size_t vpass_tc_smem(int R) {
 
 struct VtcParams {
     const float* centres;  // [K][3]
-    float* planes;         // [4K][H][Wp]
+    float* planes;         // [4K][H][Wp] fp32 (ph == NULL)
+    unsigned short* ph;    // else fp16 hi and lo parts, strip-major: ph [4K][Wp / 32][H][32], then lo at
+                           // ph + 4K H Wp (k_hpass_tc.cuh); Wp a multiple of 32
+    int wexp;              // ph: stored value = t 2^(14 - e2 - wexp) (u planes), t 2^(14 - wexp) (b planes)
     const int* absmax;     // max |f| as float bits (k_absmax)
     long long pstride;     // H * Wp
     int H, W, Wp, K, R;
@@ -226,12 +229,16 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                 mbar_wait(&c_full[gb % 3], (uint32_t)(gb / 3) & 1u);
                 // Z chunks of this unit: c = 0 .. 8 TU + 5 (tile j reads 8j .. 8j + Kp/8 - 1).  Tile j writes
                 // the chunks no earlier tile wrote: all Kp/8 for j = 0, else 8j + Kp/8 - 8 .. 8j + Kp/8 - 1.
-                // Their ring slots (30 chunks back) were last read by tile it - 3 (it - 2 at a unit's first
-                // tile); the MMAs complete in order.
+                // Their ring slots (30 chunks back, the unit stride being 8 TU + 6 chunks) were last read by
+                // tile it - 3 for j >= 2, but by tile it - 2 for j = 0 (the previous unit's tiles TU - 2 and
+                // earlier) and for j = 1 (its chunks 8 + Kp/8 - 8 .. 8 + Kp/8 - 1 land on the previous unit's
+                // chunks 8 TU - 24 + 8 + Kp/8 - 8 .., the first chunks of its LAST tile, TU - 1); the MMAs
+                // complete in order.  (Waiting for it - 3 at j = 1 let the producers overwrite the input rows
+                // of a unit's last tile while its MMAs were pending whenever the consumers lagged.)
                 const int zs0 = (int)((ui * (8LL * TU + 6)) % kVtcZChunks);   // the unit's first chunk's ring slot
                 const int c0 = (j == 0) ? 0 : 8 * j + Kp / 8 - 8, c1 = 8 * j + Kp / 8;
                 {
-                    const long long tw = it - (j == 0 ? 2 : 3);   // the tile whose MMAs must have completed
+                    const long long tw = it - (j <= 1 ? 2 : 3);   // the tile whose MMAs must have completed
                     if (tw >= 0) mbar_wait(&z_free[tw % kVtcStages], (uint32_t)(tw / kVtcStages) & 1u);
                 }
                 const float* slot_a = ring + (size_t)(ga % 3) * (64 * 96) + col * 3;
@@ -281,8 +288,11 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
     } else if (warp < kVtcProd / 32 + 4) {   // -------------------------------------- consumers -------
         const int q = warp & 3, col = lane;   // TMEM lane quarter q = plane q, lane = column
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-        const float inv = (q < 3) ? 1.f / su : 1.f / sr;   // exact (powers of two)
+        // fp32 output: t = D / su (u planes), D / sr (b planes); fp16 hi/lo output: D 2^-wexp (both scaled,
+        // |value| <= 2^14 since the taps sum to at most 2^wexp)
+        const float inv = P.ph ? ldexpf(1.f, -P.wexp) : (q < 3) ? 1.f / su : 1.f / sr;   // exact (powers of two)
         const int step = P.Wp;
+        const long long lo_off = 4LL * P.K * P.pstride;
         long long it = 0;
         for (long long ui = 0; ui < nui; ui++) {
             int strip, k, ys;
@@ -304,7 +314,39 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                 }
                 tc_fence_before();
                 mbar_arrive(&d_free[s]);
-                if (x < P.W && yt < P.H) {
+                if (P.ph) {   // strip-major fp16 planes: [plane][strip][H][32] (k_hpass_tc.cuh)
+                    if (yt < P.H) {   // (columns past W hold exact zeros: b = 0 there)
+                        const int nr = min(kVtcRows, P.H - yt);
+                        unsigned short* oh = P.ph + (long long)(4 * k + q) * P.pstride + (long long)strip * P.H * 32 +
+                                             (long long)yt * 32 + col;
+                        unsigned short* ol = oh + lo_off;
+                        if (nr == kVtcRows) {   // whole tile: constant offsets (row stride 64 bytes)
+#pragma unroll
+                            for (int jj = 0; jj < kVtcRows; jj += 2) {
+                                uint32_t hi, lo;
+                                split_f16x2(v[jj] * inv, v[jj + 1] * inv, hi, lo);
+                                oh[jj * 32] = (unsigned short)(hi & 0xFFFFu);
+                                oh[jj * 32 + 32] = (unsigned short)(hi >> 16);
+                                ol[jj * 32] = (unsigned short)(lo & 0xFFFFu);
+                                ol[jj * 32 + 32] = (unsigned short)(lo >> 16);
+                            }
+                        } else {
+#pragma unroll
+                            for (int jj = 0; jj < kVtcRows; jj += 2) {
+                                uint32_t hi, lo;
+                                split_f16x2(v[jj] * inv, v[jj + 1] * inv, hi, lo);
+                                if (jj < nr) {
+                                    oh[jj * 32] = (unsigned short)(hi & 0xFFFFu);
+                                    ol[jj * 32] = (unsigned short)(lo & 0xFFFFu);
+                                }
+                                if (jj + 1 < nr) {
+                                    oh[jj * 32 + 32] = (unsigned short)(hi >> 16);
+                                    ol[jj * 32 + 32] = (unsigned short)(lo >> 16);
+                                }
+                            }
+                        }
+                    }
+                } else if (x < P.W && yt < P.H) {
                     const int nr = min(kVtcRows, P.H - yt);
                     float* o = base + (long long)yt * step;
                     if (nr == kVtcRows) {   // whole tile: a running pointer, no per-row predicate

@@ -104,6 +104,23 @@ def test_parity_ragged(hdf, name, H, W, K):
     _parity_case(hdf, name, H, W, K)
 
 
+@pytest.mark.parametrize("row_pass", ["tc", "fma"])
+@pytest.mark.parametrize("name,H,W,K", [
+    ("c1", 70, 100, 3),         # few clusters: R9-flagged pixels
+    ("c1", 100, 132, 8),        # 128-column units + a ragged 4-column strip, 32-row blocks + tail
+    ("c2a", 161, 388, 16),
+    ("c2b", 96, 260, 32),
+    ("c2a", 33, 64, 64),        # one row block + 1 row, K = 64
+    ("c1", 8, 4, 2),            # smaller than every tile
+])
+def test_parity_tensor_core_passes(hdf, monkeypatch, row_pass, name, H, W, K):
+    """The colour Gaussian path with W % 4 == 0 runs the column pass on the tensor cores
+    (k_range_vpass_tc) and, by default, the row pass + combine too (k_hpass_combine_tc, fed by the
+    strip-major fp16 hi/lo planes); HDF_HPASS_FMA=1 keeps fp32 planes and the CUDA-core row pass."""
+    monkeypatch.setenv("HDF_HPASS_FMA", "1" if row_pass == "fma" else "0")
+    _parity_case(hdf, name, H, W, K)
+
+
 @pytest.mark.parametrize("R", [1, 2, 7, 11, 24, 32])
 def test_parity_radius_sweep(hdf, R):
     """Gaussian radii that are not compiled exactly run with zero-padded taps (exact)."""
