@@ -17,9 +17,10 @@
 //   * the MMA warp (one elected thread): waits for A[s] full and D[s] free, issues the 3 (K/8) MMAs of
 //     M = 128, N = round_up(K, 16), K-step 8 into D[s] and commits them to two mbarriers (A[s] free,
 //     D[s] full);
-//   * consumer (warpgroup 2): warp w reads TMEM lanes 32 (w % 4) .. + 31 of D[s] (its pixels' rows)
-//     with tcgen05.ld, releases D[s] (mbarrier) and stores c_k(i) to the coefficient planes
-//     (coalesced over m) while the producers already compute tile t + 1.
+//   * consumers (warpgroups 2 and 3, coefficients 0..31 and 32..63): warp w reads TMEM lanes
+//     32 (w % 4) .. + 31 of D[s] (its pixels' rows) with tcgen05.ld, releases D[s] (mbarrier) and stores
+//     c_k(i) to the coefficient planes (coalesced over m) while the producers already compute tile t + 1
+//     (one consumer warpgroup was the bottleneck: 64 stores per pixel).
 // A^+ (hi, lo) is staged once per CTA as the B operands.
 #pragma once
 #include "hdf_common.cuh"
@@ -28,7 +29,7 @@
 namespace hdf {
 
 constexpr int kTcProd = 256;      // producer threads: (half h, pixel row m)
-constexpr int kTcThreads = 416;   // + one consumer warpgroup + one MMA-issuing warp
+constexpr int kTcThreads = 544;   // + two consumer warpgroups (columns 0..31, 32..63) + one MMA-issuing warp
 constexpr int kTcM = 128;         // pixels per MMA tile (UMMA M)
 constexpr int kTcMaxK = 64;       // N = round_up(K, 16) <= 64 (larger K: the CUDA-core kernels)
 
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
             mbar_init(&a_full[s], kTcProd);
             mbar_init(&a_free[s], 1);
             mbar_init(&d_full[s], 1);
-            mbar_init(&d_free[s], kTcM);
+            mbar_init(&d_free[s], 2 * kTcM);
         }
         fence_barrier_init();
     }
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
             fence_proxy_async();   // generic-proxy writes of A[s] -> visible to the tensor core
             mbar_arrive(&a_full[s]);
         }
-    } else if (warp == (kTcProd + kTcM) / 32) {   // ---------------------------- MMA warp ----------
+    } else if (warp == (kTcProd + 2 * kTcM) / 32) {   // ------------------------ MMA warp ----------
         if ((tid & 31) == 0) {    // D = b_lo A_hi^T + b_hi A_lo^T + b_hi A_hi^T into D[s]
             const uint32_t idesc = umma_idesc_tf32(kTcM, N);
             const uint32_t sbo = (uint32_t)Kr * 32u, lbo = 128u;
@@ -257,7 +258,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
             }
         }
     } else {               // ------------------------------------------------ consumer ---------
-        const int m = tid - kTcProd;   // warps 8..11: TMEM lane quarters 0..3
+        // warpgroup cw (warps 8..11, 12..15) stores the coefficients n = 32 cw .. 32 cw + 31; warp & 3 is
+        // the TMEM lane quarter (pixel m)
+        const int cw = (tid - kTcProd) >> 7, m = (tid - kTcProd) & (kTcM - 1);
+        const int n0 = 32 * cw;
         const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
         int it = 0;
         for (long long tile = blockIdx.x; tile < ntile; tile += gridDim.x, it++) {
@@ -270,25 +274,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
                 y = i / P.W;
                 xx = i - y * P.W;
             }
-            float* o = P.cpl + y * P.Wp + xx;
+            float* o = P.cpl + (long long)n0 * P.cstride + y * P.Wp + xx;
             mbar_wait(&d_full[s], ph);
             tc_fence_after();
-            float v[kTcMaxK];
+            float v[32];
+            if (n0 < N) {
+                float t16[16];
+                tmem_ld16(tbase + lane_base + (uint32_t)s * dcols + (uint32_t)n0, t16);
 #pragma unroll
-            for (int n0 = 0; n0 < kTcMaxK; n0 += 16) {
-                if (n0 < N) {
-                    float t16[16];
-                    tmem_ld16(tbase + lane_base + (uint32_t)s * dcols + (uint32_t)n0, t16);
+                for (int j = 0; j < 16; j++) v[j] = t16[j];
+                if (n0 + 16 < N) {
+                    tmem_ld16(tbase + lane_base + (uint32_t)s * dcols + (uint32_t)(n0 + 16), t16);
 #pragma unroll
-                    for (int j = 0; j < 16; j++) v[n0 + j] = t16[j];
+                    for (int j = 0; j < 16; j++) v[16 + j] = t16[j];
                 }
             }
             tc_fence_before();
             mbar_arrive(&d_free[s]);
             if (valid) {
+                const int nn = min(32, K - n0);
 #pragma unroll
-                for (int n = 0; n < kTcMaxK; n++)
-                    if (n < K) o[(long long)n * P.cstride] = v[n];
+                for (int n = 0; n < 32; n++) {
+                    if (n < nn) o[0] = v[n];
+                    o += P.cstride;
+                }
             }
         }
     }
