@@ -42,8 +42,14 @@ HDF_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+#ifndef HDF_MBAR_SLEEP_NS
+#define HDF_MBAR_SLEEP_NS 0
+#endif
 HDF_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
+#if HDF_MBAR_SLEEP_NS > 0
+        __nanosleep(HDF_MBAR_SLEEP_NS);   // back off: a waiting warp leaves the issue slots to the others
+#endif
     }
 }
 

@@ -45,8 +45,17 @@ constexpr int kVtcThreads = kVtcProd + 128 + 64;   // + consumers + MMA warp + T
 
 inline __host__ __device__ int vtc_kp(int R) { return ((kVtcRows + 2 * R) + 15) & ~15; }
 constexpr int kVtcMaxR = 24;       // Kp <= 112: the shared-memory budget below
-constexpr int kVtcStages = 3;      // tiles in flight between the producers, the MMA warp and the consumers
-constexpr int kVtcZChunks = 30;    // Z ring: 8-row chunks (a tile reads Kp / 8 <= 14; the producers write up
+#ifndef HDF_VTC_STAGES
+#define HDF_VTC_STAGES 2
+#endif
+#ifndef HDF_VTC_RAW
+#define HDF_VTC_RAW 4
+#endif
+constexpr int kVtcStages = HDF_VTC_STAGES;   // tiles in flight between the producers, the MMA warp and the consumers
+constexpr int kVtcRaw = HDF_VTC_RAW;         // raw guide chunks (64 rows) in the TMA ring: a tile reads 2, the
+                                             // rest load ahead (the ring depth hides the L2 latency of the
+                                             // raw rows, which every cluster's unit of a strip re-reads)
+constexpr int kVtcZChunks = 6 + 8 * kVtcStages;   // Z ring: 8-row chunks (a tile reads Kp / 8 <= 14; the producers write up
                                    // to two further tiles' 8 new chunks meanwhile; even, so a 16-row K step
                                    // never wraps)
 constexpr int kVtcZChunkBytes = kVtcM * 8 * 2;
@@ -54,7 +63,8 @@ constexpr int kVtcZChunkBytes = kVtcM * 8 * 2;
 // ring [3][64][96] fp32
 inline __host__ __device__ size_t vpass_tc_smem(int R) {
     const int Kp = vtc_kp(R);
-    return (size_t)2 * kVtcRows * Kp * 2 + (size_t)2 * kVtcZChunks * kVtcZChunkBytes + (size_t)3 * 64 * 96 * 4 + 128;
+    return (size_t)2 * kVtcRows * Kp * 2 + (size_t)2 * kVtcZChunks * kVtcZChunkBytes + (size_t)kVtcRaw * 64 * 96 * 4 +
+           128;
 }
 
 struct VtcParams {
@@ -138,7 +148,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                                                                    const __grid_constant__ VtcParams P) {
     extern __shared__ __align__(128) unsigned char sm_raw[];
     unsigned char* sm_vt = sm_raw + ((128u - (smem_u32(sm_raw) & 127u)) & 127u);
-    __shared__ uint64_t c_full[3], c_free[3], z_full[kVtcStages], z_free[kVtcStages], d_full[kVtcStages],
+    __shared__ uint64_t c_full[kVtcRaw], c_free[kVtcRaw], z_full[kVtcStages], z_free[kVtcStages], d_full[kVtcStages],
         d_free[kVtcStages];
     __shared__ uint32_t tmem_base_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -149,7 +159,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
     unsigned char* Tl = Th + tbytes;
     unsigned char* ZH = Tl + tbytes;                                          // Z ring, hi
     unsigned char* ZL = ZH + (size_t)kVtcZChunks * kVtcZChunkBytes;            // Z ring, lo
-    float* ring = reinterpret_cast<float*>(ZL + (size_t)kVtcZChunks * kVtcZChunkBytes);   // [3][64][96]
+    float* ring = reinterpret_cast<float*>(ZL + (size_t)kVtcZChunks * kVtcZChunkBytes);   // [kVtcRaw][64][96]
     (void)zbytes;
 
     // the Toeplitz operand: row j (output row), column i (input row): w_{i - j - R}
@@ -164,7 +174,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
     }
     if (tid == 0) {
         prefetch_tmap(&tm_p);
-        for (int s = 0; s < 3; s++) {
+        for (int s = 0; s < kVtcRaw; s++) {
             mbar_init(&c_full[s], 1);
             mbar_init(&c_free[s], kVtcProd);
         }
@@ -195,7 +205,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
     // the tile sequence (identical in every role): tile `it` of this CTA is tile j = it % TU of its
     // unit number ui = it / TU, unit u = blockIdx.x + ui gridDim.x = the row segment of column (strip,
     // cluster).  The raw rows of a unit are its chunks c = 0 .. TU (64 rows each, from ys - R); the
-    // CTA's chunk sequence number is g = ui (TU + 1) + c, ring slot g % 3, and tile j reads chunks j, j+1.
+    // CTA's chunk sequence number is g = ui (TU + 1) + c, ring slot g % kVtcRaw, and tile j reads chunks j, j+1.
     const long long nunit = (long long)P.nstrip * P.K * P.nseg;
     const int TU = P.seglen / kVtcRows;
     const long long nui = nunit > blockIdx.x ? (nunit - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -215,6 +225,12 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
     if (warp < kVtcProd / 32) {   // ------------------------------------------------ producers -------
         const int col = tid & 31, cg = tid >> 5;   // this thread's column and first 8-row chunk
         const float c2 = P.neg_inv2sr2 * 1.4426950408889634f;
+        // b su = 2^(d2 c2 + 14 - e2) (the u planes' scale folded into the exponent: exact), b sr = (b su) 2^e2
+        const float lsu = (float)(14 - e2), sbu = ldexpf(1.f, e2);
+        // per-tile bookkeeping in 32-bit incremental form: raw chunk ga = ui (TU + 1) + j (ring slot ga %
+        // kVtcRaw, phase ga / kVtcRaw), the unit's first Z slot zs0 = ui (8 TU + 6) % kVtcZChunks
+        const int U = 8 * TU + 6;
+        int ga_slot = 0, ga_ph = 0, zs0 = 0;
         long long it = 0;
         for (long long ui = 0; ui < nui; ui++) {
             int strip, k, ys;
@@ -224,47 +240,52 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                         m2 = __ldg(P.centres + k * 3 + 2);
             for (int j = 0; j < TU; j++, it++) {
                 const int yt = ys + j * kVtcRows;
-                const long long ga = ui * (TU + 1) + j, gb = ga + 1;
-                mbar_wait(&c_full[ga % 3], (uint32_t)(ga / 3) & 1u);
-                mbar_wait(&c_full[gb % 3], (uint32_t)(gb / 3) & 1u);
-                // Z chunks of this unit: c = 0 .. 8 TU + 5 (tile j reads 8j .. 8j + Kp/8 - 1).  Tile j writes
-                // the chunks no earlier tile wrote: all Kp/8 for j = 0, else 8j + Kp/8 - 8 .. 8j + Kp/8 - 1.
-                // Their ring slots (30 chunks back, the unit stride being 8 TU + 6 chunks) were last read by
-                // tile it - 3 for j >= 2, but by tile it - 2 for j = 0 (the previous unit's tiles TU - 2 and
-                // earlier) and for j = 1 (its chunks 8 + Kp/8 - 8 .. 8 + Kp/8 - 1 land on the previous unit's
-                // chunks 8 TU - 24 + 8 + Kp/8 - 8 .., the first chunks of its LAST tile, TU - 1); the MMAs
-                // complete in order.  (Waiting for it - 3 at j = 1 let the producers overwrite the input rows
-                // of a unit's last tile while its MMAs were pending whenever the consumers lagged.)
-                const int zs0 = (int)((ui * (8LL * TU + 6)) % kVtcZChunks);   // the unit's first chunk's ring slot
+                const int gb_slot = ga_slot + 1 == kVtcRaw ? 0 : ga_slot + 1;
+                const int gb_ph = ga_slot + 1 == kVtcRaw ? ga_ph ^ 1 : ga_ph;
+                mbar_wait(&c_full[ga_slot], (uint32_t)ga_ph);
+                mbar_wait(&c_full[gb_slot], (uint32_t)gb_ph);
+                // Z chunks of this unit: c = 0 .. U - 1, U = 8 TU + 6 (tile j reads 8j .. 8j + Kp/8 - 1).  Tile j
+                // writes the chunks no earlier tile wrote: all Kp/8 for j = 0, else 8j + Kp/8 - 8 .. 8j + Kp/8 - 1.
                 const int c0 = (j == 0) ? 0 : 8 * j + Kp / 8 - 8, c1 = 8 * j + Kp / 8;
                 {
-                    const long long tw = it - (j <= 1 ? 2 : 3);   // the tile whose MMAs must have completed
-                    if (tw >= 0) mbar_wait(&z_free[tw % kVtcStages], (uint32_t)(tw / kVtcStages) & 1u);
+                    // Their ring slots held the chunk kVtcZChunks back in the CTA's chunk sequence (S = ui U + c).
+                    // The last reader of that chunk is tile min(TU - 1, c' / 8) of its unit (chunks past the last
+                    // tile's reads have none: the clamp is conservative); readers are monotonic in S, so the
+                    // highest chunk written decides, and the MMAs complete in order.  (A fixed "it - 3" let the
+                    // producers overwrite the first input rows of a unit's last tile while its MMAs were pending.)
+                    int up = 0, cp = c1 - 1 - kVtcZChunks;   // (unit offset, chunk) of S - kVtcZChunks
+                    while (cp < 0) {
+                        cp += U;
+                        up++;
+                    }
+                    const long long tw = (ui - up) * TU + min(TU - 1, cp / 8);
+                    if (ui - up >= 0 && tw >= 0) mbar_wait(&z_free[tw % kVtcStages], (uint32_t)(tw / kVtcStages) & 1u);
                 }
-                const float* slot_a = ring + (size_t)(ga % 3) * (64 * 96) + col * 3;
-                const float* slot_b = ring + (size_t)(gb % 3) * (64 * 96) + col * 3;
+                const float* slot_a = ring + (size_t)ga_slot * (64 * 96) + col * 3;
+                const float* slot_b = ring + (size_t)gb_slot * (64 * 96) + col * 3;
                 for (int cc = c0 + cg; cc < c1; cc += kVtcProd / 32) {
                     const int ch = cc - 8 * j;   // 8-row chunk within the tile
                     float zv[4][8];
-                    const float* sl = (ch < 8) ? slot_a : slot_b;
+                    const float* px = ((ch < 8) ? slot_a : slot_b) + (ch & 7) * (8 * 96);
+                    const int y8 = yt - R + ch * 8;   // image row of the chunk's first input row
 #pragma unroll
                     for (int r = 0; r < 8; r++) {
-                        const int i = ch * 8 + r;   // input row within the tile (zero-filled outside the image)
-                        const float* px = sl + (i & 63) * 96;
-                        const float p0 = px[0], p1 = px[1], p2 = px[2];
+                        const float p0 = px[r * 96], p1 = px[r * 96 + 1], p2 = px[r * 96 + 2];
                         const float t0 = p0 - m0, t1 = p1 - m1, t2 = p2 - m2;
                         const float d2 = fmaf(t2, t2, fmaf(t1, t1, t0 * t0));
-                        float b;
-                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
-                        const int yy = yt - R + i;
-                        b = (xok && yy >= 0 && yy < P.H) ? b : 0.f;   // (rows past 64 + 2R: T is zero there; a chunk may be shared with the next tile)
-                        const float bu = b * su;
+                        float bu;
+                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(bu) : "f"(fmaf(d2, c2, lsu)));
+                        // rows outside [0, H) and columns past W contribute zero (R8); rows past 64 + 2R meet zero
+                        // taps (a chunk may be shared with the next tile)
+                        bu = (xok && (unsigned)(y8 + r) < (unsigned)P.H) ? bu : 0.f;
                         zv[0][r] = bu * p0;
                         zv[1][r] = bu * p1;
                         zv[2][r] = bu * p2;
-                        zv[3][r] = b * sr;
+                        zv[3][r] = bu * sbu;
                     }
-                    const size_t zoff = (size_t)((zs0 + cc) % kVtcZChunks) * kVtcZChunkBytes;
+                    int zslot = zs0 + cc;
+                    while (zslot >= kVtcZChunks) zslot -= kVtcZChunks;
+                    const size_t zoff = (size_t)zslot * kVtcZChunkBytes;
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
                         const uint32_t off = (uint32_t)(((q * 32 + col) >> 3) * 128 + (col & 7) * 16);
@@ -279,11 +300,20 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                 }
                 // raw chunk j has no later reader in this unit (tile j + 1 reads j + 1, j + 2); the last tile
                 // also releases chunk j + 1
-                mbar_arrive(&c_free[ga % 3]);
-                if (j == TU - 1) mbar_arrive(&c_free[gb % 3]);
+                mbar_arrive(&c_free[ga_slot]);
+                if (j == TU - 1) mbar_arrive(&c_free[gb_slot]);
                 fence_proxy_async();   // generic-proxy writes of Z -> visible to the tensor core
                 mbar_arrive(&z_full[it % kVtcStages]);
+                // the next tile's first raw chunk is this tile's second; a unit's last tile also consumed the
+                // unit's extra chunk (TU + 1 chunks per unit)
+                ga_slot = gb_slot;
+                ga_ph = gb_ph;
+                if (j == TU - 1) {
+                    ga_ph = ga_slot + 1 == kVtcRaw ? ga_ph ^ 1 : ga_ph;
+                    ga_slot = ga_slot + 1 == kVtcRaw ? 0 : ga_slot + 1;
+                }
             }
+            zs0 = (zs0 + U) % kVtcZChunks;
         }
     } else if (warp < kVtcProd / 32 + 4) {   // -------------------------------------- consumers -------
         const int q = warp & 3, col = lane;   // TMEM lane quarter q = plane q, lane = column
@@ -412,15 +442,15 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
             }
         }
     } else if (lane == 0) {   // ------------------------------------------------------- TMA warp -----
-        // the CTA's raw chunks in order; chunk g waits for the release of chunk g - 3 (its ring slot)
+        // the CTA's raw chunks in order; chunk g waits for the release of chunk g - kVtcRaw (its ring slot)
         const long long nchunk = nui * (TU + 1);
         for (long long g = 0; g < nchunk; g++) {
             const long long ui = g / (TU + 1);
             const int c = (int)(g - ui * (TU + 1));
             int strip, k, ys;
             unit_of(ui, strip, k, ys);
-            const int sl = (int)(g % 3);
-            if (g >= 3) mbar_wait(&c_free[sl], (uint32_t)((g / 3) - 1) & 1u);
+            const int sl = (int)(g % kVtcRaw);
+            if (g >= kVtcRaw) mbar_wait(&c_free[sl], (uint32_t)((g / kVtcRaw) - 1) & 1u);
             mbar_arrive_expect_tx(&c_full[sl], kSlotBytes);
             tma_load_3d(ring + (size_t)sl * (64 * 96), &tm_p, &c_full[sl], strip * 96, ys - R + 64 * c, 0);
         }
