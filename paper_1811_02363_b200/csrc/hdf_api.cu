@@ -581,16 +581,16 @@ int encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2, 
     return HDF_OK;
 }
 
-// 4-D fp16 map of the strip-major planes [P][Wp / 32][H][32] (k_hpass_tc.cuh): dims (32, H, strips, P),
-// box (32, rows, 1, planes), 64-byte swizzle
+// 5-D fp16 map of the strip-major planes [P][Wp / 32][H][hi 32 | lo 32] (k_hpass_tc.cuh): dims (32 columns,
+// 2 halves, H, strips, P), box (32, 1, rows, 1, planes) -> [planes][rows][32] with 64-byte rows, 64-byte swizzle
 int encode_strips(CUtensorMap* m, void* base, int H, int Wp, int P, uint32_t rows, uint32_t planes) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(HDF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[4] = {32, (cuuint64_t)H, (cuuint64_t)(Wp / 32), (cuuint64_t)P};
-    cuuint64_t strides[3] = {64, (cuuint64_t)H * 64, (cuuint64_t)H * Wp * 2};
-    cuuint32_t box[4] = {32, rows, 1, planes};
-    cuuint32_t es[4] = {1, 1, 1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    cuuint64_t dims[5] = {32, 2, (cuuint64_t)H, (cuuint64_t)(Wp / 32), (cuuint64_t)P};
+    cuuint64_t strides[4] = {64, 128, (cuuint64_t)H * 128, (cuuint64_t)H * Wp * 4};
+    cuuint32_t box[5] = {32, 1, rows, 1, planes};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(HDF_ERR_CUDA, "cuTensorMapEncodeTiled (strips) failed (%d)", (int)r);
     return HDF_OK;
@@ -1032,18 +1032,15 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         }
         memcpy(fb.taps, t2, sizeof(t2));
     }
-    // the tensor-core row pass: tensor maps of the strip-major fp16 hi/lo planes (boxes [4 planes][32 rows]
-    // [one 32-column strip], 64-byte swizzle) and of the coefficient planes (two [32 rows][32 columns]
-    // halves per tile, 128-byte swizzle)
-    CUtensorMap thi, tlo, tcc;
+    // the tensor-core row pass: tensor map of the strip-major fp16 hi/lo planes (boxes [4 planes][32 rows]
+    // [the hi or lo half of a 32-column strip], 64-byte swizzle) and of the coefficient planes (two
+    // [32 rows][32 columns] halves per tile, 128-byte swizzle)
+    CUtensorMap tz, tcc;
     hdf::HtcParams hq;
     size_t htc_smem = 0;
     if (use_htc) {
         unsigned short* ph = reinterpret_cast<unsigned short*>(w.planes);
-        const uint64_t pl = (uint64_t)K * 4 * H * F.Wp;
-        rc = encode_strips(&thi, ph, H, F.Wp, K * 4, (uint32_t)hdf::kHtcRows, 4u);
-        if (rc) return rc;
-        rc = encode_strips(&tlo, ph + pl, H, F.Wp, K * 4, (uint32_t)hdf::kHtcRows, 4u);
+        rc = encode_strips(&tz, ph, H, F.Wp, K * 4, (uint32_t)hdf::kHtcRows, 4u);
         if (rc) return rc;
         rc = encode3d(&tcc, w.cpl, (uint64_t)W, (uint64_t)H, (uint64_t)K, (uint64_t)F.Wp * 4, (uint64_t)H * F.Wp * 4,
                       32u, (uint32_t)hdf::kHtcRows, 1u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -1085,7 +1082,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
                 hq.yb1 = ty1;
                 const long long nunit = (long long)(ty1 - ty0) * hq.nstrip;
                 hdf::k_hpass_combine_tc<<<(unsigned)std::max<long long>(1, std::min<long long>(nsm, nunit)),
-                                          hdf::kHtcThreads, htc_smem, st>>>(thi, tlo, tcc, hq);
+                                          hdf::kHtcThreads, htc_smem, st>>>(tz, tcc, hq);
                 HDF_CUDA(cudaGetLastError());
             } else {
                 HDF_CUDA(hdf::launch_hpass(F.Rp, F.box, hl, st, tp, tc, hp));

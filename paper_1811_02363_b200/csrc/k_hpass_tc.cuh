@@ -8,10 +8,10 @@
 // for M = 128 (plane, row) pairs (4 planes x 32 rows):
 //   D[M x 64] = Z[M x 128] . T^T[128 x 64]   with tcgen05.mma kind::f16, fp32 accumulation in TMEM.
 // Z comes straight from HBM: the planes are stored as fp16 hi and lo parts (t = hi + lo, ~22 bits, scaled
-// by a power of two) in a strip-major layout [plane][x / 32][y][32] (k_vpass_tc.cuh writes each 64-byte
-// row of a strip with one coalesced warp store), so one TMA box [4 planes][32 rows][one strip of 32
-// columns] (64-byte rows, SWIZZLE_64B) is already a canonical K-major SW64 operand block of K = 32: no
-// conversion on the SMs.  Strips outside the image are zero-filled by the TMA and columns past W are
+// by a power of two) in a strip-major layout [plane][x / 32][y][hi 32 | lo 32] (one 128-byte line per row of
+// a strip; k_vpass_tc.cuh writes two rows' halves per warp store), so one TMA box [4 planes][32 rows][the hi
+// (or lo) half of one strip] (64-byte rows, SWIZZLE_64B) is already a canonical K-major SW64 operand block
+// of K = 32: no conversion on the SMs.  Strips outside the image are zero-filled by the TMA and columns past W are
 // exact zeros (R8).  Precision: D = z_lo T_hi + z_hi T_lo + z_hi T_hi.
 //
 // A CTA is persistent over units (32-row block, 128-column strip of output).  For each cluster k (in
@@ -71,11 +71,11 @@ HDF_DEV uint64_t umma_desc_sw64(uint32_t saddr) {
            (4ull << 61);
 }
 
-HDF_DEV void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3) {
+HDF_DEV void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3, int c4) {
     asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
         : "memory");
 }
 
@@ -92,8 +92,7 @@ HDF_DEV void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {
 }
 HDF_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-__global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __grid_constant__ CUtensorMap tm_hi,
-                                                                     const __grid_constant__ CUtensorMap tm_lo,
+__global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __grid_constant__ CUtensorMap tm_z,
                                                                      const __grid_constant__ CUtensorMap tm_c,
                                                                      const __grid_constant__ HtcParams P) {
     extern __shared__ __align__(1024) unsigned char sm_raw[];
@@ -120,8 +119,7 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
         *reinterpret_cast<unsigned short*>(Tl + vtc_off(j, i, kHtcN)) = l;
     }
     if (tid == 0) {
-        prefetch_tmap(&tm_hi);
-        prefetch_tmap(&tm_lo);
+        prefetch_tmap(&tm_z);
         prefetch_tmap(&tm_c);
         for (int s = 0; s < kHtcNB; s++) {
             mbar_init(&box_full[s], 1);
@@ -298,8 +296,8 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
                     if (g >= kHtcNB) mbar_wait(&box_free[sl], (uint32_t)((g / kHtcNB) - 1) & 1u);
                     mbar_arrive_expect_tx(&box_full[sl], kHtcSlotBytes);
                     unsigned char* dst = ring + (size_t)sl * kHtcSlotBytes;
-                    tma_load_4d(dst, &tm_hi, &box_full[sl], 0, y0, s0 + b, 4 * k);
-                    tma_load_4d(dst + kHtcBoxBytes, &tm_lo, &box_full[sl], 0, y0, s0 + b, 4 * k);
+                    tma_load_5d(dst, &tm_z, &box_full[sl], 0, 0, y0, s0 + b, 4 * k);                   // hi half
+                    tma_load_5d(dst + kHtcBoxBytes, &tm_z, &box_full[sl], 0, 1, y0, s0 + b, 4 * k);    // lo half
                     if (b == 3 || b == 5) {   // tile (b - 3) / 2's coefficients
                         const int t = (b - 3) / 2;
                         const long long h = 2 * kk + t;

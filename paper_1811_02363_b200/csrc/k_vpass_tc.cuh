@@ -26,8 +26,11 @@
 //     one 16-byte store = 8 consecutive rows of one (plane, column)); arrive on "Z full";
 //   * MMA warp: waits "Z full" and "D free", issues 3 Kp/16 MMAs (M = 128, N = 64, K = 16) and commits
 //     them to "Z free" and "D full" (Z double-buffered in shared memory, D in TMEM);
-//   * consumers (4 warps, TMEM lane quarter = plane): load the 64 output rows of their (plane, column),
-//     release the stage, scale back and store (coalesced over the 32 columns).
+//   * consumers (4 warps, TMEM lane quarter = plane; HDF_VTC_CONS=8 splits the rows over 8): load the 64
+//     output rows of their (plane, column), release the stage and store them: fp32 planes (scaled back,
+//     coalesced over the 32 columns), or -- for the tensor-core row pass -- fp16 hi/lo parts in the
+//     strip-major layout [plane][strip][y][hi 32 | lo 32], two rows' 64-byte halves per warp store after one
+//     lane-pair exchange (k_hpass_tc.cuh).
 // The Toeplitz operand T (hi, lo) is staged once per CTA.
 #pragma once
 #include <cuda_fp16.h>
@@ -41,7 +44,12 @@ namespace hdf {
 constexpr int kVtcRows = 64;       // output rows per tile (UMMA N)
 constexpr int kVtcM = 128;         // (plane, column) pairs per tile (UMMA M): 4 planes x 32 columns
 constexpr int kVtcProd = 256;      // producer threads (8 warps)
-constexpr int kVtcThreads = kVtcProd + 128 + 64;   // + consumers + MMA warp + TMA warp
+#ifndef HDF_VTC_CONS
+#define HDF_VTC_CONS 4
+#endif
+constexpr int kVtcCons = HDF_VTC_CONS;                      // consumer warps (4: 64 rows each, 8: 32 rows each)
+constexpr int kVtcNRW = kVtcRows / (kVtcCons / 4);          // output rows per consumer thread
+constexpr int kVtcThreads = kVtcProd + 32 * kVtcCons + 64;  // + consumers + MMA warp + TMA warp
 
 inline __host__ __device__ int vtc_kp(int R) { return ((kVtcRows + 2 * R) + 15) & ~15; }
 constexpr int kVtcMaxR = 24;       // Kp <= 112: the shared-memory budget below
@@ -70,8 +78,8 @@ inline __host__ __device__ size_t vpass_tc_smem(int R) {
 struct VtcParams {
     const float* centres;  // [K][3]
     float* planes;         // [4K][H][Wp] fp32 (ph == NULL)
-    unsigned short* ph;    // else fp16 hi and lo parts, strip-major: ph [4K][Wp / 32][H][32], then lo at
-                           // ph + 4K H Wp (k_hpass_tc.cuh); Wp a multiple of 32
+    unsigned short* ph;    // else fp16 hi and lo parts, strip-major: ph [4K][Wp / 32][H][hi 32 | lo 32]
+                           // (k_hpass_tc.cuh); Wp a multiple of 32
     int wexp;              // ph: stored value = t 2^(14 - e2 - wexp) (u planes), t 2^(14 - wexp) (b planes)
     const int* absmax;     // max |f| as float bits (k_absmax)
     long long pstride;     // H * Wp
@@ -182,7 +190,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
             mbar_init(&z_full[s], kVtcProd);
             mbar_init(&z_free[s], 1);
             mbar_init(&d_full[s], 1);
-            mbar_init(&d_free[s], 128);
+            mbar_init(&d_free[s], 32 * kVtcCons);
         }
         fence_barrier_init();
     }
@@ -315,14 +323,14 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
             }
             zs0 = (zs0 + U) % kVtcZChunks;
         }
-    } else if (warp < kVtcProd / 32 + 4) {   // -------------------------------------- consumers -------
-        const int q = warp & 3, col = lane;   // TMEM lane quarter q = plane q, lane = column
+    } else if (warp < kVtcProd / 32 + kVtcCons) {   // ------------------------------- consumers -------
+        // TMEM lane quarter q = plane q, lane = column; consumer warp group h takes rows r0 .. r0 + NRW - 1
+        const int q = warp & 3, col = lane, r0 = ((warp - kVtcProd / 32) >> 2) * kVtcNRW;
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         // fp32 output: t = D / su (u planes), D / sr (b planes); fp16 hi/lo output: D 2^-wexp (both scaled,
         // |value| <= 2^14 since the taps sum to at most 2^wexp)
         const float inv = P.ph ? ldexpf(1.f, -P.wexp) : (q < 3) ? 1.f / su : 1.f / sr;   // exact (powers of two)
         const int step = P.Wp;
-        const long long lo_off = 4LL * P.K * P.pstride;
         long long it = 0;
         for (long long ui = 0; ui < nui; ui++) {
             int strip, k, ys;
@@ -334,60 +342,51 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                 const int s = (int)(it % kVtcStages);
                 mbar_wait(&d_full[s], (uint32_t)(it / kVtcStages) & 1u);
                 tc_fence_after();
-                float v[kVtcRows];
+                float v[kVtcNRW];
 #pragma unroll
-                for (int n0 = 0; n0 < kVtcRows; n0 += 16) {
+                for (int n0 = 0; n0 < kVtcNRW; n0 += 16) {
                     float t16[16];
-                    tmem_ld16(tbase + lane_base + (uint32_t)(s * kVtcRows + n0), t16);
+                    tmem_ld16(tbase + lane_base + (uint32_t)(s * kVtcRows + r0 + n0), t16);
 #pragma unroll
                     for (int jj = 0; jj < 16; jj++) v[n0 + jj] = t16[jj];
                 }
                 tc_fence_before();
                 mbar_arrive(&d_free[s]);
-                if (P.ph) {   // strip-major fp16 planes: [plane][strip][H][32] (k_hpass_tc.cuh)
-                    if (yt < P.H) {   // (columns past W hold exact zeros: b = 0 there)
-                        const int nr = min(kVtcRows, P.H - yt);
-                        unsigned short* oh = P.ph + (long long)(4 * k + q) * P.pstride + (long long)strip * P.H * 32 +
-                                             (long long)yt * 32 + col;
-                        unsigned short* ol = oh + lo_off;
-                        if (nr == kVtcRows) {   // whole tile: constant offsets (row stride 64 bytes)
+                if (P.ph) {   // strip-major fp16 planes: [plane][strip][H][hi 32 | lo 32] (k_hpass_tc.cuh)
+                    if (yt + r0 < P.H) {   // (columns past W hold exact zeros: b = 0 there)
+                        // rows r, r + 1 at a time: after one exchange with the partner lane (col ^ 1) an even lane
+                        // holds row r's (hi, lo) words of columns col, col + 1 and an odd lane row r + 1's of
+                        // columns col - 1, col, so one warp store writes two rows' 64-byte hi halves, the next
+                        // their lo halves (whole 128-byte lines per row pair)
+                        const int odd = col & 1;
+                        const uint32_t sel = odd ? 0x3276u : 0x5410u;
+                        const int nr = min(kVtcNRW, P.H - yt - r0);
+                        uint32_t* o = reinterpret_cast<uint32_t*>(P.ph) + (long long)(4 * k + q) * P.pstride +
+                                      (long long)strip * P.H * 32 + (long long)(yt + r0 + odd) * 32 + (col >> 1);
 #pragma unroll
-                            for (int jj = 0; jj < kVtcRows; jj += 2) {
-                                uint32_t hi, lo;
-                                split_f16x2(v[jj] * inv, v[jj + 1] * inv, hi, lo);
-                                oh[jj * 32] = (unsigned short)(hi & 0xFFFFu);
-                                oh[jj * 32 + 32] = (unsigned short)(hi >> 16);
-                                ol[jj * 32] = (unsigned short)(lo & 0xFFFFu);
-                                ol[jj * 32 + 32] = (unsigned short)(lo >> 16);
-                            }
-                        } else {
-#pragma unroll
-                            for (int jj = 0; jj < kVtcRows; jj += 2) {
-                                uint32_t hi, lo;
-                                split_f16x2(v[jj] * inv, v[jj + 1] * inv, hi, lo);
-                                if (jj < nr) {
-                                    oh[jj * 32] = (unsigned short)(hi & 0xFFFFu);
-                                    ol[jj * 32] = (unsigned short)(lo & 0xFFFFu);
-                                }
-                                if (jj + 1 < nr) {
-                                    oh[jj * 32 + 32] = (unsigned short)(hi >> 16);
-                                    ol[jj * 32 + 32] = (unsigned short)(lo >> 16);
-                                }
+                        for (int jj = 0; jj < kVtcNRW; jj += 2) {
+                            uint32_t hi, lo;
+                            split_f16x2(v[jj] * inv, v[jj + 1] * inv, hi, lo);   // (row r, row r + 1) per word
+                            const uint32_t ph2 = __shfl_xor_sync(0xffffffffu, hi, 1);
+                            const uint32_t pl2 = __shfl_xor_sync(0xffffffffu, lo, 1);
+                            if (nr == kVtcNRW || jj + odd < nr) {
+                                o[jj * 32] = __byte_perm(hi, ph2, sel);
+                                o[jj * 32 + 16] = __byte_perm(lo, pl2, sel);
                             }
                         }
                     }
-                } else if (x < P.W && yt < P.H) {
-                    const int nr = min(kVtcRows, P.H - yt);
-                    float* o = base + (long long)yt * step;
-                    if (nr == kVtcRows) {   // whole tile: a running pointer, no per-row predicate
+                } else if (x < P.W && yt + r0 < P.H) {
+                    const int nr = min(kVtcNRW, P.H - yt - r0);
+                    float* o = base + (long long)(yt + r0) * step;
+                    if (nr == kVtcNRW) {   // whole tile: a running pointer, no per-row predicate
 #pragma unroll
-                        for (int jj = 0; jj < kVtcRows; jj++) {
+                        for (int jj = 0; jj < kVtcNRW; jj++) {
                             o[0] = v[jj] * inv;
                             o += step;
                         }
                     } else {
 #pragma unroll
-                        for (int jj = 0; jj < kVtcRows; jj++) {
+                        for (int jj = 0; jj < kVtcNRW; jj++) {
                             if (jj < nr) o[0] = v[jj] * inv;
                             o += step;
                         }
@@ -395,7 +394,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                 }
             }
         }
-    } else if (warp == kVtcProd / 32 + 4) {   // -------------------------------------- MMA warp ---------
+    } else if (warp == kVtcProd / 32 + kVtcCons) {   // ------------------------------ MMA warp ---------
         {
             // the whole warp runs the loop (warp-uniform values in uniform registers) and one elected lane
             // issues: 32-bit incremental index math only (the ring slot of the tile's first chunk advances by
