@@ -143,19 +143,34 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
     __syncthreads();
     // Parallel (round-robin) Jacobi: each step rotates D'/2 disjoint pairs at once (D' = D rounded up
     // to even; index D' - 1 >= D is a dummy): column rotations for all pairs, then row rotations,
-    // then the next pairing; D' - 1 steps per sweep.
+    // then the next pairing; D' - 1 steps per sweep.  The pairings are tabulated once, and in the update
+    // phases warp w takes the pairs w, w + 8, .. with lane = matrix row (or column): no integer division
+    // or modulo per element (they were most of the ~3.3 us per step of the first version).
     __shared__ double rc[kPcaMaxD / 2], rs[kPcaMaxD / 2];
+    __shared__ unsigned char pp[kPcaMaxD - 1][kPcaMaxD / 2], pq[kPcaMaxD - 1][kPcaMaxD / 2];
     __shared__ int done;
     const int Dp = (D + 1) & ~1, np = Dp / 2;
+    constexpr int NW = kPcaThreads / 32;
+    for (int e = tid; e < (Dp - 1) * np; e += kPcaThreads) {
+        const int step = e / np, i = e - step * np;
+        // round robin: position 0 holds index 0, position k >= 1 holds 1 + (k - 1 + step) mod (Dp - 1);
+        // pair i = (positions i, Dp - 1 - i)
+        auto ring = [&](int k) { return k == 0 ? 0 : 1 + (k - 1 + step) % (Dp - 1); };
+        int p = ring(i), q = ring(Dp - 1 - i);
+        if (p > q) { const int t = p; p = q; q = t; }
+        pp[step][i] = (unsigned char)p;
+        pq[step][i] = (unsigned char)q;
+    }
+    __syncthreads();
     for (int sweep = 0; sweep < 60; sweep++) {
         if (warp == 0) {
             double off = 0.0, fro = 0.0;
-            for (int e = lane; e < D * D; e += 32) {
-                const int a = e / D, b = e - a * D;
-                const double v = C[a * kPcaLd + b];
-                fro += v * v;
-                if (a != b) off += v * v;
-            }
+            for (int a = 0; a < D; a++)
+                for (int b = lane; b < D; b += 32) {
+                    const double v = C[a * kPcaLd + b];
+                    fro += v * v;
+                    if (a != b) off += v * v;
+                }
             for (int o = 16; o > 0; o >>= 1) {
                 off += __shfl_xor_sync(0xffffffffu, off, o);
                 fro += __shfl_xor_sync(0xffffffffu, fro, o);
@@ -167,12 +182,8 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
         __syncthreads();
         if (done) break;
         for (int step = 0; step < Dp - 1; step++) {
-            // round robin: position 0 holds index 0, position k >= 1 holds 1 + (k - 1 + step) mod (Dp - 1);
-            // pair i = (positions i, Dp - 1 - i)
-            auto ring = [&](int k) { return k == 0 ? 0 : 1 + (k - 1 + step) % (Dp - 1); };
-            for (int i = tid; i < np; i += kPcaThreads) {   // the step's pairs (ring[i], ring[Dp - 1 - i])
-                int p = ring(i), q = ring(Dp - 1 - i);
-                if (p > q) { const int t = p; p = q; q = t; }
+            for (int i = tid; i < np; i += kPcaThreads) {   // the step's rotation angles
+                const int p = pp[step][i], q = pq[step][i];
                 double c = 1.0, sn = 0.0;
                 if (q < D) {
                     const double apq = C[p * kPcaLd + q];
@@ -180,7 +191,8 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
                         // the angle in fp32 (an inexact angle only slows the last sweeps down), the
                         // rotation itself in fp64 and exactly orthogonal to rounding: c from one Newton
                         // step of 1/sqrt(1 + t^2) seeded in fp32, s = t c
-                        const float tau = (float)((C[q * kPcaLd + q] - C[p * kPcaLd + p]) / (2.0 * apq));
+                        // (tau itself in fp32 too: an fp64 division is a long dependent chain per step)
+                        const float tau = (float)(C[q * kPcaLd + q] - C[p * kPcaLd + p]) / (2.0f * (float)apq);
                         const float tf = copysignf(1.0f, tau) / (fabsf(tau) + sqrtf(fmaf(tau, tau, 1.0f)));
                         const double t = (double)tf, u = fma(t, t, 1.0);
                         double r = (double)rsqrtf((float)u);
@@ -194,29 +206,31 @@ __global__ void __launch_bounds__(kPcaThreads) k_pca_eig(const double* part, int
                 rs[i] = sn;
             }
             __syncthreads();
-            for (int e = tid; e < np * D; e += kPcaThreads) {   // columns p, q of C and V (all rows k)
-                const int i = e / D, k = e - i * D;
-                int p = ring(i), q = ring(Dp - 1 - i);
-                if (p > q) { const int t = p; p = q; q = t; }
-                if (q >= D || rs[i] == 0.0) continue;
-                const double c = rc[i], sn = rs[i];
-                const double akp = C[k * kPcaLd + p], akq = C[k * kPcaLd + q];
-                C[k * kPcaLd + p] = c * akp - sn * akq;
-                C[k * kPcaLd + q] = sn * akp + c * akq;
-                const double vkp = V[k * kPcaLd + p], vkq = V[k * kPcaLd + q];
-                V[k * kPcaLd + p] = c * vkp - sn * vkq;
-                V[k * kPcaLd + q] = sn * vkp + c * vkq;
+            for (int i = warp; i < np; i += NW) {   // columns p, q of C and V: lane = row k
+                const double sn = rs[i];
+                const int p = pp[step][i], q = pq[step][i];
+                if (q >= D || sn == 0.0) continue;
+                const double c = rc[i];
+                for (int k = lane; k < D; k += 32) {
+                    const double akp = C[k * kPcaLd + p], akq = C[k * kPcaLd + q];
+                    C[k * kPcaLd + p] = c * akp - sn * akq;
+                    C[k * kPcaLd + q] = sn * akp + c * akq;
+                    const double vkp = V[k * kPcaLd + p], vkq = V[k * kPcaLd + q];
+                    V[k * kPcaLd + p] = c * vkp - sn * vkq;
+                    V[k * kPcaLd + q] = sn * vkp + c * vkq;
+                }
             }
             __syncthreads();
-            for (int e = tid; e < np * D; e += kPcaThreads) {   // rows p, q (all columns k)
-                const int i = e / D, k = e - i * D;
-                int p = ring(i), q = ring(Dp - 1 - i);
-                if (p > q) { const int t = p; p = q; q = t; }
-                if (q >= D || rs[i] == 0.0) continue;
-                const double c = rc[i], sn = rs[i];
-                const double apk = C[p * kPcaLd + k], aqk = C[q * kPcaLd + k];
-                C[p * kPcaLd + k] = c * apk - sn * aqk;
-                C[q * kPcaLd + k] = sn * apk + c * aqk;
+            for (int i = warp; i < np; i += NW) {   // rows p, q (all columns k): lane = column k
+                const double sn = rs[i];
+                const int p = pp[step][i], q = pq[step][i];
+                if (q >= D || sn == 0.0) continue;
+                const double c = rc[i];
+                for (int k = lane; k < D; k += 32) {
+                    const double apk = C[p * kPcaLd + k], aqk = C[q * kPcaLd + k];
+                    C[p * kPcaLd + k] = c * apk - sn * aqk;
+                    C[q * kPcaLd + k] = sn * apk + c * aqk;
+                }
             }
             __syncthreads();
         }
