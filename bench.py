@@ -136,12 +136,14 @@ def stage_work(cfg, K: int, H: int, W: int, iir: bool = False):
 SAMPLED_STRIDE = {"c5": 64, "c3": 4}
 
 
-def tc_passes(cfg, W: int, variant: str = "soft"):
+def tc_passes(cfg, H: int, W: int, nsm: int, variant: str = "soft"):
     """Which filter passes run on the tensor cores for this workload (the library's own rule, hdf_api.cu:
-    colour Gaussian FIR with f = p, 4 <= R <= 24, W % 4 == 0; HDF_VPASS_FMA / HDF_HPASS_FMA override)."""
+    colour Gaussian FIR with f = p, 4 <= R <= 24, W % 4 == 0; the row pass when its (32-row, 128-column)
+    units fill the SMs; HDF_VPASS_FMA / HDF_HPASS_FMA override)."""
     vtc = (cfg.kind == "gaussian" and variant != "iir" and cfg.bilateral and cfg.n == 3 and cfg.rho == 3
            and 4 <= cfg.radius <= 24 and W % 4 == 0 and os.environ.get("HDF_VPASS_FMA", "0") in ("", "0"))
-    htc = vtc and os.environ.get("HDF_HPASS_FMA", "0") in ("", "0")
+    env = os.environ.get("HDF_HPASS_FMA", "")
+    htc = vtc and (env == "0" if env else ((H + 31) // 32) * ((W + 127) // 128) >= nsm)
     return vtc, htc
 
 
@@ -316,7 +318,7 @@ def run_ours(args, rank: int, world: int, dist):
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
 
     # dram bytes per launch from the committed ncu --set full capture of this workload (profiles/), if any
-    vtc, htc = tc_passes(cfg, W, args.variant)
+    vtc, htc = tc_passes(cfg, H, W, nsm, args.variant)
     kname = {"vpass": "k_range_vpass_tc" if vtc else "k_range_vpass",
              "hpass": "k_hpass_combine_tc" if htc else "k_hpass_combine", "coeffs": "k_coeffs_tc"}
     # the FIR passes on the tensor cores (banded Toeplitz products, kind::f16 with the hi/lo split: 3 MMAs

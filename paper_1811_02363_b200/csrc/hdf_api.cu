@@ -811,9 +811,14 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     if (const char* e = getenv("HDF_VPASS_FMA")) {
         if (atoi(e)) use_tc = false;
     }
-    bool use_htc = use_tc && F.R <= hdf::kHtcMaxR;
+    // The tensor-core row pass parallelises over (32-row block, 128-column strip) units with every cluster
+    // inside a unit: it is used when the units fill the SMs (config 5: 4096 units; a 512 x 512 image has
+    // only 64, and there the CUDA-core row pass is faster: c2b 61 vs 95 us).  HDF_HPASS_FMA=1 / =0 forces
+    // the CUDA-core / tensor-core row pass.
+    bool use_htc = use_tc && F.R <= hdf::kHtcMaxR &&
+                   (long long)((H + hdf::kHtcRows - 1) / hdf::kHtcRows) * ((W + 127) / 128) >= nsm;
     if (const char* e = getenv("HDF_HPASS_FMA")) {
-        if (atoi(e)) use_htc = false;
+        if (*e) use_htc = use_tc && F.R <= hdf::kHtcMaxR && atoi(e) == 0;
     }
     int wexp = 0;   // 2^wexp >= the sum of the taps (the fp16 planes' scale)
     {

@@ -1,4 +1,4 @@
-"""Clustering diagnostics on the GPU: python tools/dbg_cluster.py c1 c2b ...
+"""Clustering diagnostics on the GPU: python tools/dbg_cluster.py c1 c2b c5s64 ...
 Times hdf.cluster, compares with the oracle, and summarises the worker trace (per-node split spans)."""
 import os, sys, time, numpy as np, torch
 sys.path.insert(0, '.')
@@ -8,8 +8,15 @@ for _ in range(20):
     _a @ _a
 torch.cuda.synchronize()
 for name in sys.argv[1:]:
-    cfg, f, p = synth.make(name)
+    # "c5s64": the sampled mode's input, the stride-64 sample of config 5 (R18)
+    base, _, stride = name.partition("s")
+    cfg, f, p = synth.make(base)
     pd = torch.from_numpy(p).cuda()
+    if stride:
+        st = int(stride)
+        M = (pd.numel() // cfg.rho + st - 1) // st
+        pd = hdf.sample_guide(pd, 0, st, M).reshape(M, 1, cfg.rho)
+        p = pd.cpu().numpy()
     os.environ["HDF_BISECT_TRACE"] = "0"
     ts = []
     for rep in range(5):
