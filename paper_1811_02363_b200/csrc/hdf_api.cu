@@ -359,7 +359,11 @@ int launch_cluster(const float* p, int H, int W, int rho, int K, float* centres,
     }
     A.ctamax = std::min<long long>(A.cap, 2048);   // smaller nodes: one CTA each (measured best on c2b)
     if (const char* e = getenv("HDF_BISECT_CTA_MAX")) A.ctamax = std::min<long long>(A.cap, atoll(e));
-    A.qmax = 0;   // groups of 4 CTAs for nodes of at most qmax points (cluster batches; off: measured slower)
+    // groups of 4 CTAs for nodes of at most qmax points (cluster batches): with K >= 64 the tree has enough
+    // ready mid-size nodes to keep 4x more group workers busy (the sampled c5 input, 262k points: 0.86 ->
+    // 0.74-0.76 ms, qmax 16k-32k); with K = 32 they only add speculative splits (c2b 0.50 -> 0.54 ms, c4
+    // 0.66 -> 0.71 ms), so they stay off there
+    A.qmax = K >= 64 ? std::min<long long>(4LL * A.cap, 32768) : 0;
     if (const char* e = getenv("HDF_BISECT_QUAD_MAX")) A.qmax = std::min<long long>(4LL * A.cap, atoll(e));
     {
         cudaLaunchConfig_t cfg = {};
