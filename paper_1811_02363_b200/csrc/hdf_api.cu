@@ -1471,39 +1471,74 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
         const float* pdev = fd;
         // from here on, a failure synchronises the stream before returning (copies from the caller's
         // buffers may be in flight)
+        cudaStream_t cs = copy_stream();
+        if (!cs) return fail(HDF_ERR_CUDA, "copy stream creation failed");
         auto bail = [&](int code) {
             cudaStreamSynchronize(st);
+            cudaStreamSynchronize(cs);
             return code;
         };
+        const bool sampled = cluster_stride > 1;
+        // Sampled mode: the bulk input copy runs on the copy stream while the caller's stream copies the
+        // stride sample straight from the host guide (one strided 2-D copy) and clusters it, so the
+        // clustering is hidden under the bulk copy; the filter waits for both.  Exact mode: the copy, then
+        // the clustering of every pixel, in order on the caller's stream.
+        cudaEvent_t ev_fork = nullptr, ev_in = nullptr;
+        auto destroy_io = [&]() {
+            if (ev_fork) cudaEventDestroy(ev_fork);
+            if (ev_in) cudaEventDestroy(ev_in);
+            ev_fork = ev_in = nullptr;
+        };
+        cudaStream_t in_st = st;
+        if (sampled) {
+            if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) != cudaSuccess) {
+                destroy_io();
+                return bail(fail(HDF_ERR_CUDA, "event creation failed"));
+            }
+            cudaEventRecord(ev_fork, st);   // the copy stream starts after the caller's earlier work
+            cudaStreamWaitEvent(cs, ev_fork, 0);
+            in_st = cs;
+        }
         {
-            ProfScope prof(HDF_STAGE_H2D, st);
-            if (cudaMemcpyAsync(fd, f_host, sizeof(float) * (size_t)H * W * n, cudaMemcpyHostToDevice, st) !=
-                cudaSuccess)
+            ProfScope prof(HDF_STAGE_H2D, in_st);
+            if (cudaMemcpyAsync(fd, f_host, sizeof(float) * (size_t)H * W * n, cudaMemcpyHostToDevice, in_st) !=
+                cudaSuccess) {
+                destroy_io();
                 return bail(fail(HDF_ERR_CUDA, "input copy: %s", cudaGetErrorString(cudaGetLastError())));
+            }
             if (!f_is_p) {
-                if (cudaMemcpyAsync(pd, p_host, sizeof(float) * (size_t)H * W * rho, cudaMemcpyHostToDevice, st) !=
-                    cudaSuccess)
+                if (cudaMemcpyAsync(pd, p_host, sizeof(float) * (size_t)H * W * rho, cudaMemcpyHostToDevice, in_st) !=
+                    cudaSuccess) {
+                    destroy_io();
                     return bail(fail(HDF_ERR_CUDA, "guide copy: %s", cudaGetErrorString(cudaGetLastError())));
+                }
                 pdev = pd;
             }
         }
+        if (sampled) cudaEventRecord(ev_in, cs);
         // cluster (in the filter workspace's cluster region; status read back at the end) then filter
         Carver c2(fws);
         FilterWS w = carve_filter(c2, H, W, n, rho, K, round_up(W, 32), true);
         ClusterReadback crb;
-        if (cluster_stride == 1) {
+        if (!sampled) {
             rc = launch_cluster(pdev, H, W, rho, K, cd, nullptr, nullptr, w.cluster_ws, st, &crb);
-        } else {   // the sampled mode (hdf_cluster_sampled): the stride sample, then the same procedure
+        } else {   // the sampled mode (hdf_cluster_sampled): the stride sample p.flat[0::s], then the same procedure
             const long long N = (long long)H * W, M = (N + cluster_stride - 1) / cluster_stride;
-            const unsigned nb = (unsigned)std::min<long long>((M * rho + 255) / 256, (long long)nsm_of_device() * 16);
-            hdf::k_sample_guide<<<nb, 256, 0, st>>>(pdev, rho, 0, cluster_stride, smp, M);
-            if (cudaGetLastError() != cudaSuccess) return bail(fail(HDF_ERR_CUDA, "sample launch failed"));
+            {
+                ProfScope prof(HDF_STAGE_H2D, st);
+                if (cudaMemcpy2DAsync(smp, sizeof(float) * (size_t)rho, p_host, sizeof(float) * (size_t)rho * cluster_stride,
+                                      sizeof(float) * (size_t)rho, (size_t)M, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+                    destroy_io();
+                    return bail(fail(HDF_ERR_CUDA, "sample copy: %s", cudaGetErrorString(cudaGetLastError())));
+                }
+            }
             rc = launch_cluster(smp, 1, (int)M, rho, K, cd, nullptr, nullptr, w.cluster_ws, st, &crb);
+            if (!rc) cudaStreamWaitEvent(st, ev_in, 0);   // the filter needs the whole input
         }
+        destroy_io();   // (destroying a recorded event is safe: the waits were already enqueued)
         if (rc) return bail(rc);
-        // the output rows are copied out chunk by chunk on a copy stream while the row pass continues
-        cudaStream_t cs = copy_stream();
-        if (!cs) return bail(fail(HDF_ERR_CUDA, "copy stream creation failed"));
+        // the output rows are copied out chunk by chunk on the copy stream while the row pass continues
         constexpr int kChunks = 8;
         cudaEvent_t evs[kChunks];
         int nev = 0;

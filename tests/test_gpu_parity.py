@@ -421,6 +421,27 @@ def test_k_too_large_inside_filter_pads_centres(hdf):
     assert e.value.achievable == 5
 
 
+@pytest.mark.parametrize("name,H,W,stride", [("c2a", 300, 260, 7), ("c4", 150, 173, 4), ("c1", 1030, 1100, 64)])
+def test_filter_host_sampled_equals_device_path(hdf, name, H, W, stride):
+    """The host path's sampled mode copies the stride sample straight from the host guide (a strided 2-D
+    copy) and clusters it while the bulk input copy runs on the copy stream: centres and output must be
+    bit-identical to cluster_sampled + filter on the device."""
+    cfg, f, p = synth.make(name, H, W)
+    fh = torch.from_numpy(np.ascontiguousarray(f, dtype=np.float32)).pin_memory()
+    ph = fh if p is f else torch.from_numpy(np.ascontiguousarray(p, dtype=np.float32)).pin_memory()
+    g_h, cen_h, nfl_h, info = hdf.filter_host(fh, ph, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius,
+                                               sigma_r=cfg.sigma_r, K=cfg.K, cluster_stride=stride)
+    fd = fh.cuda()
+    pd = fd if p is f else ph.cuda()
+    cen_d, _ = hdf.cluster_sampled(pd, cfg.K, stride)
+    res = hdf.filter(fd, pd, kind=cfg.kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                     centres=cen_d, count_flagged=True)
+    torch.cuda.synchronize()
+    assert torch.equal(cen_h, cen_d.cpu())
+    assert torch.equal(g_h, res.g.cpu())
+    assert nfl_h == res.n_flagged
+
+
 def test_filter_host_validates_before_copying_and_reports_illcond(hdf):
     fh = torch.rand((20, 30, 3)).pin_memory() * 255.0
     with pytest.raises(hdf.HdfError) as e:          # sigma_r <= 0: rejected before any copy
