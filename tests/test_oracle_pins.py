@@ -539,6 +539,29 @@ def test_iir_dc_gain_and_symmetry(s):
     assert abs(h.sum() / G - 1.0) < 1e-9               # the impulse response integrates to G
 
 
+@pytest.mark.parametrize("s", [0.5, 1.3, 2.5, 4.0, 8.0])
+def test_iir_impulse_response_closed_form(s):
+    """The causal recursion w_t = G B x_t + a1 w_{t-1} + a2 w_{t-2} + a3 w_{t-3} has the impulse response
+    G B sum_i r_i p_i^t (t >= 0), p_i the roots of z^3 - a1 z^2 - a2 z - a3, r_i = p_i^2 / prod_{j != i}
+    (p_i - p_j); the anti-causal pass mirrors it with gain B.  Their cascade, away from the image ends, is
+    y_t = G B^2 sum_{i,j} r_i r_j p_i^|t| / (1 - p_i p_j) -- a closed form from the coefficients alone
+    (numpy's polynomial roots), so a wrong index, sign or pass direction in the oracle's loops fails it."""
+    B, a1, a2, a3 = oracle.young_coeffs(s)
+    G = math.sqrt(2.0 * math.pi) * s
+    pr = np.roots([1.0, -a1, -a2, -a3]).astype(np.complex128)
+    assert np.all(np.abs(pr) < 1.0)                      # a stable causal recursion
+    r = np.array([pr[i] ** 2 / np.prod([pr[i] - pr[j] for j in range(3) if j != i]) for i in range(3)])
+    n = int(60 * s) + 301
+    x = np.zeros(n)
+    x[n // 2] = 1.0
+    h = oracle.young1d(x, s)
+    t = np.arange(int(6 * s) + 3)
+    want = np.real(G * B * B * np.einsum("i,j,it,ij->t", r, r, pr[:, None] ** t[None, :],
+                                         1.0 / (1.0 - pr[:, None] * pr[None, :])))
+    assert np.max(np.abs(h[n // 2 + t] - want)) < 1e-11 * abs(want[0])
+    assert np.max(np.abs(h[n // 2 - t] - want)) < 1e-11 * abs(want[0])
+
+
 @pytest.mark.parametrize("s,tol", [(0.5, 0.1), (1.0, 0.1), (2.0, 0.07), (2.5, 0.06), (5.0, 0.04), (8.0, 0.03)])
 def test_iir_impulse_response_is_gaussian(s, tol):
     n = int(20 * s) + 41
