@@ -129,11 +129,13 @@ def stage_work(cfg, K: int, H: int, W: int, iir: bool = False):
 
 
 # The sampled clustering mode's stride per workload (P:329 'any efficient clustering'), chosen from the
-# measured sweep (profiles/r02b_sampled_sweep.jsonl) and held to R15's 5% rule by
-# tests/test_gpu_cluster.py (c5: 1.008 x the exact oracle pipeline's MSE on 2^16 brute-force pixels;
-# c3: 0.99).  The NLM config c4 fails R15 at every stride tried (1.22 / 1.41 / 1.15), so it and the
-# small images (where the clustering is latency-bound, not size-bound) cluster every pixel.
-SAMPLED_STRIDE = {"c5": 64, "c3": 4}
+# measured sweeps (profiles/r02b_sampled_sweep.jsonl, profiles/r02t_sampled_sweep_c3.jsonl) and held to
+# R15's 5% rule by tests/test_gpu_cluster.py (c5: 1.008 x the exact oracle pipeline's MSE on 2^16
+# brute-force pixels; c3 at stride 16: 0.95, 1.11 ms against 1.56 ms at stride 4 once the stride sample
+# of a rho = 31 node is staged in shared memory).  The NLM config c4 fails R15 at every stride tried
+# (1.22 / 1.41 / 1.15), so it and the small images (where the clustering is latency-bound, not
+# size-bound) cluster every pixel.
+SAMPLED_STRIDE = {"c5": 64, "c3": 16}
 
 
 def tc_passes(cfg, H: int, W: int, nsm: int, variant: str = "soft"):

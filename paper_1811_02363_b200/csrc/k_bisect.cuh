@@ -1313,12 +1313,16 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
     int par = 0;
 
     // ---- 1. the CTA's members: resident tile, TMA issued now, awaited after the seed exchange ----
-    TileLd rt{nullptr, 0u};
-    if (resident) rt = tile_issue(Pg + (size_t)a * rho, np, rho, io.dynX, S);
-    // ---- 2. farthest pair of the stride sample members[0::stride] (R3) ----
     const int stride = (m + kFpCap - 1) / kFpCap, sN = (m + stride - 1) / stride;
+    // The stride sample is staged in shared memory: in its own area for rho <= kSampRho, else in the
+    // tile area (sN <= cap), whose TMA is then issued after the farthest pair has read the sample (read
+    // from global memory element by element, the sample cost ~30 us per seeding phase at rho = 31)
     const bool insm = io.dynS != nullptr;
-    if (insm) {
+    float* const sbuf = insm ? io.dynS : (sN <= A.cap ? io.dynX : nullptr);
+    TileLd rt{nullptr, 0u};
+    if (resident && insm) rt = tile_issue(Pg + (size_t)a * rho, np, rho, io.dynX, S);
+    // ---- 2. farthest pair of the stride sample members[0::stride] (R3) ----
+    if (sbuf) {
         constexpr int U = 8;
         for (int f0 = 0; f0 < sN * rho; f0 += U * kBT) {
             float vv[U];
@@ -1331,7 +1335,7 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const int f = f0 + u * kBT + tid;
-                if (f < sN * rho) io.dynS[f] = vv[u];
+                if (f < sN * rho) sbuf[f] = vv[u];
             }
         }
         __syncthreads();
@@ -1343,7 +1347,10 @@ HDF_DEV void split_node(const BisectArgs& A, Grp& g, SplitSm& S, const SplitIO& 
         if (lead) trace_ev(A, tag, v, worker);
     };
     if (insm) sample_farthest_pair<RHO, (RHO > 0)>(SampSm{smem_pin(io.dynS), rho}, sN, rho, r, C, S, mark);
+    else if (sbuf) sample_farthest_pair<RHO, false>(SampSm{smem_pin(sbuf), rho}, sN, rho, r, C, S, mark);
     else sample_farthest_pair<RHO, false>(SampGl{Pg, (size_t)stride * rho}, sN, rho, r, C, S, mark);
+    // the sample in the tile area has been read (sample_farthest_pair ends with a barrier): the tile now
+    if (resident && !insm) rt = tile_issue(Pg + (size_t)a * rho, np, rho, io.dynX, S);
     if (lead) trace_ev(A, 8, v, worker);
     g.exchange(S, par, 3, XARGMAX);
     if (lead) trace_ev(A, 9, v, worker);

@@ -183,7 +183,7 @@ def test_sampled_mode_equals_the_oracle_on_the_sample(hdf, name, stride):
     assert np.array_equal(g, p.reshape(-1, p.shape[-1])[7::stride][:100])
 
 
-@pytest.mark.parametrize("name,stride", [("c2b", 4), ("c3", 4)])
+@pytest.mark.parametrize("name,stride", [("c2b", 4), ("c3", 4), ("c3", 16)])
 def test_sampled_mode_five_percent_rule(hdf, name, stride):
     """R15 for the sampled mode: MSE([hdf_cluster_sampled -> hdf_filter] vs brute force) <= 1.05 x
     MSE([oracle.cluster (all pixels) -> oracle.filter] vs brute force).  (The NLM config c4 fails it at
