@@ -82,7 +82,8 @@ HDF_DEV uint32_t tc_off(int row, int k, int Kr) {
 // Dynamic shared memory: B_hi, B_lo [N][Kr], 2 stages of A_hi, A_lo [128][Kr], centres [N][rho].
 inline __host__ __device__ size_t coeffs_tc_smem(int K, int rho) {
     const int Kr = (K + 7) & ~7, N = (K + 15) & ~15;
-    return (size_t)(2 * N + 4 * kTcM) * Kr * 4 + (size_t)N * rho * 4 + 64;
+    // (+ the tile's guide rows [128][rho] for a runtime rho: read once per tile instead of once per centre)
+    return (size_t)(2 * N + 4 * kTcM) * Kr * 4 + (size_t)N * rho * 4 + (size_t)kTcM * rho * 4 + 64;
 }
 
 template <int RHO>   // RHO > 0: compile-time guide dimension, 0: runtime
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
     unsigned char* Bl = Bh + (size_t)N * Kr * 4;
     unsigned char* A0 = Bl + (size_t)N * Kr * 4;   // stage s: A_hi at A0 + 2 s abytes, A_lo after it
     float* mus = reinterpret_cast<float*>(A0 + 4 * abytes);
+    float* xs = mus + (size_t)N * rho;   // runtime rho: the tile's guide rows [128][rho]
     const uint32_t ncols = N <= 32 ? 64u : 128u;   // two accumulator stages of N (<= 64) columns
 
     // A^+ (hi, lo) as the B operands: row n = output coefficient n, K index l; zero-padded
@@ -162,6 +164,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
                 for (int d = 0; d < RR; d++) x[d] = xn[d];
                 if (tile + gridDim.x < ntile) load_x(tile + gridDim.x);
             }
+            if (RHO == 0) {   // runtime rho: the tile's guide rows staged once, coalesced (they are contiguous)
+                named_sync(2, kTcProd);   // the previous tile's rows have been read by both halves
+                const long long t0 = tile * kTcM;
+                const int nf = (int)(min((long long)kTcM, npix - t0) * rho);
+                for (int e = tid; e < nf; e += kTcProd) xs[e] = __ldg(P.p + t0 * rho + e);
+                named_sync(2, kTcProd);
+            }
             mbar_wait(&a_free[s], ph ^ 1u);   // the MMAs of tile it - 2 have read A[s]
             const uint32_t aH = smem_u32(A0 + 2 * s * abytes), aL = aH + (uint32_t)abytes;
             if (MUREG) {
@@ -211,8 +220,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
                                     d2 = fmaf(t, t, d2);
                                 }
                             } else {
+                                const float* xr = xs + m * rho;
                                 for (int d = 0; d < rho; d++) {
-                                    const float t = __ldg(P.p + i * rho + d) - mu[d];
+                                    const float t = xr[d] - mu[d];
                                     d2 = fmaf(t, t, d2);
                                 }
                             }
