@@ -27,6 +27,7 @@ template <int R>
 cudaError_t launch_vpass_t(bool box, const VLaunch& L, cudaStream_t st, const VParams& P) {
     if (P.rho == 3 && P.NP == 4) return vp<R, 3, 4>(box, L, st, P);
     if (P.rho == 6 && P.NP == 4) return vp<R, 6, 4>(box, L, st, P);
+    if (P.NP == 32) return vp<R, 0, 32>(box, L, st, P);   // 31-band images (config 3): planes per cluster fixed
     return vp<R, 0, 0>(box, L, st, P);
 }
 

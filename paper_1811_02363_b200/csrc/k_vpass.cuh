@@ -116,14 +116,25 @@ HDF_DEV void vfir_issue_raw(const VParams& P, float* raw, int ystart, int step, 
         const int per_row = nx * rho;
         if (vec) {   // nx == 32, W * rho % 4 == 0: rows of 8 rho 16-byte chunks
             const int cpr = 8 * rho;
+            // (row, chunk) walked with a running pair instead of a division per element (rho = 31: an
+            // integer division by 248 per 16-byte copy was 9% of the kernel's stall samples)
+            int r = threadIdx.x / cpr, w = threadIdx.x - r * cpr;
+            const int dr = NT / cpr, dw = NT - dr * cpr;
             for (int e = threadIdx.x; e < J * cpr; e += NT) {
-                const int r = e / cpr, w = e - r * cpr;
                 const int y = ystart + step * J + r;
-                if (y < 0 || y >= P.H) continue;
-                const float* src = P.p + ((long long)y * P.W + x0) * rho + 4 * w;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(raw + r * kVTX * rho + 4 * w)),
-                             "l"(src)
-                             : "memory");
+                if (y >= 0 && y < P.H) {
+                    const float* src = P.p + ((long long)y * P.W + x0) * rho + 4 * w;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                     smem_u32(raw + r * kVTX * rho + 4 * w)),
+                                 "l"(src)
+                                 : "memory");
+                }
+                r += dr;
+                w += dw;
+                if (w >= cpr) {
+                    w -= cpr;
+                    r++;
+                }
             }
         } else {
             for (int e = threadIdx.x; e < J * per_row; e += NT) {
@@ -379,7 +390,7 @@ HDF_DEV void vfir_segment(const VParams& P, float* sm_v, int strip, int group, i
     if (nsteps > 1) issue(raw0 + raw_len, 1);
     cp_async_wait_all();
     __syncthreads();
-    if (fast) vfir_stage_a_fast<J, NPL, (RHO > 0 ? RHO : 1), (NPC > 0 ? NPC : 1), NT>(P, raw0, zs0, mus, ystart, 0, x0, nk);
+    if (fast) vfir_stage_a_fast<J, NPL, (RHO > 0 ? RHO : 1), (FAST ? NPC : 1), NT>(P, raw0, zs0, mus, ystart, 0, x0, nk);
     else vfir_stage_a<J, NPL, RHO, NPC, NT>(P, raw0, zs0, mus, ystart, 0, x0, q0, kA, nk, RW);
     __syncthreads();
     int g = 0;
@@ -389,7 +400,7 @@ HDF_DEV void vfir_segment(const VParams& P, float* sm_v, int strip, int group, i
             if (g + 2 < nsteps) issue(raw0 + (g & 1) * raw_len, g + 2);
             if (g + 1 < nsteps) {
                 if (fast)
-                    vfir_stage_a_fast<J, NPL, (RHO > 0 ? RHO : 1), (NPC > 0 ? NPC : 1), NT>(
+                    vfir_stage_a_fast<J, NPL, (RHO > 0 ? RHO : 1), (FAST ? NPC : 1), NT>(
                         P, raw0 + ((g + 1) & 1) * raw_len, zs0 + ((g + 1) & 1) * zs_len, mus, ystart, g + 1, x0, nk);
                 else
                     vfir_stage_a<J, NPL, RHO, NPC, NT>(P, raw0 + ((g + 1) & 1) * raw_len, zs0 + ((g + 1) & 1) * zs_len,
