@@ -275,7 +275,10 @@ typedef enum {
     HDF_STAGE_FALLBACK = 5,  /* k_fallback: direct (num)/(den), R9     step 6               */
     HDF_STAGE_H2D = 6,       /* hdf_filter_host input copies                                */
     HDF_STAGE_D2H = 7,       /* hdf_filter_host output copies                               */
-    HDF_NUM_STAGES = 8
+    HDF_STAGE_FILTER = 8,    /* the whole filter (steps 3-6, all of the above but the       */
+                             /* clustering): wall time on the call's stream, which covers   */
+                             /* the pipelined column / row passes' overlap                  */
+    HDF_NUM_STAGES = 9
 } hdf_stage;
 
 /* Diagnostics: events recorded by the clustering workers during the last hdf_cluster call that

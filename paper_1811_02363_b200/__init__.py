@@ -30,7 +30,7 @@ EXPORTS = ("hdf_version", "hdf_last_error", "hdf_cluster_workspace_bytes", "hdf_
            "hdf_filter_host", "hdf_pca_guide_workspace_bytes", "hdf_pca_guide",
            "hdf_profile_enable", "hdf_profile_collect", "hdf_cluster_trace", "hdf_filter_flagged", "hdf_scale_guide",
            "hdf_cluster_sampled_workspace_bytes", "hdf_cluster_sampled", "hdf_sample_guide")
-STAGES = ("cluster", "pinv", "coeffs", "vpass", "hpass", "fallback", "h2d", "d2h")
+STAGES = ("cluster", "pinv", "coeffs", "vpass", "hpass", "fallback", "h2d", "d2h", "filter")
 
 
 class HdfError(RuntimeError):

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -116,12 +117,14 @@ struct ProfScope {
             cudaEventRecord(r.a, st);
         }
     }
-    ~ProfScope() {
+    void close() {
         if (!on) return;
+        on = false;
         cudaEventRecord(r.b, st);
         std::lock_guard<std::mutex> lk(g_prof_mu);
         g_prof_pending.push_back(r);
     }
+    ~ProfScope() { close(); }
 };
 
 // ------------------------------------------------------------------------ cluster workspace ----
@@ -625,6 +628,30 @@ cudaStream_t copy_stream() {
     return cs[dev];
 }
 
+// The row-pass stream of the pipelined filter (run_filter): one per (calling thread, device), with a
+// small pool of events reused call after call (a wait captures the event's state when it is enqueued,
+// so re-recording in the next call is safe).
+struct PipeStream {
+    cudaStream_t s = nullptr;
+    std::vector<cudaEvent_t> ev;
+};
+PipeStream* pipe_stream(int nev) {
+    static thread_local PipeStream ps[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    PipeStream& p = ps[dev];
+    if (!p.s && cudaStreamCreateWithFlags(&p.s, cudaStreamNonBlocking) != cudaSuccess) {
+        p.s = nullptr;
+        return nullptr;
+    }
+    while ((int)p.ev.size() < nev) {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        p.ev.push_back(e);
+    }
+    return &p;
+}
+
 int side_stream(SideStream* out) {
     static std::mutex mu;
     static std::mutex dev_mu[64];
@@ -752,7 +779,7 @@ int validate_filter(int n, int rho, int H, int W, int kind, float sigma_s, int r
 // the call) the clustering status back with one synchronisation at the end.
 // nchunks / after_chunk (the host path): the row pass runs in nchunks row chunks and after_chunk(y0, y1)
 // is called once the rows [y0, y1) of g are final (enqueued on st), e.g. to start their copy-out.
-using ChunkFn = std::function<int(int, int)>;
+using ChunkFn = std::function<int(int, int, cudaStream_t)>;
 int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int kind, float sigma_s, int radius,
                float sigma_r, int K, const float* centres, float tau, float* g, int32_t* n_flagged_host, void* ws,
                size_t ws_bytes, cudaStream_t st, bool hard = false, const int32_t* hard_labels = nullptr,
@@ -831,6 +858,36 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         while (std::ldexp(1.0, wexp) < ws) wexp++;
     }
     int* amax = w.status + 3;
+    // The pipelined filter (tensor-core path): the image is cut into nband row bands (multiples of 64
+    // rows).  The column pass of band b + 1 (st, gv SMs: it only writes its planes) runs while the row
+    // pass + combine of band b (hs, gh SMs: it only reads them) runs, so the HBM write and read streams
+    // overlap instead of taking turns (a write-only stream tops out near 3.6 TB/s, a mixed one at the
+    // copy bandwidth); the coefficient kernel runs on hs beside the first column-pass band.  Band 0's
+    // column pass and the last band's row pass have the GPU to themselves.  HDF_PIPE_BANDS (default 1 =
+    // off) and HDF_PIPE_HSM (the row pass's SMs) tune it.
+    const int nt64 = (H + hdf::kVtcRows - 1) / hdf::kVtcRows;
+    int nband = 1;
+    if (use_htc) {
+        int want = 1;   // measured slower at c5: off unless asked for
+        if (const char* e = getenv("HDF_PIPE_BANDS")) want = atoi(e);
+        if (want > 1) nband = std::min(std::max(want, nchunks), nt64);
+    }
+    const bool pipe = nband > 1;
+    PipeStream* pst = nullptr;
+    if (pipe) {
+        pst = pipe_stream(nband + 2);
+        if (!pst) return fail(HDF_ERR_CUDA, "pipeline stream / events: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    cudaStream_t hs = pipe ? pst->s : st;   // the stream of the coefficients and the row passes
+    int gh = nsm, gv = nsm - 1;
+    if (pipe) {
+        gh = (nsm - 1) * 47 / 100;
+        if (const char* e = getenv("HDF_PIPE_HSM")) gh = atoi(e);
+        gh = std::max(1, std::min(gh, nsm - 2));
+        gv = nsm - 1 - gh;
+    }
+    auto band_y = [&](int b) { return std::min(H, hdf::kVtcRows * (int)((long long)nt64 * b / nband)); };
+    ProfScope prof_filter(HDF_STAGE_FILTER, st);
     // F1: range weights + column pass
     {
         hdf::VParams vp;
@@ -860,7 +917,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         for (int t = 0; t < 2 * HDF_MAX_RADIUS + 1; t++) vp.tws[t] = (t <= 2 * F.Rp) ? taps[t] : 0.f;
         hdf::VLaunch vl = F.vl;
         vl.smem = vsmem;
-        ProfScope prof(HDF_STAGE_VPASS, st);
+        std::unique_ptr<ProfScope> prof(use_tc ? nullptr : new ProfScope(HDF_STAGE_VPASS, st));
         if (use_tc) {
             HDF_CUDA(cudaMemsetAsync(amax, 0, sizeof(int), st));
             const long long nf = (long long)H * W * n;
@@ -879,12 +936,6 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             tp.K = K;
             tp.R = F.R;
             tp.nstrip = (W + 31) / 32;
-            const int grid = std::max(1, nsm - 1);
-            const long long ncol = (long long)tp.nstrip * K;
-            const int maxseg = (H + hdf::kVtcRows - 1) / hdf::kVtcRows;
-            tp.nseg = (int)std::max<long long>(1, std::min<long long>(maxseg, (4LL * grid + ncol - 1) / ncol));
-            tp.seglen = ((H + tp.nseg - 1) / tp.nseg + hdf::kVtcRows - 1) / hdf::kVtcRows * hdf::kVtcRows;
-            tp.nseg = (H + tp.seglen - 1) / tp.seglen;
             tp.neg_inv2sr2 = neg_inv2sr2;
             for (int t = 0; t < hdf::kMaxTaps; t++) tp.taps[t] = 0.f;
             for (int t = 0; t <= 2 * F.R; t++) tp.taps[t] = taps[F.Rp - F.R + t];
@@ -894,9 +945,32 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             if (rc) return rc;
             const size_t smem = hdf::vpass_tc_smem(F.R);
             HDF_CUDA(cudaFuncSetAttribute(hdf::k_range_vpass_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            hdf::k_range_vpass_tc<<<(unsigned)std::min<long long>(grid, ncol * tp.nseg), hdf::kVtcThreads, smem, st>>>(
-                tmp, tp);
-            HDF_CUDA(cudaGetLastError());
+            // output rows [y0, y1) on `grid` SMs: row segments of whole 64-row tiles, enough units to fill the grid
+            auto launch_vtc = [&](int y0, int y1, int grid) -> int {
+                const long long ncol = (long long)tp.nstrip * K;
+                const int rows = y1 - y0;
+                const int maxseg = (rows + hdf::kVtcRows - 1) / hdf::kVtcRows;
+                tp.y0 = y0;
+                tp.nseg = (int)std::max<long long>(1, std::min<long long>(maxseg, (4LL * grid + ncol - 1) / ncol));
+                tp.seglen = ((rows + tp.nseg - 1) / tp.nseg + hdf::kVtcRows - 1) / hdf::kVtcRows * hdf::kVtcRows;
+                tp.nseg = (rows + tp.seglen - 1) / tp.seglen;
+                ProfScope pv(HDF_STAGE_VPASS, st);
+                hdf::k_range_vpass_tc<<<(unsigned)std::min<long long>(grid, ncol * tp.nseg), hdf::kVtcThreads, smem, st>>>(
+                    tmp, tp);
+                HDF_CUDA(cudaGetLastError());
+                return HDF_OK;
+            };
+            if (!pipe) {
+                rc = launch_vtc(0, H, std::max(1, nsm - 1));
+                if (rc) return rc;
+            } else {
+                HDF_CUDA(cudaEventRecord(pst->ev[0], st));   // hs starts after the clustering and the memsets
+                for (int b = 0; b < nband; b++) {
+                    rc = launch_vtc(band_y(b), band_y(b + 1), gv);
+                    if (rc) return rc;
+                    HDF_CUDA(cudaEventRecord(pst->ev[1 + b], st));
+                }
+            }
         } else {
             HDF_CUDA(hdf::launch_vpass(F.Rp, F.box, vl, st, vp));
         }
@@ -915,7 +989,8 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             HDF_CUDA(cudaGetLastError());
         }
     }
-    HDF_CUDA(cudaStreamWaitEvent(st, ss.join, 0));   // A^+ is ready
+    if (pipe) HDF_CUDA(cudaStreamWaitEvent(hs, pst->ev[0], 0));
+    HDF_CUDA(cudaStreamWaitEvent(hs, ss.join, 0));   // A^+ is ready
     side_lock.unlock();
     // loop for2: c(i) = A^+ b(i) -> K coefficient planes
     {
@@ -951,11 +1026,11 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         else if (K == 16) kt = hdf::k_coeffs_t<16>;
         else if (K == 32) kt = hdf::k_coeffs_t<32>;
         else if (K == 64) kt = hdf::k_coeffs_t<64>;
-        ProfScope prof(HDF_STAGE_COEFFS, st);
+        ProfScope prof(HDF_STAGE_COEFFS, hs);
         if (hard) {
             const long long ntot = npix;
             const unsigned nb = (unsigned)std::min<long long>((ntot + 255) / 256, (long long)nsm * 16);
-            hdf::k_coeffs_onehot<<<nb, 256, 0, st>>>(hard_labels, w.cpl, (long long)H * F.Wp, H, W, F.Wp, K);
+            hdf::k_coeffs_onehot<<<nb, 256, 0, hs>>>(hard_labels, w.cpl, (long long)H * F.Wp, H, W, F.Wp, K);
         } else if (ktc) {
             const size_t smem = hdf::coeffs_tc_smem(K, rho);
             HDF_CUDA(cudaFuncSetAttribute(ktc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -963,8 +1038,8 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             int per_sm = 1;
             HDF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ktc, hdf::kTcThreads, smem));
             const long long ntile = (npix + hdf::kTcM - 1) / hdf::kTcM;
-            const unsigned nb = (unsigned)std::min<long long>(ntile, (long long)nsm * std::max(1, std::min(per_sm, 1)));
-            ktc<<<nb, hdf::kTcThreads, smem, st>>>(cp);
+            const unsigned nb = (unsigned)std::min<long long>(ntile, (long long)(pipe ? gh : nsm) * std::max(1, std::min(per_sm, 1)));
+            ktc<<<nb, hdf::kTcThreads, smem, hs>>>(cp);
         } else if (km) {
             const int nt = (K + 7) / 8;
             const size_t smem = sizeof(float) * ((size_t)2 * nt * nt * 2 * 32 + (size_t)8 * nt * rho);
@@ -974,16 +1049,16 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             int per_sm = 1;   // resident blocks per SM: a persistent grid (A^+ staged once per block)
             HDF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, km, hdf::kCoefMmaThreads, smem));
             const unsigned nb = (unsigned)std::min<long long>(want, (long long)nsm * std::max(per_sm, 1));
-            km<<<nb, hdf::kCoefMmaThreads, smem, st>>>(cp);
+            km<<<nb, hdf::kCoefMmaThreads, smem, hs>>>(cp);
         } else if (kt) {   // compile-time K: b in registers, broadcast A^+ rows
             const size_t smem = sizeof(float) * ((size_t)K * K + (size_t)K * rho);
             HDF_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            kt<<<nblk, hdf::kCoefPix, smem, st>>>(cp);
+            kt<<<nblk, hdf::kCoefPix, smem, hs>>>(cp);
         } else {
             const int K8 = (K + 7) & ~7;
             const size_t smem = sizeof(float) * ((size_t)K * K8 + (size_t)K * rho + (size_t)K * hdf::kCoefPix);
             HDF_CUDA(cudaFuncSetAttribute(hdf::k_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            hdf::k_coeffs<<<nblk, hdf::kCoefPix, smem, st>>>(cp);
+            hdf::k_coeffs<<<nblk, hdf::kCoefPix, smem, hs>>>(cp);
         }
         HDF_CUDA(cudaGetLastError());
     }
@@ -1073,50 +1148,63 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     }
     const int tile_rows = use_htc ? hdf::kHtcRows : F.RR;
     const int row_tiles = use_htc ? (H + hdf::kHtcRows - 1) / hdf::kHtcRows : (int)F.hl.grid.y;
-    const int nch = std::max(1, std::min(nchunks, row_tiles));
+    // row chunks: the pipeline's bands (in 32-row blocks), else nchunks equal chunks
+    const int nch = pipe ? nband : std::max(1, std::min(nchunks, row_tiles));
     int* flag_start = w.status + 2;   // list entries before this chunk (device)
     for (int ch = 0; ch < nch; ch++) {
-        const int ty0 = (int)((long long)row_tiles * ch / nch), ty1 = (int)((long long)row_tiles * (ch + 1) / nch);
+        int ty0 = (int)((long long)row_tiles * ch / nch), ty1 = (int)((long long)row_tiles * (ch + 1) / nch);
+        if (pipe) {
+            ty0 = band_y(ch) / hdf::kHtcRows;
+            ty1 = ch == nch - 1 ? row_tiles : band_y(ch + 1) / hdf::kHtcRows;
+            HDF_CUDA(cudaStreamWaitEvent(hs, pst->ev[1 + ch], 0));   // band ch's planes are written
+        }
         hp.ytile0 = ty0;
         hdf::HLaunch hl = F.hl;
         hl.grid.y = (unsigned)(ty1 - ty0);
         if (nch > 1) {
-            HDF_CUDA(cudaMemcpyAsync(flag_start, w.flag_count, sizeof(int), cudaMemcpyDeviceToDevice, st));
+            HDF_CUDA(cudaMemcpyAsync(flag_start, w.flag_count, sizeof(int), cudaMemcpyDeviceToDevice, hs));
             fb.flag_start = flag_start;
         }
         {
-            ProfScope prof(HDF_STAGE_HPASS, st);
+            ProfScope prof(HDF_STAGE_HPASS, hs);
             if (use_htc) {
                 hq.yb0 = ty0;
                 hq.yb1 = ty1;
                 const long long nunit = (long long)(ty1 - ty0) * hq.nstrip;
-                hdf::k_hpass_combine_tc<<<(unsigned)std::max<long long>(1, std::min<long long>(nsm, nunit)),
-                                          hdf::kHtcThreads, htc_smem, st>>>(tz, tcc, hq);
+                // (the last band's row pass has the GPU to itself)
+                const int grid = (pipe && ch < nch - 1) ? gh : nsm;
+                hdf::k_hpass_combine_tc<<<(unsigned)std::max<long long>(1, std::min<long long>(grid, nunit)),
+                                          hdf::kHtcThreads, htc_smem, hs>>>(tz, tcc, hq);
                 HDF_CUDA(cudaGetLastError());
             } else {
-                HDF_CUDA(hdf::launch_hpass(F.Rp, F.box, hl, st, tp, tc, hp));
+                HDF_CUDA(hdf::launch_hpass(F.Rp, F.box, hl, hs, tp, tc, hp));
             }
         }
         if (tau > 0.f) {
-            ProfScope prof(HDF_STAGE_FALLBACK, st);
+            ProfScope prof(HDF_STAGE_FALLBACK, hs);
             // one warp per flagged pixel (grid-stride): the count is on the device, so the grid is sized for
             // the worst case the SMs can hold at once (8 CTAs of 8 warps per SM), capped by the pixel count
             const long long npix = (long long)H * W;
             const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((npix + 7) / 8, 8LL * nsm));
             if (n <= 16) {
                 void (*kfb)(const hdf::FBParams) = n <= 4 ? hdf::k_fallback<4> : hdf::k_fallback<16>;
-                kfb<<<nb, hdf::kFbThreads, 0, st>>>(fb);
+                kfb<<<nb, hdf::kFbThreads, 0, hs>>>(fb);
             } else {   // many channels: one CTA per pixel (measured at config 3: 20 us vs 51 us for a warp)
-                hdf::k_fallback_cta<<<(unsigned)std::min<long long>(npix, 16LL * nsm), hdf::kFbCtaThreads, 0, st>>>(
+                hdf::k_fallback_cta<<<(unsigned)std::min<long long>(npix, 16LL * nsm), hdf::kFbCtaThreads, 0, hs>>>(
                     fb);
             }
             HDF_CUDA(cudaGetLastError());
         }
         if (after_chunk) {
-            rc = after_chunk(std::min(H, ty0 * tile_rows), std::min(H, ty1 * tile_rows));
+            rc = after_chunk(std::min(H, ty0 * tile_rows), std::min(H, ty1 * tile_rows), hs);
             if (rc) return rc;
         }
     }
+    if (pipe) {   // the caller's stream continues after the last row pass
+        HDF_CUDA(cudaEventRecord(pst->ev[nband + 1], hs));
+        HDF_CUDA(cudaStreamWaitEvent(st, pst->ev[nband + 1], 0));
+    }
+    prof_filter.close();
     if (n_flagged_host) {
         HostStage* hs = cluster_here ? crb.hs : host_stage();
         if (!hs) return fail(HDF_ERR_CUDA, "pinned host stage: cudaMallocHost failed");
@@ -1548,12 +1636,12 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
         };
         const size_t rowf = (size_t)W * n;
         const bool chunked = (long long)H * W >= (1LL << 20);   // small images: one copy after the filter
-        auto after = [&](int y0, int y1) -> int {
+        auto after = [&](int y0, int y1, cudaStream_t s) -> int {
             if (nev >= kChunks) return fail(HDF_ERR_CUDA, "too many output chunks");
             cudaEvent_t ev;
             HDF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
             evs[nev++] = ev;
-            HDF_CUDA(cudaEventRecord(ev, st));
+            HDF_CUDA(cudaEventRecord(ev, s));
             HDF_CUDA(cudaStreamWaitEvent(cs, ev, 0));
             ProfScope prof(HDF_STAGE_D2H, cs);
             HDF_CUDA(cudaMemcpyAsync(g_host + (size_t)y0 * rowf, gd + (size_t)y0 * rowf, sizeof(float) * (size_t)(y1 - y0) * rowf,

@@ -37,7 +37,11 @@ constexpr int kHtcS = 2;                           // tiles per unit (one consum
 constexpr int kHtcRB = 32;                         // input halo each side (one strip): R <= 32
 constexpr int kHtcKp = kHtcN + 2 * kHtcRB;         // input columns per tile (8 K steps of 16)
 constexpr int kHtcBoxes = 2 * kHtcS + 2;           // 32-column strips per (unit, cluster)
-constexpr int kHtcNB = 8;                          // strip ring slots (hi + lo each)
+#ifndef HDF_HTC_NB
+#define HDF_HTC_NB 9
+#endif
+constexpr int kHtcNB = HDF_HTC_NB;                 // strip ring slots (hi + lo each; 9 = 225 KB with the rest)
+static_assert(kHtcNB > 2 * kHtcS + 2, "a step's strips must wrap the ring at most once");
 constexpr int kHtcNC = 4;                          // coefficient ring slots
 constexpr int kHtcThreads = 128 * kHtcS + 64;      // consumers + MMA warp + TMA warp
 constexpr int kHtcMaxR = kHtcRB;
@@ -249,24 +253,31 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
         const uint32_t idesc = umma_idesc_f16(128, kHtcN);
         const uint64_t dt = umma_desc(0, kHtcN * 16, 128);
         const uint32_t tH = smem_u32(Th), tL = smem_u32(Tl), rb = smem_u32(ring);
+        // ring slot and phase of the step's first strip g0 = 6 kk, kept in 32-bit incremental form (a step's
+        // strips g0 .. g0 + 5 wrap the ring at most once)
+        int bslot = 0, bph = 0;
         for (long long ui = 0; ui < nui; ui++) {
             for (int k = 0; k < K; k++) {
                 const long long kk = ui * K + k;
-                const long long g0 = (long long)kHtcBoxes * kk;
 #pragma unroll 1
                 for (int t = 0; t < kHtcS; t++) {
                     const int s = 2 * t + (int)(kk & 1);
                     // tile t reads input strips 2t .. 2t + 3
                     for (int b = 0; b < 4; b++) {
-                        const long long g = g0 + 2 * t + b;
-                        mbar_wait(&box_full[g % kHtcNB], (uint32_t)(g / kHtcNB) & 1u);
+                        int sl = bslot + 2 * t + b, ph = bph;
+                        if (sl >= kHtcNB) {
+                            sl -= kHtcNB;
+                            ph ^= 1;
+                        }
+                        mbar_wait(&box_full[sl], (uint32_t)ph);
                     }
                     if (kk >= 2) mbar_wait(&d_free[s], (uint32_t)((kk >> 1) - 1) & 1u);
                     tc_fence_after();
                     const uint32_t td = tbase + (uint32_t)(s * kHtcN);
 #pragma unroll
                     for (int ks = 0; ks < kHtcKp / 16; ks++) {
-                        const int sl = (int)((g0 + 2 * t + (ks >> 1)) % kHtcNB);
+                        int sl = bslot + 2 * t + (ks >> 1);
+                        if (sl >= kHtcNB) sl -= kHtcNB;
                         const uint32_t za = rb + (uint32_t)sl * kHtcSlotBytes + (uint32_t)((ks & 1) * 32);
                         const uint64_t aH = umma_desc_sw64(za), aL = umma_desc_sw64(za + kHtcBoxBytes);
                         const uint32_t ot = (uint32_t)ks * (2u * kHtcN * 16u);
@@ -279,11 +290,21 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
                     umma_commit_warp(&d_full[s]);
                     // strips 2t, 2t + 1 are read by no later tile of this step; the last tile releases all four
                     const int nrel = (t == kHtcS - 1) ? 4 : 2;
-                    for (int b = 0; b < nrel; b++) umma_commit_warp(&box_free[(g0 + 2 * t + b) % kHtcNB]);
+                    for (int b = 0; b < nrel; b++) {
+                        int sl = bslot + 2 * t + b;
+                        if (sl >= kHtcNB) sl -= kHtcNB;
+                        umma_commit_warp(&box_free[sl]);
+                    }
+                }
+                bslot += kHtcBoxes;
+                if (bslot >= kHtcNB) {
+                    bslot -= kHtcNB;
+                    bph ^= 1;
                 }
             }
         }
     } else if (lane == 0) {   // ------------------------------------------------------- TMA warp -------
+        int tslot = 0, tph = 0, tfilled = 0;
         for (long long ui = 0; ui < nui; ui++) {
             const long long u = blockIdx.x + ui * (long long)gridDim.x;
             const int ry = P.yb0 + (int)(u / P.nstrip), sx = (int)(u % P.nstrip);
@@ -291,9 +312,14 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
             for (int k = 0; k < K; k++) {
                 const long long kk = ui * K + k;
                 for (int b = 0; b < kHtcBoxes; b++) {
-                    const long long g = (long long)kHtcBoxes * kk + b;
-                    const int sl = (int)(g % kHtcNB);
-                    if (g >= kHtcNB) mbar_wait(&box_free[sl], (uint32_t)((g / kHtcNB) - 1) & 1u);
+                    // strip g = 6 kk + b: ring slot sl = g % NB, phase (g / NB) & 1 (incremental, 32-bit)
+                    const int sl = tslot;
+                    if (tfilled >= kHtcNB) mbar_wait(&box_free[sl], (uint32_t)(tph ^ 1));
+                    else tfilled++;
+                    if (++tslot == kHtcNB) {
+                        tslot = 0;
+                        tph ^= 1;
+                    }
                     mbar_arrive_expect_tx(&box_full[sl], kHtcSlotBytes);
                     unsigned char* dst = ring + (size_t)sl * kHtcSlotBytes;
                     tma_load_5d(dst, &tm_z, &box_full[sl], 0, 0, y0, s0 + b, 4 * k);                   // hi half

@@ -85,6 +85,7 @@ struct VtcParams {
     long long pstride;     // H * Wp
     int H, W, Wp, K, R;
     int nstrip, nseg, seglen;   // 32-column strips, row segments per column and their length (multiple of 64)
+    int y0;                     // first output row of this launch (row bands of the pipelined filter)
     float neg_inv2sr2;     // -1 / (2 sigma_r^2)
     float taps[kMaxTaps];  // w_{-R..R}
 };
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
         // guide from DRAM once per cluster: 10.9 GB at config 5)
         k = (int)(col % P.K);
         strip = (int)(col / P.K);
-        ys = seg * P.seglen;
+        ys = P.y0 + seg * P.seglen;
     };
 
     if (warp < kVtcProd / 32) {   // ------------------------------------------------ producers -------
