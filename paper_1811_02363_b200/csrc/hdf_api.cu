@@ -588,17 +588,20 @@ int encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2, 
     return HDF_OK;
 }
 
-// 5-D fp16 map of the strip-major planes [P][Wp / 32][H][hi 32 | lo 32] (k_hpass_tc.cuh): dims (32 columns,
-// 2 halves, H, strips, P), box (32, 1, rows, 1, planes) -> [planes][rows][32] with 64-byte rows, 64-byte swizzle
-int encode_strips(CUtensorMap* m, void* base, int H, int Wp, int P, uint32_t rows, uint32_t planes) {
+// strip-major planes [P][Wp / 32][H][32] of 2-byte (fp16, 64-byte rows, SWIZZLE_64B) or 1-byte (e4m3 as
+// uint8, 32-byte rows, SWIZZLE_32B) elements; box [planes][1 strip][rows][32]
+int encode_strips(CUtensorMap* m, void* base, int H, int Wp, int P, uint32_t rows, uint32_t planes, int esize) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return fail(HDF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[5] = {32, 2, (cuuint64_t)H, (cuuint64_t)(Wp / 32), (cuuint64_t)P};
-    cuuint64_t strides[4] = {64, 128, (cuuint64_t)H * 128, (cuuint64_t)H * Wp * 4};
-    cuuint32_t box[5] = {32, 1, rows, 1, planes};
-    cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const cuuint64_t rb = 32ull * (cuuint64_t)esize;
+    cuuint64_t dims[4] = {32, (cuuint64_t)H, (cuuint64_t)(Wp / 32), (cuuint64_t)P};
+    cuuint64_t strides[3] = {rb, (cuuint64_t)H * rb, (cuuint64_t)H * (cuuint64_t)(Wp / 32) * rb};
+    cuuint32_t box[4] = {32, rows, 1, planes};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = fn(m, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, base, dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    esize == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(HDF_ERR_CUDA, "cuTensorMapEncodeTiled (strips) failed (%d)", (int)r);
     return HDF_OK;
 }
@@ -927,6 +930,8 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             tp.centres = centres;
             tp.planes = w.planes;
             tp.ph = use_htc ? reinterpret_cast<unsigned short*>(w.planes) : nullptr;
+            // the e4m3 residuals after the 4K fp16 hi planes (3 bytes per value of the 4 the workspace holds)
+            tp.pl = use_htc ? reinterpret_cast<unsigned char*>(w.planes) + (size_t)4 * K * H * F.Wp * 2 : nullptr;
             tp.wexp = wexp;
             tp.absmax = amax;
             tp.pstride = (long long)H * F.Wp;
@@ -944,7 +949,13 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
                           (uint64_t)H * W * 3 * 4, 96u, 64u, 1u);
             if (rc) return rc;
             const size_t smem = hdf::vpass_tc_smem(F.R);
-            HDF_CUDA(cudaFuncSetAttribute(hdf::k_range_vpass_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            // consumer warps: 8 (32 rows each; the fp16 + e4m3 stores are the consumers' work), HDF_VTC_CONS=4 keeps 4
+            int cons = 8;
+            if (const char* e = getenv("HDF_VTC_CONS")) cons = atoi(e) == 4 ? 4 : 8;
+            void (*kvtc)(const CUtensorMap, const hdf::VtcParams) =
+                cons == 4 ? hdf::k_range_vpass_tc<4> : hdf::k_range_vpass_tc<8>;
+            const int vthreads = cons == 4 ? hdf::vtc_threads(4) : hdf::vtc_threads(8);
+            HDF_CUDA(cudaFuncSetAttribute(kvtc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             // output rows [y0, y1) on `grid` SMs: row segments of whole 64-row tiles, enough units to fill the grid
             auto launch_vtc = [&](int y0, int y1, int grid) -> int {
                 const long long ncol = (long long)tp.nstrip * K;
@@ -955,8 +966,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
                 tp.seglen = ((rows + tp.nseg - 1) / tp.nseg + hdf::kVtcRows - 1) / hdf::kVtcRows * hdf::kVtcRows;
                 tp.nseg = (rows + tp.seglen - 1) / tp.seglen;
                 ProfScope pv(HDF_STAGE_VPASS, st);
-                hdf::k_range_vpass_tc<<<(unsigned)std::min<long long>(grid, ncol * tp.nseg), hdf::kVtcThreads, smem, st>>>(
-                    tmp, tp);
+                kvtc<<<(unsigned)std::min<long long>(grid, ncol * tp.nseg), vthreads, smem, st>>>(tmp, tp);
                 HDF_CUDA(cudaGetLastError());
                 return HDF_OK;
             };
@@ -1116,15 +1126,18 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         }
         memcpy(fb.taps, t2, sizeof(t2));
     }
-    // the tensor-core row pass: tensor map of the strip-major fp16 hi/lo planes (boxes [4 planes][32 rows]
+    // the tensor-core row pass: tensor maps of the strip-major fp16 hi and e4m3 lo planes (boxes [4 planes][32 rows]
     // [the hi or lo half of a 32-column strip], 64-byte swizzle) and of the coefficient planes (two
     // [32 rows][32 columns] halves per tile, 128-byte swizzle)
-    CUtensorMap tz, tcc;
+    CUtensorMap tz, tzl, tcc;
     hdf::HtcParams hq;
     size_t htc_smem = 0;
     if (use_htc) {
         unsigned short* ph = reinterpret_cast<unsigned short*>(w.planes);
-        rc = encode_strips(&tz, ph, H, F.Wp, K * 4, (uint32_t)hdf::kHtcRows, 4u);
+        rc = encode_strips(&tz, ph, H, F.Wp, K * 4, (uint32_t)hdf::kHtcRows, 4u, 2);
+        if (rc) return rc;
+        rc = encode_strips(&tzl, reinterpret_cast<unsigned char*>(w.planes) + (size_t)4 * K * H * F.Wp * 2, H, F.Wp, K * 4,
+                           (uint32_t)hdf::kHtcRows, 4u, 1);
         if (rc) return rc;
         rc = encode3d(&tcc, w.cpl, (uint64_t)W, (uint64_t)H, (uint64_t)K, (uint64_t)F.Wp * 4, (uint64_t)H * F.Wp * 4,
                       32u, (uint32_t)hdf::kHtcRows, 1u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -1174,7 +1187,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
                 // (the last band's row pass has the GPU to itself)
                 const int grid = (pipe && ch < nch - 1) ? gh : nsm;
                 hdf::k_hpass_combine_tc<<<(unsigned)std::max<long long>(1, std::min<long long>(grid, nunit)),
-                                          hdf::kHtcThreads, htc_smem, hs>>>(tz, tcc, hq);
+                                          hdf::kHtcThreads, htc_smem, hs>>>(tz, tzl, tcc, hq);
                 HDF_CUDA(cudaGetLastError());
             } else {
                 HDF_CUDA(hdf::launch_hpass(F.Rp, F.box, hl, hs, tp, tc, hp));

@@ -7,12 +7,14 @@
 //   v_q(y, x0 + j) = sum_{i=0}^{127} T[j][i] t_q(y, x0 - 32 + i),   T[j][i] = w_{i - 32 - j} (0 outside [-R, R]),
 // for M = 128 (plane, row) pairs (4 planes x 32 rows):
 //   D[M x 64] = Z[M x 128] . T^T[128 x 64]   with tcgen05.mma kind::f16, fp32 accumulation in TMEM.
-// Z comes straight from HBM: the planes are stored as fp16 hi and lo parts (t = hi + lo, ~22 bits, scaled
-// by a power of two) in a strip-major layout [plane][x / 32][y][hi 32 | lo 32] (one 128-byte line per row of
-// a strip; k_vpass_tc.cuh writes two rows' halves per warp store), so one TMA box [4 planes][32 rows][the hi
-// (or lo) half of one strip] (64-byte rows, SWIZZLE_64B) is already a canonical K-major SW64 operand block
-// of K = 32: no conversion on the SMs.  Strips outside the image are zero-filled by the TMA and columns past W are
-// exact zeros (R8).  Precision: D = z_lo T_hi + z_hi T_lo + z_hi T_hi.
+// Z comes straight from HBM: the planes are stored as t = hi + lo (scaled by a power of two), hi = fp16(t)
+// in a strip-major layout [plane][x / 32][y][32] (64-byte rows) and the residual lo as e4m3(lo) in the same
+// layout with 32-byte rows (3 bytes per value; k_vpass_tc.cuh writes them), so one TMA box [4 planes][32 rows]
+// [one strip] of hi (SWIZZLE_64B) is a canonical K-major SW64 fp16 operand block of K = 32 and one of lo
+// (SWIZZLE_32B) a canonical K-major SW32 e4m3 block of K = 32: no conversion on the SMs.  Strips outside the
+// image are zero-filled by the TMA and columns past W are exact zeros (R8).
+// Precision: D = z_hi T_lo + z_hi T_hi (kind::f16, T = T_hi + T_lo its fp16 split) + z_lo T_e4m3 (kind::f8f6f4,
+// the same accumulator): t to ~2^-15 relative.
 //
 // A CTA is persistent over units (32-row block, 128-column strip of output).  For each cluster k (in
 // order) the TMA warp loads the 6 input strips x0 - 32 .. x0 + 159 (tile t reads strips 2t .. 2t + 3, so
@@ -38,20 +40,22 @@ constexpr int kHtcRB = 32;                         // input halo each side (one 
 constexpr int kHtcKp = kHtcN + 2 * kHtcRB;         // input columns per tile (8 K steps of 16)
 constexpr int kHtcBoxes = 2 * kHtcS + 2;           // 32-column strips per (unit, cluster)
 #ifndef HDF_HTC_NB
-#define HDF_HTC_NB 9
+#define HDF_HTC_NB 11
 #endif
 constexpr int kHtcNB = HDF_HTC_NB;                 // strip ring slots (hi + lo each; 9 = 225 KB with the rest)
 static_assert(kHtcNB > 2 * kHtcS + 2, "a step's strips must wrap the ring at most once");
 constexpr int kHtcNC = 4;                          // coefficient ring slots
 constexpr int kHtcThreads = 128 * kHtcS + 64;      // consumers + MMA warp + TMA warp
 constexpr int kHtcMaxR = kHtcRB;
-constexpr uint32_t kHtcBoxBytes = 4 * kHtcRows * 32 * 2;    // one part (hi or lo): 8 KB
-constexpr uint32_t kHtcSlotBytes = 2 * kHtcBoxBytes;        // hi + lo
+constexpr uint32_t kHtcBoxBytes = 4 * kHtcRows * 32 * 2;    // hi part (fp16): 8 KB
+constexpr uint32_t kHtcLoBytes = 4 * kHtcRows * 32;         // lo part (e4m3): 4 KB
+constexpr uint32_t kHtcSlotBytes = kHtcBoxBytes + kHtcLoBytes;
 constexpr uint32_t kHtcCBytes = kHtcRows * kHtcN * 4;       // 8 KB: two SW128 halves of [32][32] fp32
 constexpr int kHtcEpiCols = 16;                             // epilogue column chunk
 
 inline __host__ __device__ size_t hpass_tc_smem() {
     return (size_t)kHtcNB * kHtcSlotBytes + (size_t)kHtcNC * kHtcCBytes + (size_t)2 * kHtcN * kHtcKp * 2 +
+           (size_t)kHtcN * kHtcKp +
            (size_t)kHtcS * kHtcRows * kHtcEpiCols * 4 * 4 + 1024;
 }
 
@@ -75,6 +79,29 @@ HDF_DEV uint64_t umma_desc_sw64(uint32_t saddr) {
            (4ull << 61);
 }
 
+// The same for a K-major SWIZZLE_32B operand (8-row atoms of 32-byte rows, 256 B apart): one e4m3 K block of 32.
+HDF_DEV uint64_t umma_desc_sw32(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(256 >> 4) << 32) | (1ull << 46) |
+           (6ull << 61);
+}
+// kind::f8f6f4 (A, B e4m3 with format code 0, so the instruction descriptor is umma_idesc_f16's)
+HDF_DEV void umma_f8_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+HDF_DEV void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
 HDF_DEV void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3, int c4) {
     asm volatile(
         "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
@@ -96,7 +123,8 @@ HDF_DEV void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {
 }
 HDF_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-__global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __grid_constant__ CUtensorMap tm_z,
+__global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __grid_constant__ CUtensorMap tm_zh,
+                                                                     const __grid_constant__ CUtensorMap tm_zl,
                                                                      const __grid_constant__ CUtensorMap tm_c,
                                                                      const __grid_constant__ HtcParams P) {
     extern __shared__ __align__(1024) unsigned char sm_raw[];
@@ -106,11 +134,12 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
     __shared__ uint32_t tmem_base_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int R = P.R, Kp = kHtcKp;
-    unsigned char* ring = sm;                                              // [NB][hi 8 KB | lo 8 KB]
+    unsigned char* ring = sm;                                              // [NB][hi 8 KB | lo 4 KB]
     unsigned char* cring = ring + (size_t)kHtcNB * kHtcSlotBytes;          // [NC][2][32][32] fp32, SW128
     unsigned char* Th = cring + (size_t)kHtcNC * kHtcCBytes;
     unsigned char* Tl = Th + (size_t)kHtcN * Kp * 2;
-    float* epi = reinterpret_cast<float*>(Tl + (size_t)kHtcN * Kp * 2);   // [S][den 32 x 16 | g 32 x 16 x 3]
+    unsigned char* T8 = Tl + (size_t)kHtcN * Kp * 2;                     // T in e4m3 [64][128]
+    float* epi = reinterpret_cast<float*>(T8 + (size_t)kHtcN * Kp);      // [S][den 32 x 16 | g 32 x 16 x 3]
 
     // the Toeplitz operand: row j (output column), column i (input column x0 - 32 + i): w_{i - 32 - j}
     for (int e = tid; e < kHtcN * Kp; e += kHtcThreads) {
@@ -121,9 +150,13 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
         split_f16(w, h, l);
         *reinterpret_cast<unsigned short*>(Th + vtc_off(j, i, kHtcN)) = h;
         *reinterpret_cast<unsigned short*>(Tl + vtc_off(j, i, kHtcN)) = l;
+        // e4m3 operand, K-major no swizzle: core matrix (j / 8, i / 16) of 8 rows x 16 bytes
+        T8[(i >> 4) * (kHtcN * 16) + (j >> 3) * 128 + (j & 7) * 16 + (i & 15)] =
+            (unsigned char)(cvt_e4m3x2(0.f, w * (1.f / kLoScale)) & 0xFFu);
     }
     if (tid == 0) {
-        prefetch_tmap(&tm_z);
+        prefetch_tmap(&tm_zh);
+        prefetch_tmap(&tm_zl);
         prefetch_tmap(&tm_c);
         for (int s = 0; s < kHtcNB; s++) {
             mbar_init(&box_full[s], 1);
@@ -252,7 +285,7 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
     } else if (warp == 4 * kHtcS) {   // ------------------------------------------------ MMA warp -------
         const uint32_t idesc = umma_idesc_f16(128, kHtcN);
         const uint64_t dt = umma_desc(0, kHtcN * 16, 128);
-        const uint32_t tH = smem_u32(Th), tL = smem_u32(Tl), rb = smem_u32(ring);
+        const uint32_t tH = smem_u32(Th), tL = smem_u32(Tl), t8 = smem_u32(T8), rb = smem_u32(ring);
         // ring slot and phase of the step's first strip g0 = 6 kk, kept in 32-bit incremental form (a step's
         // strips g0 .. g0 + 5 wrap the ring at most once)
         int bslot = 0, bph = 0;
@@ -279,13 +312,20 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
                         int sl = bslot + 2 * t + (ks >> 1);
                         if (sl >= kHtcNB) sl -= kHtcNB;
                         const uint32_t za = rb + (uint32_t)sl * kHtcSlotBytes + (uint32_t)((ks & 1) * 32);
-                        const uint64_t aH = umma_desc_sw64(za), aL = umma_desc_sw64(za + kHtcBoxBytes);
+                        const uint64_t aH = umma_desc_sw64(za);
                         const uint32_t ot = (uint32_t)ks * (2u * kHtcN * 16u);
                         const uint64_t bH = dt | (uint64_t)(((tH + ot) >> 4) & 0x3FFFu);
                         const uint64_t bL = dt | (uint64_t)(((tL + ot) >> 4) & 0x3FFFu);
-                        umma_f16_warp(td, aL, bH, idesc, ks > 0 ? 1u : 0u);
-                        umma_f16_warp(td, aH, bL, idesc, 1u);
+                        umma_f16_warp(td, aH, bL, idesc, ks > 0 ? 1u : 0u);
                         umma_f16_warp(td, aH, bH, idesc, 1u);
+                    }
+#pragma unroll
+                    for (int b = 0; b < 4; b++) {   // the residuals: one e4m3 MMA (K = 32) per strip
+                        int sl = bslot + 2 * t + b;
+                        if (sl >= kHtcNB) sl -= kHtcNB;
+                        const uint64_t aL = umma_desc_sw32(rb + (uint32_t)sl * kHtcSlotBytes + kHtcBoxBytes);
+                        const uint64_t b8 = dt | (uint64_t)(((t8 + (uint32_t)b * (2u * kHtcN * 16u)) >> 4) & 0x3FFFu);
+                        umma_f8_warp(td, aL, b8, idesc, 1u);
                     }
                     umma_commit_warp(&d_full[s]);
                     // strips 2t, 2t + 1 are read by no later tile of this step; the last tile releases all four
@@ -322,8 +362,8 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
                     }
                     mbar_arrive_expect_tx(&box_full[sl], kHtcSlotBytes);
                     unsigned char* dst = ring + (size_t)sl * kHtcSlotBytes;
-                    tma_load_5d(dst, &tm_z, &box_full[sl], 0, 0, y0, s0 + b, 4 * k);                   // hi half
-                    tma_load_5d(dst + kHtcBoxBytes, &tm_z, &box_full[sl], 0, 1, y0, s0 + b, 4 * k);    // lo half
+                    tma_load_4d(dst, &tm_zh, &box_full[sl], 0, y0, s0 + b, 4 * k);                  // hi (fp16)
+                    tma_load_4d(dst + kHtcBoxBytes, &tm_zl, &box_full[sl], 0, y0, s0 + b, 4 * k);   // lo (e4m3)
                     if (b == 3 || b == 5) {   // tile (b - 3) / 2's coefficients
                         const int t = (b - 3) / 2;
                         const long long h = 2 * kk + t;

@@ -44,12 +44,8 @@ namespace hdf {
 constexpr int kVtcRows = 64;       // output rows per tile (UMMA N)
 constexpr int kVtcM = 128;         // (plane, column) pairs per tile (UMMA M): 4 planes x 32 columns
 constexpr int kVtcProd = 256;      // producer threads (8 warps)
-#ifndef HDF_VTC_CONS
-#define HDF_VTC_CONS 4
-#endif
-constexpr int kVtcCons = HDF_VTC_CONS;                      // consumer warps (4: 64 rows each, 8: 32 rows each)
-constexpr int kVtcNRW = kVtcRows / (kVtcCons / 4);          // output rows per consumer thread
-constexpr int kVtcThreads = kVtcProd + 32 * kVtcCons + 64;  // + consumers + MMA warp + TMA warp
+// consumer warps CONS (a template parameter: 4 take 64 rows each, 8 take 32 rows each)
+constexpr int vtc_threads(int cons) { return kVtcProd + 32 * cons + 64; }   // + consumers + MMA warp + TMA warp
 
 inline __host__ __device__ int vtc_kp(int R) { return ((kVtcRows + 2 * R) + 15) & ~15; }
 constexpr int kVtcMaxR = 24;       // Kp <= 112: the shared-memory budget below
@@ -78,7 +74,8 @@ inline __host__ __device__ size_t vpass_tc_smem(int R) {
 struct VtcParams {
     const float* centres;  // [K][3]
     float* planes;         // [4K][H][Wp] fp32 (ph == NULL)
-    unsigned short* ph;    // else fp16 hi and lo parts, strip-major: ph [4K][Wp / 32][H][hi 32 | lo 32]
+    unsigned short* ph;    // else fp16 hi parts, strip-major: ph [4K][Wp / 32][H][32] (64-byte rows), and
+    unsigned char* pl;     // the residuals as e4m3(lo): pl [4K][Wp / 32][H][32] (32-byte rows)
                            // (k_hpass_tc.cuh); Wp a multiple of 32
     int wexp;              // ph: stored value = t 2^(14 - e2 - wexp) (u planes), t 2^(14 - wexp) (b planes)
     const int* absmax;     // max |f| as float bits (k_absmax)
@@ -146,6 +143,26 @@ HDF_DEV void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
     lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
+// fp16 rounding of two values (rows r, r + 1 of one column): the 32-bit hi word and the fp32 residuals
+HDF_DEV uint32_t split_f16x2_res(float a, float b, float& ra, float& rb) {
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    ra = a - hf.x;
+    rb = b - hf.y;
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+// two fp32 -> e4m3 (saturating, round to nearest even): hi_val in the upper byte, lo_val in the lower
+HDF_DEV uint32_t cvt_e4m3x2(float hi_val, float lo_val) {
+    unsigned short r;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi_val), "f"(lo_val));
+    return r;
+}
+// The stored planes of the tensor-core row pass: t = hi + lo with hi = fp16(t) and the residual lo kept
+// as e4m3(kLoScale lo) (3 bytes per value; k_hpass_tc.cuh multiplies it by the taps / kLoScale).  With
+// |t| <= 2^14, |lo| <= 4 sits well inside e4m3's range unscaled; its subnormal floor (2^-10 absolute) is
+// 2^-24 of the largest value.
+constexpr float kLoScale = 1.f;
+
 // Byte offset of (row r, k) in an operand of nrow rows (multiple of 8) and Kp columns, K-major, no
 // swizzle, layout "m-groups adjacent": core matrix (r / 8, k / 8) at (k / 8) * (nrow * 16) + (r / 8) * 128.
 HDF_DEV uint32_t vtc_off(int r, int k, int nrow) {
@@ -153,8 +170,11 @@ HDF_DEV uint32_t vtc_off(int r, int k, int nrow) {
 }
 
 // f = p, rho = n = 3 (the colour bilateral filter); tm_p: p as [H][3W] fp32, box [96][64]
-__global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_constant__ CUtensorMap tm_p,
-                                                                   const __grid_constant__ VtcParams P) {
+template <int kVtcCons>
+__global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(const __grid_constant__ CUtensorMap tm_p,
+                                                                             const __grid_constant__ VtcParams P) {
+    constexpr int kVtcNRW = kVtcRows / (kVtcCons / 4);           // output rows per consumer thread
+    constexpr int kVtcThreads = vtc_threads(kVtcCons);
     extern __shared__ __align__(128) unsigned char sm_raw[];
     unsigned char* sm_vt = sm_raw + ((128u - (smem_u32(sm_raw) & 127u)) & 127u);
     __shared__ uint64_t c_full[kVtcRaw], c_free[kVtcRaw], z_full[kVtcStages], z_free[kVtcStages], d_full[kVtcStages],
@@ -235,7 +255,8 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
         const int col = tid & 31, cg = tid >> 5;   // this thread's column and first 8-row chunk
         const float c2 = P.neg_inv2sr2 * 1.4426950408889634f;
         // b su = 2^(d2 c2 + 14 - e2) (the u planes' scale folded into the exponent: exact), b sr = (b su) 2^e2
-        const float lsu = (float)(14 - e2), sbu = ldexpf(1.f, e2);
+        // (the fp16 planes' output scale 2^-wexp folded in as well: the MMA then yields the stored value)
+        const float lsu = (float)(14 - e2 - (P.ph ? P.wexp : 0)), sbu = ldexpf(1.f, e2);
         // per-tile bookkeeping in 32-bit incremental form: raw chunk ga = ui (TU + 1) + j (ring slot ga %
         // kVtcRaw, phase ga / kVtcRaw), the unit's first Z slot zs0 = ui (8 TU + 6) % kVtcZChunks
         const int U = 8 * TU + 6;
@@ -328,9 +349,9 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
         // TMEM lane quarter q = plane q, lane = column; consumer warp group h takes rows r0 .. r0 + NRW - 1
         const int q = warp & 3, col = lane, r0 = ((warp - kVtcProd / 32) >> 2) * kVtcNRW;
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-        // fp32 output: t = D / su (u planes), D / sr (b planes); fp16 hi/lo output: D 2^-wexp (both scaled,
-        // |value| <= 2^14 since the taps sum to at most 2^wexp)
-        const float inv = P.ph ? ldexpf(1.f, -P.wexp) : (q < 3) ? 1.f / su : 1.f / sr;   // exact (powers of two)
+        // fp32 output: t = D / su (u planes), D / sr (b planes); fp16 output: D itself, already t 2^(14 - e2 - wexp)
+        // (u) or t 2^(14 - wexp) (b) by the producers' scale, |value| <= 2^14 since the taps sum to at most 2^wexp
+        const float inv = (q < 3) ? 1.f / su : 1.f / sr;   // exact (powers of two); unused for the fp16 planes
         const int step = P.Wp;
         long long it = 0;
         for (long long ui = 0; ui < nui; ui++) {
@@ -353,27 +374,35 @@ __global__ void __launch_bounds__(kVtcThreads, 1) k_range_vpass_tc(const __grid_
                 }
                 tc_fence_before();
                 mbar_arrive(&d_free[s]);
-                if (P.ph) {   // strip-major fp16 planes: [plane][strip][H][hi 32 | lo 32] (k_hpass_tc.cuh)
+                if (P.ph) {   // strip-major planes: hi [plane][strip][H][32] fp16, lo [plane][strip][H][32] e4m3
                     if (yt + r0 < P.H) {   // (columns past W hold exact zeros: b = 0 there)
-                        // rows r, r + 1 at a time: after one exchange with the partner lane (col ^ 1) an even lane
-                        // holds row r's (hi, lo) words of columns col, col + 1 and an odd lane row r + 1's of
-                        // columns col - 1, col, so one warp store writes two rows' 64-byte hi halves, the next
-                        // their lo halves (whole 128-byte lines per row pair)
+                        // hi: rows r, r + 1 at a time: after one exchange with the partner lane (col ^ 1) an even
+                        // lane holds row r's words of columns col, col + 1 and an odd lane row r + 1's of columns
+                        // col - 1, col, so one warp store writes the two rows' 64-byte lines (128 contiguous bytes).
+                        // lo: rows r .. r + 3 at a time: each lane packs its column's 4 bytes, a 4 x 4 byte transpose
+                        // over lane groups of 4 leaves lane 4m + i with row r + i of columns 4m .. 4m + 3, so one
+                        // warp store writes the four rows' 32-byte lines.
                         const int odd = col & 1;
                         const uint32_t sel = odd ? 0x3276u : 0x5410u;
+                        const uint32_t sel1 = odd ? 0x3715u : 0x6240u, sel2 = (lane & 2) ? 0x3276u : 0x5410u;
                         const int nr = min(kVtcNRW, P.H - yt - r0);
-                        uint32_t* o = reinterpret_cast<uint32_t*>(P.ph) + (long long)(4 * k + q) * P.pstride +
-                                      (long long)strip * P.H * 32 + (long long)(yt + r0 + odd) * 32 + (col >> 1);
+                        const long long row0 = ((long long)(4 * k + q) * (P.Wp >> 5) + strip) * P.H + (yt + r0);
+                        uint32_t* oh = reinterpret_cast<uint32_t*>(P.ph) + row0 * 16 + odd * 16 + (col >> 1);
+                        uint32_t* ol = reinterpret_cast<uint32_t*>(P.pl) + row0 * 8 + (lane & 3) * 8 + (lane >> 2);
 #pragma unroll
-                        for (int jj = 0; jj < kVtcNRW; jj += 2) {
-                            uint32_t hi, lo;
-                            split_f16x2(v[jj] * inv, v[jj + 1] * inv, hi, lo);   // (row r, row r + 1) per word
-                            const uint32_t ph2 = __shfl_xor_sync(0xffffffffu, hi, 1);
-                            const uint32_t pl2 = __shfl_xor_sync(0xffffffffu, lo, 1);
-                            if (nr == kVtcNRW || jj + odd < nr) {
-                                o[jj * 32] = __byte_perm(hi, ph2, sel);
-                                o[jj * 32 + 16] = __byte_perm(lo, pl2, sel);
-                            }
+                        for (int jj = 0; jj < kVtcNRW; jj += 4) {
+                            float l0, l1, l2, l3;
+                            const uint32_t h01 = split_f16x2_res(v[jj], v[jj + 1], l0, l1);
+                            const uint32_t h23 = split_f16x2_res(v[jj + 2], v[jj + 3], l2, l3);
+                            const uint32_t p01 = __shfl_xor_sync(0xffffffffu, h01, 1);
+                            const uint32_t p23 = __shfl_xor_sync(0xffffffffu, h23, 1);
+                            const uint32_t lw = cvt_e4m3x2(l1 * kLoScale, l0 * kLoScale) |
+                                                (cvt_e4m3x2(l3 * kLoScale, l2 * kLoScale) << 16);
+                            const uint32_t a = __byte_perm(lw, __shfl_xor_sync(0xffffffffu, lw, 1), sel1);
+                            const uint32_t b = __byte_perm(a, __shfl_xor_sync(0xffffffffu, a, 2), sel2);
+                            if (nr == kVtcNRW || jj + odd < nr) oh[jj * 16] = __byte_perm(h01, p01, sel);
+                            if (nr == kVtcNRW || jj + 2 + odd < nr) oh[(jj + 2) * 16] = __byte_perm(h23, p23, sel);
+                            if (nr == kVtcNRW || jj + (lane & 3) < nr) ol[jj * 8] = b;
                         }
                     }
                 } else if (x < P.W && yt + r0 < P.H) {
