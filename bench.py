@@ -386,17 +386,20 @@ def run_ours(args, rank: int, world: int, dist):
                  "path": "tensor cores (tcgen05 kind::f16, Toeplitz FIR, fp16 hi/lo split)",
                  "tc_issued_tflops": round(tc_flop[name] / t / 1e12, 2),
                  "tc_frac_of_f16_peak": round(tc_flop[name] / t / f16_peak, 4)}
-            if name == "vpass":   # it only writes: against the write-only bandwidth too
-                wb = 4 * H * W * (cfg.n + 1) * K
+            # bytes per stored plane value: fp16 hi + e4m3 residual for the tensor-core row pass, else fp32
+            pbytes = 3 if htc else 4
+            if name == "vpass":   # it only writes: the bytes it stores against the write-only bandwidth
+                wb = pbytes * H * W * (cfg.n + 1) * K
                 r["write_roof"] = {"achieved": round(wb / t / 1e9, 1), "peak": round(write_peak, 1), "unit": "GB/s",
                                    "frac": round(wb / t / 1e9 / write_peak, 4),
-                                   "peak_basis": "4 GiB fill measured in this run (best of 6)"}
+                                   "peak_basis": "4 GiB fill measured in this run (best of 6)",
+                                   "bytes": f"the planes as stored ({pbytes} bytes per value)"}
             if name == "hpass":   # it only reads (the planes and the coefficient planes): the read-only bandwidth
-                rb = 4 * H * W * ((cfg.n + 1) * K + K)
+                rb = H * W * (pbytes * (cfg.n + 1) * K + 4 * K)
                 r["read_roof"] = {"achieved": round(rb / t / 1e9, 1), "peak": round(read_peak, 1), "unit": "GB/s",
                                   "frac": round(rb / t / 1e9 / read_peak, 4),
                                   "peak_basis": "fp32 sum over 4 GiB measured in this run (best of 6)",
-                                  "bytes": "planes + coefficient planes read once"}
+                                  "bytes": f"planes as stored ({pbytes} bytes per value) + fp32 coefficient planes, read once"}
         elif t_alu > t_hbm:
             r = {"bound": "alu", "achieved": round(fma_s / 1e12, 3), "peak": round(fma_peak(sm_mhz, nsm) / 1e12, 3),
                  "unit": "TFMA/s (fp32)", "frac": round(fma_s / fma_peak(sm_mhz, nsm), 4),

@@ -952,8 +952,12 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             // consumer warps: 8 (32 rows each; the fp16 + e4m3 stores are the consumers' work), HDF_VTC_CONS=4 keeps 4
             int cons = 8;
             if (const char* e = getenv("HDF_VTC_CONS")) cons = atoi(e) == 4 ? 4 : 8;
+            // the stacked Toeplitz operand (k_vpass_tc.cuh, NS) only when HDF_VTC_NSTACK=1 (measured: see DESIGN.md)
+            bool vns = false;
+            if (const char* e = getenv("HDF_VTC_NSTACK")) vns = atoi(e) != 0;
             void (*kvtc)(const CUtensorMap, const hdf::VtcParams) =
-                cons == 4 ? hdf::k_range_vpass_tc<4> : hdf::k_range_vpass_tc<8>;
+                cons == 4 ? hdf::k_range_vpass_tc<4, false>
+                          : (vns ? hdf::k_range_vpass_tc<8, true> : hdf::k_range_vpass_tc<8, false>);
             const int vthreads = cons == 4 ? hdf::vtc_threads(4) : hdf::vtc_threads(8);
             HDF_CUDA(cudaFuncSetAttribute(kvtc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             // output rows [y0, y1) on `grid` SMs: row segments of whole 64-row tiles, enough units to fill the grid
@@ -1132,6 +1136,8 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     CUtensorMap tz, tzl, tcc;
     hdf::HtcParams hq;
     size_t htc_smem = 0;
+    void (*khtc)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const hdf::HtcParams) =
+        hdf::k_hpass_combine_tc<true>;
     if (use_htc) {
         unsigned short* ph = reinterpret_cast<unsigned short*>(w.planes);
         rc = encode_strips(&tz, ph, H, F.Wp, K * 4, (uint32_t)hdf::kHtcRows, 4u, 2);
@@ -1156,8 +1162,12 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         for (int t = 0; t < hdf::kMaxTaps; t++) hq.taps[t] = 0.f;
         for (int t = 0; t <= 2 * F.R; t++) hq.taps[t] = taps[F.Rp - F.R + t];
         htc_smem = hdf::hpass_tc_smem();
-        HDF_CUDA(cudaFuncSetAttribute(hdf::k_hpass_combine_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)htc_smem));
+        // the stacked Toeplitz operand (one N = 128 MMA per K step instead of two of N = 64) is the default;
+        // HDF_HTC_NSTACK=0 keeps the two-MMA form
+        if (const char* e = getenv("HDF_HTC_NSTACK")) {
+            if (*e && atoi(e) == 0) khtc = hdf::k_hpass_combine_tc<false>;
+        }
+        HDF_CUDA(cudaFuncSetAttribute(khtc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)htc_smem));
     }
     const int tile_rows = use_htc ? hdf::kHtcRows : F.RR;
     const int row_tiles = use_htc ? (H + hdf::kHtcRows - 1) / hdf::kHtcRows : (int)F.hl.grid.y;
@@ -1186,8 +1196,8 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
                 const long long nunit = (long long)(ty1 - ty0) * hq.nstrip;
                 // (the last band's row pass has the GPU to itself)
                 const int grid = (pipe && ch < nch - 1) ? gh : nsm;
-                hdf::k_hpass_combine_tc<<<(unsigned)std::max<long long>(1, std::min<long long>(grid, nunit)),
-                                          hdf::kHtcThreads, htc_smem, hs>>>(tz, tzl, tcc, hq);
+                khtc<<<(unsigned)std::max<long long>(1, std::min<long long>(grid, nunit)), hdf::kHtcThreads, htc_smem,
+                       hs>>>(tz, tzl, tcc, hq);
                 HDF_CUDA(cudaGetLastError());
             } else {
                 HDF_CUDA(hdf::launch_hpass(F.Rp, F.box, hl, hs, tp, tc, hp));

@@ -123,6 +123,11 @@ HDF_DEV void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {
 }
 HDF_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// NS (the default): the two fp16 MMAs of a K step that share the operand z_hi run as ONE MMA of N = 128 against
+// the stacked Toeplitz operand [T_hi; T_lo] (z_hi is read from shared memory once instead of twice: the kernel is
+// bound by shared-memory bandwidth); the accumulator stage is then 128 columns (z_hi T_hi +
+// z_lo T_8 in columns 0..63, z_hi T_lo in 64..127: all 512 TMEM columns) and the consumers add the halves.
+template <bool NS>
 __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __grid_constant__ CUtensorMap tm_zh,
                                                                      const __grid_constant__ CUtensorMap tm_zl,
                                                                      const __grid_constant__ CUtensorMap tm_c,
@@ -134,6 +139,8 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
     __shared__ uint32_t tmem_base_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int R = P.R, Kp = kHtcKp;
+    constexpr uint32_t kStageCols = NS ? 2 * kHtcN : kHtcN;          // TMEM columns per accumulator stage
+    constexpr uint32_t kTmemCols = 2 * kHtcS * kStageCols;           // 256, or all 512
     unsigned char* ring = sm;                                              // [NB][hi 8 KB | lo 4 KB]
     unsigned char* cring = ring + (size_t)kHtcNB * kHtcSlotBytes;          // [NC][2][32][32] fp32, SW128
     unsigned char* Th = cring + (size_t)kHtcNC * kHtcCBytes;
@@ -148,8 +155,13 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
         const float w = (t >= -R && t <= R) ? P.taps[t + R] : 0.f;
         unsigned short h, l;
         split_f16(w, h, l);
-        *reinterpret_cast<unsigned short*>(Th + vtc_off(j, i, kHtcN)) = h;
-        *reinterpret_cast<unsigned short*>(Tl + vtc_off(j, i, kHtcN)) = l;
+        if (NS) {   // one operand of 128 rows: T_hi in rows 0..63, T_lo in rows 64..127 (Th and Tl are contiguous)
+            *reinterpret_cast<unsigned short*>(Th + vtc_off(j, i, 2 * kHtcN)) = h;
+            *reinterpret_cast<unsigned short*>(Th + vtc_off(kHtcN + j, i, 2 * kHtcN)) = l;
+        } else {
+            *reinterpret_cast<unsigned short*>(Th + vtc_off(j, i, kHtcN)) = h;
+            *reinterpret_cast<unsigned short*>(Tl + vtc_off(j, i, kHtcN)) = l;
+        }
         // e4m3 operand, K-major no swizzle: core matrix (j / 8, i / 16) of 8 rows x 16 bytes
         T8[(i >> 4) * (kHtcN * 16) + (j >> 3) * 128 + (j & 7) * 16 + (i & 15)] =
             (unsigned char)(cvt_e4m3x2(0.f, w * (1.f / kLoScale)) & 0xFFu);
@@ -174,7 +186,7 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                     "r"(256)
+                     "r"(kTmemCols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -215,12 +227,39 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
                 mbar_wait(&d_full[s], (uint32_t)(kk >> 1) & 1u);
                 tc_fence_after();
                 uint32_t d0[32], d1[32];
+                const unsigned char* cb = cring + (size_t)cs * kHtcCBytes + r * 128;
+                if (NS) {   // columns j and 64 + j of the stage: (z_hi T_hi + z_lo T_8) + z_hi T_lo
+                    const uint32_t ta = tbase + lane_base + (uint32_t)s * kStageCols;
+                    tmem_ld32_nw(ta, d0);
+                    tmem_ld32_nw(ta + 64, d1);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c4 = 0; c4 < 8; c4++) {   // half 0: columns 0..31 (16-byte chunks swizzled by r & 7)
+                        const float4 cv = *reinterpret_cast<const float4*>(cb + ((c4 ^ (r & 7)) << 4));
+                        acc[4 * c4 + 0] = fmaf(cv.x, __uint_as_float(d0[4 * c4 + 0]) + __uint_as_float(d1[4 * c4 + 0]), acc[4 * c4 + 0]);
+                        acc[4 * c4 + 1] = fmaf(cv.y, __uint_as_float(d0[4 * c4 + 1]) + __uint_as_float(d1[4 * c4 + 1]), acc[4 * c4 + 1]);
+                        acc[4 * c4 + 2] = fmaf(cv.z, __uint_as_float(d0[4 * c4 + 2]) + __uint_as_float(d1[4 * c4 + 2]), acc[4 * c4 + 2]);
+                        acc[4 * c4 + 3] = fmaf(cv.w, __uint_as_float(d0[4 * c4 + 3]) + __uint_as_float(d1[4 * c4 + 3]), acc[4 * c4 + 3]);
+                    }
+                    tmem_ld32_nw(ta + 32, d0);
+                    tmem_ld32_nw(ta + 96, d1);
+                    tmem_wait_ld();
+                    tc_fence_before();
+                    mbar_arrive(&d_free[s]);
+#pragma unroll
+                    for (int c4 = 0; c4 < 8; c4++) {   // half 1: columns 32..63
+                        const float4 cv = *reinterpret_cast<const float4*>(cb + 4096 + ((c4 ^ (r & 7)) << 4));
+                        acc[32 + 4 * c4 + 0] = fmaf(cv.x, __uint_as_float(d0[4 * c4 + 0]) + __uint_as_float(d1[4 * c4 + 0]), acc[32 + 4 * c4 + 0]);
+                        acc[32 + 4 * c4 + 1] = fmaf(cv.y, __uint_as_float(d0[4 * c4 + 1]) + __uint_as_float(d1[4 * c4 + 1]), acc[32 + 4 * c4 + 1]);
+                        acc[32 + 4 * c4 + 2] = fmaf(cv.z, __uint_as_float(d0[4 * c4 + 2]) + __uint_as_float(d1[4 * c4 + 2]), acc[32 + 4 * c4 + 2]);
+                        acc[32 + 4 * c4 + 3] = fmaf(cv.w, __uint_as_float(d0[4 * c4 + 3]) + __uint_as_float(d1[4 * c4 + 3]), acc[32 + 4 * c4 + 3]);
+                    }
+                } else {
                 tmem_ld32_nw(tbase + lane_base + (uint32_t)(s * kHtcN), d0);
                 tmem_ld32_nw(tbase + lane_base + (uint32_t)(s * kHtcN + 32), d1);
                 tmem_wait_ld();
                 tc_fence_before();
                 mbar_arrive(&d_free[s]);
-                const unsigned char* cb = cring + (size_t)cs * kHtcCBytes + r * 128;
 #pragma unroll
                 for (int c4 = 0; c4 < 8; c4++) {   // half 0: columns 0..31 (16-byte chunks swizzled by r & 7)
                     const float4 cv = *reinterpret_cast<const float4*>(cb + ((c4 ^ (r & 7)) << 4));
@@ -236,6 +275,7 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
                     acc[32 + 4 * c4 + 1] = fmaf(cv.y, __uint_as_float(d1[4 * c4 + 1]), acc[32 + 4 * c4 + 1]);
                     acc[32 + 4 * c4 + 2] = fmaf(cv.z, __uint_as_float(d1[4 * c4 + 2]), acc[32 + 4 * c4 + 2]);
                     acc[32 + 4 * c4 + 3] = fmaf(cv.w, __uint_as_float(d1[4 * c4 + 3]), acc[32 + 4 * c4 + 3]);
+                }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&c_free[cs]);
@@ -283,8 +323,8 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
             }
         }
     } else if (warp == 4 * kHtcS) {   // ------------------------------------------------ MMA warp -------
-        const uint32_t idesc = umma_idesc_f16(128, kHtcN);
-        const uint64_t dt = umma_desc(0, kHtcN * 16, 128);
+        const uint32_t idesc = umma_idesc_f16(128, kHtcN), idesc_s = umma_idesc_f16(128, 2 * kHtcN);
+        const uint64_t dt = umma_desc(0, kHtcN * 16, 128), dts = umma_desc(0, 2 * kHtcN * 16, 128);
         const uint32_t tH = smem_u32(Th), tL = smem_u32(Tl), t8 = smem_u32(T8), rb = smem_u32(ring);
         // ring slot and phase of the step's first strip g0 = 6 kk, kept in 32-bit incremental form (a step's
         // strips g0 .. g0 + 5 wrap the ring at most once)
@@ -306,18 +346,24 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
                     }
                     if (kk >= 2) mbar_wait(&d_free[s], (uint32_t)((kk >> 1) - 1) & 1u);
                     tc_fence_after();
-                    const uint32_t td = tbase + (uint32_t)(s * kHtcN);
+                    const uint32_t td = tbase + (uint32_t)s * kStageCols;
 #pragma unroll
                     for (int ks = 0; ks < kHtcKp / 16; ks++) {
                         int sl = bslot + 2 * t + (ks >> 1);
                         if (sl >= kHtcNB) sl -= kHtcNB;
                         const uint32_t za = rb + (uint32_t)sl * kHtcSlotBytes + (uint32_t)((ks & 1) * 32);
                         const uint64_t aH = umma_desc_sw64(za);
-                        const uint32_t ot = (uint32_t)ks * (2u * kHtcN * 16u);
-                        const uint64_t bH = dt | (uint64_t)(((tH + ot) >> 4) & 0x3FFFu);
-                        const uint64_t bL = dt | (uint64_t)(((tL + ot) >> 4) & 0x3FFFu);
-                        umma_f16_warp(td, aH, bL, idesc, ks > 0 ? 1u : 0u);
-                        umma_f16_warp(td, aH, bH, idesc, 1u);
+                        if (NS) {   // z_hi [T_hi; T_lo]^T: 128 accumulator columns
+                            const uint32_t ot = (uint32_t)ks * (2u * 2u * kHtcN * 16u);
+                            const uint64_t bS = dts | (uint64_t)(((tH + ot) >> 4) & 0x3FFFu);
+                            umma_f16_warp(td, aH, bS, idesc_s, ks > 0 ? 1u : 0u);
+                        } else {
+                            const uint32_t ot = (uint32_t)ks * (2u * kHtcN * 16u);
+                            const uint64_t bH = dt | (uint64_t)(((tH + ot) >> 4) & 0x3FFFu);
+                            const uint64_t bL = dt | (uint64_t)(((tL + ot) >> 4) & 0x3FFFu);
+                            umma_f16_warp(td, aH, bL, idesc, ks > 0 ? 1u : 0u);
+                            umma_f16_warp(td, aH, bH, idesc, 1u);
+                        }
                     }
 #pragma unroll
                     for (int b = 0; b < 4; b++) {   // the residuals: one e4m3 MMA (K = 32) per strip
@@ -383,7 +429,7 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(256) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kTmemCols) : "memory");
     }
 }
 

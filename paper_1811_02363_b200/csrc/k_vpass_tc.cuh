@@ -170,7 +170,10 @@ HDF_DEV uint32_t vtc_off(int r, int k, int nrow) {
 }
 
 // f = p, rho = n = 3 (the colour bilateral filter); tm_p: p as [H][3W] fp32, box [96][64]
-template <int kVtcCons>
+// NS: the two MMAs of a K step that share the operand z_hi run as one MMA of N = 128 against the stacked Toeplitz
+// operand [T_hi; T_lo] (z_hi is read from shared memory once; an accumulator stage is then 128 TMEM columns:
+// z_hi T_hi + z_lo T_hi in columns 0..63, z_hi T_lo in 64..127, added by the consumers)
+template <int kVtcCons, bool NS>
 __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(const __grid_constant__ CUtensorMap tm_p,
                                                                              const __grid_constant__ VtcParams P) {
     constexpr int kVtcNRW = kVtcRows / (kVtcCons / 4);           // output rows per consumer thread
@@ -184,6 +187,8 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
     const int R = P.R, Kp = vtc_kp(R);
     const size_t tbytes = (size_t)kVtcRows * Kp * 2, zbytes = (size_t)kVtcM * Kp * 2;
     constexpr uint32_t kSlotBytes = 64 * 96 * 4;
+    constexpr uint32_t kStageCols = NS ? 2 * kVtcRows : kVtcRows;   // TMEM columns per accumulator stage
+    constexpr uint32_t kTmemCols = kVtcStages * kStageCols <= 256 ? 256 : 512;
     unsigned char* Th = sm_vt;
     unsigned char* Tl = Th + tbytes;
     unsigned char* ZH = Tl + tbytes;                                          // Z ring, hi
@@ -198,8 +203,13 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
         const float w = (t >= -R && t <= R) ? P.taps[t + R] : 0.f;
         unsigned short h, l;
         split_f16(w, h, l);
-        *reinterpret_cast<unsigned short*>(Th + vtc_off(j, i, kVtcRows)) = h;
-        *reinterpret_cast<unsigned short*>(Tl + vtc_off(j, i, kVtcRows)) = l;
+        if (NS) {   // one operand of 128 rows: T_hi in rows 0..63, T_lo in rows 64..127 (Th and Tl are contiguous)
+            *reinterpret_cast<unsigned short*>(Th + vtc_off(j, i, 2 * kVtcRows)) = h;
+            *reinterpret_cast<unsigned short*>(Th + vtc_off(kVtcRows + j, i, 2 * kVtcRows)) = l;
+        } else {
+            *reinterpret_cast<unsigned short*>(Th + vtc_off(j, i, kVtcRows)) = h;
+            *reinterpret_cast<unsigned short*>(Tl + vtc_off(j, i, kVtcRows)) = l;
+        }
     }
     if (tid == 0) {
         prefetch_tmap(&tm_p);
@@ -217,7 +227,7 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                     "r"(256)
+                     "r"(kTmemCols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -368,9 +378,14 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
 #pragma unroll
                 for (int n0 = 0; n0 < kVtcNRW; n0 += 16) {
                     float t16[16];
-                    tmem_ld16(tbase + lane_base + (uint32_t)(s * kVtcRows + r0 + n0), t16);
+                    tmem_ld16(tbase + lane_base + (uint32_t)s * kStageCols + (uint32_t)(r0 + n0), t16);
 #pragma unroll
                     for (int jj = 0; jj < 16; jj++) v[n0 + jj] = t16[jj];
+                    if (NS) {
+                        tmem_ld16(tbase + lane_base + (uint32_t)s * kStageCols + (uint32_t)(kVtcRows + r0 + n0), t16);
+#pragma unroll
+                        for (int jj = 0; jj < 16; jj++) v[n0 + jj] += t16[jj];
+                    }
                 }
                 tc_fence_before();
                 mbar_arrive(&d_free[s]);
@@ -429,8 +444,9 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
             // the whole warp runs the loop (warp-uniform values in uniform registers) and one elected lane
             // issues: 32-bit incremental index math only (the ring slot of the tile's first chunk advances by
             // 8 per tile and by 8 TU + 6 per unit, modulo the ring)
-            const uint32_t idesc = umma_idesc_f16(kVtcM, kVtcRows);
-            const uint64_t dz = umma_desc(0, kVtcZChunkBytes, 128), dt = umma_desc(0, kVtcRows * 16, 128);
+            const uint32_t idesc = umma_idesc_f16(kVtcM, kVtcRows), idesc_s = umma_idesc_f16(kVtcM, 2 * kVtcRows);
+            const uint64_t dz = umma_desc(0, kVtcZChunkBytes, 128),
+                           dt = umma_desc(0, (NS ? 2 : 1) * kVtcRows * 16, 128);
             const uint32_t tH = smem_u32(Th), tL = smem_u32(Tl), zH = smem_u32(ZH), zL = smem_u32(ZL);
             const int per_unit = (8 * TU + 6) % kVtcZChunks;
             int ubase = (int)((long long)0 % kVtcZChunks);
@@ -442,18 +458,23 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
                     mbar_wait(&z_full[s], (uint32_t)wrap);
                     if (it >= kVtcStages) mbar_wait(&d_free[s], (uint32_t)(wrap ^ 1));
                     tc_fence_after();
-                    const uint32_t td = tbase + (uint32_t)(s * kVtcRows);
+                    const uint32_t td = tbase + (uint32_t)s * kStageCols;
                     int slot = base;
                     for (int ks = 0; ks < Kp / 16; ks++) {
                         const uint32_t oz = (uint32_t)slot * (uint32_t)kVtcZChunkBytes;
-                        const uint32_t ot = (uint32_t)ks * (2u * kVtcRows * 16u);
+                        const uint32_t ot = (uint32_t)ks * ((NS ? 4u : 2u) * kVtcRows * 16u);
                         const uint64_t aL = dz | (uint64_t)(((zL + oz) >> 4) & 0x3FFFu);
                         const uint64_t aH = dz | (uint64_t)(((zH + oz) >> 4) & 0x3FFFu);
-                        const uint64_t bH = dt | (uint64_t)(((tH + ot) >> 4) & 0x3FFFu);
-                        const uint64_t bL = dt | (uint64_t)(((tL + ot) >> 4) & 0x3FFFu);
-                        umma_f16_warp(td, aL, bH, idesc, ks > 0 ? 1u : 0u);
-                        umma_f16_warp(td, aH, bL, idesc, 1u);
-                        umma_f16_warp(td, aH, bH, idesc, 1u);
+                        const uint64_t bH = dt | (uint64_t)(((tH + ot) >> 4) & 0x3FFFu);   // NS: rows 0..63 of the stack
+                        if (NS) {
+                            umma_f16_warp(td, aH, bH, idesc_s, ks > 0 ? 1u : 0u);   // z_hi [T_hi; T_lo]^T
+                            umma_f16_warp(td, aL, bH, idesc, 1u);                   // z_lo T_hi^T
+                        } else {
+                            const uint64_t bL = dt | (uint64_t)(((tL + ot) >> 4) & 0x3FFFu);
+                            umma_f16_warp(td, aL, bH, idesc, ks > 0 ? 1u : 0u);
+                            umma_f16_warp(td, aH, bL, idesc, 1u);
+                            umma_f16_warp(td, aH, bH, idesc, 1u);
+                        }
                         slot += 2;
                         if (slot >= kVtcZChunks) slot -= kVtcZChunks;
                     }
@@ -488,7 +509,7 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(256) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kTmemCols) : "memory");
     }
 }
 
