@@ -572,6 +572,11 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
+bool getenv_on(const char* name) {
+    const char* e = getenv(name);
+    return e && atoi(e) != 0;
+}
+
 int encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t pitch_bytes,
              uint64_t plane_bytes, uint32_t b0, uint32_t b1, uint32_t b2,
              CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
@@ -1007,6 +1012,16 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     HDF_CUDA(cudaStreamWaitEvent(hs, ss.join, 0));   // A^+ is ready
     side_lock.unlock();
     // loop for2: c(i) = A^+ b(i) -> K coefficient planes
+    // (HDF_C24=1: in 24 bits when k_coeffs_tc feeds the stacked-operand tensor-core row pass, CoefParams.  Off by
+    // default: measured slower at config 5 -- the coefficient kernel's consumers are bound by instruction issue, not
+    // by the bytes they write (1.44 -> 1.61 ms with the pack/transpose shuffles), and the row pass is not bound by
+    // HBM reads (3.33 -> 3.36 ms))
+    bool htc_ns = true;
+    if (const char* e = getenv("HDF_HTC_NSTACK")) {
+        if (*e && atoi(e) == 0) htc_ns = false;
+    }
+    const bool c24 = getenv_on("HDF_C24") && use_htc && htc_ns && !hard && K <= hdf::kTcMaxK && K % 4 == 0 &&
+                     W % 4 == 0 && !getenv_on("HDF_COEFFS_MMA") && !getenv_on("HDF_COEFFS_FMA");
     {
         hdf::CoefParams cp;
         cp.p = p;
@@ -1014,6 +1029,10 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         cp.Ap32 = w.Ap32;
         cp.cpl = w.cpl;
         cp.cstride = (long long)H * F.Wp;
+        if (c24) {   // 24-bit planes inside the same buffer: [K][H][Wp] 16-bit words, then [K][H][Wp] bytes
+            cp.ch = reinterpret_cast<unsigned short*>(w.cpl);
+            cp.cm = reinterpret_cast<unsigned char*>(w.cpl) + (size_t)K * H * F.Wp * 2;
+        }
         cp.H = H;
         cp.W = W;
         cp.Wp = F.Wp;
@@ -1133,11 +1152,11 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     // the tensor-core row pass: tensor maps of the strip-major fp16 hi and e4m3 lo planes (boxes [4 planes][32 rows]
     // [the hi or lo half of a 32-column strip], 64-byte swizzle) and of the coefficient planes (two
     // [32 rows][32 columns] halves per tile, 128-byte swizzle)
-    CUtensorMap tz, tzl, tcc;
+    CUtensorMap tz, tzl, tcc, tcm;
     hdf::HtcParams hq;
     size_t htc_smem = 0;
-    void (*khtc)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const hdf::HtcParams) =
-        hdf::k_hpass_combine_tc<true>;
+    void (*khtc)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const hdf::HtcParams) =
+        c24 ? hdf::k_hpass_combine_tc<true, true> : hdf::k_hpass_combine_tc<true, false>;
     if (use_htc) {
         unsigned short* ph = reinterpret_cast<unsigned short*>(w.planes);
         rc = encode_strips(&tz, ph, H, F.Wp, K * 4, (uint32_t)hdf::kHtcRows, 4u, 2);
@@ -1145,9 +1164,21 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         rc = encode_strips(&tzl, reinterpret_cast<unsigned char*>(w.planes) + (size_t)4 * K * H * F.Wp * 2, H, F.Wp, K * 4,
                            (uint32_t)hdf::kHtcRows, 4u, 1);
         if (rc) return rc;
-        rc = encode3d(&tcc, w.cpl, (uint64_t)W, (uint64_t)H, (uint64_t)K, (uint64_t)F.Wp * 4, (uint64_t)H * F.Wp * 4,
-                      32u, (uint32_t)hdf::kHtcRows, 1u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CU_TENSOR_MAP_SWIZZLE_128B);
-        if (rc) return rc;
+        if (c24) {   // boxes [32 rows][64 columns] of the 16-bit words (128-byte swizzle) and of the bytes (64-byte)
+            rc = encode3d(&tcc, w.cpl, (uint64_t)W, (uint64_t)H, (uint64_t)K, (uint64_t)F.Wp * 2, (uint64_t)H * F.Wp * 2,
+                          (uint32_t)hdf::kHtcN, (uint32_t)hdf::kHtcRows, 1u, CU_TENSOR_MAP_DATA_TYPE_UINT16,
+                          CU_TENSOR_MAP_SWIZZLE_128B);
+            if (rc) return rc;
+            rc = encode3d(&tcm, reinterpret_cast<unsigned char*>(w.cpl) + (size_t)K * H * F.Wp * 2, (uint64_t)W, (uint64_t)H,
+                          (uint64_t)K, (uint64_t)F.Wp, (uint64_t)H * F.Wp, (uint32_t)hdf::kHtcN, (uint32_t)hdf::kHtcRows, 1u,
+                          CU_TENSOR_MAP_DATA_TYPE_UINT8, CU_TENSOR_MAP_SWIZZLE_64B);
+            if (rc) return rc;
+        } else {
+            rc = encode3d(&tcc, w.cpl, (uint64_t)W, (uint64_t)H, (uint64_t)K, (uint64_t)F.Wp * 4, (uint64_t)H * F.Wp * 4,
+                          32u, (uint32_t)hdf::kHtcRows, 1u, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CU_TENSOR_MAP_SWIZZLE_128B);
+            if (rc) return rc;
+            tcm = tcc;
+        }
         hq.g = g;
         hq.flag_count = w.flag_count;
         hq.flag_list = w.flag_list;
@@ -1164,9 +1195,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         htc_smem = hdf::hpass_tc_smem();
         // the stacked Toeplitz operand (one N = 128 MMA per K step instead of two of N = 64) is the default;
         // HDF_HTC_NSTACK=0 keeps the two-MMA form
-        if (const char* e = getenv("HDF_HTC_NSTACK")) {
-            if (*e && atoi(e) == 0) khtc = hdf::k_hpass_combine_tc<false>;
-        }
+        if (!htc_ns) khtc = hdf::k_hpass_combine_tc<false, false>;
         HDF_CUDA(cudaFuncSetAttribute(khtc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)htc_smem));
     }
     const int tile_rows = use_htc ? hdf::kHtcRows : F.RR;
@@ -1197,7 +1226,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
                 // (the last band's row pass has the GPU to itself)
                 const int grid = (pipe && ch < nch - 1) ? gh : nsm;
                 khtc<<<(unsigned)std::max<long long>(1, std::min<long long>(grid, nunit)), hdf::kHtcThreads, htc_smem,
-                       hs>>>(tz, tzl, tcc, hq);
+                       hs>>>(tz, tzl, tcc, tcm, hq);
                 HDF_CUDA(cudaGetLastError());
             } else {
                 HDF_CUDA(hdf::launch_hpass(F.Rp, F.box, hl, hs, tp, tc, hp));

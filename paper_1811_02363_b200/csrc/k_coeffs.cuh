@@ -195,6 +195,12 @@ struct CoefParams {
     long long cstride;   // H * Wp
     int H, W, Wp, rho, K;
     float neg_inv2sr2;
+    // k_coeffs_tc only: when ch != NULL the coefficients are stored in 24 bits for the tensor-core row pass
+    // (k_hpass_tc.cuh) instead of cpl: ch [K][H][Wp] = the upper 16 bits of the fp32 value, cm [K][H][Wp] = one byte
+    // m such that the value is rebuilt as bits (ch << 16 | m << 8 | m) (m = round(low 16 bits / 257): 15 explicit
+    // mantissa bits, relative error <= 2^-16).  Needs K % 4 == 0 and W % 4 == 0.
+    unsigned short* ch = nullptr;
+    unsigned char* cm = nullptr;
 };
 
 #ifndef HDF_COEFFS_MMA_ONLY   // inst_coeffs.cu compiles only k_coeffs_mma

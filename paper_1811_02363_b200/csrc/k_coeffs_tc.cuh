@@ -301,7 +301,45 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
             }
             tc_fence_before();
             mbar_arrive(&d_free[s]);
-            if (valid) {
+            if (P.ch) {   // 24-bit planes (CoefParams): packed over lane pairs (hi 16 bits) and lane quads (the byte)
+                // the lane's pixel i has x = lane (mod 4) (W % 4 == 0, tiles of 128 pixels), so a lane pair / quad is a
+                // pixel pair / quad of one row, all valid or all invalid; every lane runs the shuffles
+                const int lane = tid & 31, odd = lane & 1, l3 = lane & 3;
+                const int nn = min(32, K - n0);
+                const long long pb = y * P.Wp + xx;
+                // plane n0 + odd, pixels (x - odd, x - odd + 1): one 32-bit word; two planes further per pair
+                uint32_t* oh = reinterpret_cast<uint32_t*>(P.ch + (long long)(n0 + odd) * P.cstride + (pb - odd));
+                // plane n0 + l3, pixels x - l3 .. x - l3 + 3: one 32-bit word; four planes further per group
+                uint32_t* om = reinterpret_cast<uint32_t*>(P.cm + (long long)(n0 + l3) * P.cstride + (pb - l3));
+                const uint32_t sel1 = odd ? 0x3715u : 0x6240u, sel2 = (lane & 2) ? 0x3276u : 0x5410u;
+#pragma unroll
+                for (int n = 0; n < 32; n += 4) {
+                    uint32_t e[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const uint32_t w = __float_as_uint(v[n + u]);
+                        const uint32_t m = ((w & 0xFFFFu) * 255u + 32768u) >> 16;
+                        e[u] = __byte_perm(w, m, 0x3244);   // the stored value's bits: (hi16, m, m)
+                    }
+                    const uint32_t r01 = __shfl_xor_sync(0xffffffffu, odd ? e[0] : e[1], 1);
+                    const uint32_t r23 = __shfl_xor_sync(0xffffffffu, odd ? e[2] : e[3], 1);
+                    // even lane: (own coefficient n, partner's n) of pixels (x, x + 1); odd lane: (partner's n + 1, own)
+                    const uint32_t h01 = __byte_perm(odd ? r01 : e[0], odd ? e[1] : r01, 0x7632);
+                    const uint32_t h23 = __byte_perm(odd ? r23 : e[2], odd ? e[3] : r23, 0x7632);
+                    // the bytes of coefficients n .. n + 3, then a 4 x 4 byte transpose over the lane quad: lane l3 ends
+                    // with coefficient n + l3 of the quad's four pixels
+                    const uint32_t lw = __byte_perm(__byte_perm(e[0], e[1], 0x0051), __byte_perm(e[2], e[3], 0x0051), 0x5410);
+                    const uint32_t ta = __byte_perm(lw, __shfl_xor_sync(0xffffffffu, lw, 1), sel1);
+                    const uint32_t tb = __byte_perm(ta, __shfl_xor_sync(0xffffffffu, ta, 2), sel2);
+                    if (valid && n < nn) {
+                        oh[0] = h01;
+                        oh[P.cstride] = h23;   // (32-bit words: two planes of 16-bit values further)
+                        om[0] = tb;
+                    }
+                    oh += 2 * P.cstride;
+                    om += P.cstride;
+                }
+            } else if (valid) {
                 const int nn = min(32, K - n0);
 #pragma unroll
                 for (int n = 0; n < 32; n++) {

@@ -123,15 +123,60 @@ HDF_DEV void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {
 }
 HDF_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// One half (32 columns) of a consumer's combine step: acc[32 HALF + j] += c(r, 32 HALF + j) (da[j] + db[j]).
+// The coefficient block of the (tile, cluster) sits in its ring slot `cb` either as fp32 (two SWIZZLE_128B [32][32]
+// halves, 4 KB each) or in 24 bits (C24; CoefParams in k_coeffs.cuh): the upper 16 bits as one SWIZZLE_128B box
+// [32 rows][64 columns] of 16-bit words and, 4 KB further, the byte m as one SWIZZLE_64B box [32][64]; a value is
+// rebuilt with one PRMT as bits (hi16, m, m).  Every lane reads its own row r: the swizzles make the 16-byte
+// chunks of 8 consecutive rows fall into distinct banks.
+template <bool C24, int HALF>
+HDF_DEV void htc_fma_half(float (&acc)[kHtcN], const uint32_t (&da)[32], const uint32_t (&db)[32],
+                          const unsigned char* cb, int r) {
+    if (C24) {
+        const unsigned char* ch = cb + r * 128;
+        const unsigned char* cm = cb + 4096 + r * 64;
+        uint4 mv = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int c8l = 0; c8l < 4; c8l++) {
+            const int c8 = 4 * HALF + c8l;   // 16-byte chunk of the hi row: columns 8 c8 .. 8 c8 + 7
+            const uint4 hv = *reinterpret_cast<const uint4*>(ch + ((c8 ^ (r & 7)) << 4));
+            if ((c8l & 1) == 0) mv = *reinterpret_cast<const uint4*>(cm + (((c8 >> 1) ^ ((r >> 1) & 3)) << 4));
+            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, mw[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const int j = 8 * c8l + e;
+                const uint32_t sel = (uint32_t)(((2 * (e & 1) + 1) << 12) | ((2 * (e & 1)) << 8) | ((4 + (e & 3)) << 4) |
+                                                (4 + (e & 3)));
+                const float cv = __uint_as_float(__byte_perm(hw[e >> 1], mw[((c8l & 1) * 8 + e) >> 2], sel));
+                acc[32 * HALF + j] = fmaf(cv, __uint_as_float(da[j]) + __uint_as_float(db[j]), acc[32 * HALF + j]);
+            }
+        }
+    } else {
+        const unsigned char* cr = cb + r * 128 + HALF * 4096;
+#pragma unroll
+        for (int c4 = 0; c4 < 8; c4++) {   // 16-byte chunks swizzled by r & 7
+            const float4 cv = *reinterpret_cast<const float4*>(cr + ((c4 ^ (r & 7)) << 4));
+            const int j = 4 * c4;
+            acc[32 * HALF + j + 0] = fmaf(cv.x, __uint_as_float(da[j + 0]) + __uint_as_float(db[j + 0]), acc[32 * HALF + j + 0]);
+            acc[32 * HALF + j + 1] = fmaf(cv.y, __uint_as_float(da[j + 1]) + __uint_as_float(db[j + 1]), acc[32 * HALF + j + 1]);
+            acc[32 * HALF + j + 2] = fmaf(cv.z, __uint_as_float(da[j + 2]) + __uint_as_float(db[j + 2]), acc[32 * HALF + j + 2]);
+            acc[32 * HALF + j + 3] = fmaf(cv.w, __uint_as_float(da[j + 3]) + __uint_as_float(db[j + 3]), acc[32 * HALF + j + 3]);
+        }
+    }
+}
+
 // NS (the default): the two fp16 MMAs of a K step that share the operand z_hi run as ONE MMA of N = 128 against
 // the stacked Toeplitz operand [T_hi; T_lo] (z_hi is read from shared memory once instead of twice: the kernel is
 // bound by shared-memory bandwidth); the accumulator stage is then 128 columns (z_hi T_hi +
 // z_lo T_8 in columns 0..63, z_hi T_lo in 64..127: all 512 TMEM columns) and the consumers add the halves.
-template <bool NS>
+// C24 (with NS only): the coefficient planes in 24 bits (tm_c: the 16-bit part, tm_cm: the byte), see htc_fma_half.
+template <bool NS, bool C24>
 __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __grid_constant__ CUtensorMap tm_zh,
                                                                      const __grid_constant__ CUtensorMap tm_zl,
                                                                      const __grid_constant__ CUtensorMap tm_c,
+                                                                     const __grid_constant__ CUtensorMap tm_cm,
                                                                      const __grid_constant__ HtcParams P) {
+    static_assert(NS || !C24, "the 24-bit coefficient planes are read by the stacked-operand consumers only");
     extern __shared__ __align__(1024) unsigned char sm_raw[];
     unsigned char* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
     __shared__ uint64_t box_full[kHtcNB], box_free[kHtcNB], c_full[kHtcNC], c_free[kHtcNC], d_full[2 * kHtcS],
@@ -170,6 +215,7 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
         prefetch_tmap(&tm_zh);
         prefetch_tmap(&tm_zl);
         prefetch_tmap(&tm_c);
+        if (C24) prefetch_tmap(&tm_cm);
         for (int s = 0; s < kHtcNB; s++) {
             mbar_init(&box_full[s], 1);
             mbar_init(&box_free[s], 1);
@@ -227,33 +273,20 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
                 mbar_wait(&d_full[s], (uint32_t)(kk >> 1) & 1u);
                 tc_fence_after();
                 uint32_t d0[32], d1[32];
-                const unsigned char* cb = cring + (size_t)cs * kHtcCBytes + r * 128;
+                const unsigned char* cslot = cring + (size_t)cs * kHtcCBytes;
+                const unsigned char* cb = cslot + r * 128;
                 if (NS) {   // columns j and 64 + j of the stage: (z_hi T_hi + z_lo T_8) + z_hi T_lo
                     const uint32_t ta = tbase + lane_base + (uint32_t)s * kStageCols;
                     tmem_ld32_nw(ta, d0);
                     tmem_ld32_nw(ta + 64, d1);
                     tmem_wait_ld();
-#pragma unroll
-                    for (int c4 = 0; c4 < 8; c4++) {   // half 0: columns 0..31 (16-byte chunks swizzled by r & 7)
-                        const float4 cv = *reinterpret_cast<const float4*>(cb + ((c4 ^ (r & 7)) << 4));
-                        acc[4 * c4 + 0] = fmaf(cv.x, __uint_as_float(d0[4 * c4 + 0]) + __uint_as_float(d1[4 * c4 + 0]), acc[4 * c4 + 0]);
-                        acc[4 * c4 + 1] = fmaf(cv.y, __uint_as_float(d0[4 * c4 + 1]) + __uint_as_float(d1[4 * c4 + 1]), acc[4 * c4 + 1]);
-                        acc[4 * c4 + 2] = fmaf(cv.z, __uint_as_float(d0[4 * c4 + 2]) + __uint_as_float(d1[4 * c4 + 2]), acc[4 * c4 + 2]);
-                        acc[4 * c4 + 3] = fmaf(cv.w, __uint_as_float(d0[4 * c4 + 3]) + __uint_as_float(d1[4 * c4 + 3]), acc[4 * c4 + 3]);
-                    }
+                    htc_fma_half<C24, 0>(acc, d0, d1, cslot, r);
                     tmem_ld32_nw(ta + 32, d0);
                     tmem_ld32_nw(ta + 96, d1);
                     tmem_wait_ld();
                     tc_fence_before();
                     mbar_arrive(&d_free[s]);
-#pragma unroll
-                    for (int c4 = 0; c4 < 8; c4++) {   // half 1: columns 32..63
-                        const float4 cv = *reinterpret_cast<const float4*>(cb + 4096 + ((c4 ^ (r & 7)) << 4));
-                        acc[32 + 4 * c4 + 0] = fmaf(cv.x, __uint_as_float(d0[4 * c4 + 0]) + __uint_as_float(d1[4 * c4 + 0]), acc[32 + 4 * c4 + 0]);
-                        acc[32 + 4 * c4 + 1] = fmaf(cv.y, __uint_as_float(d0[4 * c4 + 1]) + __uint_as_float(d1[4 * c4 + 1]), acc[32 + 4 * c4 + 1]);
-                        acc[32 + 4 * c4 + 2] = fmaf(cv.z, __uint_as_float(d0[4 * c4 + 2]) + __uint_as_float(d1[4 * c4 + 2]), acc[32 + 4 * c4 + 2]);
-                        acc[32 + 4 * c4 + 3] = fmaf(cv.w, __uint_as_float(d0[4 * c4 + 3]) + __uint_as_float(d1[4 * c4 + 3]), acc[32 + 4 * c4 + 3]);
-                    }
+                    htc_fma_half<C24, 1>(acc, d0, d1, cslot, r);
                 } else {
                 tmem_ld32_nw(tbase + lane_base + (uint32_t)(s * kHtcN), d0);
                 tmem_ld32_nw(tbase + lane_base + (uint32_t)(s * kHtcN + 32), d1);
@@ -415,11 +448,16 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
                         const long long h = 2 * kk + t;
                         const int cs = (int)(h % kHtcNC);
                         if (h >= kHtcNC) mbar_wait(&c_free[cs], (uint32_t)((h / kHtcNC) - 1) & 1u);
-                        mbar_arrive_expect_tx(&c_full[cs], kHtcCBytes);
+                        mbar_arrive_expect_tx(&c_full[cs], C24 ? 4096u + 2048u : kHtcCBytes);
                         unsigned char* cd = cring + (size_t)cs * kHtcCBytes;
                         const int xt = sx * (kHtcS * kHtcN) + kHtcN * t;
-                        tma_load_3d(cd, &tm_c, &c_full[cs], xt, y0, k);
-                        tma_load_3d(cd + 4096, &tm_c, &c_full[cs], xt + 32, y0, k);
+                        if (C24) {   // [32 rows][64 columns]: 16-bit words (4 KB), bytes (2 KB)
+                            tma_load_3d(cd, &tm_c, &c_full[cs], xt, y0, k);
+                            tma_load_3d(cd + 4096, &tm_cm, &c_full[cs], xt, y0, k);
+                        } else {
+                            tma_load_3d(cd, &tm_c, &c_full[cs], xt, y0, k);
+                            tma_load_3d(cd + 4096, &tm_c, &c_full[cs], xt + 32, y0, k);
+                        }
                     }
                 }
             }

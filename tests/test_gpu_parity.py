@@ -159,6 +159,23 @@ def test_parity_tau_disabled(hdf):
     assert d.max() <= MAX_TOL and d.mean() <= MEAN_TOL
 
 
+@pytest.mark.parametrize("env", [{"HDF_HTC_NSTACK": "0"}, {"HDF_VTC_NSTACK": "1"}, {"HDF_C24": "1"},
+                                 {"HDF_C24": "1", "HDF_VTC_NSTACK": "1"}])
+@pytest.mark.parametrize("name,H,W,K", [
+    ("c1", 100, 132, 8),        # 128-column units + a ragged 4-column strip, 32-row blocks + tail
+    ("c2a", 161, 388, 16),
+    ("c2a", 33, 64, 64),        # one row block + 1 row, K = 64
+])
+def test_parity_tensor_core_variants(hdf, monkeypatch, env, name, H, W, K):
+    """The non-default forms of the tensor-core passes: the row pass with two N = 64 MMAs per K step instead
+    of the stacked operand, the column pass with the stacked operand, and the 24-bit coefficient planes
+    (k_coeffs_tc -> k_hpass_combine_tc<true, true>)."""
+    monkeypatch.setenv("HDF_HPASS_FMA", "0")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _parity_case(hdf, name, H, W, K)
+
+
 # ---- full-size config 5 on sampled pixels (the oracle computes them one by one) ----------------
 @pytest.mark.slow
 def test_parity_c5_sampled(hdf):
