@@ -151,6 +151,36 @@ HDF_DEV uint32_t split_f16x2_res(float a, float b, float& ra, float& rb) {
     rb = b - hf.y;
     return *reinterpret_cast<const uint32_t*>(&h);
 }
+// packed f32x2 forms (one FP32-pipe instruction per register pair; ffma2 / fadd2 / fsub2 are in k_vpass.cuh)
+HDF_DEV unsigned long long pack2(float lo, float hi) {
+    unsigned long long d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+    return d;
+}
+HDF_DEV void unpack2(unsigned long long v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+HDF_DEV unsigned long long fmul2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// fp16 rounding of a packed pair: the 32-bit hi word and the packed fp32 residuals (one packed subtraction)
+HDF_DEV uint32_t split_f16x2_res2(unsigned long long ab, unsigned long long& res) {
+    float a, b;
+    unpack2(ab, a, b);
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    res = fsub2(ab, pack2(hf.x, hf.y));
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+// hi and lo words of a packed pair
+HDF_DEV void split_f16x2p(unsigned long long ab, uint32_t& hi, uint32_t& lo) {
+    unsigned long long res;
+    hi = split_f16x2_res2(ab, res);
+    float ra, rb;
+    unpack2(res, ra, rb);
+    const __half2 l = __floats2half2_rn(ra, rb);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
+}
 // two fp32 -> e4m3 (saturating, round to nearest even): hi_val in the upper byte, lo_val in the lower
 HDF_DEV uint32_t cvt_e4m3x2(float hi_val, float lo_val) {
     unsigned short r;
@@ -162,6 +192,7 @@ HDF_DEV uint32_t cvt_e4m3x2(float hi_val, float lo_val) {
 // |t| <= 2^14, |lo| <= 4 sits well inside e4m3's range unscaled; its subnormal floor (2^-10 absolute) is
 // 2^-24 of the largest value.
 constexpr float kLoScale = 1.f;
+static_assert(kLoScale == 1.f, "the whole-tile store path of k_range_vpass_tc stores the residuals unscaled");
 
 // Byte offset of (row r, k) in an operand of nrow rows (multiple of 8) and Kp columns, K-major, no
 // swizzle, layout "m-groups adjacent": core matrix (r / 8, k / 8) at (k / 8) * (nrow * 16) + (r / 8) * 128.
@@ -269,6 +300,10 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
         const float lsu = (float)(14 - e2 - (P.ph ? P.wexp : 0)), sbu = ldexpf(1.f, e2);
         // per-tile bookkeeping in 32-bit incremental form: raw chunk ga = ui (TU + 1) + j (ring slot ga %
         // kVtcRaw, phase ga / kVtcRaw), the unit's first Z slot zs0 = ui (8 TU + 6) % kVtcZChunks
+        const unsigned long long c2p = pack2(c2, c2), lsup = pack2(lsu, lsu), sbup = pack2(sbu, sbu);
+        // this thread's 16-byte slot inside a Z chunk: (plane 0, col) at ((col >> 3) * 128 + (col & 7) * 16); plane q is
+        // 4 row groups (512 bytes) further
+        const uint32_t zcol = (uint32_t)((col >> 3) * 128 + (col & 7) * 16);
         const int U = 8 * TU + 6;
         int ga_slot = 0, ga_ph = 0, zs0 = 0;
         long long it = 0;
@@ -278,6 +313,7 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
             const bool xok = strip * 32 + col < P.W;
             const float m0 = __ldg(P.centres + k * 3), m1 = __ldg(P.centres + k * 3 + 1),
                         m2 = __ldg(P.centres + k * 3 + 2);
+            const unsigned long long m0p = pack2(m0, m0), m1p = pack2(m1, m1), m2p = pack2(m2, m2);
             for (int j = 0; j < TU; j++, it++) {
                 const int yt = ys + j * kVtcRows;
                 const int gb_slot = ga_slot + 1 == kVtcRaw ? 0 : ga_slot + 1;
@@ -305,37 +341,61 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
                 const float* slot_b = ring + (size_t)gb_slot * (64 * 96) + col * 3;
                 for (int cc = c0 + cg; cc < c1; cc += kVtcProd / 32) {
                     const int ch = cc - 8 * j;   // 8-row chunk within the tile
-                    float zv[4][8];
+                    unsigned long long zv[4][4];   // [plane][row pair] packed (rows 2i, 2i + 1)
                     const float* px = ((ch < 8) ? slot_a : slot_b) + (ch & 7) * (8 * 96);
                     const int y8 = yt - R + ch * 8;   // image row of the chunk's first input row
+                    if (xok && y8 >= 0 && y8 + 8 <= P.H) {   // the whole chunk inside the image: packed, no row tests
 #pragma unroll
-                    for (int r = 0; r < 8; r++) {
-                        const float p0 = px[r * 96], p1 = px[r * 96 + 1], p2 = px[r * 96 + 2];
-                        const float t0 = p0 - m0, t1 = p1 - m1, t2 = p2 - m2;
-                        const float d2 = fmaf(t2, t2, fmaf(t1, t1, t0 * t0));
-                        float bu;
-                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(bu) : "f"(fmaf(d2, c2, lsu)));
-                        // rows outside [0, H) and columns past W contribute zero (R8); rows past 64 + 2R meet zero
-                        // taps (a chunk may be shared with the next tile)
-                        bu = (xok && (unsigned)(y8 + r) < (unsigned)P.H) ? bu : 0.f;
-                        zv[0][r] = bu * p0;
-                        zv[1][r] = bu * p1;
-                        zv[2][r] = bu * p2;
-                        zv[3][r] = bu * sbu;
+                        for (int i = 0; i < 4; i++) {
+                            const unsigned long long p0 = pack2(px[(2 * i) * 96], px[(2 * i + 1) * 96]);
+                            const unsigned long long p1 = pack2(px[(2 * i) * 96 + 1], px[(2 * i + 1) * 96 + 1]);
+                            const unsigned long long p2 = pack2(px[(2 * i) * 96 + 2], px[(2 * i + 1) * 96 + 2]);
+                            const unsigned long long t0 = fsub2(p0, m0p), t1 = fsub2(p1, m1p), t2 = fsub2(p2, m2p);
+                            const unsigned long long d2 = ffma2(t2, t2, ffma2(t1, t1, fmul2(t0, t0)));
+                            float a0, a1, b0, b1;
+                            unpack2(ffma2(d2, c2p, lsup), a0, a1);
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b0) : "f"(a0));
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b1) : "f"(a1));
+                            const unsigned long long bu = pack2(b0, b1);
+                            zv[0][i] = fmul2(bu, p0);
+                            zv[1][i] = fmul2(bu, p1);
+                            zv[2][i] = fmul2(bu, p2);
+                            zv[3][i] = fmul2(bu, sbup);
+                        }
+                    } else {
+                        float zs[4][8];
+#pragma unroll
+                        for (int r = 0; r < 8; r++) {
+                            const float p0 = px[r * 96], p1 = px[r * 96 + 1], p2 = px[r * 96 + 2];
+                            const float t0 = p0 - m0, t1 = p1 - m1, t2 = p2 - m2;
+                            const float d2 = fmaf(t2, t2, fmaf(t1, t1, t0 * t0));
+                            float bu;
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(bu) : "f"(fmaf(d2, c2, lsu)));
+                            // rows outside [0, H) and columns past W contribute zero (R8); rows past 64 + 2R meet zero
+                            // taps (a chunk may be shared with the next tile)
+                            bu = (xok && (unsigned)(y8 + r) < (unsigned)P.H) ? bu : 0.f;
+                            zs[0][r] = bu * p0;
+                            zs[1][r] = bu * p1;
+                            zs[2][r] = bu * p2;
+                            zs[3][r] = bu * sbu;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; q++)
+#pragma unroll
+                            for (int i = 0; i < 4; i++) zv[q][i] = pack2(zs[q][2 * i], zs[q][2 * i + 1]);
                     }
                     int zslot = zs0 + cc;
                     while (zslot >= kVtcZChunks) zslot -= kVtcZChunks;
-                    const size_t zoff = (size_t)zslot * kVtcZChunkBytes;
+                    const uint32_t zoff = (uint32_t)zslot * (uint32_t)kVtcZChunkBytes + zcol;
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
-                        const uint32_t off = (uint32_t)(((q * 32 + col) >> 3) * 128 + (col & 7) * 16);
                         uint4 h4, l4;
-                        split_f16x2(zv[q][0], zv[q][1], h4.x, l4.x);
-                        split_f16x2(zv[q][2], zv[q][3], h4.y, l4.y);
-                        split_f16x2(zv[q][4], zv[q][5], h4.z, l4.z);
-                        split_f16x2(zv[q][6], zv[q][7], h4.w, l4.w);
-                        *reinterpret_cast<uint4*>(ZH + zoff + off) = h4;
-                        *reinterpret_cast<uint4*>(ZL + zoff + off) = l4;
+                        split_f16x2p(zv[q][0], h4.x, l4.x);
+                        split_f16x2p(zv[q][1], h4.y, l4.y);
+                        split_f16x2p(zv[q][2], h4.z, l4.z);
+                        split_f16x2p(zv[q][3], h4.w, l4.w);
+                        *reinterpret_cast<uint4*>(ZH + zoff + q * 512) = h4;
+                        *reinterpret_cast<uint4*>(ZL + zoff + q * 512) = l4;
                     }
                 }
                 // raw chunk j has no later reader in this unit (tile j + 1 reads j + 1, j + 2); the last tile
@@ -404,20 +464,40 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
                         const long long row0 = ((long long)(4 * k + q) * (P.Wp >> 5) + strip) * P.H + (yt + r0);
                         uint32_t* oh = reinterpret_cast<uint32_t*>(P.ph) + row0 * 16 + odd * 16 + (col >> 1);
                         uint32_t* ol = reinterpret_cast<uint32_t*>(P.pl) + row0 * 8 + (lane & 3) * 8 + (lane >> 2);
+                        if (nr == kVtcNRW) {   // whole tile: packed residuals, no row tests, fixed store offsets
 #pragma unroll
-                        for (int jj = 0; jj < kVtcNRW; jj += 4) {
-                            float l0, l1, l2, l3;
-                            const uint32_t h01 = split_f16x2_res(v[jj], v[jj + 1], l0, l1);
-                            const uint32_t h23 = split_f16x2_res(v[jj + 2], v[jj + 3], l2, l3);
-                            const uint32_t p01 = __shfl_xor_sync(0xffffffffu, h01, 1);
-                            const uint32_t p23 = __shfl_xor_sync(0xffffffffu, h23, 1);
-                            const uint32_t lw = cvt_e4m3x2(l1 * kLoScale, l0 * kLoScale) |
-                                                (cvt_e4m3x2(l3 * kLoScale, l2 * kLoScale) << 16);
-                            const uint32_t a = __byte_perm(lw, __shfl_xor_sync(0xffffffffu, lw, 1), sel1);
-                            const uint32_t b = __byte_perm(a, __shfl_xor_sync(0xffffffffu, a, 2), sel2);
-                            if (nr == kVtcNRW || jj + odd < nr) oh[jj * 16] = __byte_perm(h01, p01, sel);
-                            if (nr == kVtcNRW || jj + 2 + odd < nr) oh[(jj + 2) * 16] = __byte_perm(h23, p23, sel);
-                            if (nr == kVtcNRW || jj + (lane & 3) < nr) ol[jj * 8] = b;
+                            for (int jj = 0; jj < kVtcNRW; jj += 4) {
+                                unsigned long long q01, q23;
+                                const uint32_t h01 = split_f16x2_res2(pack2(v[jj], v[jj + 1]), q01);
+                                const uint32_t h23 = split_f16x2_res2(pack2(v[jj + 2], v[jj + 3]), q23);
+                                float l0, l1, l2, l3;
+                                unpack2(q01, l0, l1);
+                                unpack2(q23, l2, l3);
+                                const uint32_t p01 = __shfl_xor_sync(0xffffffffu, h01, 1);
+                                const uint32_t p23 = __shfl_xor_sync(0xffffffffu, h23, 1);
+                                const uint32_t lw = cvt_e4m3x2(l1, l0) | (cvt_e4m3x2(l3, l2) << 16);
+                                const uint32_t a = __byte_perm(lw, __shfl_xor_sync(0xffffffffu, lw, 1), sel1);
+                                const uint32_t b = __byte_perm(a, __shfl_xor_sync(0xffffffffu, a, 2), sel2);
+                                oh[jj * 16] = __byte_perm(h01, p01, sel);
+                                oh[(jj + 2) * 16] = __byte_perm(h23, p23, sel);
+                                ol[jj * 8] = b;
+                            }
+                        } else {
+#pragma unroll
+                            for (int jj = 0; jj < kVtcNRW; jj += 4) {
+                                float l0, l1, l2, l3;
+                                const uint32_t h01 = split_f16x2_res(v[jj], v[jj + 1], l0, l1);
+                                const uint32_t h23 = split_f16x2_res(v[jj + 2], v[jj + 3], l2, l3);
+                                const uint32_t p01 = __shfl_xor_sync(0xffffffffu, h01, 1);
+                                const uint32_t p23 = __shfl_xor_sync(0xffffffffu, h23, 1);
+                                const uint32_t lw = cvt_e4m3x2(l1 * kLoScale, l0 * kLoScale) |
+                                                    (cvt_e4m3x2(l3 * kLoScale, l2 * kLoScale) << 16);
+                                const uint32_t a = __byte_perm(lw, __shfl_xor_sync(0xffffffffu, lw, 1), sel1);
+                                const uint32_t b = __byte_perm(a, __shfl_xor_sync(0xffffffffu, a, 2), sel2);
+                                if (jj + odd < nr) oh[jj * 16] = __byte_perm(h01, p01, sel);
+                                if (jj + 2 + odd < nr) oh[(jj + 2) * 16] = __byte_perm(h23, p23, sel);
+                                if (jj + (lane & 3) < nr) ol[jj * 8] = b;
+                            }
                         }
                     }
                 } else if (x < P.W && yt + r0 < P.H) {
