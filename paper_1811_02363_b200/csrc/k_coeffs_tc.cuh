@@ -83,7 +83,8 @@ HDF_DEV uint32_t tc_off(int row, int k, int Kr) {
 inline __host__ __device__ size_t coeffs_tc_smem(int K, int rho) {
     const int Kr = (K + 7) & ~7, N = (K + 15) & ~15;
     // (+ the tile's guide rows [128][rho] for a runtime rho: read once per tile instead of once per centre)
-    return (size_t)(2 * N + 4 * kTcM) * Kr * 4 + (size_t)N * rho * 4 + (size_t)kTcM * rho * 4 + 64;
+    // (+ the centres once more, pair-interleaved, for the packed rho = 3 evaluations)
+    return (size_t)(2 * N + 4 * kTcM) * Kr * 4 + (size_t)2 * N * rho * 4 + (size_t)kTcM * rho * 4 + 64;
 }
 
 template <int RHO>   // RHO > 0: compile-time guide dimension, 0: runtime
@@ -100,7 +101,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
     unsigned char* Bl = Bh + (size_t)N * Kr * 4;
     unsigned char* A0 = Bl + (size_t)N * Kr * 4;   // stage s: A_hi at A0 + 2 s abytes, A_lo after it
     float* mus = reinterpret_cast<float*>(A0 + 4 * abytes);
-    float* xs = mus + (size_t)N * rho;   // runtime rho: the tile's guide rows [128][rho]
+    float* mup = mus + (size_t)N * rho;  // centre pairs [N / 2][rho][2]: (mu_{2i}[d], mu_{2i+1}[d]) adjacent (one LDS.64)
+    float* xs = mup + (size_t)N * rho;   // runtime rho: the tile's guide rows [128][rho]
     const uint32_t ncols = N <= 32 ? 64u : 128u;   // two accumulator stages of N (<= 64) columns
 
     // A^+ (hi, lo) as the B operands: row n = output coefficient n, K index l; zero-padded
@@ -111,7 +113,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
         *reinterpret_cast<uint32_t*>(Bh + tc_off(nn, l, Kr)) = h;
         *reinterpret_cast<uint32_t*>(Bl + tc_off(nn, l, Kr)) = tf32_lo(a, h);
     }
-    for (int e = tid; e < N * rho; e += kTcThreads) mus[e] = (e < K * rho) ? P.centres[e] : 0.f;
+    for (int e = tid; e < N * rho; e += kTcThreads) {
+        const float m = (e < K * rho) ? P.centres[e] : 0.f;
+        const int l = e / rho, d = e - l * rho;
+        mus[e] = m;
+        mup[((l >> 1) * rho + d) * 2 + (l & 1)] = m;
+    }
     if (tid == 0) {
         for (int s = 0; s < 2; s++) {
             mbar_init(&a_full[s], kTcProd);
@@ -143,7 +150,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
         const int la = half ? lh : 0, lb = half ? Kr : lh;
         // rho = 3: the half's 32 evaluations fully unrolled (independent; centre loads at fixed offsets)
         constexpr bool MUREG = (RHO == 3);
-        const float* mh = mus + la * RR;
         // compile-time rho: the guide values of the next tile are loaded one tile ahead
         float xn[RR];
         auto load_x = [&](long long tile) {
@@ -173,25 +179,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
             }
             mbar_wait(&a_free[s], ph ^ 1u);   // the MMAs of tile it - 2 have read A[s]
             const uint32_t aH = smem_u32(A0 + 2 * s * abytes), aL = aH + (uint32_t)abytes;
-            if (MUREG) {
+            if (MUREG) {   // packed f32x2 arithmetic on centre pairs (l, l + 1): la and lb are multiples of 4
+                const unsigned long long xp0 = pack2(x[0], x[0]), xp1 = pack2(x[1 % RR], x[1 % RR]),
+                                         xp2 = pack2(x[2 % RR], x[2 % RR]), c2p = pack2(c2, c2);
+                const float* mq = mup + la * RR;
 #pragma unroll
                 for (int j0 = 0; j0 < 32; j0 += 4) {
                     if (la + j0 < lb) {
                         uint32_t h[4], q[4];
 #pragma unroll
-                        for (int u = 0; u < 4; u++) {
+                        for (int u = 0; u < 4; u += 2) {
                             const int j = j0 + u;
-                            float d2 = 0.f;
-#pragma unroll
-                            for (int d = 0; d < RR; d++) {
-                                const float t = x[d] - mh[j * RR + d];
-                                d2 = fmaf(t, t, d2);
-                            }
-                            float b;
-                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(d2 * c2));
-                            b = (valid && la + j < K) ? b : 0.f;
-                            h[u] = tf32_hi(b);
-                            q[u] = tf32_lo(b, h[u]);
+                            const float* mp = mq + j * RR;   // pair (la + j) / 2: [d][2]
+                            const unsigned long long t0 = fsub2(xp0, *reinterpret_cast<const unsigned long long*>(mp));
+                            const unsigned long long t1 = fsub2(xp1, *reinterpret_cast<const unsigned long long*>(mp + 2));
+                            const unsigned long long t2 = fsub2(xp2, *reinterpret_cast<const unsigned long long*>(mp + 4));
+                            const unsigned long long d2 = ffma2(t2, t2, ffma2(t1, t1, fmul2(t0, t0)));
+                            float a0, a1, b0, b1;
+                            unpack2(fmul2(d2, c2p), a0, a1);
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b0) : "f"(a0));
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(b1) : "f"(a1));
+                            b0 = (valid && la + j < K) ? b0 : 0.f;
+                            b1 = (valid && la + j + 1 < K) ? b1 : 0.f;
+                            h[u] = tf32_hi(b0);
+                            h[u + 1] = tf32_hi(b1);
+                            float l0, l1;
+                            unpack2(fsub2(pack2(b0, b1), pack2(__uint_as_float(h[u]), __uint_as_float(h[u + 1]))), l0, l1);
+                            q[u] = __float_as_uint(l0);
+                            q[u + 1] = __float_as_uint(l1);
                         }
                         const uint32_t off = tc_off(m, la + j0, Kr);
                         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aH + off), "r"(h[0]), "r"(h[1]),

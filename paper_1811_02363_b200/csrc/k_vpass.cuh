@@ -45,22 +45,7 @@ struct VParams {
     float tws[2 * HDF_MAX_RADIUS + 1];           // w_{-R..R} (scalar path)
 };
 
-// packed f32x2 arithmetic (sm_100a)
-HDF_DEV unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
-    unsigned long long d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-HDF_DEV unsigned long long fadd2(unsigned long long a, unsigned long long b) {
-    unsigned long long d;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-HDF_DEV unsigned long long fsub2(unsigned long long a, unsigned long long b) {
-    unsigned long long d;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
+// (packed f32x2 arithmetic: ffma2 / fadd2 / fsub2 / fmul2 / pack2 / unpack2 in hdf_common.cuh)
 HDF_DEV unsigned long long lds_u64(const void* p) {
     unsigned long long v;
     asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)));

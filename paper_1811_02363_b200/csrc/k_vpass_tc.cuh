@@ -151,18 +151,6 @@ HDF_DEV uint32_t split_f16x2_res(float a, float b, float& ra, float& rb) {
     rb = b - hf.y;
     return *reinterpret_cast<const uint32_t*>(&h);
 }
-// packed f32x2 forms (one FP32-pipe instruction per register pair; ffma2 / fadd2 / fsub2 are in k_vpass.cuh)
-HDF_DEV unsigned long long pack2(float lo, float hi) {
-    unsigned long long d;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
-    return d;
-}
-HDF_DEV void unpack2(unsigned long long v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
-HDF_DEV unsigned long long fmul2(unsigned long long a, unsigned long long b) {
-    unsigned long long d;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
 // fp16 rounding of a packed pair: the 32-bit hi word and the packed fp32 residuals (one packed subtraction)
 HDF_DEV uint32_t split_f16x2_res2(unsigned long long ab, unsigned long long& res) {
     float a, b;
