@@ -296,8 +296,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
             const bool valid = i < npix;
             long long y = 0, xx = 0;
             if (valid) {
-                y = i / P.W;
-                xx = i - y * P.W;
+                if (npix <= 0x7fffffffLL) {   // 32-bit division (the 64-bit one was 5% of this kernel's stall samples)
+                    const unsigned yi = (unsigned)i / (unsigned)P.W;
+                    y = yi;
+                    xx = (unsigned)i - yi * (unsigned)P.W;
+                } else {
+                    y = i / P.W;
+                    xx = i - y * P.W;
+                }
             }
             float* o = P.cpl + (long long)n0 * P.cstride + y * P.Wp + xx;
             mbar_wait(&d_full[s], ph);
@@ -356,10 +362,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_coeffs_tc(const __grid_consta
                 }
             } else if (valid) {
                 const int nn = min(32, K - n0);
+                if (nn == 32) {   // all 32 planes: no per-plane test
 #pragma unroll
-                for (int n = 0; n < 32; n++) {
-                    if (n < nn) o[0] = v[n];
-                    o += P.cstride;
+                    for (int n = 0; n < 32; n++) {
+                        o[0] = v[n];
+                        o += P.cstride;
+                    }
+                } else {
+#pragma unroll
+                    for (int n = 0; n < 32; n++) {
+                        if (n < nn) o[0] = v[n];
+                        o += P.cstride;
+                    }
                 }
             }
         }
