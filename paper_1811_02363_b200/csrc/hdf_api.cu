@@ -946,6 +946,8 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             tp.K = K;
             tp.R = F.R;
             tp.nstrip = (W + 31) / 32;
+            tp.csleep = 0;
+            if (const char* e = getenv("HDF_VTC_CSLEEP")) tp.csleep = std::max(0, atoi(e));
             tp.neg_inv2sr2 = neg_inv2sr2;
             for (int t = 0; t < hdf::kMaxTaps; t++) tp.taps[t] = 0.f;
             for (int t = 0; t <= 2 * F.R; t++) tp.taps[t] = taps[F.Rp - F.R + t];
@@ -1189,6 +1191,8 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         hq.R = F.R;
         hq.nstrip = (W + hdf::kHtcS * hdf::kHtcN - 1) / (hdf::kHtcS * hdf::kHtcN);
         hq.wexp = wexp;
+        hq.csleep = 0;
+        if (const char* e = getenv("HDF_HTC_CSLEEP")) hq.csleep = std::max(0, atoi(e));
         hq.tau_floor = hp.tau_floor;
         for (int t = 0; t < hdf::kMaxTaps; t++) hq.taps[t] = 0.f;
         for (int t = 0; t <= 2 * F.R; t++) hq.taps[t] = taps[F.Rp - F.R + t];

@@ -53,6 +53,14 @@ HDF_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// The same with a run-time back-off (ns; 0 = plain spinning): for the roles that are not on the critical path, whose
+// spinning would take issue slots from the ones that are.
+HDF_DEV void mbar_wait_backoff(uint64_t* bar, uint32_t parity, int ns) {
+    while (!mbar_try_wait(bar, parity)) {
+        if (ns > 0) __nanosleep((unsigned)ns);
+    }
+}
+
 // 3-D tiled TMA load global -> shared, completion signalled on `bar` (complete_tx::bytes).
 HDF_DEV void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
     asm volatile(

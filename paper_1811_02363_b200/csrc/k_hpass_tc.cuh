@@ -67,6 +67,7 @@ struct HtcParams {
     int H, W, K, R;
     int nstrip;            // 128-column output strips
     int yb0, yb1;          // 32-row blocks [yb0, yb1) of this launch (the host path launches row chunks)
+    int csleep;            // back-off (ns) of the consumers' mbarrier waits (HDF_HTC_CSLEEP)
     int wexp;              // the planes are stored as t 2^(14 - e2 - wexp) (u) and t 2^(14 - wexp) (b)
     float tau_floor;       // tau omega(0) phi(0); <= 0 disables flagging
     float taps[kMaxTaps];  // w_{-R..R} at [t + R]
@@ -269,8 +270,8 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
                 const long long h = 2 * kk + t;
                 const int cs = (int)(h % kHtcNC);
                 const int s = 2 * t + (int)(kk & 1);
-                mbar_wait(&c_full[cs], (uint32_t)(h / kHtcNC) & 1u);
-                mbar_wait(&d_full[s], (uint32_t)(kk >> 1) & 1u);
+                mbar_wait_backoff(&c_full[cs], (uint32_t)(h / kHtcNC) & 1u, P.csleep);
+                mbar_wait_backoff(&d_full[s], (uint32_t)(kk >> 1) & 1u, P.csleep);
                 tc_fence_after();
                 uint32_t d0[32], d1[32];
                 const unsigned char* cslot = cring + (size_t)cs * kHtcCBytes;

@@ -83,6 +83,7 @@ struct VtcParams {
     int H, W, Wp, K, R;
     int nstrip, nseg, seglen;   // 32-column strips, row segments per column and their length (multiple of 64)
     int y0;                     // first output row of this launch (row bands of the pipelined filter)
+    int csleep;                 // back-off (ns) of the consumers' and the TMA warp's mbarrier waits (HDF_VTC_CSLEEP)
     float neg_inv2sr2;     // -1 / (2 sigma_r^2)
     float taps[kMaxTaps];  // w_{-R..R}
 };
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
             for (int j = 0; j < TU; j++, it++) {
                 const int yt = ys + j * kVtcRows;
                 const int s = (int)(it % kVtcStages);
-                mbar_wait(&d_full[s], (uint32_t)(it / kVtcStages) & 1u);
+                mbar_wait_backoff(&d_full[s], (uint32_t)(it / kVtcStages) & 1u, P.csleep);
                 tc_fence_after();
                 float v[kVtcNRW];
 #pragma unroll
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(vtc_threads(kVtcCons), 1) k_range_vpass_tc(con
             int strip, k, ys;
             unit_of(ui, strip, k, ys);
             const int sl = (int)(g % kVtcRaw);
-            if (g >= kVtcRaw) mbar_wait(&c_free[sl], (uint32_t)((g / kVtcRaw) - 1) & 1u);
+            if (g >= kVtcRaw) mbar_wait_backoff(&c_free[sl], (uint32_t)((g / kVtcRaw) - 1) & 1u, P.csleep);
             mbar_arrive_expect_tx(&c_full[sl], kSlotBytes);
             tma_load_3d(ring + (size_t)sl * (64 * 96), &tm_p, &c_full[sl], strip * 96, ys - R + 64 * c, 0);
         }
