@@ -531,6 +531,8 @@ struct FilterWS {
     void* cluster_ws;
 };
 
+constexpr int kMaxInBands = 16;
+
 FilterWS carve_filter(Carver& cv, int H, int W, int n, int rho, int K, int Wp, bool with_cluster) {
     FilterWS w;
     const int NP = n + 1;
@@ -539,7 +541,7 @@ FilterWS carve_filter(Carver& cv, int H, int W, int n, int rho, int K, int Wp, b
     w.Ap32 = cv.take<float>((size_t)K * K);
     w.Ap64 = cv.take<double>((size_t)K * K);
     w.Vscratch = cv.take<double>((size_t)K * K);
-    w.status = cv.take<int>(4);
+    w.status = cv.take<int>(4 + kMaxInBands);   // [A^+ status, flag count, flag start, -, max |f| per input band]
     w.flag_count = w.status + 1;
     w.flag_list = cv.take<int>((size_t)H * W);
     w.labels = cv.take<int>((size_t)H * W);
@@ -788,10 +790,14 @@ int validate_filter(int n, int rho, int H, int W, int kind, float sigma_s, int r
 // nchunks / after_chunk (the host path): the row pass runs in nchunks row chunks and after_chunk(y0, y1)
 // is called once the rows [y0, y1) of g are final (enqueued on st), e.g. to start their copy-out.
 using ChunkFn = std::function<int(int, int, cudaStream_t)>;
+// before_rows(y_end, s): make stream s wait until the input rows [0, y_end) are on the device (hdf_filter_host copies
+// the input in row chunks; the tensor-core column pass then runs in row bands, each as soon as its rows arrived)
+using RowsFn = std::function<int(int, cudaStream_t)>;
 int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int kind, float sigma_s, int radius,
                float sigma_r, int K, const float* centres, float tau, float* g, int32_t* n_flagged_host, void* ws,
                size_t ws_bytes, cudaStream_t st, bool hard = false, const int32_t* hard_labels = nullptr,
-               int nchunks = 1, const ChunkFn& after_chunk = ChunkFn()) {
+               int nchunks = 1, const ChunkFn& after_chunk = ChunkFn(), const RowsFn& before_rows = RowsFn(),
+               int in_bands = 1) {
     FilterPlan F;
     size_t vsmem = 0;
     int rc = validate_scalars(n, rho, H, W, kind, sigma_r, K, tau, hard);
@@ -814,6 +820,10 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
     ClusterReadback crb;
     const bool cluster_here = !centres;
     if (!centres) {
+        if (before_rows) {
+            rc = before_rows(H, st);
+            if (rc) return rc;
+        }
         int32_t* lab = hard ? w.labels : nullptr;
         rc = launch_cluster(p, H, W, rho, K, w.centres, lab, nullptr, w.cluster_ws, st,
                             n_flagged_host ? &crb : nullptr);
@@ -865,7 +875,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         for (int t = 0; t <= 2 * F.Rp; t++) ws += (double)taps[t];
         while (std::ldexp(1.0, wexp) < ws) wexp++;
     }
-    int* amax = w.status + 3;
+    int* amax = w.status + 4;   // [kMaxInBands]: max |f| over the input rows of each column-pass band
     // The pipelined filter (tensor-core path): the image is cut into nband row bands (multiples of 64
     // rows).  The column pass of band b + 1 (st, gv SMs: it only writes its planes) runs while the row
     // pass + combine of band b (hs, gh SMs: it only reads them) runs, so the HBM write and read streams
@@ -881,6 +891,17 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         if (want > 1) nband = std::min(std::max(want, nchunks), nt64);
     }
     const bool pipe = nband > 1;
+    // input bands (hdf_filter_host): uniform bands of ib_rows rows (a multiple of 64) for the tensor-core passes
+    int nib = 1, ib_rows = std::max(H, 1);
+    if (before_rows && use_htc && !pipe && in_bands > 1) {
+        const int want = std::min(std::min(in_bands, kMaxInBands), nt64);
+        ib_rows = hdf::kVtcRows * ((nt64 + want - 1) / want);
+        nib = (H + ib_rows - 1) / ib_rows;
+        if (nib <= 1) {
+            nib = 1;
+            ib_rows = std::max(H, 1);
+        }
+    }
     PipeStream* pst = nullptr;
     if (pipe) {
         pst = pipe_stream(nband + 2);
@@ -926,11 +947,22 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         hdf::VLaunch vl = F.vl;
         vl.smem = vsmem;
         std::unique_ptr<ProfScope> prof(use_tc ? nullptr : new ProfScope(HDF_STAGE_VPASS, st));
+        if (!use_tc && before_rows) {
+            rc = before_rows(H, st);
+            if (rc) return rc;
+        }
         if (use_tc) {
-            HDF_CUDA(cudaMemsetAsync(amax, 0, sizeof(int), st));
-            const long long nf = (long long)H * W * n;
-            hdf::k_absmax<<<(unsigned)std::min<long long>((nf + 255) / 256, (long long)nsm * 8), 256, 0, st>>>(f, nf, amax);
-            HDF_CUDA(cudaGetLastError());
+            HDF_CUDA(cudaMemsetAsync(amax, 0, sizeof(int) * kMaxInBands, st));
+            if (nib == 1) {   // one band: the scale from max |f| over the whole image
+                if (before_rows) {
+                    rc = before_rows(H, st);
+                    if (rc) return rc;
+                }
+                const long long nf = (long long)H * W * n;
+                hdf::k_absmax<<<(unsigned)std::min<long long>((nf + 255) / 256, (long long)nsm * 8), 256, 0, st>>>(f, nf,
+                                                                                                                amax);
+                HDF_CUDA(cudaGetLastError());
+            }
             hdf::VtcParams tp;
             tp.centres = centres;
             tp.planes = w.planes;
@@ -981,7 +1013,23 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
                 HDF_CUDA(cudaGetLastError());
                 return HDF_OK;
             };
-            if (!pipe) {
+            if (!pipe && nib > 1) {
+                // the input arrives in row chunks: band b (rows [b ib_rows, (b + 1) ib_rows)) starts when its input rows
+                // [y0 - R, y1 + R) are on the device, with its own power-of-two scale from max |f| over those rows
+                for (int b = 0; b < nib; b++) {
+                    const int y0 = b * ib_rows, y1 = std::min(H, y0 + ib_rows);
+                    const int i0 = std::max(0, y0 - F.R), i1 = std::min(H, y1 + F.R);
+                    rc = before_rows(i1, st);
+                    if (rc) return rc;
+                    const long long nf = (long long)(i1 - i0) * W * n;
+                    hdf::k_absmax<<<(unsigned)std::min<long long>((nf + 255) / 256, (long long)nsm * 8), 256, 0, st>>>(
+                        f + (size_t)i0 * W * n, nf, amax + b);
+                    HDF_CUDA(cudaGetLastError());
+                    tp.absmax = amax + b;
+                    rc = launch_vtc(y0, y1, std::max(1, nsm - 1));
+                    if (rc) return rc;
+                }
+            } else if (!pipe) {
                 rc = launch_vtc(0, H, std::max(1, nsm - 1));
                 if (rc) return rc;
             } else {
@@ -1185,6 +1233,7 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
         hq.flag_count = w.flag_count;
         hq.flag_list = w.flag_list;
         hq.absmax = amax;
+        hq.band_rows = ib_rows;
         hq.H = H;
         hq.W = W;
         hq.K = K;
@@ -1627,16 +1676,29 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
         // stride sample straight from the host guide (one strided 2-D copy) and clusters it, so the
         // clustering is hidden under the bulk copy; the filter waits for both.  Exact mode: the copy, then
         // the clustering of every pixel, in order on the caller's stream.
-        cudaEvent_t ev_fork = nullptr, ev_in = nullptr;
+        // The bulk copy goes in kInChunks row chunks, each followed by an event: the tensor-core column pass runs in
+        // row bands, each as soon as its rows (+ R halo rows) are on the device (run_filter, before_rows), so most of
+        // the input copy is hidden under the column pass instead of preceding it.
+        constexpr int kInChunks = 8;
+        const bool in_chunked = sampled && (long long)H * W >= (1LL << 20);
+        const int nin = in_chunked ? std::min(kInChunks, H) : 1;
+        cudaEvent_t ev_fork = nullptr, ev_in = nullptr, ev_rows[kInChunks] = {};
         auto destroy_io = [&]() {
             if (ev_fork) cudaEventDestroy(ev_fork);
             if (ev_in) cudaEventDestroy(ev_in);
+            for (int c = 0; c < kInChunks; c++)
+                if (ev_rows[c]) cudaEventDestroy(ev_rows[c]);
             ev_fork = ev_in = nullptr;
+            for (int c = 0; c < kInChunks; c++) ev_rows[c] = nullptr;
         };
+        auto in_row = [&](int c) { return (int)((long long)H * c / nin); };   // first row of input chunk c
         cudaStream_t in_st = st;
         if (sampled) {
-            if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-                cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) != cudaSuccess) {
+            bool ok = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+                      cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) == cudaSuccess;
+            for (int c = 0; ok && in_chunked && c < nin; c++)
+                ok = cudaEventCreateWithFlags(&ev_rows[c], cudaEventDisableTiming) == cudaSuccess;
+            if (!ok) {
                 destroy_io();
                 return bail(fail(HDF_ERR_CUDA, "event creation failed"));
             }
@@ -1646,19 +1708,23 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
         }
         {
             ProfScope prof(HDF_STAGE_H2D, in_st);
-            if (cudaMemcpyAsync(fd, f_host, sizeof(float) * (size_t)H * W * n, cudaMemcpyHostToDevice, in_st) !=
-                cudaSuccess) {
-                destroy_io();
-                return bail(fail(HDF_ERR_CUDA, "input copy: %s", cudaGetErrorString(cudaGetLastError())));
-            }
-            if (!f_is_p) {
-                if (cudaMemcpyAsync(pd, p_host, sizeof(float) * (size_t)H * W * rho, cudaMemcpyHostToDevice, in_st) !=
-                    cudaSuccess) {
+            for (int c = 0; c < nin; c++) {
+                const size_t r0 = (size_t)in_row(c), r1 = (size_t)in_row(c + 1);
+                if (cudaMemcpyAsync(fd + r0 * W * n, f_host + r0 * W * n, sizeof(float) * (r1 - r0) * W * n,
+                                    cudaMemcpyHostToDevice, in_st) != cudaSuccess) {
                     destroy_io();
-                    return bail(fail(HDF_ERR_CUDA, "guide copy: %s", cudaGetErrorString(cudaGetLastError())));
+                    return bail(fail(HDF_ERR_CUDA, "input copy: %s", cudaGetErrorString(cudaGetLastError())));
                 }
-                pdev = pd;
+                if (!f_is_p) {
+                    if (cudaMemcpyAsync(pd + r0 * W * rho, p_host + r0 * W * rho, sizeof(float) * (r1 - r0) * W * rho,
+                                        cudaMemcpyHostToDevice, in_st) != cudaSuccess) {
+                        destroy_io();
+                        return bail(fail(HDF_ERR_CUDA, "guide copy: %s", cudaGetErrorString(cudaGetLastError())));
+                    }
+                }
+                if (in_chunked) cudaEventRecord(ev_rows[c], in_st);
             }
+            if (!f_is_p) pdev = pd;
         }
         if (sampled) cudaEventRecord(ev_in, cs);
         // cluster (in the filter workspace's cluster region; status read back at the end) then filter
@@ -1671,17 +1737,49 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
             const long long N = (long long)H * W, M = (N + cluster_stride - 1) / cluster_stride;
             {
                 ProfScope prof(HDF_STAGE_H2D, st);
-                if (cudaMemcpy2DAsync(smp, sizeof(float) * (size_t)rho, p_host, sizeof(float) * (size_t)rho * cluster_stride,
-                                      sizeof(float) * (size_t)rho, (size_t)M, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+                // Pinned (or registered) host memory is addressable from the device: k_sample_guide then gathers the
+                // sample straight out of the caller's buffer over PCIe (M short reads in flight at once) instead of a
+                // strided 2-D DMA copy of M rho-float rows (~4 ms for 262k rows at config 5).  HDF_HOST_SAMPLE_DMA=1 or
+                // pageable memory keeps the 2-D copy.
+                const float* p_dev_view = nullptr;
+                if (!getenv_on("HDF_HOST_SAMPLE_DMA")) {
+                    cudaPointerAttributes pa;
+                    if (cudaPointerGetAttributes(&pa, p_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                        pa.devicePointer)
+                        p_dev_view = static_cast<const float*>(pa.devicePointer);
+                    else
+                        cudaGetLastError();   // (pageable memory: not an error here)
+                }
+                if (p_dev_view) {
+                    const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((M * rho + 255) / 256, 1184));
+                    hdf::k_sample_guide<<<nb, 256, 0, st>>>(p_dev_view, rho, 0, cluster_stride, smp, M);
+                    if (cudaGetLastError() != cudaSuccess) {
+                        destroy_io();
+                        return bail(fail(HDF_ERR_CUDA, "sample gather launch failed"));
+                    }
+                } else if (cudaMemcpy2DAsync(smp, sizeof(float) * (size_t)rho, p_host,
+                                             sizeof(float) * (size_t)rho * cluster_stride, sizeof(float) * (size_t)rho,
+                                             (size_t)M, cudaMemcpyHostToDevice, st) != cudaSuccess) {
                     destroy_io();
                     return bail(fail(HDF_ERR_CUDA, "sample copy: %s", cudaGetErrorString(cudaGetLastError())));
                 }
             }
             rc = launch_cluster(smp, 1, (int)M, rho, K, cd, nullptr, nullptr, w.cluster_ws, st, &crb);
-            if (!rc) cudaStreamWaitEvent(st, ev_in, 0);   // the filter needs the whole input
+            if (!rc && !in_chunked) cudaStreamWaitEvent(st, ev_in, 0);   // the filter needs the whole input
         }
-        destroy_io();   // (destroying a recorded event is safe: the waits were already enqueued)
-        if (rc) return bail(rc);
+        if (rc) {
+            destroy_io();
+            return bail(rc);
+        }
+        // rows [0, y_end) are on the device once the chunk holding row y_end - 1 has been copied
+        RowsFn before_rows;
+        if (in_chunked)
+            before_rows = [&](int y_end, cudaStream_t s) -> int {
+                int c = 0;
+                while (c + 1 < nin && in_row(c + 1) < y_end) c++;
+                HDF_CUDA(cudaStreamWaitEvent(s, ev_rows[c], 0));
+                return HDF_OK;
+            };
         // the output rows are copied out chunk by chunk on the copy stream while the row pass continues
         constexpr int kChunks = 8;
         cudaEvent_t evs[kChunks];
@@ -1705,7 +1803,8 @@ int hdf_filter_host(const float* f_host, int n, const float* p_host, int rho, in
             return HDF_OK;
         };
         rc = run_filter(fd, n, pdev, rho, H, W, kind, sigma_s, radius, sigma_r, K, cd, tau, gd, nullptr, fws, fbytes,
-                        st, false, nullptr, chunked ? kChunks : 1, after);
+                        st, false, nullptr, chunked ? kChunks : 1, after, before_rows, in_chunked ? 4 : 1);
+        destroy_io();   // (destroying a recorded event is safe: the waits were already enqueued)
         if (rc) {
             cudaStreamSynchronize(cs);
             release();

@@ -63,7 +63,8 @@ struct HtcParams {
     float* g;              // [H][W][3]
     int* flag_count;
     int* flag_list;
-    const int* absmax;     // max |f| as float bits (k_absmax): the u planes' scale
+    const int* absmax;     // max |f| as float bits (k_absmax): the u planes' scale, one entry per band of band_rows rows
+    int band_rows;         // rows per band of the column pass (multiple of 64; >= H: one band)
     int H, W, K, R;
     int nstrip;            // 128-column output strips
     int yb0, yb1;          // 32-row blocks [yb0, yb1) of this launch (the host path launches row chunks)
@@ -256,12 +257,15 @@ __global__ void __launch_bounds__(kHtcThreads, 1) k_hpass_combine_tc(const __gri
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         float* den_s = epi + (size_t)t * (kHtcRows * kHtcEpiCols * 4);   // [32][16]
         float* g_s = den_s + kHtcRows * kHtcEpiCols;                     // [32][16][3]
-        int e2;
-        frexpf(fmaxf(__int_as_float(*P.absmax), 1e-30f), &e2);
-        const float inv_su = ldexpf(1.f, e2 + P.wexp - 14), inv_sb = ldexpf(1.f, P.wexp - 14);
+        const float inv_sb = ldexpf(1.f, P.wexp - 14);
         for (long long ui = 0; ui < nui; ui++) {
             const long long u = blockIdx.x + ui * (long long)gridDim.x;
             const int ry = P.yb0 + (int)(u / P.nstrip), sx = (int)(u % P.nstrip);
+            // the u planes' scale of this row block's band (the column pass ran in bands when the input arrived in
+            // row chunks: hdf_filter_host)
+            int e2;
+            frexpf(fmaxf(__int_as_float(P.absmax[(ry * kHtcRows) / P.band_rows]), 1e-30f), &e2);
+            const float inv_su = ldexpf(1.f, e2 + P.wexp - 14);
             float acc[kHtcN];
 #pragma unroll
             for (int j = 0; j < kHtcN; j++) acc[j] = 0.f;
