@@ -234,7 +234,10 @@ int hdf_filter_hard(const float *f, int n, const float *p, int rho, int H, int W
  * hdf_filter_host -- the whole hot path end to end from HOST buffers: copies f and p to the device
  * workspace, clusters, filters, and copies g back, all on `stream`, then synchronises it once.
  *   f_host [H][W][n], p_host [H][W][rho] (may be the same pointer), g_host [H][W][n]: host float32
- *   (pinned memory gives full-rate copies; pageable memory works but is slower).
+ *   (pinned memory gives full-rate copies; pageable memory works but is slower).  With cluster_stride > 1 on
+ *   images of 2^20 pixels or more the input is copied in row chunks and the tensor-core column pass starts on
+ *   the rows that have arrived (same result: the planes' power-of-two scale is then taken per row band), and the
+ *   stride sample is gathered straight from p_host by a kernel when that memory is pinned (device-addressable).
  *   cluster_stride  1: the exact clustering of every pixel (hdf_cluster); s > 1: the sampled mode
  *            (hdf_cluster_sampled with stride s)
  *   centres_host [K][rho] out, may be NULL.  n_flagged_host, info_host: out, may be NULL.
