@@ -991,9 +991,10 @@ int run_filter(const float* f, int n, const float* p, int rho, int H, int W, int
             // consumer warps: 8 (32 rows each; the fp16 + e4m3 stores are the consumers' work), HDF_VTC_CONS=4 keeps 4
             int cons = 8;
             if (const char* e = getenv("HDF_VTC_CONS")) cons = atoi(e) == 4 ? 4 : 8;
-            // the stacked Toeplitz operand (k_vpass_tc.cuh, NS) only when HDF_VTC_NSTACK=1 (measured: see DESIGN.md)
-            bool vns = false;
-            if (const char* e = getenv("HDF_VTC_NSTACK")) vns = atoi(e) != 0;
+            // the stacked Toeplitz operand (k_vpass_tc.cuh, NS): a consistent 1-2% at config 5;
+            // HDF_VTC_NSTACK=0 keeps the three-MMA form
+            bool vns = true;
+            if (const char* e = getenv("HDF_VTC_NSTACK")) vns = !(*e) || atoi(e) != 0;
             void (*kvtc)(const CUtensorMap, const hdf::VtcParams) =
                 cons == 4 ? hdf::k_range_vpass_tc<4, false>
                           : (vns ? hdf::k_range_vpass_tc<8, true> : hdf::k_range_vpass_tc<8, false>);

@@ -159,8 +159,8 @@ def test_parity_tau_disabled(hdf):
     assert d.max() <= MAX_TOL and d.mean() <= MEAN_TOL
 
 
-@pytest.mark.parametrize("env", [{"HDF_HTC_NSTACK": "0"}, {"HDF_VTC_NSTACK": "1"}, {"HDF_C24": "1"},
-                                 {"HDF_C24": "1", "HDF_VTC_NSTACK": "1"}])
+@pytest.mark.parametrize("env", [{"HDF_HTC_NSTACK": "0"}, {"HDF_VTC_NSTACK": "0"}, {"HDF_C24": "1"},
+                                 {"HDF_C24": "1", "HDF_VTC_NSTACK": "0"}])
 @pytest.mark.parametrize("name,H,W,K", [
     ("c1", 100, 132, 8),        # 128-column units + a ragged 4-column strip, 32-row blocks + tail
     ("c2a", 161, 388, 16),
@@ -168,7 +168,8 @@ def test_parity_tau_disabled(hdf):
 ])
 def test_parity_tensor_core_variants(hdf, monkeypatch, env, name, H, W, K):
     """The non-default forms of the tensor-core passes: the row pass with two N = 64 MMAs per K step instead
-    of the stacked operand, the column pass with the stacked operand, and the 24-bit coefficient planes
+    of the stacked operand, the column pass with three MMAs per K step instead of the stacked operand, and the
+    24-bit coefficient planes
     (k_coeffs_tc -> k_hpass_combine_tc<true, true>)."""
     monkeypatch.setenv("HDF_HPASS_FMA", "0")
     for k, v in env.items():
