@@ -308,8 +308,8 @@ def run_ours(args, rank: int, world: int, dist):
         flush.fill_(i & 0xFF)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        hdf.filter_host(fh, ph, kind=kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
-                        K=K, out=gh, ws=ws2, cluster_stride=args.cluster_stride)
+        host_res = hdf.filter_host(fh, ph, kind=kind, sigma_s=cfg.sigma_s, radius=cfg.radius, sigma_r=cfg.sigma_r,
+                                   K=K, out=gh, ws=ws2, cluster_stride=args.cluster_stride)
         b.record(stream)
         b.synchronize()
         e2e_ms.append(a.elapsed_time(b))
@@ -484,6 +484,8 @@ def run_ours(args, rank: int, world: int, dist):
         "filter": filt, "roofline": roof, "filter_roofline": filter_roof, "gpu_launches": launches, "clocks": clk,
         "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         **({"exact_cluster": exact} if exact else {}),
+        # pixels whose normaliser fell under tau omega(0) phi(0) and took the direct window sum (R9), last e2e step
+        "n_flagged": int(host_res[2]),
     }
 
 
