@@ -19,8 +19,10 @@
 // A CTA is persistent over units (32-row block, 128-column strip of output).  For each cluster k (in
 // order) the TMA warp loads the 6 input strips x0 - 32 .. x0 + 159 (tile t reads strips 2t .. 2t + 3, so
 // the middle two are shared) and the two tiles' coefficient blocks c_k [32 rows][64 columns] fp32; the MMA
-// warp issues each tile's 3 x 8 MMAs into a TMEM stage; consumer warpgroup t (TMEM lane quarter = plane
-// q, lane = row) reads tile t's 64 filtered values per (plane, row) and accumulates
+// warp issues each tile's MMAs into a TMEM stage (per K step of 16 columns z_hi against the stacked operand
+// [T_hi; T_lo], N = 128, and per strip one kind::f8f6f4 MMA z_lo T_e4m3, N = 64; NS = false: two N = 64 fp16
+// MMAs per K step); consumer warpgroup t (TMEM lane quarter = plane q, lane = row) reads tile t's 64 filtered
+// values per (plane, row) (the sum of the stage's two halves) and accumulates
 //   num_q(y, x) += c_k(y, x) v_{k,q}(y, x)    (q < 3),     den(y, x) += c_k(y, x) r_k(y, x)    (q = 3)
 // in registers over all k.  The epilogue exchanges den through shared memory, writes g = num / den
 // (coalesced, [H][W][3]) and appends the pixels with den < tau omega(0) phi(0) to the R9 list.

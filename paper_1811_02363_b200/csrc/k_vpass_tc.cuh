@@ -16,21 +16,22 @@
 //
 // One CTA per SM (persistent over (32-column strip, cluster) columns x row segments, in tiles of 64
 // output rows; every unit has the same number of tiles), warp-specialised:
-//   * the MMA warp's lane 0 also streams the raw guide rows of the strip, [64 rows x 32 pixels x 3] per
-//     TMA box (rows outside the image zero-filled), into a ring of 3 slots: a tile reads 2 consecutive
-//     slots (Kp <= 128 rows), the next slot loads while it computes, and each slot is released by the
-//     last tile that reads it;
-//   * producers (8 warps): z for the Kp input rows of the strip's 32 columns and the cluster's 4 planes
-//     (b_k = exp2(-|p - mu_k|^2 log2(e) / 2 sigma_r^2), u_k = b_k f, f = p) from the raw stage, split,
-//     stored into the Z operand in the canonical K-major no-swizzle layout (8 x 16-byte core matrices;
-//     one 16-byte store = 8 consecutive rows of one (plane, column)); arrive on "Z full";
-//   * MMA warp: waits "Z full" and "D free", issues 3 Kp/16 MMAs (M = 128, N = 64, K = 16) and commits
-//     them to "Z free" and "D full" (Z double-buffered in shared memory, D in TMEM);
-//   * consumers (4 warps, TMEM lane quarter = plane; HDF_VTC_CONS=8 splits the rows over 8): load the 64
-//     output rows of their (plane, column), release the stage and store them: fp32 planes (scaled back,
-//     coalesced over the 32 columns), or -- for the tensor-core row pass -- fp16 hi/lo parts in the
-//     strip-major layout [plane][strip][y][hi 32 | lo 32], two rows' 64-byte halves per warp store after one
-//     lane-pair exchange (k_hpass_tc.cuh).
+//   * a TMA warp streams the raw guide rows of the strip, [64 rows x 32 pixels x 3] per TMA box (rows outside the
+//     image zero-filled), into a ring of kVtcRaw slots: a tile reads 2 consecutive slots (Kp <= 128 rows), the next
+//     ones load while it computes, and each slot is released by the last tile that reads it;
+//   * producers (8 warps): z for the new 8-row chunks of the strip's 32 columns and the cluster's 4 planes
+//     (b_k = exp2(-|p - mu_k|^2 log2(e) / 2 sigma_r^2), u_k = b_k f, f = p; packed f32x2 arithmetic on row pairs)
+//     from the raw stage, split, stored into the Z ring in the canonical K-major no-swizzle layout (8 x 16-byte
+//     core matrices; one 16-byte store = 8 consecutive rows of one (plane, column)); arrive on "Z full";
+//   * MMA warp: waits "Z full" and "D free", issues the tile's MMAs (M = 128, K = 16 per step: with the stacked
+//     operand z_hi [T_hi; T_lo]^T, N = 128, and z_lo T_hi^T, N = 64; else the three N = 64 products) and commits
+//     them to "Z free" and "D full" (kVtcStages tiles in flight, D in TMEM);
+//   * consumers (8 warps of 32 rows each, TMEM lane quarter = plane; HDF_VTC_CONS=4: 4 warps of 64 rows): load
+//     the output rows of their (plane, column), release the stage and store them: fp32 planes (scaled back,
+//     coalesced over the 32 columns), or -- for the tensor-core row pass -- 3 bytes per value in the strip-major
+//     layout: hi = fp16 [plane][strip][y][32] (two rows' 64-byte lines per warp store after a lane-pair exchange)
+//     and the residual as e4m3 in the same order (four rows' 32-byte lines per warp store after a 4 x 4 byte
+//     transpose over lane quads) (k_hpass_tc.cuh).
 // The Toeplitz operand T (hi, lo) is staged once per CTA.
 #pragma once
 #include <cuda_fp16.h>
