@@ -27,11 +27,11 @@ if has full; then
   for c in $CONFIGS; do
     CMD="python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline"
     $CMD > gpurun_out/ncu_plain_${TAG}_$c.log 2>&1 && \
-    ncu --set full --clock-control none --import-source on -k regex:"${NCU_K:-k_range_vpass|k_hpass_combine|k_coeffs_mma|k_bisect|k_fallback}" -s ${NCU_S:-15} -c ${NCU_C:-5} -o gpurun_out/prof_${TAG}_$c $CMD > gpurun_out/ncu_full_${TAG}_$c.log 2>&1; echo full $c rc=$?
+    ncu --set full --clock-control none --import-source on -k regex:"${NCU_K:-k_range_vpass|k_hpass_combine|k_coeffs|k_bisect|k_fallback}" -s ${NCU_S:-15} -c ${NCU_C:-5} -o gpurun_out/prof_${TAG}_$c $CMD > gpurun_out/ncu_full_${TAG}_$c.log 2>&1; echo full $c rc=$?
     # the reports are large: export the raw page and the per-line source page here, keep the report only if asked
     ncu -i gpurun_out/prof_${TAG}_$c.ncu-rep --page raw --csv > gpurun_out/raw_${TAG}_$c.csv 2>/dev/null
     python tools/ncu_summary.py --full-only gpurun_out/prof_${TAG}_$c.ncu-rep > gpurun_out/summary_${TAG}_$c.md 2>&1
-    for k in ${NCU_SRC:-k_range_vpass k_hpass_combine}; do
+    for k in ${NCU_SRC:-k_range_vpass k_hpass_combine k_coeffs_tc}; do
       python tools/ncu_lines.py gpurun_out/prof_${TAG}_$c.ncu-rep 40 $k > gpurun_out/lines_${TAG}_${c}_$k.txt 2>&1
     done
     [ -n "$KEEP_REP" ] || rm -f gpurun_out/prof_${TAG}_$c.ncu-rep
