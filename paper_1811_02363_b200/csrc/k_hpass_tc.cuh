@@ -53,7 +53,10 @@ constexpr uint32_t kHtcBoxBytes = 4 * kHtcRows * 32 * 2;    // hi part (fp16): 8
 constexpr uint32_t kHtcLoBytes = 4 * kHtcRows * 32;         // lo part (e4m3): 4 KB
 constexpr uint32_t kHtcSlotBytes = kHtcBoxBytes + kHtcLoBytes;
 constexpr uint32_t kHtcCBytes = kHtcRows * kHtcN * 4;       // 8 KB: two SW128 halves of [32][32] fp32
-constexpr int kHtcEpiCols = 16;                             // epilogue column chunk
+#ifndef HDF_HTC_EPI
+#define HDF_HTC_EPI 16
+#endif
+constexpr int kHtcEpiCols = HDF_HTC_EPI;                    // epilogue column chunk (8 frees 8 KB: a 12th ring slot fits)
 
 inline __host__ __device__ size_t hpass_tc_smem() {
     return (size_t)kHtcNB * kHtcSlotBytes + (size_t)kHtcNC * kHtcCBytes + (size_t)2 * kHtcN * kHtcKp * 2 +
